@@ -1,0 +1,275 @@
+/*
+ * pd_b200.h -- C ABI of the B200-native bond-based peridynamics time step.
+ *
+ * This is the drop-in boundary for the reference engine
+ * (/root/reference/proj/include/peridyn/engine.hpp).  Every entry point takes
+ * plain pointers and sizes; there are no C++ or torch types in the
+ * signatures, no exceptions cross the ABI, and every function returns a
+ * status code whose value names the exception type the reference would have
+ * thrown (pd_last_error() holds the reference's message text).
+ *
+ * Descriptor structs mirror the reference's value types field for field:
+ *   pd_particles      <- ParticleSet          (types.hpp:52-60)
+ *   pd_neighbor_list  <- NeighborList         (types.hpp:66-76)
+ *   pd_law            <- DamageLaw            (types.hpp:83-96)
+ *   pd_damage_model   <- DamageModel          (types.hpp:99-110)
+ *   pd_state          <- SimulationState      (types.hpp:115-122)
+ *   pd_ramp           <- RampProfile          (types.hpp:131-142)
+ *   pd_boundary       <- BoundaryConditions   (types.hpp:145-155)
+ *   pd_corrections    <- Corrections          (types.hpp:161-165)
+ *   pd_force_field    <- ForceField           (types.hpp:170-178)
+ *   pd_bundle         <- ModelBundle          (engine.hpp:90-98)
+ *   pd_options        <- SimulateOptions      (engine.hpp:100-106)
+ *   pd_tip_record     <- TipRecord            (engine.hpp:110-114)
+ * Arrays are the reference's flat row-major layouts (n x 3 for vectors,
+ * n x N for per-slot arrays), so a std::vector's data()/size() pass through
+ * unchanged.  A NULL pointer with size 0 means "empty vector".
+ */
+#ifndef PD_B200_H
+#define PD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PD_ABI_VERSION 1
+#define PD_MAX_BREAKPOINTS 8 /* per law; the reference allows any count (types.hpp:86) */
+#define PD_MAX_LAWS 256      /* bond_type is uint8 (types.hpp:71) */
+
+/* Status codes.  Each maps to the exception type the reference throws. */
+enum {
+    PD_OK = 0,
+    PD_E_INVALID_ARGUMENT = 1, /* std::invalid_argument (size mismatches, engine.cpp:34-46) */
+    PD_E_DOMAIN = 2,           /* std::domain_error (dt <= 0, rho <= 0, engine.cpp:177-190) */
+    PD_E_RUNTIME = 3,          /* std::runtime_error (non-finite u at step K, engine.cpp:23-28) */
+    PD_E_CUDA = 4,             /* CUDA failure (no reference counterpart) */
+    PD_E_NO_DEVICE = 5         /* no sm_100 device visible */
+};
+
+/* KernelVariant (engine.hpp:15) plus the B200 fast path.
+ * PD_BOND_PARALLEL: fp64, bitwise equal to compute_forces_bond_parallel.
+ * PD_NODE_PARALLEL: fp64, bitwise equal to compute_forces_node_parallel.
+ * PD_FAST:          fp64 state/integration, fp32 bond arithmetic; tolerance
+ *                   documented in DESIGN.md (not bitwise). */
+enum { PD_BOND_PARALLEL = 0, PD_NODE_PARALLEL = 1, PD_FAST = 2 };
+
+/* IntegratorKind (engine.hpp:87) */
+enum { PD_VELOCITY_VERLET = 0, PD_EULER = 1, PD_EULER_CROMER = 2 };
+
+/* BCKind (types.hpp:127) */
+enum { PD_BC_FREE = 0, PD_BC_DISPLACEMENT = 1, PD_BC_FORCE = 2 };
+
+/* RampProfile::Kind (types.hpp:132) */
+enum { PD_RAMP_CONSTANT = 0, PD_RAMP_LINEAR = 1, PD_RAMP_QUINTIC = 2 };
+
+typedef struct pd_particles {
+    int64_t n;             /* volume.size() */
+    const double* coords;  /* n x 3 */
+    int64_t coords_size;   /* coords.size() */
+    const double* volume;  /* n */
+    const double* density; /* n */
+    int64_t density_size;  /* density.size() */
+} pd_particles;
+
+typedef struct pd_neighbor_list {
+    int64_t n;                      /* n_neigh.size() */
+    int64_t group_size;             /* N, a power of two */
+    int32_t* entries;               /* n x N, -1 = broken or padding (mutated by the force pass) */
+    int32_t* n_neigh;               /* n (mutated by the force pass) */
+    const int32_t* initial_n_neigh; /* n */
+    const uint8_t* bond_type;       /* n x N or NULL */
+    int64_t bond_type_size;         /* bond_type.size() */
+    double horizon;
+} pd_neighbor_list;
+
+typedef struct pd_law {
+    double stiffness;     /* micromodulus c */
+    int32_t n_breakpoints; /* >= 1; 1 = PMB */
+    double breakpoints[PD_MAX_BREAKPOINTS];
+    double forces[PD_MAX_BREAKPOINTS];
+} pd_law;
+
+typedef struct pd_damage_model {
+    const pd_law* laws;
+    int32_t n_laws;
+    double damping; /* eta */
+} pd_damage_model;
+
+typedef struct pd_corrections {
+    const double* lambda; /* n x N or NULL */
+    int64_t lambda_size;
+    const double* beta; /* n x N or NULL */
+    int64_t beta_size;
+    const uint8_t* no_failure; /* n or NULL */
+    int64_t no_failure_size;
+} pd_corrections;
+
+typedef struct pd_state {
+    double* u; /* n x 3 */
+    double* v; /* n x 3 */
+    double* a; /* n x 3 */
+    int64_t step;
+    pd_neighbor_list connectivity;
+    double* bond_history; /* n x N or NULL */
+    int64_t bond_history_size;
+} pd_state;
+
+typedef struct pd_force_field {
+    double* body_force;     /* n x 3 (written) */
+    double* external_force; /* n x 3 (read by integrators; preserved by the force pass) */
+} pd_force_field;
+
+typedef struct pd_ramp {
+    int32_t kind;
+    int64_t rise_steps;
+    double target_scale;
+} pd_ramp;
+
+typedef struct pd_boundary {
+    const uint8_t* kind; /* n x 3, PD_BC_* */
+    int64_t kind_size;
+    const double* magnitude; /* n x 3 */
+    int64_t magnitude_size;
+    const uint8_t* ramp_id; /* n x 3 */
+    int64_t ramp_id_size;
+    const pd_ramp* ramps;
+    int32_t n_ramps;
+    const uint8_t* no_failure; /* n */
+    int64_t no_failure_size;
+    /* tip_sets (std::map order): set k holds tip_nodes[tip_offsets[k] .. tip_offsets[k+1]) */
+    int32_t n_tip_sets;
+    const int64_t* tip_offsets;
+    const int64_t* tip_nodes;
+} pd_boundary;
+
+typedef struct pd_bundle {
+    pd_particles particles;
+    pd_damage_model model;
+    pd_corrections corrections;
+    pd_boundary bc;
+    double dt;
+} pd_bundle;
+
+typedef struct pd_options {
+    int64_t steps;
+    int64_t write_every; /* 0 = no periodic writes */
+    int64_t first_step;
+    int32_t integrator; /* PD_VELOCITY_VERLET | PD_EULER | PD_EULER_CROMER */
+    int32_t variant;    /* PD_BOND_PARALLEL | PD_NODE_PARALLEL | PD_FAST */
+} pd_options;
+
+typedef struct pd_tip_record {
+    int64_t step;
+    double mean_u[3], mean_v[3], mean_a[3];
+    double body_force_sum[3], external_force_sum[3];
+} pd_tip_record;
+
+/* WriteHook (engine.hpp:118).  Called at every write step with host views of
+ * the state and forces; a nonzero return aborts the run with PD_E_RUNTIME. */
+typedef int (*pd_write_hook)(void* user, const pd_state* state, const pd_force_field* forces);
+
+/* ---- library ---------------------------------------------------------- */
+
+int pd_abi_version(void);
+/* Message of the last failing call on this thread ("" after success). */
+const char* pd_last_error(void);
+/* Number of usable sm_100 devices (0 on a machine without a B200). */
+int pd_device_count(void);
+
+/* ---- one-shot drop-ins (host buffers in, host buffers out) ------------ */
+
+/* compute_forces(variant, state, particles, model, corrections, out)
+ * (engine.hpp:35-36, engine.cpp:163-169).  Mutates state->connectivity.entries,
+ * n_neigh and bond_history exactly as the reference; writes out->body_force;
+ * out->external_force is not touched. */
+int pd_compute_forces(int32_t variant, pd_state* state, const pd_particles* particles,
+                      const pd_damage_model* model, const pd_corrections* corrections,
+                      pd_force_field* out);
+
+/* simulate(bundle, state, options, on_write) (engine.hpp:128-129,
+ * engine.cpp:374-425).  The caller sizes state->bond_history to n x N when the
+ * model needs history (the reference resizes it itself, engine.cpp:382-384).
+ * Tip records of every write step are appended to tips_out in
+ * (write step, tip set) order; n_tips_out receives the count.  When
+ * tips_capacity is too small the run fails with PD_E_INVALID_ARGUMENT before
+ * any work. */
+int pd_simulate(const pd_bundle* bundle, pd_state* state, const pd_options* options,
+                pd_write_hook on_write, void* user, pd_tip_record* tips_out,
+                int64_t tips_capacity, int64_t* n_tips_out);
+
+/* local_damage over all nodes from a host connectivity (formulas.hpp:49-55,
+ * io.cpp:243-247): phi_i = 1 - n_neigh_i / initial_i, 0 when initial_i == 0. */
+int pd_damage(const pd_neighbor_list* family, double* phi_out);
+
+/* ---- family construction on the device (geometry.cpp:97-211) ---------- */
+
+typedef struct pd_family pd_family;
+
+/* build_family(coords, horizon, grid_hint) (geometry.hpp:60-62): rows sorted
+ * ascending, padded with -1 to N = bit_ceil(max family size); identical to the
+ * reference's cell-list result.  grid_hint = {ox, oy, oz, spacing, nx, ny, nz}
+ * or NULL.  The rows stay on the device until pd_family_download. */
+int pd_build_family(const double* coords, int64_t n, double horizon, const double* grid_hint,
+                    pd_family** out, int64_t* group_size_out);
+/* entries: n x N; n_neigh and initial_n_neigh: n (both = family sizes). */
+int pd_family_download(pd_family* family, int32_t* entries, int32_t* n_neigh,
+                       int32_t* initial_n_neigh);
+void pd_family_free(pd_family* family);
+
+/* ---- device-resident context ------------------------------------------ */
+
+typedef struct pd_ctx pd_ctx;
+
+/* Field selectors for pd_ctx_download / write hooks (bitmask). */
+enum {
+    PD_FIELD_U = 1,
+    PD_FIELD_V = 2,
+    PD_FIELD_A = 4,
+    PD_FIELD_CONNECTIVITY = 8, /* entries + n_neigh */
+    PD_FIELD_HISTORY = 16,
+    PD_FIELD_FORCES = 32, /* body_force + external_force of the last step */
+    PD_FIELD_ALL = 63
+};
+
+int pd_ctx_create(int device, pd_ctx** out);
+void pd_ctx_destroy(pd_ctx* ctx);
+
+/* Upload the fixed model and an initial state; validates like
+ * ModelBundle::validate (engine.cpp:335-341) and NeighborList::validate. */
+int pd_ctx_upload(pd_ctx* ctx, const pd_bundle* bundle, const pd_state* state, int32_t variant);
+
+/* Advance the resident state (simulate() semantics, without host copies
+ * except at write steps when a hook is given; fields = PD_FIELD_* the hook
+ * needs). */
+int pd_ctx_run(pd_ctx* ctx, const pd_options* options, pd_write_hook on_write, void* user,
+               int32_t hook_fields, pd_tip_record* tips_out, int64_t tips_capacity,
+               int64_t* n_tips_out);
+
+/* One force pass on the resident state (compute_forces semantics). */
+int pd_ctx_compute_forces(pd_ctx* ctx);
+
+/* Copy the resident state back into host arrays (only the selected fields;
+ * pointers of unselected fields may be NULL). */
+int pd_ctx_download(pd_ctx* ctx, pd_state* state, pd_force_field* forces, int32_t fields);
+
+/* Damage phi of every node from the resident alive mask (K3). */
+int pd_ctx_damage(pd_ctx* ctx, double* phi_out);
+
+/* The cudaStream_t every kernel of this context is launched on, so callers
+ * can bracket a run with events on the right stream. */
+void* pd_ctx_stream(pd_ctx* ctx);
+
+/* Kernel launches issued by this context since creation. */
+int64_t pd_ctx_launch_count(pd_ctx* ctx);
+
+/* Live directed bonds in the resident alive mask (sum of n_neigh). */
+int64_t pd_ctx_live_bonds(pd_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PD_B200_H */

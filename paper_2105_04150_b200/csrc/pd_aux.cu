@@ -1,0 +1,253 @@
+// pd_aux.cu -- small per-node kernels around the fused step: layout packing,
+// the Verlet prologue drift, finite checks, connectivity materialisation,
+// damage (K3) and tip reductions (K6).  fp64 arithmetic uses explicit __d*_rn
+// intrinsics so results are bitwise equal to the reference.
+#include <cuda_runtime.h>
+
+#include "pd_device.cuh"
+#include "pd_internal.h"
+
+namespace pdb {
+namespace {
+
+constexpr int TPB = 256;
+
+inline dim3 grid_for(long long n) { return dim3(unsigned((n + TPB - 1) / TPB)); }
+
+__global__ void pack_xv_kernel(const double* coords, const double* volume, long long n,
+                               double4* xv) {
+    const long long i = blockIdx.x * (long long)TPB + threadIdx.x;
+    if (i < n)
+        xv[i] = make_double4(coords[3 * i], coords[3 * i + 1], coords[3 * i + 2], volume[i]);
+}
+
+__global__ void pack_u_kernel(const double* u, const uint8_t* nofail, long long n, double4* out) {
+    const long long i = blockIdx.x * (long long)TPB + threadIdx.x;
+    if (i < n)
+        out[i] = make_double4(u[3 * i], u[3 * i + 1], u[3 * i + 2],
+                              (nofail && nofail[i]) ? 1.0 : 0.0);
+}
+
+__global__ void unpack_u_kernel(const double4* u, long long n, double* out) {
+    const long long i = blockIdx.x * (long long)TPB + threadIdx.x;
+    if (i < n) {
+        const double4 x = u[i];
+        out[3 * i] = x.x;
+        out[3 * i + 1] = x.y;
+        out[3 * i + 2] = x.z;
+    }
+}
+
+// alive bit k of row i <=> entries[i*N+k] >= 0 (engine.cpp:56-58 skips j < 0)
+__global__ void init_alive_kernel(const int32_t* entries, long long n, int N, int W,
+                                  uint32_t* alive) {
+    const long long w = blockIdx.x * (long long)TPB + threadIdx.x;
+    if (w >= n * W)
+        return;
+    const long long i = w / W;
+    const int base = int(w - i * W) * 32;
+    const int cnt = N < 32 ? N : 32;
+    uint32_t word = 0;
+    for (int b = 0; b < cnt; ++b)
+        if (entries[i * N + base + b] >= 0)
+            word |= 1u << b;
+    alive[w] = word;
+}
+
+// Memory safety: any live entry must index a node of this context.
+__global__ void validate_entries_kernel(const int32_t* entries, long long n, int N,
+                                        unsigned long long* bad_row) {
+    const long long idx = blockIdx.x * (long long)TPB + threadIdx.x;
+    if (idx >= n * N)
+        return;
+    const int32_t j = entries[idx];
+    if (j >= n || (j < 0 && j != -1))
+        atomicMin(bad_row, (unsigned long long)(idx / N));
+}
+
+// verlet_drift (engine.cpp:221-233) + apply_displacement_positions(s+1)
+// (engine.cpp:262-272) ahead of the first fused step of a run.
+__global__ void vv_prologue_kernel(DevArgs A) {
+    const long long i = A.begin + blockIdx.x * (long long)TPB + threadIdx.x;
+    if (i >= A.end)
+        return;
+    const double dt = A.dt;
+    const double half_dt2 = __ddiv_rn(__dmul_rn(dt, dt), 2.0);
+    const double4 u = A.u_in[i];
+    const double u0[3] = {u.x, u.y, u.z};
+    double un[3];
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+        un[ax] = __dadd_rn(__dadd_rn(u0[ax], __dmul_rn(A.v[3 * i + ax], dt)),
+                           __dmul_rn(A.a[3 * i + ax], half_dt2));
+        if (A.bc_kind && A.bc_kind[3 * i + ax] == PD_BC_DISPLACEMENT)
+            un[ax] = __dmul_rn(A.bc_mag[3 * i + ax], ramp_scale(A.ramps[A.bc_ramp[3 * i + ax]],
+                                                                A.step + 1));
+    }
+    A.u_out[i] = make_double4(un[0], un[1], un[2], u.w);
+    if (!finite3(un[0], un[1], un[2]))
+        atomicMin((unsigned long long*)A.err_step, (unsigned long long)A.step);
+}
+
+// check_state_finite (engine.cpp:23-28)
+__global__ void check_finite_kernel(const double4* u, long long begin, long long end,
+                                    long long step, long long* err) {
+    const long long i = begin + blockIdx.x * (long long)TPB + threadIdx.x;
+    if (i >= end)
+        return;
+    const double4 x = u[i];
+    if (!finite3(x.x, x.y, x.z))
+        atomicMin((unsigned long long*)err, (unsigned long long)step);
+}
+
+__global__ void materialize_entries_kernel(const int32_t* entries, const uint32_t* alive,
+                                           long long n, int N, int W, int32_t* out) {
+    const long long idx = blockIdx.x * (long long)TPB + threadIdx.x;
+    if (idx >= n * N)
+        return;
+    const long long i = idx / N;
+    const int k = int(idx - i * N);
+    const uint32_t word = alive[i * W + (k >> 5)];
+    out[idx] = ((word >> (k & 31)) & 1u) ? entries[idx] : -1;
+}
+
+// local_damage via make_snapshot (formulas.hpp:49-55, io.cpp:243-247)
+__global__ void damage_kernel(const int32_t* n_neigh, const int32_t* initial, long long n,
+                              double* phi) {
+    const long long i = blockIdx.x * (long long)TPB + threadIdx.x;
+    if (i >= n)
+        return;
+    const int32_t init = initial[i];
+    phi[i] = init > 0 ? __dsub_rn(1.0, __ddiv_rn((double)n_neigh[i], (double)init)) : 0.0;
+}
+
+__global__ void sum_kernel(const int32_t* x, long long n, unsigned long long* out) {
+    __shared__ unsigned long long part[TPB / 32];
+    unsigned long long acc = 0;
+    for (long long i = blockIdx.x * (long long)TPB + threadIdx.x; i < n;
+         i += (long long)gridDim.x * TPB)
+        acc += (unsigned long long)x[i];
+    for (int o = 16; o > 0; o /= 2)
+        acc += __shfl_down_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0)
+        part[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (int w = 0; w < TPB / 32; ++w)
+            t += part[w];
+        atomicAdd(out, t);
+    }
+}
+
+// record_tips (engine.cpp:349-370): one thread per tip set, sequential sums
+// in set order so the result matches the reference bit for bit.
+__global__ void tips_kernel(const double4* u, const double* v, const double* a, const double4* xv,
+                            const double* body, const double* ext, int n_sets,
+                            const long long* offsets, const long long* nodes, long long step,
+                            pd_tip_record* out) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n_sets)
+        return;
+    pd_tip_record r;
+    r.step = step;
+    for (int ax = 0; ax < 3; ++ax)
+        r.mean_u[ax] = r.mean_v[ax] = r.mean_a[ax] = r.body_force_sum[ax] =
+            r.external_force_sum[ax] = 0.0;
+    const long long b = offsets[s], e = offsets[s + 1];
+    for (long long t = b; t < e; ++t) {
+        const long long i = nodes[t];
+        const double4 ui = u[i];
+        const double uu[3] = {ui.x, ui.y, ui.z};
+        const double vol = xv[i].w;
+        for (int ax = 0; ax < 3; ++ax) {
+            r.mean_u[ax] = __dadd_rn(r.mean_u[ax], uu[ax]);
+            r.mean_v[ax] = __dadd_rn(r.mean_v[ax], v[3 * i + ax]);
+            r.mean_a[ax] = __dadd_rn(r.mean_a[ax], a[3 * i + ax]);
+            r.body_force_sum[ax] = __dadd_rn(r.body_force_sum[ax], __dmul_rn(body[3 * i + ax], vol));
+            r.external_force_sum[ax] =
+                __dadd_rn(r.external_force_sum[ax], __dmul_rn(ext[3 * i + ax], vol));
+        }
+    }
+    if (e > b) {
+        const double inv = __ddiv_rn(1.0, (double)(e - b));
+        for (int ax = 0; ax < 3; ++ax) {
+            r.mean_u[ax] = __dmul_rn(r.mean_u[ax], inv);
+            r.mean_v[ax] = __dmul_rn(r.mean_v[ax], inv);
+            r.mean_a[ax] = __dmul_rn(r.mean_a[ax], inv);
+        }
+    }
+    out[s] = r;
+}
+
+} // namespace
+
+void launch_pack_xv(const double* coords, const double* volume, long long n, double4* xv,
+                    cudaStream_t st) {
+    if (n > 0)
+        pack_xv_kernel<<<grid_for(n), TPB, 0, st>>>(coords, volume, n, xv);
+}
+
+void launch_pack_u(const double* u, const uint8_t* nofail, long long n, double4* out,
+                   cudaStream_t st) {
+    if (n > 0)
+        pack_u_kernel<<<grid_for(n), TPB, 0, st>>>(u, nofail, n, out);
+}
+
+void launch_unpack_u(const double4* u, long long n, double* out, cudaStream_t st) {
+    if (n > 0)
+        unpack_u_kernel<<<grid_for(n), TPB, 0, st>>>(u, n, out);
+}
+
+void launch_init_alive(const int32_t* entries, long long n, int N, int W, uint32_t* alive,
+                       cudaStream_t st) {
+    if (n > 0)
+        init_alive_kernel<<<grid_for(n * W), TPB, 0, st>>>(entries, n, N, W, alive);
+}
+
+void launch_validate_entries(const int32_t* entries, long long n, int N,
+                             unsigned long long* bad_row, cudaStream_t st) {
+    if (n > 0)
+        validate_entries_kernel<<<grid_for(n * N), TPB, 0, st>>>(entries, n, N, bad_row);
+}
+
+void launch_vv_prologue(const DevArgs& A, cudaStream_t st) {
+    if (A.end > A.begin)
+        vv_prologue_kernel<<<grid_for(A.end - A.begin), TPB, 0, st>>>(A);
+}
+
+void launch_check_finite(const double4* u, long long begin, long long end, long long step,
+                         long long* err, cudaStream_t st) {
+    if (end > begin)
+        check_finite_kernel<<<grid_for(end - begin), TPB, 0, st>>>(u, begin, end, step, err);
+}
+
+void launch_materialize_entries(const int32_t* entries, const uint32_t* alive, long long n, int N,
+                                int W, int32_t* out, cudaStream_t st) {
+    if (n > 0)
+        materialize_entries_kernel<<<grid_for(n * N), TPB, 0, st>>>(entries, alive, n, N, W, out);
+}
+
+void launch_damage(const int32_t* n_neigh, const int32_t* initial, long long n, double* phi,
+                   cudaStream_t st) {
+    if (n > 0)
+        damage_kernel<<<grid_for(n), TPB, 0, st>>>(n_neigh, initial, n, phi);
+}
+
+void launch_sum(const int32_t* x, long long n, unsigned long long* out, cudaStream_t st) {
+    long long blocks = (n + TPB - 1) / TPB;
+    if (blocks > 148 * 8)
+        blocks = 148 * 8;
+    if (n > 0)
+        sum_kernel<<<unsigned(blocks), TPB, 0, st>>>(x, n, out);
+}
+
+void launch_tips(const double4* u, const double* v, const double* a, const double4* xv,
+                 const double* body, const double* ext, int n_sets, const long long* offsets,
+                 const long long* nodes, long long step, pd_tip_record* out, cudaStream_t st) {
+    if (n_sets > 0)
+        tips_kernel<<<(n_sets + 63) / 64, 64, 0, st>>>(u, v, a, xv, body, ext, n_sets, offsets,
+                                                       nodes, step, out);
+}
+
+} // namespace pdb

@@ -1,0 +1,218 @@
+// pd_device.cuh -- device-side layouts shared by the B200 kernels.
+//
+// HBM layout of one resident model (one pd_ctx), n nodes, group size N:
+//   xv       double4[n]   {x, y, z, V_j}            gathered per live slot (32 B, LDG.256)
+//   u[2]     double4[n]   {ux, uy, uz, no_fail_j}   double-buffered displacement; the
+//                                                   4th lane carries the node's no-failure
+//                                                   flag so the per-slot gather needs no
+//                                                   extra load (engine.cpp:79-80)
+//   v, a     double[3n]   per-node streams (reference flat layout)
+//   rho      double[n]
+//   entries  int32[n*N]   the row list as uploaded (never rewritten; breaks live in alive)
+//   alive    uint32[n*W]  W = max(1, N/32); bit k of row i == (entries[i*N+k] != -1)
+//                         in the reference's mutable list (engine.cpp:81-83, 93-96)
+//   hist     double[n*N]  only for n-linear laws (types.hpp:120)
+//   btype    uint8[n*N]   optional bond types (types.hpp:71)
+//   lambda, beta double[n*N] optional (types.hpp:161-165)
+//   bc_*     per node-axis boundary arrays (types.hpp:145-155), NULL when all free
+#pragma once
+
+#include <cstdint>
+
+#include "../../include/pd_b200.h"
+
+namespace pdb {
+
+struct DevLaw {
+    double c;
+    int nbp;
+    int pad_;
+    double bp[PD_MAX_BREAKPOINTS];
+    double f[PD_MAX_BREAKPOINTS];
+};
+
+struct DevRamp {
+    int kind;
+    int pad_;
+    long long rise;
+    double target;
+};
+
+constexpr long long kNoError = 0x7fffffffffffffffLL;
+
+struct DevArgs {
+    long long n;        // nodes in this context (owned + ghost)
+    long long begin;    // first node this launch computes
+    long long end;      // one past the last node this launch computes
+    int N;              // group size
+    int log2N;
+    int W;              // alive words per row
+    int n_laws;
+    const double4* xv;
+    const double4* u_in;
+    double4* u_out;
+    double* v;
+    double* a;
+    const double* rho;
+    const int32_t* entries;
+    uint32_t* alive;
+    int32_t* n_neigh;         // live count per row, decremented on breaks
+    double* hist;
+    const uint8_t* btype;
+    const double* lambda;
+    const double* beta;
+    const uint8_t* bc_kind;   // 3n or NULL
+    const double* bc_mag;     // 3n
+    const uint8_t* bc_ramp;   // 3n
+    const DevRamp* ramps;
+    double* body_force;       // 3n, stored when store_forces
+    double* ext_force;        // 3n, stored when store_forces
+    long long* err_step;      // first step whose force pass sees non-finite u
+    long long step;           // the step s this launch advances (s -> s+1)
+    double dt;
+    double damping;
+    int store_forces;
+    int do_drift;             // VV: produce next step's drifted u into u_out
+};
+
+// RampProfile::scale/rate/accel (types.cpp:119-169); same operation order, so
+// with FMA contraction disabled the device values equal the host's bit for bit.
+__device__ __forceinline__ double ramp_scale(const DevRamp& r, long long step) {
+    if (r.kind == PD_RAMP_CONSTANT)
+        return r.target;
+    if (r.rise <= 0 || step >= r.rise)
+        return r.target;
+    if (r.kind == PD_RAMP_LINEAR)
+        return __ddiv_rn(__dmul_rn(r.target, (double)step), (double)r.rise);
+    const double t = __ddiv_rn((double)step, (double)r.rise);
+    // target * t * t * t * (10 + t * (-15 + 6 * t))
+    const double inner = __dadd_rn(10.0, __dmul_rn(t, __dadd_rn(-15.0, __dmul_rn(6.0, t))));
+    return __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(r.target, t), t), t), inner);
+}
+
+__device__ __forceinline__ double ramp_rate(const DevRamp& r, long long step) {
+    if (r.kind == PD_RAMP_CONSTANT)
+        return 0.0;
+    if (r.rise <= 0 || step >= r.rise)
+        return 0.0;
+    if (r.kind == PD_RAMP_LINEAR)
+        return __ddiv_rn(r.target, (double)r.rise);
+    const double t = __ddiv_rn((double)step, (double)r.rise);
+    // target * 30 * t * t * (t - 1) * (t - 1) / rise
+    double x = __dmul_rn(r.target, 30.0);
+    x = __dmul_rn(x, t);
+    x = __dmul_rn(x, t);
+    x = __dmul_rn(x, __dsub_rn(t, 1.0));
+    x = __dmul_rn(x, __dsub_rn(t, 1.0));
+    return __ddiv_rn(x, (double)r.rise);
+}
+
+__device__ __forceinline__ double ramp_accel(const DevRamp& r, long long step) {
+    if (r.kind != PD_RAMP_QUINTIC)
+        return 0.0;
+    if (r.rise <= 0 || step >= r.rise)
+        return 0.0;
+    const double t = __ddiv_rn((double)step, (double)r.rise);
+    // target * 60 * t * (2 * t - 1) * (t - 1) / (rise * rise)
+    double x = __dmul_rn(r.target, 60.0);
+    x = __dmul_rn(x, t);
+    x = __dmul_rn(x, __dsub_rn(__dmul_rn(2.0, t), 1.0));
+    x = __dmul_rn(x, __dsub_rn(t, 1.0));
+    return __ddiv_rn(x, __dmul_rn((double)r.rise, (double)r.rise));
+}
+
+__device__ __forceinline__ bool finite3(double x, double y, double z) {
+    return isfinite(x) && isfinite(y) && isfinite(z);
+}
+
+// Per-node integrator epilogue shared by every force kernel.  fp64 with
+// explicit round-to-nearest intrinsics (never contracted), so the exact and
+// fast paths integrate identically given the same body force.
+//   MODE 1: verlet_kick + apply_displacement_kinematics(s+1)  (engine.cpp:235-252, 274-286)
+//           then verlet_drift + apply_displacement_positions(s+2) for the next
+//           step into u_out (engine.cpp:221-233, 262-272; driver order :397-404)
+//   MODE 2: step_euler (engine.cpp:187-202), MODE 3: step_euler_cromer (:204-219),
+//           then positions + kinematics of step s+1 (driver order :405-415)
+// External force: external_force.assign(0) then += mag * scale (engine.cpp:288-297),
+// evaluated at s+1 (Verlet) or s (Euler).
+template <int MODE>
+__device__ __forceinline__ void node_epilogue(const DevArgs& A, long long i, const double4& ui,
+                                              double fx, double fy, double fz) {
+    const double Fb[3] = {fx, fy, fz};
+    const double u0[3] = {ui.x, ui.y, ui.z};
+    const long long s = A.step;
+    const double dt = A.dt;
+    int kind[3];
+    double mag[3] = {0.0, 0.0, 0.0};
+    DevRamp ramp[3];
+    double Fe[3], v[3], a[3], un[3];
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+        kind[ax] = A.bc_kind ? int(A.bc_kind[3 * i + ax]) : PD_BC_FREE;
+        if (kind[ax] != PD_BC_FREE) {
+            mag[ax] = A.bc_mag[3 * i + ax];
+            ramp[ax] = A.ramps[A.bc_ramp[3 * i + ax]];
+        }
+        Fe[ax] = kind[ax] == PD_BC_FORCE
+                     ? __dadd_rn(0.0, __dmul_rn(mag[ax], ramp_scale(ramp[ax], MODE == 1 ? s + 1 : s)))
+                     : 0.0;
+        v[ax] = A.v[3 * i + ax];
+        a[ax] = A.a[3 * i + ax];
+    }
+    const double inv = __ddiv_rn(1.0, A.rho[i]);
+    bool write_u = true;
+    if (MODE == 1) {
+        const double half = __ddiv_rn(dt, 2.0);
+        const double half_dt2 = __ddiv_rn(__dmul_rn(dt, dt), 2.0);
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+            const double vh = __dadd_rn(v[ax], __dmul_rn(a[ax], half));
+            double an = __dmul_rn(__dsub_rn(__dadd_rn(Fb[ax], Fe[ax]), __dmul_rn(vh, A.damping)), inv);
+            double vn = __dadd_rn(vh, __dmul_rn(an, half));
+            if (kind[ax] == PD_BC_DISPLACEMENT) {
+                vn = __ddiv_rn(__dmul_rn(mag[ax], ramp_rate(ramp[ax], s + 1)), dt);
+                an = __ddiv_rn(__dmul_rn(mag[ax], ramp_accel(ramp[ax], s + 1)), __dmul_rn(dt, dt));
+            }
+            v[ax] = vn;
+            a[ax] = an;
+            un[ax] = __dadd_rn(__dadd_rn(u0[ax], __dmul_rn(vn, dt)), __dmul_rn(an, half_dt2));
+            if (kind[ax] == PD_BC_DISPLACEMENT)
+                un[ax] = __dmul_rn(mag[ax], ramp_scale(ramp[ax], s + 2));
+        }
+        write_u = A.do_drift != 0;
+    } else {
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+            const double acc = __dmul_rn(__dadd_rn(Fb[ax], Fe[ax]), inv);
+            const double v_old = v[ax];
+            const double v_new = __dadd_rn(v_old, __dmul_rn(acc, dt));
+            a[ax] = acc;
+            v[ax] = v_new;
+            un[ax] = __dadd_rn(u0[ax], __dmul_rn(MODE == 2 ? v_old : v_new, dt));
+            if (kind[ax] == PD_BC_DISPLACEMENT) {
+                un[ax] = __dmul_rn(mag[ax], ramp_scale(ramp[ax], s + 1));
+                v[ax] = __ddiv_rn(__dmul_rn(mag[ax], ramp_rate(ramp[ax], s + 1)), dt);
+                a[ax] = __ddiv_rn(__dmul_rn(mag[ax], ramp_accel(ramp[ax], s + 1)), __dmul_rn(dt, dt));
+            }
+        }
+    }
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+        A.v[3 * i + ax] = v[ax];
+        A.a[3 * i + ax] = a[ax];
+    }
+    if (A.store_forces) {
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+            A.body_force[3 * i + ax] = Fb[ax];
+            A.ext_force[3 * i + ax] = Fe[ax];
+        }
+    }
+    if (write_u) {
+        A.u_out[i] = make_double4(un[0], un[1], un[2], ui.w);
+        if (!finite3(un[0], un[1], un[2]))
+            atomicMin((unsigned long long*)A.err_step, (unsigned long long)(s + 1));
+    }
+}
+
+} // namespace pdb

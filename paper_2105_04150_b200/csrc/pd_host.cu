@@ -1,0 +1,897 @@
+// pd_host.cu -- the C ABI (include/pd_b200.h): validation with the reference's
+// error types and messages, device residency, the per-step launch loop, and
+// the host views handed to write hooks.
+//
+// Reference contracts followed here:
+//   ModelBundle::validate            engine.cpp:335-341 -> types.cpp:6-21, 92-99, 181-196
+//   check_force_inputs               engine.cpp:30-49
+//   compute_forces (dispatcher)      engine.cpp:163-169
+//   simulate (loop, cadence, tips)   engine.cpp:374-425, record_tips :349-370
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "pd_device.cuh"
+#include "pd_internal.h"
+
+using namespace pdb;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+int ok() {
+    g_err.clear();
+    return PD_OK;
+}
+
+} // namespace
+
+int pdb::set_error(int code, const char* msg) {
+    g_err = msg;
+    return code;
+}
+
+namespace {
+
+#define PD_CK(expr)                                                                              \
+    do {                                                                                         \
+        cudaError_t e_ = (expr);                                                                 \
+        if (e_ != cudaSuccess)                                                                   \
+            return fail(PD_E_CUDA, "CUDA error %s at %s:%d (%s)", cudaGetErrorString(e_),        \
+                        __FILE__, __LINE__, #expr);                                              \
+    } while (0)
+
+#define PD_TRY(expr)                                                                             \
+    do {                                                                                         \
+        int rc_ = (expr);                                                                        \
+        if (rc_ != PD_OK)                                                                        \
+            return rc_;                                                                          \
+    } while (0)
+
+template <class T> struct DevBuf {
+    T* p = nullptr;
+    size_t count = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p)
+            cudaFree(p);
+        p = nullptr;
+        count = 0;
+    }
+    cudaError_t alloc(size_t n) {
+        if (n == count && p)
+            return cudaSuccess;
+        release();
+        if (n == 0)
+            return cudaSuccess;
+        count = n;
+        return cudaMalloc(&p, n * sizeof(T));
+    }
+    cudaError_t upload(const T* host, size_t n, cudaStream_t st) {
+        cudaError_t e = alloc(n);
+        if (e != cudaSuccess || n == 0)
+            return e;
+        return cudaMemcpyAsync(p, host, n * sizeof(T), cudaMemcpyHostToDevice, st);
+    }
+};
+
+// ---- validation with the reference's messages -----------------------------
+
+int law_validate(const pd_law& l) {
+    if (!(l.stiffness > 0))
+        return fail(PD_E_INVALID_ARGUMENT, "DamageLaw: stiffness must be positive");
+    if (l.n_breakpoints < 1)
+        return fail(PD_E_INVALID_ARGUMENT,
+                    "DamageLaw: breakpoints and forces must match and be non-empty");
+    if (l.n_breakpoints > PD_MAX_BREAKPOINTS)
+        return fail(PD_E_INVALID_ARGUMENT, "DamageLaw: more than %d breakpoints is not supported",
+                    PD_MAX_BREAKPOINTS);
+    double prev = 0;
+    for (int k = 0; k < l.n_breakpoints; ++k) {
+        if (!(l.breakpoints[k] > prev))
+            return fail(PD_E_INVALID_ARGUMENT,
+                        "DamageLaw: breakpoints must be strictly increasing and positive");
+        prev = l.breakpoints[k];
+    }
+    const double f0 = l.stiffness * l.breakpoints[0];
+    if (std::abs(l.forces[0] - f0) > 1e-9 * std::max(std::abs(f0), 1.0))
+        return fail(PD_E_INVALID_ARGUMENT, "DamageLaw: envelope must leave the origin with slope c");
+    return PD_OK;
+}
+
+int model_validate(const pd_damage_model& m) {
+    if (m.n_laws < 1 || !m.laws)
+        return fail(PD_E_INVALID_ARGUMENT, "DamageModel: no laws defined");
+    if (m.n_laws > PD_MAX_LAWS)
+        return fail(PD_E_INVALID_ARGUMENT, "DamageModel: more than %d laws", PD_MAX_LAWS);
+    for (int k = 0; k < m.n_laws; ++k)
+        PD_TRY(law_validate(m.laws[k]));
+    if (m.damping < 0)
+        return fail(PD_E_INVALID_ARGUMENT, "DamageModel: negative damping");
+    return PD_OK;
+}
+
+bool needs_history(const pd_damage_model& m) {
+    for (int k = 0; k < m.n_laws; ++k)
+        if (m.laws[k].n_breakpoints > 1)
+            return true;
+    return false;
+}
+
+int particles_validate(const pd_particles& p) {
+    const int64_t n = p.n;
+    if (n < 1)
+        return fail(PD_E_INVALID_ARGUMENT, "ParticleSet: empty");
+    if (p.coords_size != 3 * n || p.density_size != n)
+        return fail(PD_E_INVALID_ARGUMENT, "ParticleSet: field lengths differ");
+    for (int64_t i = 0; i < n; ++i) {
+        if (!(p.volume[i] > 0))
+            return fail(PD_E_INVALID_ARGUMENT, "ParticleSet: non-positive volume at node %lld",
+                        (long long)i);
+        if (!(p.density[i] > 0))
+            return fail(PD_E_INVALID_ARGUMENT, "ParticleSet: non-positive density at node %lld",
+                        (long long)i);
+    }
+    return PD_OK;
+}
+
+int bc_validate(const pd_boundary& bc, int64_t n) {
+    if (bc.kind_size != 3 * n || bc.magnitude_size != 3 * n || bc.ramp_id_size != 3 * n ||
+        bc.no_failure_size != n)
+        return fail(PD_E_INVALID_ARGUMENT,
+                    "BoundaryConditions: field lengths do not match node count");
+    if (bc.n_ramps < 1)
+        return fail(PD_E_INVALID_ARGUMENT, "BoundaryConditions: no ramp profiles");
+    for (int64_t k = 0; k < 3 * n; ++k)
+        if (bc.ramp_id[k] >= bc.n_ramps)
+            return fail(PD_E_INVALID_ARGUMENT, "BoundaryConditions: ramp id out of range");
+    for (int32_t s = 0; s < bc.n_tip_sets; ++s)
+        for (int64_t t = bc.tip_offsets[s]; t < bc.tip_offsets[s + 1]; ++t)
+            if (bc.tip_nodes[t] < 0 || bc.tip_nodes[t] >= n)
+                return fail(PD_E_INVALID_ARGUMENT,
+                            "BoundaryConditions: tip set #%d has an invalid node index", s);
+    return PD_OK;
+}
+
+int group_validate(int64_t N) {
+    if (N < 1 || (N & (N - 1)) != 0)
+        return fail(PD_E_INVALID_ARGUMENT, "NeighborList: group size must be a power of two");
+    if (N > 256)
+        return fail(PD_E_INVALID_ARGUMENT,
+                    "NeighborList: group size %lld exceeds the supported maximum of 256",
+                    (long long)N);
+    return PD_OK;
+}
+
+} // namespace
+
+// ---- the resident context ---------------------------------------------------
+
+struct pd_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int64_t launches = 0;
+
+    int64_t n = 0;
+    int N = 0, W = 0, log2N = 0;
+    int variant = PD_BOND_PARALLEL;
+    bool history = false;
+    bool has_bc = false;
+    int n_laws = 0;
+    double damping = 0, dt = 0;
+    int64_t step = 0;
+    int cur = 0;
+
+    DevBuf<double4> xv, u[2];
+    DevBuf<double> v, a, rho, hist, lambda, beta, body, ext;
+    DevBuf<int32_t> entries, n_neigh, initial, scratch_i32;
+    DevBuf<uint32_t> alive;
+    DevBuf<uint8_t> btype, bc_kind, bc_ramp, nofail;
+    DevBuf<double> bc_mag, scratch_f64;
+    DevBuf<DevRamp> ramps;
+    DevBuf<long long> err, tip_offsets, tip_nodes;
+    DevBuf<unsigned long long> counter;
+    DevBuf<pd_tip_record> tips;
+    int n_tip_sets = 0;
+    bool forces_valid = false;
+
+    DevArgs args() const {
+        DevArgs A{};
+        A.n = n;
+        A.begin = 0;
+        A.end = n;
+        A.N = N;
+        A.log2N = log2N;
+        A.W = W;
+        A.n_laws = n_laws;
+        A.xv = xv.p;
+        A.u_in = u[cur].p;
+        A.u_out = u[cur ^ 1].p;
+        A.v = v.p;
+        A.a = a.p;
+        A.rho = rho.p;
+        A.entries = entries.p;
+        A.alive = alive.p;
+        A.n_neigh = n_neigh.p;
+        A.hist = hist.p;
+        A.btype = btype.p;
+        A.lambda = lambda.p;
+        A.beta = beta.p;
+        A.bc_kind = has_bc ? bc_kind.p : nullptr;
+        A.bc_mag = bc_mag.p;
+        A.bc_ramp = bc_ramp.p;
+        A.ramps = ramps.p;
+        A.body_force = body.p;
+        A.ext_force = ext.p;
+        A.err_step = err.p;
+        A.step = step;
+        A.dt = dt;
+        A.damping = damping;
+        A.store_forces = 0;
+        A.do_drift = 0;
+        return A;
+    }
+};
+
+namespace {
+
+int select_device(pd_ctx* ctx) {
+    PD_CK(cudaSetDevice(ctx->device));
+    return PD_OK;
+}
+
+int upload_laws(pd_ctx* ctx, const pd_damage_model& m) {
+    std::vector<DevLaw> laws(size_t(m.n_laws));
+    for (int k = 0; k < m.n_laws; ++k) {
+        DevLaw& d = laws[size_t(k)];
+        std::memset(&d, 0, sizeof d);
+        d.c = m.laws[k].stiffness;
+        d.nbp = m.laws[k].n_breakpoints;
+        for (int b = 0; b < d.nbp; ++b) {
+            d.bp[b] = m.laws[k].breakpoints[b];
+            d.f[b] = m.laws[k].forces[b];
+        }
+    }
+    exact_set_laws(laws.data(), m.n_laws, ctx->stream);
+    PD_CK(cudaGetLastError());
+    ctx->n_laws = m.n_laws;
+    ctx->damping = m.damping;
+    ctx->history = needs_history(m);
+    return PD_OK;
+}
+
+// Geometry, connectivity, corrections and the mutable state.  Validation of
+// the caller's sizes is done by the callers (they differ between
+// compute_forces and simulate, as in the reference).
+int upload_common(pd_ctx* ctx, const pd_particles& p, const pd_state& st,
+                  const pd_damage_model& m, const pd_corrections& corr,
+                  const uint8_t* nofail, int64_t nofail_size) {
+    cudaStream_t s = ctx->stream;
+    const int64_t n = st.connectivity.n;
+    const int64_t N = st.connectivity.group_size;
+    PD_TRY(group_validate(N));
+    if (p.coords_size != 3 * n || !p.coords || !p.volume)
+        return fail(PD_E_INVALID_ARGUMENT, "ParticleSet: field lengths differ");
+    ctx->n = n;
+    ctx->N = int(N);
+    ctx->W = N < 32 ? 1 : int(N / 32);
+    ctx->log2N = 0;
+    while ((int64_t(1) << ctx->log2N) < N)
+        ++ctx->log2N;
+    const int64_t slots = n * N;
+
+    // bond types must index a law (out of range is UB in the reference)
+    if (st.connectivity.bond_type_size != 0) {
+        if (st.connectivity.bond_type_size != slots)
+            return fail(PD_E_INVALID_ARGUMENT, "NeighborList: bond_type size mismatch");
+        for (int64_t k = 0; k < slots; ++k)
+            if (st.connectivity.entries[k] >= 0 && st.connectivity.bond_type[k] >= m.n_laws)
+                return fail(PD_E_INVALID_ARGUMENT,
+                            "DamageModel: unknown bond type %d",
+                            int(st.connectivity.bond_type[k]));
+    }
+    PD_TRY(upload_laws(ctx, m));
+
+    // xv = {x, y, z, V}
+    PD_CK(ctx->scratch_f64.upload(p.coords, size_t(3 * n), s));
+    PD_CK(ctx->rho.alloc(size_t(n)));
+    PD_CK(cudaMemcpyAsync(ctx->rho.p, p.volume, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    PD_CK(ctx->xv.alloc(size_t(n)));
+    launch_pack_xv(ctx->scratch_f64.p, ctx->rho.p, n, ctx->xv.p, s);
+    ++ctx->launches;
+    if (p.density && p.density_size == n)
+        PD_CK(cudaMemcpyAsync(ctx->rho.p, p.density, sizeof(double) * n, cudaMemcpyHostToDevice,
+                              s));
+
+    // u = {ux, uy, uz, no_failure}
+    PD_CK(ctx->scratch_f64.upload(st.u, size_t(3 * n), s));
+    PD_CK(ctx->nofail.alloc(size_t(n)));
+    if (nofail && nofail_size == n)
+        PD_CK(cudaMemcpyAsync(ctx->nofail.p, nofail, size_t(n), cudaMemcpyHostToDevice, s));
+    else
+        PD_CK(cudaMemsetAsync(ctx->nofail.p, 0, size_t(n), s));
+    PD_CK(ctx->u[0].alloc(size_t(n)));
+    PD_CK(ctx->u[1].alloc(size_t(n)));
+    ctx->cur = 0;
+    launch_pack_u(ctx->scratch_f64.p, ctx->nofail.p, n, ctx->u[0].p, s);
+    ++ctx->launches;
+
+    PD_CK(ctx->v.alloc(size_t(3 * n)));
+    PD_CK(ctx->a.alloc(size_t(3 * n)));
+    if (st.v)
+        PD_CK(cudaMemcpyAsync(ctx->v.p, st.v, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s));
+    else
+        PD_CK(cudaMemsetAsync(ctx->v.p, 0, sizeof(double) * 3 * n, s));
+    if (st.a)
+        PD_CK(cudaMemcpyAsync(ctx->a.p, st.a, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s));
+    else
+        PD_CK(cudaMemsetAsync(ctx->a.p, 0, sizeof(double) * 3 * n, s));
+
+    // connectivity: immutable row list + alive mask + counts
+    PD_CK(ctx->entries.upload(st.connectivity.entries, size_t(slots), s));
+    PD_CK(ctx->n_neigh.upload(st.connectivity.n_neigh, size_t(n), s));
+    PD_CK(ctx->initial.upload(st.connectivity.initial_n_neigh, size_t(n), s));
+    PD_CK(ctx->alive.alloc(size_t(n * ctx->W)));
+    PD_CK(ctx->counter.alloc(1));
+    const unsigned long long none = ~0ull;
+    PD_CK(cudaMemcpyAsync(ctx->counter.p, &none, sizeof none, cudaMemcpyHostToDevice, s));
+    launch_validate_entries(ctx->entries.p, n, ctx->N, ctx->counter.p, s);
+    launch_init_alive(ctx->entries.p, n, ctx->N, ctx->W, ctx->alive.p, s);
+    ctx->launches += 2;
+    unsigned long long bad = 0;
+    PD_CK(cudaMemcpyAsync(&bad, ctx->counter.p, sizeof bad, cudaMemcpyDeviceToHost, s));
+    PD_CK(cudaStreamSynchronize(s));
+    if (bad != none)
+        return fail(PD_E_INVALID_ARGUMENT, "NeighborList: entry out of range in row %llu", bad);
+
+    if (st.connectivity.bond_type_size != 0)
+        PD_CK(ctx->btype.upload(st.connectivity.bond_type, size_t(slots), s));
+    else
+        ctx->btype.release();
+    if (ctx->history) {
+        if (st.bond_history && st.bond_history_size == slots)
+            PD_CK(ctx->hist.upload(st.bond_history, size_t(slots), s));
+        else {
+            PD_CK(ctx->hist.alloc(size_t(slots)));
+            PD_CK(cudaMemsetAsync(ctx->hist.p, 0, sizeof(double) * slots, s));
+        }
+    } else {
+        ctx->hist.release();
+    }
+    if (corr.lambda_size != 0)
+        PD_CK(ctx->lambda.upload(corr.lambda, size_t(slots), s));
+    else
+        ctx->lambda.release();
+    if (corr.beta_size != 0)
+        PD_CK(ctx->beta.upload(corr.beta, size_t(slots), s));
+    else
+        ctx->beta.release();
+
+    PD_CK(ctx->err.alloc(1));
+    PD_CK(ctx->body.alloc(size_t(3 * n)));
+    PD_CK(ctx->ext.alloc(size_t(3 * n)));
+    PD_CK(cudaMemsetAsync(ctx->body.p, 0, sizeof(double) * 3 * n, s));
+    PD_CK(cudaMemsetAsync(ctx->ext.p, 0, sizeof(double) * 3 * n, s));
+    ctx->forces_valid = false;
+    ctx->step = st.step;
+    ctx->scratch_f64.release();
+    PD_CK(cudaStreamSynchronize(s));
+    return PD_OK;
+}
+
+int upload_bc(pd_ctx* ctx, const pd_boundary& bc) {
+    cudaStream_t s = ctx->stream;
+    const int64_t n = ctx->n;
+    bool any = false;
+    for (int64_t k = 0; k < 3 * n && !any; ++k)
+        any = bc.kind[k] != PD_BC_FREE;
+    ctx->has_bc = any;
+    if (any) {
+        PD_CK(ctx->bc_kind.upload(bc.kind, size_t(3 * n), s));
+        PD_CK(ctx->bc_mag.upload(bc.magnitude, size_t(3 * n), s));
+        PD_CK(ctx->bc_ramp.upload(bc.ramp_id, size_t(3 * n), s));
+    }
+    std::vector<DevRamp> ramps(size_t(bc.n_ramps));
+    for (int k = 0; k < bc.n_ramps; ++k) {
+        ramps[size_t(k)].kind = bc.ramps[k].kind;
+        ramps[size_t(k)].pad_ = 0;
+        ramps[size_t(k)].rise = bc.ramps[k].rise_steps;
+        ramps[size_t(k)].target = bc.ramps[k].target_scale;
+    }
+    PD_CK(ctx->ramps.upload(ramps.data(), ramps.size(), s));
+    ctx->n_tip_sets = bc.n_tip_sets;
+    if (bc.n_tip_sets > 0) {
+        std::vector<long long> off(size_t(bc.n_tip_sets + 1));
+        for (int k = 0; k <= bc.n_tip_sets; ++k)
+            off[size_t(k)] = bc.tip_offsets[k];
+        PD_CK(ctx->tip_offsets.upload(off.data(), off.size(), s));
+        const int64_t total = bc.tip_offsets[bc.n_tip_sets];
+        std::vector<long long> nodes(size_t(std::max<int64_t>(total, 1)), 0);
+        for (int64_t t = 0; t < total; ++t)
+            nodes[size_t(t)] = bc.tip_nodes[t];
+        PD_CK(ctx->tip_nodes.upload(nodes.data(), nodes.size(), s));
+    }
+    PD_CK(cudaStreamSynchronize(s));
+    return PD_OK;
+}
+
+// Copy selected resident fields into host arrays of `st` / `forces`.
+int download(pd_ctx* ctx, pd_state* st, pd_force_field* forces, int32_t fields) {
+    cudaStream_t s = ctx->stream;
+    const int64_t n = ctx->n;
+    const int64_t slots = n * ctx->N;
+    if ((fields & PD_FIELD_U) && st && st->u) {
+        PD_CK(ctx->scratch_f64.alloc(size_t(3 * n)));
+        launch_unpack_u(ctx->u[ctx->cur].p, n, ctx->scratch_f64.p, s);
+        ++ctx->launches;
+        PD_CK(cudaMemcpyAsync(st->u, ctx->scratch_f64.p, sizeof(double) * 3 * n,
+                              cudaMemcpyDeviceToHost, s));
+    }
+    if ((fields & PD_FIELD_V) && st && st->v)
+        PD_CK(cudaMemcpyAsync(st->v, ctx->v.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s));
+    if ((fields & PD_FIELD_A) && st && st->a)
+        PD_CK(cudaMemcpyAsync(st->a, ctx->a.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s));
+    if ((fields & PD_FIELD_CONNECTIVITY) && st) {
+        if (st->connectivity.entries) {
+            PD_CK(ctx->scratch_i32.alloc(size_t(slots)));
+            launch_materialize_entries(ctx->entries.p, ctx->alive.p, n, ctx->N, ctx->W,
+                                       ctx->scratch_i32.p, s);
+            ++ctx->launches;
+            PD_CK(cudaMemcpyAsync(st->connectivity.entries, ctx->scratch_i32.p,
+                                  sizeof(int32_t) * slots, cudaMemcpyDeviceToHost, s));
+        }
+        if (st->connectivity.n_neigh)
+            PD_CK(cudaMemcpyAsync(st->connectivity.n_neigh, ctx->n_neigh.p, sizeof(int32_t) * n,
+                                  cudaMemcpyDeviceToHost, s));
+    }
+    if ((fields & PD_FIELD_HISTORY) && st && st->bond_history && ctx->history) {
+        if (st->bond_history_size != slots)
+            return fail(PD_E_INVALID_ARGUMENT, "download: bond_history must be sized n x N");
+        PD_CK(cudaMemcpyAsync(st->bond_history, ctx->hist.p, sizeof(double) * slots,
+                              cudaMemcpyDeviceToHost, s));
+    }
+    if ((fields & PD_FIELD_FORCES) && forces) {
+        if (forces->body_force)
+            PD_CK(cudaMemcpyAsync(forces->body_force, ctx->body.p, sizeof(double) * 3 * n,
+                                  cudaMemcpyDeviceToHost, s));
+        if (forces->external_force)
+            PD_CK(cudaMemcpyAsync(forces->external_force, ctx->ext.p, sizeof(double) * 3 * n,
+                                  cudaMemcpyDeviceToHost, s));
+    }
+    if (st)
+        st->step = ctx->step;
+    PD_CK(cudaStreamSynchronize(s));
+    return PD_OK;
+}
+
+int launch_step(pd_ctx* ctx, DevArgs& A, int mode) {
+    if (ctx->variant == PD_FAST)
+        return fail(PD_E_INVALID_ARGUMENT, "PD_FAST kernel is not available in this build");
+    PD_CK(launch_exact(A, mode, ctx->variant == PD_NODE_PARALLEL, ctx->stream));
+    ++ctx->launches;
+    return PD_OK;
+}
+
+// Host view of the hook's state: the caller's arrays when the run is a
+// one-shot simulate (state is mutated in place like the reference), else the
+// staging vectors below.
+struct HookStage {
+    std::vector<double> u, v, a, hist, body, ext;
+    std::vector<int32_t> entries, n_neigh;
+};
+
+int run_loop(pd_ctx* ctx, const pd_options& opt, pd_write_hook hook, void* user,
+             int32_t hook_fields, pd_state* hook_state, pd_tip_record* tips_out,
+             int64_t tips_capacity, int64_t* n_tips_out) {
+    cudaStream_t s = ctx->stream;
+    if (n_tips_out)
+        *n_tips_out = 0;
+    if (opt.steps < 1)
+        return fail(PD_E_INVALID_ARGUMENT, "simulate: steps must be >= 1");
+    if (opt.integrator < PD_VELOCITY_VERLET || opt.integrator > PD_EULER_CROMER)
+        return fail(PD_E_INVALID_ARGUMENT, "simulate: unknown integrator");
+    const int64_t first = opt.first_step, last = opt.first_step + opt.steps;
+    int64_t writes = 0;
+    if (opt.write_every > 0)
+        for (int64_t w = (first / opt.write_every + 1) * opt.write_every; w <= last;
+             w += opt.write_every)
+            if (w > first)
+                ++writes;
+    const int64_t n_records = writes * ctx->n_tip_sets;
+    if (n_records > tips_capacity)
+        return fail(PD_E_INVALID_ARGUMENT, "simulate: tips_out capacity too small");
+    if (n_records > 0)
+        PD_CK(ctx->tips.alloc(size_t(n_records)));
+
+    const bool vv = opt.integrator == PD_VELOCITY_VERLET;
+    const int mode = vv ? 1 : (opt.integrator == PD_EULER ? 2 : 3);
+    const long long none = kNoError;
+    PD_CK(cudaMemcpyAsync(ctx->err.p, &none, sizeof none, cudaMemcpyHostToDevice, s));
+    ctx->step = first;
+    const int cur0 = ctx->cur;
+    DevArgs A = ctx->args();
+    A.step = first;
+    if (vv) {
+        launch_vv_prologue(A, s);
+        ctx->cur ^= 1;
+    } else {
+        launch_check_finite(ctx->u[ctx->cur].p, 0, ctx->n, first, ctx->err.p, s);
+    }
+    ++ctx->launches;
+
+    HookStage stage;
+    int64_t rec = 0;
+    int rc = PD_OK;
+    int64_t failed_at = -1;
+    for (int64_t st = first; st < last; ++st) {
+        const bool is_write = opt.write_every > 0 && (st + 1) % opt.write_every == 0;
+        A = ctx->args();
+        A.step = st;
+        A.store_forces = is_write && (ctx->n_tip_sets > 0 || hook);
+        A.do_drift = st + 1 < last;
+        PD_TRY(launch_step(ctx, A, mode));
+        if (!vv)
+            ctx->cur ^= 1;
+        if (is_write) {
+            if (ctx->n_tip_sets > 0) {
+                launch_tips(ctx->u[ctx->cur].p, ctx->v.p, ctx->a.p, ctx->xv.p, ctx->body.p,
+                            ctx->ext.p, ctx->n_tip_sets, ctx->tip_offsets.p, ctx->tip_nodes.p,
+                            st + 1, ctx->tips.p + rec, s);
+                ++ctx->launches;
+                rec += ctx->n_tip_sets;
+            }
+            if (hook) {
+                long long err = none;
+                PD_CK(cudaMemcpyAsync(&err, ctx->err.p, sizeof err, cudaMemcpyDeviceToHost, s));
+                PD_CK(cudaStreamSynchronize(s));
+                if (err <= st) {
+                    failed_at = err;
+                    break;
+                }
+                const int64_t saved = ctx->step;
+                ctx->step = st + 1;
+                pd_force_field ff{nullptr, nullptr};
+                pd_state view{};
+                if (hook_state) {
+                    view = *hook_state;
+                } else {
+                    const int64_t n = ctx->n, slots = n * ctx->N;
+                    view.connectivity.n = n;
+                    view.connectivity.group_size = ctx->N;
+                    if (hook_fields & PD_FIELD_U)
+                        stage.u.resize(size_t(3 * n)), view.u = stage.u.data();
+                    if (hook_fields & PD_FIELD_V)
+                        stage.v.resize(size_t(3 * n)), view.v = stage.v.data();
+                    if (hook_fields & PD_FIELD_A)
+                        stage.a.resize(size_t(3 * n)), view.a = stage.a.data();
+                    if (hook_fields & PD_FIELD_CONNECTIVITY) {
+                        stage.entries.resize(size_t(slots));
+                        stage.n_neigh.resize(size_t(n));
+                        view.connectivity.entries = stage.entries.data();
+                        view.connectivity.n_neigh = stage.n_neigh.data();
+                    }
+                    if ((hook_fields & PD_FIELD_HISTORY) && ctx->history) {
+                        stage.hist.resize(size_t(slots));
+                        view.bond_history = stage.hist.data();
+                        view.bond_history_size = slots;
+                    }
+                }
+                if (hook_fields & PD_FIELD_FORCES) {
+                    stage.body.resize(size_t(3 * ctx->n));
+                    stage.ext.resize(size_t(3 * ctx->n));
+                    ff.body_force = stage.body.data();
+                    ff.external_force = stage.ext.data();
+                }
+                PD_TRY(download(ctx, &view, &ff, hook_fields));
+                ctx->step = saved;
+                if (hook(user, &view, &ff) != 0) {
+                    rc = fail(PD_E_RUNTIME, "simulate: write hook failed at step %lld",
+                              (long long)(st + 1));
+                    ctx->step = st + 1;
+                    break;
+                }
+            }
+        }
+        if (vv && st + 1 < last)
+            ctx->cur ^= 1;
+        ctx->step = st + 1;
+    }
+    long long err = none;
+    PD_CK(cudaMemcpyAsync(&err, ctx->err.p, sizeof err, cudaMemcpyDeviceToHost, s));
+    PD_CK(cudaStreamSynchronize(s));
+    if (failed_at < 0 && err < last)
+        failed_at = err;
+    int64_t keep = rec;
+    if (failed_at >= 0) {
+        // The reference threw inside the force pass of step `failed_at`: the
+        // state is the one that force pass saw.
+        const int64_t e = failed_at;
+        ctx->cur = vv ? (cur0 ^ 1 ^ int((e - first) & 1)) : (cur0 ^ int((e - first) & 1));
+        ctx->step = e;
+        keep = 0;
+        if (opt.write_every > 0)
+            for (int64_t w = first + 1; w <= e; ++w)
+                if (w % opt.write_every == 0)
+                    keep += ctx->n_tip_sets;
+        rc = fail(PD_E_RUNTIME, "compute_forces: non-finite displacement at step %lld",
+                  (long long)e);
+    }
+    keep = std::min(keep, rec);
+    if (keep > 0 && tips_out)
+        PD_CK(cudaMemcpy(tips_out, ctx->tips.p, sizeof(pd_tip_record) * keep,
+                         cudaMemcpyDeviceToHost));
+    if (n_tips_out)
+        *n_tips_out = keep;
+    ctx->forces_valid = true;
+    return rc;
+}
+
+} // namespace
+
+// ---- C ABI ------------------------------------------------------------------
+
+extern "C" {
+
+int pd_abi_version(void) { return PD_ABI_VERSION; }
+
+const char* pd_last_error(void) { return g_err.c_str(); }
+
+int pd_device_count(void) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    int usable = 0;
+    for (int d = 0; d < count; ++d) {
+        cudaDeviceProp prop;
+        if (cudaGetDeviceProperties(&prop, d) == cudaSuccess && prop.major >= 10)
+            ++usable;
+    }
+    return usable;
+}
+
+int pd_ctx_create(int device, pd_ctx** out) {
+    *out = nullptr;
+    if (pd_device_count() == 0)
+        return fail(PD_E_NO_DEVICE, "no sm_100 (B200) device is visible to the CUDA runtime");
+    auto* ctx = new pd_ctx;
+    ctx->device = device;
+    if (select_device(ctx) != PD_OK) {
+        delete ctx;
+        return PD_E_CUDA;
+    }
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        delete ctx;
+        return fail(PD_E_CUDA, "cudaStreamCreate failed");
+    }
+    *out = ctx;
+    return ok();
+}
+
+void pd_ctx_destroy(pd_ctx* ctx) {
+    if (!ctx)
+        return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+void* pd_ctx_stream(pd_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+int64_t pd_ctx_launch_count(pd_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int pd_ctx_upload(pd_ctx* ctx, const pd_bundle* b, const pd_state* st, int32_t variant) {
+    PD_TRY(select_device(ctx));
+    if (variant < PD_BOND_PARALLEL || variant > PD_FAST)
+        return fail(PD_E_INVALID_ARGUMENT, "unknown kernel variant %d", variant);
+    // ModelBundle::validate (engine.cpp:335-341)
+    PD_TRY(particles_validate(b->particles));
+    PD_TRY(model_validate(b->model));
+    PD_TRY(bc_validate(b->bc, b->particles.n));
+    if (!(b->dt > 0))
+        return fail(PD_E_INVALID_ARGUMENT, "ModelBundle: dt must be positive");
+    if (st->connectivity.n != b->particles.n)
+        return fail(PD_E_INVALID_ARGUMENT, "simulate: state does not match the bundle");
+    // simulate: corr.no_failure = bc.no_failure (engine.cpp:386-387)
+    PD_TRY(upload_common(ctx, b->particles, *st, b->model, b->corrections, b->bc.no_failure,
+                         b->bc.no_failure_size));
+    const int64_t slots = ctx->n * ctx->N;
+    if (b->corrections.lambda_size != 0 && b->corrections.lambda_size != slots)
+        return fail(PD_E_INVALID_ARGUMENT, "compute_forces: lambda size mismatch");
+    if (b->corrections.beta_size != 0 && b->corrections.beta_size != slots)
+        return fail(PD_E_INVALID_ARGUMENT, "compute_forces: beta size mismatch");
+    PD_TRY(upload_bc(ctx, b->bc));
+    ctx->variant = variant;
+    ctx->dt = b->dt;
+    return ok();
+}
+
+int pd_ctx_run(pd_ctx* ctx, const pd_options* options, pd_write_hook on_write, void* user,
+               int32_t hook_fields, pd_tip_record* tips_out, int64_t tips_capacity,
+               int64_t* n_tips_out) {
+    PD_TRY(select_device(ctx));
+    const int rc = run_loop(ctx, *options, on_write, user, hook_fields, nullptr, tips_out,
+                            tips_capacity, n_tips_out);
+    return rc == PD_OK ? ok() : rc;
+}
+
+int pd_ctx_compute_forces(pd_ctx* ctx) {
+    PD_TRY(select_device(ctx));
+    cudaStream_t s = ctx->stream;
+    const long long none = kNoError;
+    PD_CK(cudaMemcpyAsync(ctx->err.p, &none, sizeof none, cudaMemcpyHostToDevice, s));
+    launch_check_finite(ctx->u[ctx->cur].p, 0, ctx->n, ctx->step, ctx->err.p, s);
+    ++ctx->launches;
+    long long err = none;
+    PD_CK(cudaMemcpyAsync(&err, ctx->err.p, sizeof err, cudaMemcpyDeviceToHost, s));
+    PD_CK(cudaStreamSynchronize(s));
+    if (err != none)
+        return fail(PD_E_RUNTIME, "compute_forces: non-finite displacement at step %lld",
+                    (long long)ctx->step);
+    DevArgs A = ctx->args();
+    PD_TRY(launch_step(ctx, A, 0));
+    PD_CK(cudaStreamSynchronize(s));
+    ctx->forces_valid = true;
+    return ok();
+}
+
+int pd_ctx_download(pd_ctx* ctx, pd_state* state, pd_force_field* forces, int32_t fields) {
+    PD_TRY(select_device(ctx));
+    PD_TRY(download(ctx, state, forces, fields));
+    return ok();
+}
+
+int pd_ctx_damage(pd_ctx* ctx, double* phi_out) {
+    PD_TRY(select_device(ctx));
+    cudaStream_t s = ctx->stream;
+    PD_CK(ctx->scratch_f64.alloc(size_t(ctx->n)));
+    launch_damage(ctx->n_neigh.p, ctx->initial.p, ctx->n, ctx->scratch_f64.p, s);
+    ++ctx->launches;
+    PD_CK(cudaMemcpyAsync(phi_out, ctx->scratch_f64.p, sizeof(double) * ctx->n,
+                          cudaMemcpyDeviceToHost, s));
+    PD_CK(cudaStreamSynchronize(s));
+    return ok();
+}
+
+int64_t pd_ctx_live_bonds(pd_ctx* ctx) {
+    if (select_device(ctx) != PD_OK)
+        return -1;
+    cudaStream_t s = ctx->stream;
+    if (ctx->counter.alloc(1) != cudaSuccess)
+        return -1;
+    cudaMemsetAsync(ctx->counter.p, 0, sizeof(unsigned long long), s);
+    launch_sum(ctx->n_neigh.p, ctx->n, ctx->counter.p, s);
+    ++ctx->launches;
+    unsigned long long total = 0;
+    cudaMemcpyAsync(&total, ctx->counter.p, sizeof total, cudaMemcpyDeviceToHost, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess)
+        return -1;
+    return int64_t(total);
+}
+
+int pd_compute_forces(int32_t variant, pd_state* state, const pd_particles* particles,
+                      const pd_damage_model* model, const pd_corrections* corr,
+                      pd_force_field* out) {
+    // check_force_inputs (engine.cpp:30-49), in the reference's order
+    const int64_t n = state->connectivity.n;
+    if (particles->n != n)
+        return fail(PD_E_INVALID_ARGUMENT, "compute_forces: particle set does not match state");
+    const int64_t slots = n * state->connectivity.group_size;
+    if (corr->lambda_size != 0 && corr->lambda_size != slots)
+        return fail(PD_E_INVALID_ARGUMENT, "compute_forces: lambda size mismatch");
+    if (corr->beta_size != 0 && corr->beta_size != slots)
+        return fail(PD_E_INVALID_ARGUMENT, "compute_forces: beta size mismatch");
+    if (corr->no_failure_size != 0 && corr->no_failure_size != n)
+        return fail(PD_E_INVALID_ARGUMENT, "compute_forces: no_failure size mismatch");
+    if (model->n_laws >= 1 && needs_history(*model) && state->bond_history_size != slots)
+        return fail(PD_E_INVALID_ARGUMENT, "compute_forces: model needs per-bond history");
+    if (state->connectivity.bond_type_size != 0 && model->n_laws < 2 &&
+        state->connectivity.bond_type_size != slots)
+        return fail(PD_E_INVALID_ARGUMENT, "compute_forces: bond_type size mismatch");
+    PD_TRY(model_validate(*model));
+    for (int64_t k = 0; k < 3 * n; ++k)
+        if (!std::isfinite(state->u[k]))
+            return fail(PD_E_RUNTIME, "compute_forces: non-finite displacement at step %lld",
+                        (long long)state->step);
+    if (variant < PD_BOND_PARALLEL || variant > PD_FAST)
+        return fail(PD_E_INVALID_ARGUMENT, "unknown kernel variant %d", variant);
+    if (n == 0)
+        return ok();
+
+    pd_ctx* ctx = nullptr;
+    PD_TRY(pd_ctx_create(0, &ctx));
+    struct Guard {
+        pd_ctx* c;
+        ~Guard() { pd_ctx_destroy(c); }
+    } guard{ctx};
+    pd_state st = *state;
+    st.v = nullptr;
+    st.a = nullptr;
+    PD_TRY(upload_common(ctx, *particles, st, *model, *corr, corr->no_failure,
+                         corr->no_failure_size));
+    ctx->variant = variant;
+    DevArgs A = ctx->args();
+    PD_TRY(launch_step(ctx, A, 0));
+    pd_force_field ff{out->body_force, nullptr};
+    PD_TRY(download(ctx, state, &ff,
+                    PD_FIELD_CONNECTIVITY | PD_FIELD_HISTORY | PD_FIELD_FORCES));
+    return ok();
+}
+
+int pd_simulate(const pd_bundle* bundle, pd_state* state, const pd_options* options,
+                pd_write_hook on_write, void* user, pd_tip_record* tips_out,
+                int64_t tips_capacity, int64_t* n_tips_out) {
+    if (n_tips_out)
+        *n_tips_out = 0;
+    if (options->steps < 1)
+        return fail(PD_E_INVALID_ARGUMENT, "simulate: steps must be >= 1");
+    if (bundle->model.n_laws >= 1 && needs_history(bundle->model) &&
+        state->bond_history_size != state->connectivity.n * state->connectivity.group_size)
+        return fail(PD_E_INVALID_ARGUMENT, "simulate: bond_history must be sized n x N");
+    pd_ctx* ctx = nullptr;
+    PD_TRY(pd_ctx_create(0, &ctx));
+    struct Guard {
+        pd_ctx* c;
+        ~Guard() { pd_ctx_destroy(c); }
+    } guard{ctx};
+    PD_TRY(pd_ctx_upload(ctx, bundle, state, options->variant));
+    int rc = run_loop(ctx, *options, on_write, user, PD_FIELD_ALL, state, tips_out, tips_capacity,
+                      n_tips_out);
+    // the state is the caller's in every outcome, as the reference mutates in place
+    const int rc2 = download(ctx, state, nullptr,
+                             PD_FIELD_U | PD_FIELD_V | PD_FIELD_A | PD_FIELD_CONNECTIVITY |
+                                 PD_FIELD_HISTORY);
+    if (rc != PD_OK)
+        return rc;
+    if (rc2 != PD_OK)
+        return rc2;
+    return ok();
+}
+
+int pd_damage(const pd_neighbor_list* family, double* phi) {
+    // local_damage's range check (formulas.hpp:49-55) on the inputs, then K3 on the device
+    const int64_t n = family->n;
+    for (int64_t i = 0; i < n; ++i) {
+        const int32_t init = family->initial_n_neigh[i];
+        const int32_t cur = family->n_neigh[i];
+        if (init > 0 && (cur < 0 || cur > init))
+            return fail(PD_E_DOMAIN, "local_damage: current count out of range");
+    }
+    if (n == 0)
+        return ok();
+    pd_ctx* ctx = nullptr;
+    PD_TRY(pd_ctx_create(0, &ctx));
+    struct Guard {
+        pd_ctx* c;
+        ~Guard() { pd_ctx_destroy(c); }
+    } guard{ctx};
+    cudaStream_t s = ctx->stream;
+    ctx->n = n;
+    PD_CK(ctx->n_neigh.upload(family->n_neigh, size_t(n), s));
+    PD_CK(ctx->initial.upload(family->initial_n_neigh, size_t(n), s));
+    return pd_ctx_damage(ctx, phi);
+}
+
+} // extern "C"

@@ -1,0 +1,292 @@
+"""Host mirror of the reference engine API (include/peridyn/engine.hpp) over a
+pd-style C ABI.
+
+`Backend(lib, prefix)` binds any library exporting the pd_b200.h entry points
+under `prefix`.  The product binds libpd_b200.so ("pd_"); the test checkers
+under oracle/ bind the same calls on their own libraries, so a parity test
+drives the GPU and its checker through identical Python code.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional
+
+import numpy as np
+
+from . import abi
+from .abi import HOOK, Marshal, check
+from .types import (ForceField, IntegratorKind, KernelVariant, ModelBundle, SimulateOptions,
+                    SimulateResult, SimulationState, TipRecord, WriteHook)
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libpd_b200.so")
+
+
+class Backend:
+    def __init__(self, lib: C.CDLL, prefix: str):
+        self.lib = lib
+        self.prefix = prefix
+        self._last = getattr(lib, prefix + "last_error")
+        self._last.restype = C.c_char_p
+        self._cf = getattr(lib, prefix + "compute_forces")
+        self._cf.argtypes = [C.c_int32, C.POINTER(abi.pd_state), C.POINTER(abi.pd_particles),
+                             C.POINTER(abi.pd_damage_model), C.POINTER(abi.pd_corrections),
+                             C.POINTER(abi.pd_force_field)]
+        self._sim = getattr(lib, prefix + "simulate")
+        self._sim.argtypes = [C.POINTER(abi.pd_bundle), C.POINTER(abi.pd_state),
+                              C.POINTER(abi.pd_options), HOOK, C.c_void_p,
+                              C.POINTER(abi.pd_tip_record), C.c_int64, C.POINTER(C.c_int64)]
+
+    def last_error(self) -> str:
+        return self._last().decode()
+
+    def _check(self, rc: int) -> None:
+        check(rc, self._last)
+
+    # compute_forces (engine.hpp:35-36, engine.cpp:163-169)
+    def compute_forces(self, variant, state: SimulationState, particles, model, corrections,
+                       out: ForceField) -> None:
+        n = state.size()
+        if np.asarray(out.body_force).size != 3 * n:
+            out.body_force = np.zeros(3 * n)
+        if np.asarray(out.external_force).size != 3 * n:
+            out.external_force = np.zeros(3 * n)
+        m = Marshal()
+        st = m.state(state)
+        p = m.particles(particles)
+        md = m.model(model)
+        cr = m.corrections(corrections)
+        ff = m.forces(out)
+        rc = self._cf(int(variant), C.byref(st), C.byref(p), C.byref(md), C.byref(cr),
+                      C.byref(ff))
+        state.step = st.step
+        self._check(rc)
+
+    # simulate (engine.hpp:128-129, engine.cpp:374-425)
+    def simulate(self, bundle: ModelBundle, state: SimulationState, options: SimulateOptions,
+                 on_write: Optional[WriteHook] = None) -> SimulateResult:
+        n = bundle.particles.size()
+        slots = state.size() * int(state.connectivity.group_size)
+        if bundle.model.needs_history() and np.asarray(
+                state.bond_history if state.bond_history is not None else []).size != slots:
+            state.bond_history = np.zeros(slots)  # engine.cpp:382-384
+        names = sorted(bundle.bc.tip_sets)
+        writes = 0
+        if options.write_every > 0 and options.steps > 0:
+            writes = sum(1 for s in range(options.first_step, options.first_step + options.steps)
+                         if (s + 1) % options.write_every == 0)
+        cap = max(1, writes * len(names))
+        recs = (abi.pd_tip_record * cap)()
+        n_recs = C.c_int64(0)
+        m = Marshal()
+        b = m.bundle(bundle)
+        st = m.state(state)
+        o = Marshal.options(options)
+        errors = []
+
+        def bridge(_user, view, ff):
+            try:
+                v = view.contents
+                state.step = v.step
+                seen = _state_view(v, state) if v.u else state
+                forces = ForceField(
+                    np.ctypeslib.as_array(ff.contents.body_force, (3 * n,)).copy(),
+                    np.ctypeslib.as_array(ff.contents.external_force, (3 * n,)).copy())
+                on_write(seen, forces)
+                return 0
+            except BaseException as exc:  # propagate after the C call unwinds
+                errors.append(exc)
+                return 1
+
+        hook = HOOK(bridge) if on_write is not None else HOOK()
+        rc = self._sim(C.byref(b), C.byref(st), C.byref(o), hook, None, recs, cap,
+                       C.byref(n_recs))
+        state.step = st.step
+        if errors:
+            raise errors[0]
+        self._check(rc)
+        result = SimulateResult({name: [] for name in names} if names else {})
+        for k in range(n_recs.value):
+            r = recs[k]
+            rec = TipRecord(int(r.step), np.array(r.mean_u[:]), np.array(r.mean_v[:]),
+                            np.array(r.mean_a[:]), np.array(r.body_force_sum[:]),
+                            np.array(r.external_force_sum[:]))
+            result.tips[names[k % len(names)]].append(rec)
+        return result
+
+
+def _state_view(v, like: SimulationState) -> SimulationState:
+    """Copy of the state a write hook sees, read through the pd_state view."""
+    n = like.size()
+    N = int(like.connectivity.group_size)
+    arr = np.ctypeslib.as_array
+    fam = like.connectivity.copy()
+    fam.entries = arr(v.connectivity.entries, (n * N,)).copy()
+    fam.n_neigh = arr(v.connectivity.n_neigh, (n,)).copy()
+    hist = arr(v.bond_history, (v.bond_history_size,)).copy() if v.bond_history_size else np.zeros(0)
+    return SimulationState(arr(v.u, (3 * n,)).copy(), arr(v.v, (3 * n,)).copy(),
+                           arr(v.a, (3 * n,)).copy(), int(v.step), fam, hist)
+
+
+# ---- the product library --------------------------------------------------------
+
+_LIB: Optional[C.CDLL] = None
+_BACKEND: Optional[Backend] = None
+
+
+def library() -> C.CDLL:
+    """libpd_b200.so; raises if it was not built (there is no CPU fallback)."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise abi.CudaError(f"{LIB_PATH} is not built; run __graft_entry__.build()")
+        lib = C.CDLL(LIB_PATH)
+        lib.pd_ctx_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
+        lib.pd_ctx_destroy.argtypes = [C.c_void_p]
+        lib.pd_ctx_upload.argtypes = [C.c_void_p, C.POINTER(abi.pd_bundle),
+                                      C.POINTER(abi.pd_state), C.c_int32]
+        lib.pd_ctx_run.argtypes = [C.c_void_p, C.POINTER(abi.pd_options), HOOK, C.c_void_p,
+                                   C.c_int32, C.POINTER(abi.pd_tip_record), C.c_int64,
+                                   C.POINTER(C.c_int64)]
+        lib.pd_ctx_compute_forces.argtypes = [C.c_void_p]
+        lib.pd_ctx_download.argtypes = [C.c_void_p, C.POINTER(abi.pd_state),
+                                        C.POINTER(abi.pd_force_field), C.c_int32]
+        lib.pd_ctx_damage.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
+        lib.pd_ctx_stream.argtypes = [C.c_void_p]
+        lib.pd_ctx_stream.restype = C.c_void_p
+        lib.pd_ctx_launch_count.argtypes = [C.c_void_p]
+        lib.pd_ctx_launch_count.restype = C.c_int64
+        lib.pd_ctx_live_bonds.argtypes = [C.c_void_p]
+        lib.pd_ctx_live_bonds.restype = C.c_int64
+        lib.pd_damage.argtypes = [C.POINTER(abi.pd_neighbor_list), C.POINTER(C.c_double)]
+        lib.pd_last_error.restype = C.c_char_p
+        _LIB = lib
+    return _LIB
+
+
+def backend() -> Backend:
+    global _BACKEND
+    if _BACKEND is None:
+        _BACKEND = Backend(library(), "pd_")
+    return _BACKEND
+
+
+def device_count() -> int:
+    return int(library().pd_device_count())
+
+
+def compute_forces(variant, state, particles, model, corrections, out) -> None:
+    """compute_forces(KernelVariant, ...) on the B200 (engine.cpp:163-169)."""
+    backend().compute_forces(variant, state, particles, model, corrections, out)
+
+
+def simulate(bundle, state, options, on_write=None) -> SimulateResult:
+    """simulate(bundle, state, options, on_write) on the B200 (engine.cpp:374-425)."""
+    return backend().simulate(bundle, state, options, on_write)
+
+
+def local_damage(family) -> np.ndarray:
+    """phi_i = 1 - n_neigh_i / initial_i per node (formulas.hpp:49-55), on the GPU."""
+    lib = library()
+    m = Marshal()
+    f = m.family(family)
+    phi = np.zeros(family.node_count())
+    check(lib.pd_damage(C.byref(f), phi.ctypes.data_as(C.POINTER(C.c_double))),
+          lib.pd_last_error)
+    return phi
+
+
+class Context:
+    """A device-resident model + state (pd_ctx): upload once, advance many
+    steps with no host traffic except at write steps, download on demand."""
+
+    def __init__(self, device: int = 0):
+        self.lib = library()
+        h = C.c_void_p()
+        check(self.lib.pd_ctx_create(device, C.byref(h)), self.lib.pd_last_error)
+        self.h = h
+        self.n = 0
+        self.N = 0
+        self.history = False
+
+    def close(self) -> None:
+        if self.h:
+            self.lib.pd_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        check(rc, self.lib.pd_last_error)
+
+    def upload(self, bundle: ModelBundle, state: SimulationState,
+               variant: KernelVariant = KernelVariant.bond_parallel) -> None:
+        m = Marshal()
+        b = m.bundle(bundle)
+        st = m.state(state)
+        self._check(self.lib.pd_ctx_upload(self.h, C.byref(b), C.byref(st), int(variant)))
+        self.n = state.size()
+        self.N = int(state.connectivity.group_size)
+        self.history = bundle.model.needs_history()
+        self.tip_names = sorted(bundle.bc.tip_sets)
+
+    def run(self, steps: int, first_step: int, integrator=IntegratorKind.velocity_verlet,
+            write_every: int = 0, variant=KernelVariant.bond_parallel) -> SimulateResult:
+        opts = abi.pd_options(int(steps), int(write_every), int(first_step), int(integrator),
+                              int(variant))
+        names = self.tip_names
+        writes = 0
+        if write_every > 0:
+            writes = sum(1 for s in range(first_step, first_step + steps)
+                         if (s + 1) % write_every == 0)
+        cap = max(1, writes * len(names))
+        recs = (abi.pd_tip_record * cap)()
+        n_recs = C.c_int64(0)
+        self._check(self.lib.pd_ctx_run(self.h, C.byref(opts), HOOK(), None, 0, recs, cap,
+                                        C.byref(n_recs)))
+        result = SimulateResult({name: [] for name in names})
+        for k in range(n_recs.value):
+            r = recs[k]
+            result.tips[names[k % len(names)]].append(
+                TipRecord(int(r.step), np.array(r.mean_u[:]), np.array(r.mean_v[:]),
+                          np.array(r.mean_a[:]), np.array(r.body_force_sum[:]),
+                          np.array(r.external_force_sum[:])))
+        return result
+
+    def compute_forces(self) -> None:
+        self._check(self.lib.pd_ctx_compute_forces(self.h))
+
+    def download(self, state: SimulationState, forces: Optional[ForceField] = None,
+                 fields: int = abi.PD_FIELD_ALL) -> None:
+        m = Marshal()
+        if self.history and np.asarray(state.bond_history).size != self.n * self.N:
+            state.bond_history = np.zeros(self.n * self.N)
+        st = m.state(state)
+        if forces is not None:
+            forces.resize(self.n)
+            ff = m.forces(forces)
+            fp = C.byref(ff)
+        else:
+            fp = None
+            fields &= ~abi.PD_FIELD_FORCES
+        self._check(self.lib.pd_ctx_download(self.h, C.byref(st), fp, int(fields)))
+        state.step = st.step
+
+    def damage(self) -> np.ndarray:
+        phi = np.zeros(self.n)
+        self._check(self.lib.pd_ctx_damage(self.h, phi.ctypes.data_as(C.POINTER(C.c_double))))
+        return phi
+
+    def stream(self) -> int:
+        return int(self.lib.pd_ctx_stream(self.h) or 0)
+
+    def launch_count(self) -> int:
+        return int(self.lib.pd_ctx_launch_count(self.h))
+
+    def live_bonds(self) -> int:
+        return int(self.lib.pd_ctx_live_bonds(self.h))

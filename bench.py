@@ -1,0 +1,283 @@
+#!/usr/bin/env python
+"""Benchmark: explicit bond-based peridynamics time step on B200.
+
+Workload (BASELINE.json configs[3], at N=1 the metric's 10M-node case): the
+reference bench lattice (bench.cpp:76-104) -- cubic lattice 216^3 =
+10,077,696 nodes, spacing 1, V = rho = 1, PMB c = 1, s_c = 1e6 (no breaking),
+dt = 1e-3, horizon 3 (N = 128, 1,209,979,144 live directed bonds), seeded u,
+velocity-Verlet.  One "step" = one simulate() time step (fused force + break +
+reduce + kick + next drift), run device-resident through the C ABI.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--variant fast|exact]
+  python bench.py --impl reference      # the reference CPU path on host cores
+
+Prints ONE JSON line (rank 0).  Metric: live directed bond evaluations per
+second (whole job), with ms/step, the HBM roofline of the fused step kernel,
+an end-to-end number through the host-buffer simulate() call, the reference
+CPU baseline and the SM clocks seen during the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+METRIC = "bond evals/sec & ms/step at 1M/10M nodes; % of HBM peak; 1/2/4/8 GPU"
+UNIT = "bond_evals/s"
+HORIZON = 3.0
+
+
+def algorithmic_bytes(n: int, N: int, live: int, r: int = 8) -> int:
+    """4B + 2 ceil(nN/8) + n (7*3r + 2r)."""
+    return 4 * live + 2 * ((n * N + 7) // 8) + n * (7 * 3 * r + 2 * r)
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for name, flag in zip(names, f[5:9]):
+                if flag.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def build_workload(counts):
+    import scenarios as S
+    from paper_2105_04150_b200 import geometry, make_state
+    bundle, h, g = S.bench_lattice_bundle(counts)
+    fam = geometry.build_family(bundle.particles.coords, h, g)
+    state = make_state(fam, False)
+    state.u = S.seed_displacements(bundle.particles.coords)
+    return bundle, fam, state
+
+
+def cpu_baseline(counts_full, steps=2):
+    """The reference CPU path (oracle/_ref, built from /root/reference/proj/src)
+    on a bounded sample of the workload: a z-slab of the full lattice."""
+    sample = (counts_full[0], counts_full[1], min(counts_full[2], 24))
+    threads = os.cpu_count() or 1
+    try:
+        from oracle.pyoracle import Reference
+        ref = Reference(threads=threads)
+        secs, live, build_s = ref.bench_lattice(sample, HORIZON, 1e6, steps, threads)
+        kind = "reference"
+    except OSError:
+        import scenarios as S
+        from oracle.pyoracle import COracle
+        from paper_2105_04150_b200 import SimulateOptions, make_state
+        orc = COracle(threads=threads)
+        bundle, h, g = S.bench_lattice_bundle(sample)
+        fam = orc.build_family(bundle.particles.coords, h, g.hint())
+        st = make_state(fam, False)
+        st.u = S.seed_displacements(bundle.particles.coords)
+        t0 = time.perf_counter()
+        orc.simulate(bundle, st, SimulateOptions(steps))
+        secs = time.perf_counter() - t0
+        live = int(fam.n_neigh.sum())
+        kind = "port"
+    n = sample[0] * sample[1] * sample[2]
+    return {"value": live * steps / secs, "unit": UNIT, "cores": threads, "kind": kind,
+            "ms_per_step": 1e3 * secs / steps,
+            "sample": f"{sample[0]}x{sample[1]}x{sample[2]} = {n} nodes z-slab of the same "
+                      f"lattice, {steps} velocity-Verlet steps of simulate(bond_parallel), "
+                      f"{live} live bonds"}
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    counts = (args.size, args.size, args.size)
+    steps_each = 2
+    vals = []
+    cb = None
+    for _ in range(args.warmup + args.steps):
+        cb = cpu_baseline(counts, steps_each)
+        vals.append(cb["value"])
+    timed = vals[args.warmup:]
+    value = statistics.median(timed)
+    n = counts[0] * counts[1] * counts[2]
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"cfg4 lattice {args.size}^3 = {n} nodes, delta=3dx (N=128), "
+                               "PMB, velocity-Verlet (reference CPU, bounded z-slab sample)",
+                   "nodes": n},
+        "cpu_baseline": cb,
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--variant", default="fast", choices=["exact", "fast"])
+    ap.add_argument("--size", type=int, default=216)
+    ap.add_argument("--e2e-steps", type=int, default=100)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+    from paper_2105_04150_b200 import (IntegratorKind, KernelVariant, SimulateOptions, engine)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        raise SystemExit("multi-GPU slabs: not in this build yet")
+    torch.cuda.set_device(local)
+    variant = KernelVariant.fast if args.variant == "fast" else KernelVariant.bond_parallel
+    counts = (args.size, args.size, args.size)
+    t_setup = time.perf_counter()
+    bundle, fam, state0 = build_workload(counts)
+    n = bundle.particles.size()
+    N = int(fam.group_size)
+    live = int(fam.n_neigh.sum())
+    setup_s = time.perf_counter() - t_setup
+
+    ctx = engine.Context(local)
+    ctx.upload(bundle, state0, variant)
+    stream = torch.cuda.ExternalStream(ctx.stream())
+    step = 0
+    ctx.run(args.warmup, step, IntegratorKind.velocity_verlet, 0, variant)
+    step += args.warmup
+    torch.cuda.synchronize()
+    launches0 = ctx.launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        ctx.run(args.steps, step, IntegratorKind.velocity_verlet, 0, variant)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = ctx.launch_count() - launches0
+    ms_total = ev0.elapsed_time(ev1)
+    ms_step = ms_total / args.steps
+    live_end = ctx.live_bonds()
+    value = live * args.steps / (ms_total / 1e3)
+    peak, peak_kind = measured_peaks()
+    bytes_step = algorithmic_bytes(n, N, live)
+    achieved = bytes_step / (ms_step / 1e3) / 1e9
+    ctx.close()
+    del ctx
+
+    # end to end: one simulate() call through the C ABI from host buffers
+    from paper_2105_04150_b200 import make_state
+    st = make_state(fam, False)
+    st.u = state0.u.copy()
+    e2e_steps = args.e2e_steps
+    h2d = (3 * n * 8 * 3 + 2 * n * 8 + 3 * n * 8 + n * N * 4 + 3 * n * 4 + 4 * n)
+    d2h = (3 * n * 8 * 3 + n * N * 4 + n * 4)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    engine.simulate(bundle, st, SimulateOptions(e2e_steps, 0, 0, IntegratorKind.velocity_verlet,
+                                                variant))
+    e2e_s = time.perf_counter() - t0
+    e2e_value = live * e2e_steps / e2e_s
+
+    cpu = None if args.no_cpu else cpu_baseline(counts)
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64" if variant != KernelVariant.fast else "f32 bond math / f64 state",
+        "data": "synthetic",
+        "config": {"workload": f"cfg4 lattice {args.size}^3 = {n} nodes, delta=3dx (N={N}), "
+                               f"PMB c=1 s_c=1e6, velocity-Verlet, dt=1e-3, seeded u",
+                   "nodes": n, "group_size": N, "live_bonds": live, "variant": args.variant,
+                   "l2": f"inputs larger than L2 ({bytes_step / 1e9:.2f} GB/step algorithmic)",
+                   "setup_s": round(setup_s, 2)},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
+                     "bytes_per_step": bytes_step},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d // e2e_steps,
+                "d2h_bytes_per_step": d2h // e2e_steps,
+                "how": f"one simulate() call via the C ABI, {e2e_steps} steps, host buffers "
+                       "(upload + run + download inside the timed region)"},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+        "live_bonds_end": live_end,
+    }
+    if rank == 0:
+        print(json.dumps(out))
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,568 @@
+// pd_fast.cu -- the fast path: shared-memory-staged tiles, fp32 bond arithmetic,
+// fp64 state and integration.  Tolerance-bound against the fp64 reference
+// (DESIGN.md states the bound; tests/test_gpu_fast.py checks it).
+//
+// Per step, one CTA per tile (see pd_fast.cuh):
+//   1. stage the tile's halo: for each halo node, fp64 x and u are read once
+//      (L2-resident neighbourhood), shifted by the tile's reference point and
+//      rounded to fp32: x_l = x - O_t, u_l = u - U_t.  Differences of these are
+//      accurate to ~1e-7 relative to the bond length / the local displacement
+//      variation -- unlike fp32 absolute coordinates (1e-5 at 216 spacings);
+//   2. each thread walks its compacted row 8 slots per 16-byte index load and
+//      evaluates bond_contribution (engine.cpp:53-109) in fp32:
+//        xi = x_j - x_i, eta = u_j - u_i, cur = xi + eta
+//        s  = eta.(xi + cur) / (|xi| (|cur| + |xi|))      (cancellation free)
+//      with MUFU rsqrt/rcp; a break writes 0xFFFF into the slot (like the
+//      reference writes -1) and decrements n_neigh;
+//   3. the fp64 integrator epilogue (pd_device.cuh:node_epilogue) -- identical
+//      code to the exact path -- advances v, a and writes the next drifted u.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <thread>
+#include <unordered_map>
+#include <unordered_set>
+#include <vector>
+
+#include "pd_device.cuh"
+#include "pd_fast.cuh"
+#include "pd_internal.h"
+
+namespace pdb {
+
+__constant__ FastLaw c_flaws[PD_MAX_LAWS];
+
+void fast_set_laws(const DevLaw* laws, int n, cudaStream_t stream) {
+    std::vector<FastLaw> f(static_cast<size_t>(n));
+    for (int k = 0; k < n; ++k) {
+        std::memset(&f[size_t(k)], 0, sizeof(FastLaw));
+        f[size_t(k)].c = float(laws[k].c);
+        f[size_t(k)].nbp = laws[k].nbp;
+        for (int b = 0; b < laws[k].nbp; ++b) {
+            f[size_t(k)].bp[b] = float(laws[k].bp[b]);
+            f[size_t(k)].f[b] = float(laws[k].f[b]);
+        }
+    }
+    cudaMemcpyToSymbolAsync(c_flaws, f.data(), sizeof(FastLaw) * size_t(n), 0,
+                            cudaMemcpyHostToDevice, stream);
+    cudaStreamSynchronize(stream);
+}
+
+namespace {
+
+__device__ __forceinline__ float rsqrt_approx(float x) {
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ float f_envelope(const FastLaw& law, float s) {
+    float s_prev = 0.f, f_prev = 0.f;
+    for (int k = 0; k < law.nbp; ++k) {
+        const float s_k = law.bp[k];
+        if (s < s_k || k + 1 == law.nbp)
+            return f_prev + (s - s_prev) / (s_k - s_prev) * (law.f[k] - f_prev);
+        s_prev = s_k;
+        f_prev = law.f[k];
+    }
+    return law.c * s;
+}
+
+// CAP = shared-memory records reserved for the halo (+1 for the dummy record
+// at position 0 that dead/padding slots point at: it sits 1e15 away, carries
+// zero volume and the no-failure flag, so it contributes exactly 0 and never
+// breaks -- the slot loop needs no branch).
+template <int MODE, bool GENERAL, int CAP>
+__global__ void __launch_bounds__(FAST_T, (CAP <= 3072 ? 2 : 1)) fast_step_kernel(DevArgs A, FastDev F) {
+    if (MODE != 0 && *(volatile long long*)A.err_step != kNoError)
+        return;
+    extern __shared__ float4 smem[];
+    const int tile = F.tile0 + int(blockIdx.x);
+    const int ts = F.tile_start[tile];
+    const int te = F.tile_start[tile + 1];
+    const long long h0 = F.halo_off[tile];
+    const int H = int(F.halo_off[tile + 1] - h0);
+    float4* sx = smem;        // {x - O_t, c*V (PMB) or V}
+    float4* su = smem + CAP;  // {u - U_t, no_fail}
+
+    // 1. stage the halo in tile-local fp32 coordinates
+    const double4 O = A.xv[ts];
+    const double4 U0 = A.u_in[ts];
+    const double vscale = GENERAL ? 1.0 : double(F.pmb_c);
+    if (threadIdx.x == 0) {
+        sx[0] = make_float4(1e15f, 0.f, 0.f, 0.f);
+        su[0] = make_float4(0.f, 0.f, 0.f, 1.f);
+    }
+    for (int h = threadIdx.x; h < H; h += blockDim.x) {
+        const int id = F.halo[h0 + h];
+        const double4 x = A.xv[id];
+        const double4 u = A.u_in[id];
+        sx[h + 1] = make_float4(float(x.x - O.x), float(x.y - O.y), float(x.z - O.z),
+                                float(x.w * vscale));
+        su[h + 1] = make_float4(float(u.x - U0.x), float(u.y - U0.y), float(u.z - U0.z),
+                                float(u.w));
+    }
+    __syncthreads();
+
+    const int t = threadIdx.x;
+    const long long i = ts + t;
+    if (i >= te)
+        return;
+
+    // 2. the node's bonds
+    const int own = F.own_slot[i];
+    const float4 xi = sx[own];
+    const float4 ui = su[own];
+    const bool nfi = ui.w != 0.f;
+    const float sc_pmb = F.pmb_sc;
+    const float2 nxi = make_float2(-xi.x, -xi.y);
+    const float2 nui = make_float2(-ui.x, -ui.y);
+    float2 fxy = make_float2(0.f, 0.f);
+    float fz = 0.f;
+    int broke = 0;
+    unsigned short* lrow = F.lidx + F.slot_off[tile] + (long long)t * 8;
+    const int nkb = F.kmax8[tile] >> 3;
+    const long long kstride = (long long)F.T * 8;
+    uint4 wnext = nkb > 0 ? *reinterpret_cast<const uint4*>(lrow) : make_uint4(0, 0, 0, 0);
+    for (int kb = 0; kb < nkb; ++kb, lrow += kstride) {
+        const uint4 w = wnext;
+        if (kb + 1 < nkb)  // prefetch the next 8 slots while these compute
+            wnext = *reinterpret_cast<const uint4*>(lrow + kstride);
+        const unsigned words[4] = {w.x, w.y, w.z, w.w};
+        unsigned bmask = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const unsigned li = (q & 1) ? (words[q >> 1] >> 16) : (words[q >> 1] & 0xFFFFu);
+            const float4 xr = sx[li];
+            const float4 ur = su[li];
+            // x/y in packed f32x2 (FADD2/FMUL2/FFMA2), z scalar
+            const float2 exy = __fadd2_rn(make_float2(xr.x, xr.y), nxi);
+            const float2 hxy = __fadd2_rn(make_float2(ur.x, ur.y), nui);
+            const float2 cxy = __fadd2_rn(exy, hxy);
+            const float2 sxy = __fadd2_rn(exy, cxy);
+            const float ez = xr.z - xi.z, hz = ur.z - ui.z;
+            const float cz = ez + hz;
+            const float2 e2 = __fmul2_rn(exy, exy);
+            const float2 c2 = __fmul2_rn(cxy, cxy);
+            const float2 n2 = __fmul2_rn(hxy, sxy);
+            const float ref2 = fmaf(ez, ez, e2.x + e2.y);
+            const float cur2 = fmaf(cz, cz, c2.x + c2.y);
+            const float num = fmaf(hz, ez + cz, n2.x + n2.y);
+            const float cx = cxy.x, cy = cxy.y;
+            const float rr = rsqrt_approx(ref2);
+            const float rc = rsqrt_approx(cur2);
+            const float s = num * rr * rcp_approx(cur2 * rc + ref2 * rr);
+            const bool no_fail = nfi || ur.w != 0.f;
+            float f;
+            if (!GENERAL) {
+                if (s >= sc_pmb && !no_fail) {
+                    bmask |= 1u << q;  // stored after the 8 slots, off the hot path
+                    continue;
+                }
+                f = s;  // c is folded into the staged volume
+            } else {
+                const long long sidx = (lrow - F.lidx) + q;
+                const FastLaw& law = c_flaws[F.btype ? int(F.btype[sidx]) : 0];
+                if (no_fail) {
+                    f = law.c * s;
+                } else if (law.nbp == 1) {
+                    if (s >= law.bp[0]) {
+                        lrow[q] = 0;
+                        ++broke;
+                        continue;
+                    }
+                    f = law.c * s;
+                } else {
+                    const float s_c = law.bp[law.nbp - 1];
+                    const float hh = F.hist[sidx];
+                    if (s > hh)
+                        F.hist[sidx] = s;
+                    if (hh >= s_c || s >= s_c) {
+                        lrow[q] = 0;
+                        ++broke;
+                        continue;
+                    }
+                    f = (s >= hh) ? f_envelope(law, s)
+                                  : (hh <= 0.f ? law.c : f_envelope(law, hh) / hh) * s;
+                }
+                if (F.lambda)
+                    f *= F.lambda[sidx];
+                if (F.beta)
+                    f *= F.beta[sidx];
+            }
+            const float scale = f * xr.w * rc;
+            fxy = __ffma2_rn(cxy, make_float2(scale, scale), fxy);
+            fz = fmaf(cz, scale, fz);
+            (void)cx;
+            (void)cy;
+        }
+        if (!GENERAL && bmask) {
+            for (int q = 0; q < 8; ++q)
+                if (bmask >> q & 1u)
+                    lrow[q] = 0;
+            broke += __popc(bmask);
+        }
+    }
+    if (broke)
+        A.n_neigh[i] -= broke;
+
+    // 3. fp64 epilogue
+    if (MODE == 0) {
+        A.body_force[3 * i] = double(fxy.x);
+        A.body_force[3 * i + 1] = double(fxy.y);
+        A.body_force[3 * i + 2] = double(fz);
+        return;
+    }
+    node_epilogue<MODE>(A, i, A.u_in[i], double(fxy.x), double(fxy.y), double(fz));
+}
+
+template <int MODE, bool GENERAL, int CAP>
+cudaError_t launch_cap(const DevArgs& A, const FastDev& F, int tiles, cudaStream_t st) {
+    static bool configured = false;
+    const int smem = 2 * CAP * int(sizeof(float4));
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(fast_step_kernel<MODE, GENERAL, CAP>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess)
+            return e;
+        configured = true;
+    }
+    fast_step_kernel<MODE, GENERAL, CAP><<<tiles, F.T, smem, st>>>(A, F);
+    return cudaGetLastError();
+}
+
+template <int MODE, bool GENERAL>
+cudaError_t launch_one(const DevArgs& A, const FastDev& F, int tiles, int max_halo,
+                       cudaStream_t st) {
+    if (max_halo + 1 <= 3072)
+        return launch_cap<MODE, GENERAL, 3072>(A, F, tiles, st);
+    return launch_cap<MODE, GENERAL, FAST_MAX_HALO + 1>(A, F, tiles, st);
+}
+
+// ---- layout permutation / materialisation kernels ---------------------------
+
+template <class T, int W>
+__global__ void gather_rows_kernel(const T* in, T* out, const int* map, long long n) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n)
+        return;
+    const long long src = map[i];
+#pragma unroll
+    for (int w = 0; w < W; ++w)
+        out[i * W + w] = in[src * W + w];
+}
+
+// Per original row: rebuild entries (-1 where broken) and fp64 history from
+// the compact tile layout (live slots in slot order).
+__global__ void fast_materialize_kernel(const int32_t* entries0, const int* inv,
+                                        const int* tile_of, const int* tile_start,
+                                        const long long* slot_off, int T,
+                                        const unsigned short* lidx, const float* hist32,
+                                        long long n, int N, int32_t* entries_out,
+                                        double* hist_out) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n)
+        return;
+    const int ii = inv[i];
+    const int tile = tile_of[ii];
+    const int t = ii - tile_start[tile];
+    const long long base = slot_off[tile] + (long long)t * 8;
+    int c = 0;
+    for (int k = 0; k < N; ++k) {
+        const int32_t e = entries0[i * N + k];
+        if (e < 0) {
+            if (entries_out)
+                entries_out[i * N + k] = -1;
+            continue;
+        }
+        const long long s = base + (long long)(c >> 3) * T * 8 + (c & 7);
+        if (entries_out)
+            entries_out[i * N + k] = lidx[s] == 0 ? -1 : e;
+        if (hist_out && hist32)
+            hist_out[i * N + k] = double(hist32[s]);
+        ++c;
+    }
+}
+
+} // namespace
+
+cudaError_t launch_fast(const DevArgs& A, const FastDev& F, int mode, bool general, int tiles,
+                        int max_halo, cudaStream_t st) {
+    if (tiles <= 0)
+        return cudaSuccess;
+    if (general) {
+        switch (mode) {
+        case 0: return launch_one<0, true>(A, F, tiles, max_halo, st);
+        case 1: return launch_one<1, true>(A, F, tiles, max_halo, st);
+        case 2: return launch_one<2, true>(A, F, tiles, max_halo, st);
+        default: return launch_one<3, true>(A, F, tiles, max_halo, st);
+        }
+    }
+    switch (mode) {
+    case 0: return launch_one<0, false>(A, F, tiles, max_halo, st);
+    case 1: return launch_one<1, false>(A, F, tiles, max_halo, st);
+    case 2: return launch_one<2, false>(A, F, tiles, max_halo, st);
+    default: return launch_one<3, false>(A, F, tiles, max_halo, st);
+    }
+}
+
+template <class T, int W>
+void launch_gather_rows(const T* in, T* out, const int* map, long long n, cudaStream_t st) {
+    if (n > 0)
+        gather_rows_kernel<T, W><<<unsigned((n + 255) / 256), 256, 0, st>>>(in, out, map, n);
+}
+
+template void launch_gather_rows<double4, 1>(const double4*, double4*, const int*, long long,
+                                             cudaStream_t);
+template void launch_gather_rows<double, 1>(const double*, double*, const int*, long long,
+                                            cudaStream_t);
+template void launch_gather_rows<double, 3>(const double*, double*, const int*, long long,
+                                            cudaStream_t);
+template void launch_gather_rows<int32_t, 1>(const int32_t*, int32_t*, const int*, long long,
+                                             cudaStream_t);
+template void launch_gather_rows<uint8_t, 3>(const uint8_t*, uint8_t*, const int*, long long,
+                                             cudaStream_t);
+
+void launch_fast_materialize(const int32_t* entries0, const int* inv, const int* tile_of,
+                             const int* tile_start, const long long* slot_off, int T,
+                             const unsigned short* lidx, const float* hist32, long long n, int N,
+                             int32_t* entries_out, double* hist_out, cudaStream_t st) {
+    if (n > 0)
+        fast_materialize_kernel<<<unsigned((n + 127) / 128), 128, 0, st>>>(
+            entries0, inv, tile_of, tile_start, slot_off, T, lidx, hist32, n, N, entries_out,
+            hist_out);
+}
+
+// ---- host-side layout construction -------------------------------------------
+
+int fast_build_layout(FastHostLayout& L, int64_t n, int N, const int32_t* entries,
+                      const double* coords, const uint8_t* btype, const double* lambda,
+                      const double* beta, const double* hist, bool history) {
+    // bricks of ~8 nodes per axis from the bounding box and mean spacing
+    double lo[3], hi[3];
+    for (int d = 0; d < 3; ++d)
+        lo[d] = hi[d] = coords[d];
+    for (int64_t i = 1; i < n; ++i)
+        for (int d = 0; d < 3; ++d) {
+            lo[d] = std::min(lo[d], coords[3 * i + d]);
+            hi[d] = std::max(hi[d], coords[3 * i + d]);
+        }
+    double ext[3], prod = 1.0;
+    int dims = 0;
+    for (int d = 0; d < 3; ++d) {
+        ext[d] = hi[d] - lo[d];
+        if (ext[d] > 0) {
+            prod *= ext[d];
+            ++dims;
+        }
+    }
+    const double h = dims == 0 ? 1.0 : std::pow(prod / double(n), 1.0 / dims);
+    long long nb[3];
+    double len[3];
+    for (int d = 0; d < 3; ++d) {
+        nb[d] = ext[d] > 0 ? std::max(1LL, (long long)std::llround(ext[d] / (8.0 * h))) : 1;
+        len[d] = ext[d] > 0 ? ext[d] / double(nb[d]) : 1.0;
+    }
+    // lattice-like axes (few distinct coordinates): bricks of exactly 8 grid
+    // planes, so warps cover whole 8-node x-runs and neighbour runs stay
+    // bank-aligned; otherwise bins of ~8 mean spacings
+    std::unordered_map<double, long long> rank[3];
+    bool lattice[3] = {false, false, false};
+    for (int d = 0; d < 3; ++d) {
+        std::unordered_set<double> vals;
+        bool ok = true;
+        for (int64_t i = 0; i < n && ok; ++i) {
+            vals.insert(coords[3 * i + d]);
+            ok = vals.size() <= 4096;
+        }
+        if (!ok)
+            continue;
+        std::vector<double> sorted(vals.begin(), vals.end());
+        std::sort(sorted.begin(), sorted.end());
+        for (size_t k = 0; k < sorted.size(); ++k)
+            rank[d][sorted[k]] = (long long)k;
+        lattice[d] = true;
+        nb[d] = (long long)(sorted.size() + 7) / 8;
+    }
+    const long long nbricks = nb[0] * nb[1] * nb[2];
+    std::vector<long long> brick(static_cast<size_t>(n));
+    std::vector<long long> count(size_t(nbricks + 1), 0);
+    for (int64_t i = 0; i < n; ++i) {
+        long long b[3];
+        for (int d = 0; d < 3; ++d) {
+            long long c;
+            if (lattice[d])
+                c = rank[d][coords[3 * i + d]] / 8;
+            else
+                c = ext[d] > 0 ? (long long)std::floor((coords[3 * i + d] - lo[d]) / len[d]) : 0;
+            b[d] = std::min(std::max(c, 0LL), nb[d] - 1);
+        }
+        brick[size_t(i)] = (b[2] * nb[1] + b[1]) * nb[0] + b[0];
+        ++count[size_t(brick[size_t(i)] + 1)];
+    }
+    for (long long b = 0; b < nbricks; ++b)
+        count[size_t(b + 1)] += count[size_t(b)];
+    L.perm.assign(size_t(n), 0);
+    L.inv.assign(size_t(n), 0);
+    {
+        std::vector<long long> fill(count.begin(), count.end() - 1);
+        for (int64_t i = 0; i < n; ++i)
+            L.perm[size_t(fill[size_t(brick[size_t(i)])]++)] = int(i);
+    }
+    for (int64_t ii = 0; ii < n; ++ii)
+        L.inv[size_t(L.perm[size_t(ii)])] = int(ii);
+
+    // tiles: <= FAST_T consecutive internal nodes of one brick
+    L.T = FAST_T;
+    L.tile_start.clear();
+    for (long long b = 0; b < nbricks; ++b)
+        for (long long s = count[size_t(b)]; s < count[size_t(b + 1)]; s += FAST_T)
+            L.tile_start.push_back(int(s));
+    L.tile_start.push_back(int(n));
+    const int tiles = int(L.tile_start.size()) - 1;
+    L.n_tiles = tiles;
+    L.tile_of.assign(size_t(n), 0);
+    L.own_slot.assign(size_t(n), 0);
+    for (int t = 0; t < tiles; ++t)
+        for (int ii = L.tile_start[size_t(t)]; ii < L.tile_start[size_t(t + 1)]; ++ii)
+            L.tile_of[size_t(ii)] = t;
+
+    struct TileOut {
+        std::vector<int> halo;
+        std::vector<unsigned short> lidx;
+        std::vector<float> hist, lambda, beta;
+        std::vector<uint8_t> btype;
+        int kmax8 = 0;
+    };
+    std::vector<TileOut> out(static_cast<size_t>(tiles));
+    int error = 0;
+    auto work = [&](int t0, int t1) {
+        std::vector<int> ids;
+        for (int t = t0; t < t1; ++t) {
+            TileOut& o = out[size_t(t)];
+            const int ts = L.tile_start[size_t(t)], te = L.tile_start[size_t(t + 1)];
+            ids.clear();
+            int kmax = 0;
+            for (int ii = ts; ii < te; ++ii) {
+                ids.push_back(ii);
+                const int64_t i = L.perm[size_t(ii)];
+                int live = 0;
+                for (int k = 0; k < N; ++k) {
+                    const int32_t j = entries[i * N + k];
+                    if (j >= 0) {
+                        ids.push_back(L.inv[size_t(j)]);
+                        ++live;
+                    }
+                }
+                kmax = std::max(kmax, live);
+            }
+            // shared-memory order = reference (original) node order: on a lattice an
+            // x-run of neighbours stays contiguous across brick boundaries, so a
+            // quarter-warp's 16-byte loads hit distinct banks
+            for (int& id : ids)
+                id = L.perm[size_t(id)];
+            std::sort(ids.begin(), ids.end());
+            ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
+            if (ids.size() > size_t(FAST_MAX_HALO)) {
+                error = 1;
+                continue;
+            }
+            o.halo.resize(ids.size());
+            for (size_t q = 0; q < ids.size(); ++q)
+                o.halo[q] = L.inv[size_t(ids[q])];
+            for (int ii = ts; ii < te; ++ii)
+                L.own_slot[size_t(ii)] = (unsigned short)(
+                    1 + (std::lower_bound(ids.begin(), ids.end(), L.perm[size_t(ii)]) - ids.begin()));
+            o.kmax8 = (kmax + 7) / 8 * 8;
+            const size_t slots = size_t(o.kmax8) * FAST_T;
+            o.lidx.assign(slots, 0);
+            if (history)
+                o.hist.assign(slots, 0.f);
+            if (btype)
+                o.btype.assign(slots, 0);
+            if (lambda)
+                o.lambda.assign(slots, 1.f);
+            if (beta)
+                o.beta.assign(slots, 1.f);
+            for (int ii = ts; ii < te; ++ii) {
+                const int tt = ii - ts;
+                const int64_t i = L.perm[size_t(ii)];
+                int c = 0;
+                for (int k = 0; k < N; ++k) {
+                    const int32_t j = entries[i * N + k];
+                    if (j < 0)
+                        continue;
+                    const size_t s = size_t(c >> 3) * FAST_T * 8 + size_t(tt) * 8 + size_t(c & 7);
+                    o.lidx[s] = (unsigned short)(1 + (std::lower_bound(ids.begin(), ids.end(), j) -
+                                                      ids.begin()));
+                    const int64_t idx = i * N + k;
+                    if (history)
+                        o.hist[s] = hist ? float(hist[idx]) : 0.f;
+                    if (btype)
+                        o.btype[s] = btype[idx];
+                    if (lambda)
+                        o.lambda[s] = float(lambda[idx]);
+                    if (beta)
+                        o.beta[s] = float(beta[idx]);
+                    ++c;
+                }
+            }
+        }
+    };
+    const int threads = std::max(1, std::min(32, int(std::thread::hardware_concurrency())));
+    std::vector<std::thread> pool;
+    const int chunk = (tiles + threads - 1) / threads;
+    for (int w = 0; w < threads; ++w) {
+        const int t0 = w * chunk, t1 = std::min(tiles, t0 + chunk);
+        if (t0 < t1)
+            pool.emplace_back(work, t0, t1);
+    }
+    for (auto& th : pool)
+        th.join();
+    if (error)
+        return 1;
+
+    L.halo_off.assign(size_t(tiles + 1), 0);
+    L.slot_off.assign(size_t(tiles), 0);
+    L.kmax8.assign(size_t(tiles), 0);
+    long long slots = 0;
+    L.max_halo = 0;
+    for (int t = 0; t < tiles; ++t) {
+        L.halo_off[size_t(t + 1)] = L.halo_off[size_t(t)] + (long long)out[size_t(t)].halo.size();
+        L.slot_off[size_t(t)] = slots;
+        slots += (long long)out[size_t(t)].lidx.size();
+        L.kmax8[size_t(t)] = out[size_t(t)].kmax8;
+        L.max_halo = std::max(L.max_halo, int(out[size_t(t)].halo.size()));
+    }
+    L.total_slots = slots;
+    L.halo.resize(size_t(L.halo_off[size_t(tiles)]));
+    L.lidx.resize(size_t(slots));
+    L.hist.resize(history ? size_t(slots) : 0);
+    L.btype.resize(btype ? size_t(slots) : 0);
+    L.lambda.resize(lambda ? size_t(slots) : 0);
+    L.beta.resize(beta ? size_t(slots) : 0);
+    for (int t = 0; t < tiles; ++t) {
+        TileOut& o = out[size_t(t)];
+        std::copy(o.halo.begin(), o.halo.end(), L.halo.begin() + L.halo_off[size_t(t)]);
+        std::copy(o.lidx.begin(), o.lidx.end(), L.lidx.begin() + L.slot_off[size_t(t)]);
+        if (history)
+            std::copy(o.hist.begin(), o.hist.end(), L.hist.begin() + L.slot_off[size_t(t)]);
+        if (btype)
+            std::copy(o.btype.begin(), o.btype.end(), L.btype.begin() + L.slot_off[size_t(t)]);
+        if (lambda)
+            std::copy(o.lambda.begin(), o.lambda.end(), L.lambda.begin() + L.slot_off[size_t(t)]);
+        if (beta)
+            std::copy(o.beta.begin(), o.beta.end(), L.beta.begin() + L.slot_off[size_t(t)]);
+    }
+    return 0;
+}
+
+} // namespace pdb

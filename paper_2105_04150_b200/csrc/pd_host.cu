@@ -65,36 +65,6 @@ namespace {
             return rc_;                                                                          \
     } while (0)
 
-template <class T> struct DevBuf {
-    T* p = nullptr;
-    size_t count = 0;
-    DevBuf() = default;
-    DevBuf(const DevBuf&) = delete;
-    DevBuf& operator=(const DevBuf&) = delete;
-    ~DevBuf() { release(); }
-    void release() {
-        if (p)
-            cudaFree(p);
-        p = nullptr;
-        count = 0;
-    }
-    cudaError_t alloc(size_t n) {
-        if (n == count && p)
-            return cudaSuccess;
-        release();
-        if (n == 0)
-            return cudaSuccess;
-        count = n;
-        return cudaMalloc(&p, n * sizeof(T));
-    }
-    cudaError_t upload(const T* host, size_t n, cudaStream_t st) {
-        cudaError_t e = alloc(n);
-        if (e != cudaSuccess || n == 0)
-            return e;
-        return cudaMemcpyAsync(p, host, n * sizeof(T), cudaMemcpyHostToDevice, st);
-    }
-};
-
 // ---- validation with the reference's messages -----------------------------
 
 int law_validate(const pd_law& l) {
@@ -215,6 +185,42 @@ struct pd_ctx {
     int n_tip_sets = 0;
     bool forces_valid = false;
 
+    // fast path (PD_FAST): internal brick order + tile layout (pd_fast.cuh)
+    bool fast = false;
+    bool general = false;
+    float pmb_c = 0, pmb_sc = 0;
+    int n_tiles = 0, max_halo = 0;
+    DevBuf<int> perm, inv, tile_of, tile_start, kmax8, halo;
+    DevBuf<unsigned short> own_slot;
+    DevBuf<long long> halo_off, slot_off;
+    DevBuf<unsigned short> lidx;
+    DevBuf<float> hist32, lambda32, beta32;
+    DevBuf<uint8_t> btype_c;
+    DevBuf<double4> scratch_d4;
+    DevBuf<int32_t> scratch_n;
+    DevBuf<uint8_t> scratch_u8;
+
+    FastDev fast_args() const {
+        FastDev F{};
+        F.T = FAST_T;
+        F.n_tiles = n_tiles;
+        F.tile0 = 0;
+        F.tile_start = tile_start.p;
+        F.halo_off = halo_off.p;
+        F.halo = halo.p;
+        F.slot_off = slot_off.p;
+        F.kmax8 = kmax8.p;
+        F.own_slot = own_slot.p;
+        F.lidx = lidx.p;
+        F.hist = hist32.p;
+        F.btype = btype_c.p;
+        F.lambda = lambda32.p;
+        F.beta = beta32.p;
+        F.pmb_c = pmb_c;
+        F.pmb_sc = pmb_sc;
+        return F;
+    }
+
     DevArgs args() const {
         DevArgs A{};
         A.n = n;
@@ -290,6 +296,7 @@ int upload_common(pd_ctx* ctx, const pd_particles& p, const pd_state& st,
     const int64_t n = st.connectivity.n;
     const int64_t N = st.connectivity.group_size;
     PD_TRY(group_validate(N));
+    ctx->fast = false;
     if (p.coords_size != 3 * n || !p.coords || !p.volume)
         return fail(PD_E_INVALID_ARGUMENT, "ParticleSet: field lengths differ");
     ctx->n = n;
@@ -435,48 +442,89 @@ int upload_bc(pd_ctx* ctx, const pd_boundary& bc) {
     return PD_OK;
 }
 
-// Copy selected resident fields into host arrays of `st` / `forces`.
+// Copy selected resident fields into host arrays of `st` / `forces` (in the
+// reference's node order; the fast path gathers out of its brick order).
 int download(pd_ctx* ctx, pd_state* st, pd_force_field* forces, int32_t fields) {
     cudaStream_t s = ctx->stream;
     const int64_t n = ctx->n;
     const int64_t slots = n * ctx->N;
+    const int* inv = ctx->fast ? ctx->inv.p : nullptr;
+    auto vec3_out = [&](const double* dev, double* host) -> int {
+        const double* src = dev;
+        if (inv) {
+            PD_CK(ctx->scratch_f64.alloc(size_t(3 * n)));
+            launch_gather_rows<double, 3>(dev, ctx->scratch_f64.p, inv, n, s);
+            ++ctx->launches;
+            src = ctx->scratch_f64.p;
+        }
+        PD_CK(cudaMemcpyAsync(host, src, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s));
+        PD_CK(cudaStreamSynchronize(s));
+        return PD_OK;
+    };
     if ((fields & PD_FIELD_U) && st && st->u) {
+        const double4* src = ctx->u[ctx->cur].p;
+        if (inv) {
+            PD_CK(ctx->scratch_d4.alloc(size_t(n)));
+            launch_gather_rows<double4, 1>(src, ctx->scratch_d4.p, inv, n, s);
+            ++ctx->launches;
+            src = ctx->scratch_d4.p;
+        }
         PD_CK(ctx->scratch_f64.alloc(size_t(3 * n)));
-        launch_unpack_u(ctx->u[ctx->cur].p, n, ctx->scratch_f64.p, s);
+        launch_unpack_u(src, n, ctx->scratch_f64.p, s);
         ++ctx->launches;
         PD_CK(cudaMemcpyAsync(st->u, ctx->scratch_f64.p, sizeof(double) * 3 * n,
                               cudaMemcpyDeviceToHost, s));
+        PD_CK(cudaStreamSynchronize(s));
     }
     if ((fields & PD_FIELD_V) && st && st->v)
-        PD_CK(cudaMemcpyAsync(st->v, ctx->v.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s));
+        PD_TRY(vec3_out(ctx->v.p, st->v));
     if ((fields & PD_FIELD_A) && st && st->a)
-        PD_CK(cudaMemcpyAsync(st->a, ctx->a.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s));
+        PD_TRY(vec3_out(ctx->a.p, st->a));
+    const bool want_hist = (fields & PD_FIELD_HISTORY) && st && st->bond_history && ctx->history;
+    if (want_hist && st->bond_history_size != slots)
+        return fail(PD_E_INVALID_ARGUMENT, "download: bond_history must be sized n x N");
     if ((fields & PD_FIELD_CONNECTIVITY) && st) {
         if (st->connectivity.entries) {
             PD_CK(ctx->scratch_i32.alloc(size_t(slots)));
-            launch_materialize_entries(ctx->entries.p, ctx->alive.p, n, ctx->N, ctx->W,
-                                       ctx->scratch_i32.p, s);
+            if (ctx->fast)
+                launch_fast_materialize(ctx->entries.p, ctx->inv.p, ctx->tile_of.p,
+                                        ctx->tile_start.p, ctx->slot_off.p, FAST_T, ctx->lidx.p,
+                                        nullptr, n, ctx->N, ctx->scratch_i32.p, nullptr, s);
+            else
+                launch_materialize_entries(ctx->entries.p, ctx->alive.p, n, ctx->N, ctx->W,
+                                           ctx->scratch_i32.p, s);
             ++ctx->launches;
             PD_CK(cudaMemcpyAsync(st->connectivity.entries, ctx->scratch_i32.p,
                                   sizeof(int32_t) * slots, cudaMemcpyDeviceToHost, s));
         }
-        if (st->connectivity.n_neigh)
-            PD_CK(cudaMemcpyAsync(st->connectivity.n_neigh, ctx->n_neigh.p, sizeof(int32_t) * n,
+        if (st->connectivity.n_neigh) {
+            const int32_t* src = ctx->n_neigh.p;
+            if (inv) {
+                PD_CK(ctx->scratch_n.alloc(size_t(n)));
+                launch_gather_rows<int32_t, 1>(src, ctx->scratch_n.p, inv, n, s);
+                ++ctx->launches;
+                src = ctx->scratch_n.p;
+            }
+            PD_CK(cudaMemcpyAsync(st->connectivity.n_neigh, src, sizeof(int32_t) * n,
                                   cudaMemcpyDeviceToHost, s));
+        }
+        PD_CK(cudaStreamSynchronize(s));
     }
-    if ((fields & PD_FIELD_HISTORY) && st && st->bond_history && ctx->history) {
-        if (st->bond_history_size != slots)
-            return fail(PD_E_INVALID_ARGUMENT, "download: bond_history must be sized n x N");
+    if (want_hist) {
+        if (ctx->fast) {
+            launch_fast_materialize(ctx->entries.p, ctx->inv.p, ctx->tile_of.p, ctx->tile_start.p,
+                                    ctx->slot_off.p, FAST_T, ctx->lidx.p, ctx->hist32.p, n,
+                                    ctx->N, nullptr, ctx->hist.p, s);
+            ++ctx->launches;
+        }
         PD_CK(cudaMemcpyAsync(st->bond_history, ctx->hist.p, sizeof(double) * slots,
                               cudaMemcpyDeviceToHost, s));
     }
     if ((fields & PD_FIELD_FORCES) && forces) {
         if (forces->body_force)
-            PD_CK(cudaMemcpyAsync(forces->body_force, ctx->body.p, sizeof(double) * 3 * n,
-                                  cudaMemcpyDeviceToHost, s));
+            PD_TRY(vec3_out(ctx->body.p, forces->body_force));
         if (forces->external_force)
-            PD_CK(cudaMemcpyAsync(forces->external_force, ctx->ext.p, sizeof(double) * 3 * n,
-                                  cudaMemcpyDeviceToHost, s));
+            PD_TRY(vec3_out(ctx->ext.p, forces->external_force));
     }
     if (st)
         st->step = ctx->step;
@@ -484,9 +532,115 @@ int download(pd_ctx* ctx, pd_state* st, pd_force_field* forces, int32_t fields) 
     return PD_OK;
 }
 
+// Renumber the resident node arrays into the fast path's brick order and
+// build its tile layout from the host copies of the rows.
+int setup_fast(pd_ctx* ctx, const pd_particles& p, const pd_state& st,
+               const pd_damage_model& m, const pd_corrections& corr, pd_boundary* bc_tips) {
+    cudaStream_t s = ctx->stream;
+    const int64_t n = ctx->n;
+    FastHostLayout L;
+    const bool hist_in = ctx->history && st.bond_history &&
+                         st.bond_history_size == n * int64_t(ctx->N);
+    if (fast_build_layout(L, n, ctx->N, st.connectivity.entries, p.coords,
+                          st.connectivity.bond_type_size ? st.connectivity.bond_type : nullptr,
+                          corr.lambda_size ? corr.lambda : nullptr,
+                          corr.beta_size ? corr.beta : nullptr,
+                          hist_in ? st.bond_history : nullptr, ctx->history) != 0)
+        return fail(PD_E_INVALID_ARGUMENT,
+                    "PD_FAST: a tile neighbourhood exceeds %d nodes of shared memory; use "
+                    "PD_BOND_PARALLEL for this mesh", FAST_MAX_HALO);
+    ctx->n_tiles = L.n_tiles;
+    ctx->max_halo = L.max_halo;
+    PD_CK(ctx->perm.upload(L.perm.data(), L.perm.size(), s));
+    PD_CK(ctx->inv.upload(L.inv.data(), L.inv.size(), s));
+    PD_CK(ctx->tile_of.upload(L.tile_of.data(), L.tile_of.size(), s));
+    PD_CK(ctx->tile_start.upload(L.tile_start.data(), L.tile_start.size(), s));
+    PD_CK(ctx->kmax8.upload(L.kmax8.data(), L.kmax8.size(), s));
+    PD_CK(ctx->own_slot.upload(L.own_slot.data(), L.own_slot.size(), s));
+    PD_CK(ctx->halo.upload(L.halo.data(), L.halo.size(), s));
+    PD_CK(ctx->halo_off.upload(L.halo_off.data(), L.halo_off.size(), s));
+    PD_CK(ctx->slot_off.upload(L.slot_off.data(), L.slot_off.size(), s));
+    PD_CK(ctx->lidx.upload(L.lidx.data(), L.lidx.size(), s));
+    if (!L.hist.empty())
+        PD_CK(ctx->hist32.upload(L.hist.data(), L.hist.size(), s));
+    if (!L.btype.empty())
+        PD_CK(ctx->btype_c.upload(L.btype.data(), L.btype.size(), s));
+    if (!L.lambda.empty())
+        PD_CK(ctx->lambda32.upload(L.lambda.data(), L.lambda.size(), s));
+    if (!L.beta.empty())
+        PD_CK(ctx->beta32.upload(L.beta.data(), L.beta.size(), s));
+    // permute node arrays into internal order
+    const int* perm = ctx->perm.p;
+    PD_CK(ctx->scratch_d4.alloc(size_t(n)));
+    launch_gather_rows<double4, 1>(ctx->xv.p, ctx->scratch_d4.p, perm, n, s);
+    PD_CK(cudaMemcpyAsync(ctx->xv.p, ctx->scratch_d4.p, sizeof(double4) * n,
+                          cudaMemcpyDeviceToDevice, s));
+    launch_gather_rows<double4, 1>(ctx->u[ctx->cur].p, ctx->scratch_d4.p, perm, n, s);
+    PD_CK(cudaMemcpyAsync(ctx->u[ctx->cur].p, ctx->scratch_d4.p, sizeof(double4) * n,
+                          cudaMemcpyDeviceToDevice, s));
+    PD_CK(ctx->scratch_f64.alloc(size_t(3 * n)));
+    for (double* arr : {ctx->v.p, ctx->a.p}) {
+        launch_gather_rows<double, 3>(arr, ctx->scratch_f64.p, perm, n, s);
+        PD_CK(cudaMemcpyAsync(arr, ctx->scratch_f64.p, sizeof(double) * 3 * n,
+                              cudaMemcpyDeviceToDevice, s));
+    }
+    launch_gather_rows<double, 1>(ctx->rho.p, ctx->scratch_f64.p, perm, n, s);
+    PD_CK(cudaMemcpyAsync(ctx->rho.p, ctx->scratch_f64.p, sizeof(double) * n,
+                          cudaMemcpyDeviceToDevice, s));
+    PD_CK(ctx->scratch_n.alloc(size_t(n)));
+    for (int32_t* arr : {ctx->n_neigh.p, ctx->initial.p}) {
+        launch_gather_rows<int32_t, 1>(arr, ctx->scratch_n.p, perm, n, s);
+        PD_CK(cudaMemcpyAsync(arr, ctx->scratch_n.p, sizeof(int32_t) * n,
+                              cudaMemcpyDeviceToDevice, s));
+    }
+    if (ctx->has_bc) {
+        PD_CK(ctx->scratch_u8.alloc(size_t(3 * n)));
+        for (uint8_t* arr : {ctx->bc_kind.p, ctx->bc_ramp.p}) {
+            launch_gather_rows<uint8_t, 3>(arr, ctx->scratch_u8.p, perm, n, s);
+            PD_CK(cudaMemcpyAsync(arr, ctx->scratch_u8.p, 3 * n, cudaMemcpyDeviceToDevice, s));
+        }
+        launch_gather_rows<double, 3>(ctx->bc_mag.p, ctx->scratch_f64.p, perm, n, s);
+        PD_CK(cudaMemcpyAsync(ctx->bc_mag.p, ctx->scratch_f64.p, sizeof(double) * 3 * n,
+                              cudaMemcpyDeviceToDevice, s));
+    }
+    ctx->launches += 10;
+    // tip sets refer to reference node numbers
+    if (bc_tips && ctx->n_tip_sets > 0) {
+        const int64_t total = bc_tips->tip_offsets[bc_tips->n_tip_sets];
+        std::vector<long long> nodes(size_t(std::max<int64_t>(total, 1)), 0);
+        for (int64_t t = 0; t < total; ++t)
+            nodes[size_t(t)] = L.inv[size_t(bc_tips->tip_nodes[t])];
+        PD_CK(ctx->tip_nodes.upload(nodes.data(), nodes.size(), s));
+    }
+    // the single-PMB-law specialisation needs no per-slot law data
+    ctx->general = m.n_laws > 1 || ctx->history || !L.btype.empty() || !L.lambda.empty() ||
+                   !L.beta.empty();
+    ctx->pmb_c = float(m.laws[0].stiffness);
+    ctx->pmb_sc = float(m.laws[0].breakpoints[0]);
+    std::vector<DevLaw> laws(size_t(m.n_laws));
+    for (int k = 0; k < m.n_laws; ++k) {
+        std::memset(&laws[size_t(k)], 0, sizeof(DevLaw));
+        laws[size_t(k)].c = m.laws[k].stiffness;
+        laws[size_t(k)].nbp = m.laws[k].n_breakpoints;
+        for (int b = 0; b < laws[size_t(k)].nbp; ++b) {
+            laws[size_t(k)].bp[b] = m.laws[k].breakpoints[b];
+            laws[size_t(k)].f[b] = m.laws[k].forces[b];
+        }
+    }
+    fast_set_laws(laws.data(), m.n_laws, s);
+    PD_CK(cudaGetLastError());
+    ctx->fast = true;
+    PD_CK(cudaStreamSynchronize(s));
+    return PD_OK;
+}
+
 int launch_step(pd_ctx* ctx, DevArgs& A, int mode) {
-    if (ctx->variant == PD_FAST)
-        return fail(PD_E_INVALID_ARGUMENT, "PD_FAST kernel is not available in this build");
+    if (ctx->fast) {
+        PD_CK(launch_fast(A, ctx->fast_args(), mode, ctx->general, ctx->n_tiles, ctx->max_halo,
+                          ctx->stream));
+        ++ctx->launches;
+        return PD_OK;
+    }
     PD_CK(launch_exact(A, mode, ctx->variant == PD_NODE_PARALLEL, ctx->stream));
     ++ctx->launches;
     return PD_OK;
@@ -523,6 +677,11 @@ int run_loop(pd_ctx* ctx, const pd_options& opt, pd_write_hook hook, void* user,
     if (n_records > 0)
         PD_CK(ctx->tips.alloc(size_t(n_records)));
 
+    if ((opt.variant == PD_FAST) != ctx->fast)
+        return fail(PD_E_INVALID_ARGUMENT,
+                    "simulate: the variant must match the one the model was uploaded for");
+    if (opt.variant != PD_FAST)
+        ctx->variant = opt.variant;
     const bool vv = opt.integrator == PD_VELOCITY_VERLET;
     const int mode = vv ? 1 : (opt.integrator == PD_EULER ? 2 : 3);
     const long long none = kNoError;
@@ -723,6 +882,10 @@ int pd_ctx_upload(pd_ctx* ctx, const pd_bundle* b, const pd_state* st, int32_t v
     if (b->corrections.beta_size != 0 && b->corrections.beta_size != slots)
         return fail(PD_E_INVALID_ARGUMENT, "compute_forces: beta size mismatch");
     PD_TRY(upload_bc(ctx, b->bc));
+    if (variant == PD_FAST) {
+        pd_boundary bc = b->bc;
+        PD_TRY(setup_fast(ctx, b->particles, *st, b->model, b->corrections, &bc));
+    }
     ctx->variant = variant;
     ctx->dt = b->dt;
     return ok();
@@ -766,11 +929,16 @@ int pd_ctx_download(pd_ctx* ctx, pd_state* state, pd_force_field* forces, int32_
 int pd_ctx_damage(pd_ctx* ctx, double* phi_out) {
     PD_TRY(select_device(ctx));
     cudaStream_t s = ctx->stream;
-    PD_CK(ctx->scratch_f64.alloc(size_t(ctx->n)));
+    PD_CK(ctx->scratch_f64.alloc(size_t(2 * ctx->n)));
     launch_damage(ctx->n_neigh.p, ctx->initial.p, ctx->n, ctx->scratch_f64.p, s);
     ++ctx->launches;
-    PD_CK(cudaMemcpyAsync(phi_out, ctx->scratch_f64.p, sizeof(double) * ctx->n,
-                          cudaMemcpyDeviceToHost, s));
+    const double* phi = ctx->scratch_f64.p;
+    if (ctx->fast) {
+        launch_gather_rows<double, 1>(phi, ctx->scratch_f64.p + ctx->n, ctx->inv.p, ctx->n, s);
+        ++ctx->launches;
+        phi = ctx->scratch_f64.p + ctx->n;
+    }
+    PD_CK(cudaMemcpyAsync(phi_out, phi, sizeof(double) * ctx->n, cudaMemcpyDeviceToHost, s));
     PD_CK(cudaStreamSynchronize(s));
     return ok();
 }
@@ -831,6 +999,8 @@ int pd_compute_forces(int32_t variant, pd_state* state, const pd_particles* part
     st.a = nullptr;
     PD_TRY(upload_common(ctx, *particles, st, *model, *corr, corr->no_failure,
                          corr->no_failure_size));
+    if (variant == PD_FAST)
+        PD_TRY(setup_fast(ctx, *particles, st, *model, *corr, nullptr));
     ctx->variant = variant;
     DevArgs A = ctx->args();
     PD_TRY(launch_step(ctx, A, 0));

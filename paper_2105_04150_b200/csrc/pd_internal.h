@@ -3,12 +3,71 @@
 
 #include <cuda_runtime.h>
 
+#include <cstddef>
+#include <vector>
+
 #include "pd_device.cuh"
+#include "pd_fast.cuh"
 
 namespace pdb {
 
+// Owning device buffer (cudaMalloc'd), resized on demand.
+template <class T> struct DevBuf {
+    T* p = nullptr;
+    size_t count = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p)
+            cudaFree(p);
+        p = nullptr;
+        count = 0;
+    }
+    cudaError_t alloc(size_t n) {
+        if (n == count && p)
+            return cudaSuccess;
+        release();
+        if (n == 0)
+            return cudaSuccess;
+        count = n;
+        return cudaMalloc(&p, n * sizeof(T));
+    }
+    cudaError_t upload(const T* host, size_t n, cudaStream_t st) {
+        cudaError_t e = alloc(n);
+        if (e != cudaSuccess || n == 0)
+            return e;
+        return cudaMemcpyAsync(p, host, n * sizeof(T), cudaMemcpyHostToDevice, st);
+    }
+};
+
 // pd_host.cu: record the message pd_last_error() returns; returns code.
 int set_error(int code, const char* msg);
+
+// pd_fast.cu -- host copy of the tile layout (see pd_fast.cuh)
+struct FastHostLayout {
+    int T = 0, n_tiles = 0, max_halo = 0;
+    long long total_slots = 0;
+    std::vector<int> perm, inv, tile_of, tile_start, kmax8, halo;
+    std::vector<unsigned short> own_slot;
+    std::vector<long long> halo_off, slot_off;
+    std::vector<unsigned short> lidx;
+    std::vector<float> hist, lambda, beta;
+    std::vector<uint8_t> btype;
+};
+int fast_build_layout(FastHostLayout& L, int64_t n, int N, const int32_t* entries,
+                      const double* coords, const uint8_t* btype, const double* lambda,
+                      const double* beta, const double* hist, bool history);
+void fast_set_laws(const DevLaw* laws, int n, cudaStream_t stream);
+cudaError_t launch_fast(const DevArgs& A, const FastDev& F, int mode, bool general, int tiles,
+                        int max_halo, cudaStream_t st);
+template <class T, int W>
+void launch_gather_rows(const T* in, T* out, const int* map, long long n, cudaStream_t st);
+void launch_fast_materialize(const int32_t* entries0, const int* inv, const int* tile_of,
+                             const int* tile_start, const long long* slot_off, int T,
+                             const unsigned short* lidx, const float* hist32, long long n, int N,
+                             int32_t* entries_out, double* hist_out, cudaStream_t st);
 
 // pd_exact.cu
 void exact_set_laws(const DevLaw* laws, int n, cudaStream_t stream);

@@ -72,7 +72,7 @@ __global__ void vv_prologue_kernel(DevArgs A) {
     if (i >= A.end)
         return;
     const double dt = A.dt;
-    const double half_dt2 = __ddiv_rn(__dmul_rn(dt, dt), 2.0);
+    const double half_dt2 = A.half_dt2;
     const double4 u = A.u_in[i];
     const double u0[3] = {u.x, u.y, u.z};
     double un[3];
@@ -119,6 +119,12 @@ __global__ void damage_kernel(const int32_t* n_neigh, const int32_t* initial, lo
         return;
     const int32_t init = initial[i];
     phi[i] = init > 0 ? __dsub_rn(1.0, __ddiv_rn((double)n_neigh[i], (double)init)) : 0.0;
+}
+
+__global__ void inv_kernel(const double* x, long long n, double* out) {
+    const long long i = blockIdx.x * (long long)TPB + threadIdx.x;
+    if (i < n)
+        out[i] = __ddiv_rn(1.0, x[i]);
 }
 
 __global__ void sum_kernel(const int32_t* x, long long n, unsigned long long* out) {
@@ -232,6 +238,11 @@ void launch_damage(const int32_t* n_neigh, const int32_t* initial, long long n, 
                    cudaStream_t st) {
     if (n > 0)
         damage_kernel<<<grid_for(n), TPB, 0, st>>>(n_neigh, initial, n, phi);
+}
+
+void launch_inv(const double* x, long long n, double* out, cudaStream_t st) {
+    if (n > 0)
+        inv_kernel<<<grid_for(n), TPB, 0, st>>>(x, n, out);
 }
 
 void launch_sum(const int32_t* x, long long n, unsigned long long* out, cudaStream_t st) {

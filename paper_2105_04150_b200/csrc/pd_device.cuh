@@ -54,6 +54,7 @@ struct DevArgs {
     double* v;
     double* a;
     const double* rho;
+    const double* inv_rho;    // 1/rho, precomputed once (Real(1) / density[i], engine.cpp:244)
     const int32_t* entries;
     uint32_t* alive;
     int32_t* n_neigh;         // live count per row, decremented on breaks
@@ -70,6 +71,9 @@ struct DevArgs {
     long long* err_step;      // first step whose force pass sees non-finite u
     long long step;           // the step s this launch advances (s -> s+1)
     double dt;
+    double half_dt;           // dt / 2   (host-computed, same IEEE result)
+    double half_dt2;          // dt * dt / 2
+    double dt2;               // dt * dt
     double damping;
     int store_forces;
     int do_drift;             // VV: produce next step's drifted u into u_out
@@ -159,11 +163,11 @@ __device__ __forceinline__ void node_epilogue(const DevArgs& A, long long i, con
         v[ax] = A.v[3 * i + ax];
         a[ax] = A.a[3 * i + ax];
     }
-    const double inv = __ddiv_rn(1.0, A.rho[i]);
+    const double inv = A.inv_rho[i];
     bool write_u = true;
     if (MODE == 1) {
-        const double half = __ddiv_rn(dt, 2.0);
-        const double half_dt2 = __ddiv_rn(__dmul_rn(dt, dt), 2.0);
+        const double half = A.half_dt;
+        const double half_dt2 = A.half_dt2;
 #pragma unroll
         for (int ax = 0; ax < 3; ++ax) {
             const double vh = __dadd_rn(v[ax], __dmul_rn(a[ax], half));
@@ -171,7 +175,7 @@ __device__ __forceinline__ void node_epilogue(const DevArgs& A, long long i, con
             double vn = __dadd_rn(vh, __dmul_rn(an, half));
             if (kind[ax] == PD_BC_DISPLACEMENT) {
                 vn = __ddiv_rn(__dmul_rn(mag[ax], ramp_rate(ramp[ax], s + 1)), dt);
-                an = __ddiv_rn(__dmul_rn(mag[ax], ramp_accel(ramp[ax], s + 1)), __dmul_rn(dt, dt));
+                an = __ddiv_rn(__dmul_rn(mag[ax], ramp_accel(ramp[ax], s + 1)), A.dt2);
             }
             v[ax] = vn;
             a[ax] = an;
@@ -192,7 +196,7 @@ __device__ __forceinline__ void node_epilogue(const DevArgs& A, long long i, con
             if (kind[ax] == PD_BC_DISPLACEMENT) {
                 un[ax] = __dmul_rn(mag[ax], ramp_scale(ramp[ax], s + 1));
                 v[ax] = __ddiv_rn(__dmul_rn(mag[ax], ramp_rate(ramp[ax], s + 1)), dt);
-                a[ax] = __ddiv_rn(__dmul_rn(mag[ax], ramp_accel(ramp[ax], s + 1)), __dmul_rn(dt, dt));
+                a[ax] = __ddiv_rn(__dmul_rn(mag[ax], ramp_accel(ramp[ax], s + 1)), A.dt2);
             }
         }
     }

@@ -76,99 +76,144 @@ __device__ __forceinline__ float f_envelope(const FastLaw& law, float s) {
     return law.c * s;
 }
 
-// CAP = shared-memory records reserved for the halo (+1 for the dummy record
-// at position 0 that dead/padding slots point at: it sits 1e15 away, carries
-// zero volume and the no-failure flag, so it contributes exactly 0 and never
-// breaks -- the slot loop needs no branch).
-template <int MODE, bool GENERAL, int CAP>
-__global__ void __launch_bounds__(FAST_T, (CAP <= 3072 ? 2 : 1)) fast_step_kernel(DevArgs A, FastDev F) {
+// Shared-memory records (CAP reserved per array; position 0 is a dummy that
+// dead/padding slots point at -- 1e18 away with zero volume, so its
+// contribution is 0 (or ~1e-18 relative with a uniform volume) and its stretch
+// never reaches s_c; the slot loop needs no branch):
+//   sA[p] = {x, y, ux, uy} - (O_t, U_t)  LDS.128 (x/y pairs feed FADD2 directly)
+//   sB[p] = {z, uz} - (O_t, U_t)         LDS.64
+//   sV[p] = c * V_j (PMB) or V_j         LDS.32, only when volumes differ
+// = 24 B per bond with uniform volumes, 28 B otherwise.  A slot stores the
+// byte offset 8*p of its neighbour's sB record (sA is at 16*p); no-failure
+// neighbours are staged last, so "offset >= nf_start" flags them.
+//
+// KIND 0: single PMB law, uniform volume, no no-failure node (c*V constant)
+// KIND 1: single PMB law, per-node volume and/or no-failure nodes
+// KIND 2: general -- bond types, n-linear laws with fp32 history, lambda, beta
+template <int MODE, int KIND, int CAP>
+__global__ void __launch_bounds__(FAST_T, (CAP <= 4096 ? 2 : 1))
+    fast_step_kernel(DevArgs A, FastDev F) {
     if (MODE != 0 && *(volatile long long*)A.err_step != kNoError)
         return;
     extern __shared__ float4 smem[];
+    float4* sA = smem;
+    float2* sB = reinterpret_cast<float2*>(smem + CAP);
+    float* sV = reinterpret_cast<float*>(sB + CAP);
+    const char* cA = reinterpret_cast<const char*>(sA);
+    const char* cB = reinterpret_cast<const char*>(sB);
+    const char* cV = reinterpret_cast<const char*>(sV);
     const int tile = F.tile0 + int(blockIdx.x);
     const int ts = F.tile_start[tile];
     const int te = F.tile_start[tile + 1];
     const long long h0 = F.halo_off[tile];
     const int H = int(F.halo_off[tile + 1] - h0);
-    float4* sx = smem;        // {x - O_t, c*V (PMB) or V}
-    float4* su = smem + CAP;  // {u - U_t, no_fail}
 
-    // 1. stage the halo in tile-local fp32 coordinates
-    const double4 O = A.xv[ts];
-    const double4 U0 = A.u_in[ts];
-    const double vscale = GENERAL ? 1.0 : double(F.pmb_c);
-    if (threadIdx.x == 0) {
-        sx[0] = make_float4(1e15f, 0.f, 0.f, 0.f);
-        su[0] = make_float4(0.f, 0.f, 0.f, 1.f);
-    }
-    for (int h = threadIdx.x; h < H; h += blockDim.x) {
-        const int id = F.halo[h0 + h];
-        const double4 x = A.xv[id];
-        const double4 u = A.u_in[id];
-        sx[h + 1] = make_float4(float(x.x - O.x), float(x.y - O.y), float(x.z - O.z),
-                                float(x.w * vscale));
-        su[h + 1] = make_float4(float(u.x - U0.x), float(u.y - U0.y), float(u.z - U0.z),
-                                float(u.w));
-    }
-    __syncthreads();
-
+    // the first slot-index groups stream in while the halo is staged; they are a
+    // read-once stream (evict-first, so the halo's x/u stay in L2)
     const int t = threadIdx.x;
     const long long i = ts + t;
-    if (i >= te)
+    const bool active = i < te;
+    unsigned short* lrow = F.lidx + F.slot_off[tile] + (long long)t * 8;
+    const int nkb = active ? (F.kmax8[tile] >> 3) : 0;
+    const long long kstride = (long long)F.T * 8;
+    uint4 wnext = nkb > 0 ? __ldcs(reinterpret_cast<const uint4*>(lrow)) : make_uint4(0, 0, 0, 0);
+    uint4 wnext2 =
+        nkb > 1 ? __ldcs(reinterpret_cast<const uint4*>(lrow + kstride)) : make_uint4(0, 0, 0, 0);
+    const unsigned own_raw = active ? unsigned(F.own_slot[i]) : 0u;
+    const unsigned nf_start = KIND == 0 ? 0u : unsigned(F.nf_start[tile]);
+
+    // 1. stage the halo in tile-local fp32 coordinates (2 records in flight)
+    const double4 O = A.xv[ts];
+    const double4 U0 = A.u_in[ts];
+    const double vscale = KIND == 2 ? 1.0 : double(F.pmb_c);
+    if (threadIdx.x == 0) {
+        sA[0] = make_float4(1e18f, 0.f, 0.f, 0.f);
+        sB[0] = make_float2(0.f, 0.f);
+        if (KIND != 0)
+            sV[0] = 0.f;
+    }
+    for (int h = threadIdx.x; h < H; h += 2 * blockDim.x) {
+        int id[2];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int hh = h + r * int(blockDim.x);
+            id[r] = hh < H ? F.halo[h0 + hh] : -1;
+        }
+        double4 x[2], u[2];
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+            if (id[r] >= 0) {
+                x[r] = A.xv[id[r]];
+                u[r] = A.u_in[id[r]];
+            }
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+            if (id[r] >= 0) {
+                const int hh = h + r * int(blockDim.x) + 1;
+                sA[hh] = make_float4(float(x[r].x - O.x), float(x[r].y - O.y),
+                                     float(u[r].x - U0.x), float(u[r].y - U0.y));
+                sB[hh] = make_float2(float(x[r].z - O.z), float(u[r].z - U0.z));
+                if (KIND != 0)
+                    sV[hh] = float(x[r].w * vscale);
+            }
+    }
+    __syncthreads();
+    if (!active)
         return;
 
     // 2. the node's bonds
-    const int own = F.own_slot[i];
-    const float4 xi = sx[own];
-    const float4 ui = su[own];
-    const bool nfi = ui.w != 0.f;
-    const float sc_pmb = F.pmb_sc;
-    const float2 nxi = make_float2(-xi.x, -xi.y);
-    const float2 nui = make_float2(-ui.x, -ui.y);
+    const unsigned own = own_raw & 0x1FFFu;
+    const float4 ai = sA[own];
+    const float2 bi = sB[own];
+    const float2 nxi = make_float2(-ai.x, -ai.y);  // x/y in packed f32x2, z scalar
+    const float2 nui = make_float2(-ai.z, -ai.w);
+    const float xiz = bi.x, uiz = bi.y;
+    // a no-failure node's bonds never break: lift its critical stretch to +inf
+    const float sc_pmb = (own_raw & 0x8000u) ? __int_as_float(0x7f800000) : F.pmb_sc;
+    const bool nfi = (own_raw & 0x8000u) != 0;
+    const float cv_uniform = F.pmb_cv;
     float2 fxy = make_float2(0.f, 0.f);
     float fz = 0.f;
     int broke = 0;
-    unsigned short* lrow = F.lidx + F.slot_off[tile] + (long long)t * 8;
-    const int nkb = F.kmax8[tile] >> 3;
-    const long long kstride = (long long)F.T * 8;
-    uint4 wnext = nkb > 0 ? *reinterpret_cast<const uint4*>(lrow) : make_uint4(0, 0, 0, 0);
     for (int kb = 0; kb < nkb; ++kb, lrow += kstride) {
         const uint4 w = wnext;
-        if (kb + 1 < nkb)  // prefetch the next 8 slots while these compute
-            wnext = *reinterpret_cast<const uint4*>(lrow + kstride);
+        wnext = wnext2;
+        if (kb + 2 < nkb)
+            wnext2 = __ldcs(reinterpret_cast<const uint4*>(lrow + 2 * kstride));
         const unsigned words[4] = {w.x, w.y, w.z, w.w};
         unsigned bmask = 0;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            const unsigned li = (q & 1) ? (words[q >> 1] >> 16) : (words[q >> 1] & 0xFFFFu);
-            const float4 xr = sx[li];
-            const float4 ur = su[li];
-            // x/y in packed f32x2 (FADD2/FMUL2/FFMA2), z scalar
-            const float2 exy = __fadd2_rn(make_float2(xr.x, xr.y), nxi);
-            const float2 hxy = __fadd2_rn(make_float2(ur.x, ur.y), nui);
+            const unsigned offB = (q & 1) ? (words[q >> 1] >> 16) : (words[q >> 1] & 0xFFFFu);
+            const float4 ar = *reinterpret_cast<const float4*>(cA + 2 * offB);
+            const float2 br = *reinterpret_cast<const float2*>(cB + offB);
+            const float2 exy = __fadd2_rn(make_float2(ar.x, ar.y), nxi);
+            const float2 hxy = __fadd2_rn(make_float2(ar.z, ar.w), nui);
             const float2 cxy = __fadd2_rn(exy, hxy);
             const float2 sxy = __fadd2_rn(exy, cxy);
-            const float ez = xr.z - xi.z, hz = ur.z - ui.z;
+            const float ez = br.x - xiz, hz = br.y - uiz;
             const float cz = ez + hz;
             const float2 e2 = __fmul2_rn(exy, exy);
-            const float2 c2 = __fmul2_rn(cxy, cxy);
             const float2 n2 = __fmul2_rn(hxy, sxy);
             const float ref2 = fmaf(ez, ez, e2.x + e2.y);
-            const float cur2 = fmaf(cz, cz, c2.x + c2.y);
-            const float num = fmaf(hz, ez + cz, n2.x + n2.y);
-            const float cx = cxy.x, cy = cxy.y;
+            const float num = fmaf(hz, ez + cz, n2.x + n2.y);  // eta.(2 xi + eta)
+            const float cur2 = ref2 + num;                     // |xi + eta|^2
             const float rr = rsqrt_approx(ref2);
             const float rc = rsqrt_approx(cur2);
+            // s = (|cur| - |xi|) / |xi| = eta.(xi + cur) / (|xi| (|cur| + |xi|))
             const float s = num * rr * rcp_approx(cur2 * rc + ref2 * rr);
-            const bool no_fail = nfi || ur.w != 0.f;
             float f;
-            if (!GENERAL) {
-                if (s >= sc_pmb && !no_fail) {
+            if (KIND != 2) {
+                const bool brk = KIND == 0 ? (s >= sc_pmb) : (s >= sc_pmb && offB < nf_start);
+                if (brk) {
                     bmask |= 1u << q;  // stored after the 8 slots, off the hot path
                     continue;
                 }
-                f = s;  // c is folded into the staged volume
+                f = s * (KIND == 0 ? cv_uniform : *reinterpret_cast<const float*>(cV + (offB >> 1)));
             } else {
+                if (offB == 0)
+                    continue;  // broken/padding: its history must not re-trigger the break
+                const bool no_fail = nfi || offB >= nf_start;
                 const long long sidx = (lrow - F.lidx) + q;
                 const FastLaw& law = c_flaws[F.btype ? int(F.btype[sidx]) : 0];
                 if (no_fail) {
@@ -197,14 +242,13 @@ __global__ void __launch_bounds__(FAST_T, (CAP <= 3072 ? 2 : 1)) fast_step_kerne
                     f *= F.lambda[sidx];
                 if (F.beta)
                     f *= F.beta[sidx];
+                f *= *reinterpret_cast<const float*>(cV + (offB >> 1));
             }
-            const float scale = f * xr.w * rc;
+            const float scale = f * rc;
             fxy = __ffma2_rn(cxy, make_float2(scale, scale), fxy);
             fz = fmaf(cz, scale, fz);
-            (void)cx;
-            (void)cy;
         }
-        if (!GENERAL && bmask) {
+        if (KIND != 2 && bmask) {
             for (int q = 0; q < 8; ++q)
                 if (bmask >> q & 1u)
                     lrow[q] = 0;
@@ -224,27 +268,38 @@ __global__ void __launch_bounds__(FAST_T, (CAP <= 3072 ? 2 : 1)) fast_step_kerne
     node_epilogue<MODE>(A, i, A.u_in[i], double(fxy.x), double(fxy.y), double(fz));
 }
 
-template <int MODE, bool GENERAL, int CAP>
+template <int MODE, int KIND, int CAP>
 cudaError_t launch_cap(const DevArgs& A, const FastDev& F, int tiles, cudaStream_t st) {
     static bool configured = false;
-    const int smem = 2 * CAP * int(sizeof(float4));
+    const int smem = CAP * int(sizeof(float4) + sizeof(float2) + (KIND == 0 ? 0 : sizeof(float)));
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(fast_step_kernel<MODE, GENERAL, CAP>,
+        cudaError_t e = cudaFuncSetAttribute(fast_step_kernel<MODE, KIND, CAP>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess)
             return e;
         configured = true;
     }
-    fast_step_kernel<MODE, GENERAL, CAP><<<tiles, F.T, smem, st>>>(A, F);
+    fast_step_kernel<MODE, KIND, CAP><<<tiles, F.T, smem, st>>>(A, F);
     return cudaGetLastError();
 }
 
-template <int MODE, bool GENERAL>
+template <int MODE, int KIND>
 cudaError_t launch_one(const DevArgs& A, const FastDev& F, int tiles, int max_halo,
                        cudaStream_t st) {
-    if (max_halo + 1 <= 3072)
-        return launch_cap<MODE, GENERAL, 3072>(A, F, tiles, st);
-    return launch_cap<MODE, GENERAL, FAST_MAX_HALO + 1>(A, F, tiles, st);
+    if (max_halo + 1 <= 4096)
+        return launch_cap<MODE, KIND, 4096>(A, F, tiles, st);
+    return launch_cap<MODE, KIND, FAST_MAX_HALO + 1>(A, F, tiles, st);
+}
+
+template <int KIND>
+cudaError_t launch_kind(const DevArgs& A, const FastDev& F, int mode, int tiles, int max_halo,
+                        cudaStream_t st) {
+    switch (mode) {
+    case 0: return launch_one<0, KIND>(A, F, tiles, max_halo, st);
+    case 1: return launch_one<1, KIND>(A, F, tiles, max_halo, st);
+    case 2: return launch_one<2, KIND>(A, F, tiles, max_halo, st);
+    default: return launch_one<3, KIND>(A, F, tiles, max_halo, st);
+    }
 }
 
 // ---- layout permutation / materialisation kernels ---------------------------
@@ -294,24 +349,15 @@ __global__ void fast_materialize_kernel(const int32_t* entries0, const int* inv,
 
 } // namespace
 
-cudaError_t launch_fast(const DevArgs& A, const FastDev& F, int mode, bool general, int tiles,
+cudaError_t launch_fast(const DevArgs& A, const FastDev& F, int mode, int kind, int tiles,
                         int max_halo, cudaStream_t st) {
     if (tiles <= 0)
         return cudaSuccess;
-    if (general) {
-        switch (mode) {
-        case 0: return launch_one<0, true>(A, F, tiles, max_halo, st);
-        case 1: return launch_one<1, true>(A, F, tiles, max_halo, st);
-        case 2: return launch_one<2, true>(A, F, tiles, max_halo, st);
-        default: return launch_one<3, true>(A, F, tiles, max_halo, st);
-        }
-    }
-    switch (mode) {
-    case 0: return launch_one<0, false>(A, F, tiles, max_halo, st);
-    case 1: return launch_one<1, false>(A, F, tiles, max_halo, st);
-    case 2: return launch_one<2, false>(A, F, tiles, max_halo, st);
-    default: return launch_one<3, false>(A, F, tiles, max_halo, st);
-    }
+    if (kind == 0)
+        return launch_kind<0>(A, F, mode, tiles, max_halo, st);
+    if (kind == 1)
+        return launch_kind<1>(A, F, mode, tiles, max_halo, st);
+    return launch_kind<2>(A, F, mode, tiles, max_halo, st);
 }
 
 template <class T, int W>
@@ -345,7 +391,8 @@ void launch_fast_materialize(const int32_t* entries0, const int* inv, const int*
 
 int fast_build_layout(FastHostLayout& L, int64_t n, int N, const int32_t* entries,
                       const double* coords, const uint8_t* btype, const double* lambda,
-                      const double* beta, const double* hist, bool history) {
+                      const double* beta, const double* hist, bool history,
+                      const uint8_t* nofail) {
     // bricks of ~8 nodes per axis from the bounding box and mean spacing
     double lo[3], hi[3];
     for (int d = 0; d < 3; ++d)
@@ -371,9 +418,11 @@ int fast_build_layout(FastHostLayout& L, int64_t n, int N, const int32_t* entrie
         nb[d] = ext[d] > 0 ? std::max(1LL, (long long)std::llround(ext[d] / (8.0 * h))) : 1;
         len[d] = ext[d] > 0 ? ext[d] / double(nb[d]) : 1.0;
     }
-    // lattice-like axes (few distinct coordinates): bricks of exactly 8 grid
-    // planes, so warps cover whole 8-node x-runs and neighbour runs stay
-    // bank-aligned; otherwise bins of ~8 mean spacings
+    // lattice-like axes (few distinct coordinates): bricks of exactly 16 x 4 x 8
+    // grid planes, so a half-warp covers a whole 16-node x-run and its
+    // neighbour runs are contiguous shared-memory records (conflict-free
+    // LDS.64 over 16 lanes, LDS.128 over 8); otherwise bins of ~8 mean spacings
+    const long long kBrick[3] = {16, 4, 8};
     std::unordered_map<double, long long> rank[3];
     bool lattice[3] = {false, false, false};
     for (int d = 0; d < 3; ++d) {
@@ -390,7 +439,7 @@ int fast_build_layout(FastHostLayout& L, int64_t n, int N, const int32_t* entrie
         for (size_t k = 0; k < sorted.size(); ++k)
             rank[d][sorted[k]] = (long long)k;
         lattice[d] = true;
-        nb[d] = (long long)(sorted.size() + 7) / 8;
+        nb[d] = (long long)(sorted.size() + kBrick[d] - 1) / kBrick[d];
     }
     const long long nbricks = nb[0] * nb[1] * nb[2];
     std::vector<long long> brick(static_cast<size_t>(n));
@@ -400,7 +449,7 @@ int fast_build_layout(FastHostLayout& L, int64_t n, int N, const int32_t* entrie
         for (int d = 0; d < 3; ++d) {
             long long c;
             if (lattice[d])
-                c = rank[d][coords[3 * i + d]] / 8;
+                c = rank[d][coords[3 * i + d]] / kBrick[d];
             else
                 c = ext[d] > 0 ? (long long)std::floor((coords[3 * i + d] - lo[d]) / len[d]) : 0;
             b[d] = std::min(std::max(c, 0LL), nb[d] - 1);
@@ -440,7 +489,7 @@ int fast_build_layout(FastHostLayout& L, int64_t n, int N, const int32_t* entrie
         std::vector<unsigned short> lidx;
         std::vector<float> hist, lambda, beta;
         std::vector<uint8_t> btype;
-        int kmax8 = 0;
+        int kmax8 = 0, nf_start = 0x7fffffff;
     };
     std::vector<TileOut> out(static_cast<size_t>(tiles));
     int error = 0;
@@ -466,21 +515,41 @@ int fast_build_layout(FastHostLayout& L, int64_t n, int N, const int32_t* entrie
             }
             // shared-memory order = reference (original) node order: on a lattice an
             // x-run of neighbours stays contiguous across brick boundaries, so a
-            // quarter-warp's 16-byte loads hit distinct banks
+            // quarter-warp's 16-byte loads hit distinct banks.  No-failure nodes go
+            // last so a slot offset >= nf_start identifies them.
             for (int& id : ids)
                 id = L.perm[size_t(id)];
             std::sort(ids.begin(), ids.end());
             ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
-            if (ids.size() > size_t(FAST_MAX_HALO)) {
+            if (nofail)
+                std::stable_partition(ids.begin(), ids.end(),
+                                      [&](int j) { return nofail[j] == 0; });
+            if (ids.size() + 1 > size_t(FAST_MAX_HALO + 1)) {
                 error = 1;
                 continue;
             }
+            o.nf_start = 0x7fffffff;
+            size_t split = ids.size();  // ids[0, split) regular, [split, end) no-failure
             o.halo.resize(ids.size());
-            for (size_t q = 0; q < ids.size(); ++q)
+            for (size_t q = 0; q < ids.size(); ++q) {
                 o.halo[q] = L.inv[size_t(ids[q])];
-            for (int ii = ts; ii < te; ++ii)
-                L.own_slot[size_t(ii)] = (unsigned short)(
-                    1 + (std::lower_bound(ids.begin(), ids.end(), L.perm[size_t(ii)]) - ids.begin()));
+                if (nofail && nofail[ids[q]] && split == ids.size()) {
+                    split = q;
+                    o.nf_start = 8 * (int(q) + 1);
+                }
+            }
+            // shared-memory position (halo index + 1) of reference node j
+            auto pos_of = [&](int j) {
+                const bool nf = nofail && nofail[j];
+                auto lo = nf ? ids.begin() + std::ptrdiff_t(split) : ids.begin();
+                auto hi = nf ? ids.end() : ids.begin() + std::ptrdiff_t(split);
+                return int(std::lower_bound(lo, hi, j) - ids.begin()) + 1;
+            };
+            for (int ii = ts; ii < te; ++ii) {
+                const int orig = L.perm[size_t(ii)];
+                L.own_slot[size_t(ii)] = (unsigned short)(pos_of(orig) |
+                                                          ((nofail && nofail[orig]) ? 0x8000 : 0));
+            }
             o.kmax8 = (kmax + 7) / 8 * 8;
             const size_t slots = size_t(o.kmax8) * FAST_T;
             o.lidx.assign(slots, 0);
@@ -501,8 +570,7 @@ int fast_build_layout(FastHostLayout& L, int64_t n, int N, const int32_t* entrie
                     if (j < 0)
                         continue;
                     const size_t s = size_t(c >> 3) * FAST_T * 8 + size_t(tt) * 8 + size_t(c & 7);
-                    o.lidx[s] = (unsigned short)(1 + (std::lower_bound(ids.begin(), ids.end(), j) -
-                                                      ids.begin()));
+                    o.lidx[s] = (unsigned short)(8 * pos_of(j));
                     const int64_t idx = i * N + k;
                     if (history)
                         o.hist[s] = hist ? float(hist[idx]) : 0.f;
@@ -531,6 +599,7 @@ int fast_build_layout(FastHostLayout& L, int64_t n, int N, const int32_t* entrie
         return 1;
 
     L.halo_off.assign(size_t(tiles + 1), 0);
+    L.nf_start.assign(size_t(tiles), 0x7fffffff);
     L.slot_off.assign(size_t(tiles), 0);
     L.kmax8.assign(size_t(tiles), 0);
     long long slots = 0;
@@ -540,6 +609,7 @@ int fast_build_layout(FastHostLayout& L, int64_t n, int N, const int32_t* entrie
         L.slot_off[size_t(t)] = slots;
         slots += (long long)out[size_t(t)].lidx.size();
         L.kmax8[size_t(t)] = out[size_t(t)].kmax8;
+        L.nf_start[size_t(t)] = out[size_t(t)].nf_start;
         L.max_halo = std::max(L.max_halo, int(out[size_t(t)].halo.size()));
     }
     L.total_slots = slots;

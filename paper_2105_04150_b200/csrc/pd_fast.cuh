@@ -7,9 +7,10 @@
 //                                       reference (owned nodes included), staged
 //                                       into shared memory once per step as
 //                                       fp32 {x - O_t, V} and {u - U_t, no_fail}
-//   lidx   uint16 per live slot          shared-memory index of the neighbour
-//                                       (halo position + 1); 0 = broken or
-//                                       padding (a dummy record that adds 0).  Slot c of
+//   lidx   uint16 per live slot          bits 0-14: shared-memory index of the
+//                                       neighbour (halo position + 1); 0 = broken
+//                                       or padding (a dummy record that adds 0);
+//                                       bit 15: the neighbour is a no-fail node.  Slot c of
 //                                       tile-thread t lives at
 //                                       slot_off[t] + (c/8)*T*8 + t*8 + c%8, so
 //                                       one 16-byte load fetches 8 slots and a
@@ -23,7 +24,7 @@
 namespace pdb {
 
 constexpr int FAST_T = 512;           // threads (= owned nodes) per tile
-constexpr int FAST_MAX_HALO = 6400;   // (6400 + 1) * 32 B = 200 KB of shared memory
+constexpr int FAST_MAX_HALO = 7000;   // (7000 + 1) * 28 B = 196 KB of shared memory; 8*(7000+1) < 65536
 
 struct FastDev {
     int T;
@@ -34,13 +35,16 @@ struct FastDev {
     const int* halo;           // internal ids
     const long long* slot_off; // n_tiles
     const int* kmax8;          // per tile, multiple of 8
-    const unsigned short* own_slot; // shared-memory position of each (internal) node in its tile
+    const unsigned short* own_slot; // shared-memory position of each (internal) node in its tile,
+                                    // bit 15 = the node is a no-failure node
+    const int* nf_start;       // per tile: first slot offset that names a no-failure node
     unsigned short* lidx;
     float* hist;               // compact fp32 history (n-linear laws)
     const uint8_t* btype;      // compact bond types or NULL
     const float* lambda;       // compact or NULL
     const float* beta;         // compact or NULL
     float pmb_c, pmb_sc;       // the single-PMB-law specialisation
+    float pmb_cv;              // c * V when every volume is equal (KIND 0)
 };
 
 struct FastLaw {

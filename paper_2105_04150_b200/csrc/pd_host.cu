@@ -173,7 +173,7 @@ struct pd_ctx {
     int cur = 0;
 
     DevBuf<double4> xv, u[2];
-    DevBuf<double> v, a, rho, hist, lambda, beta, body, ext;
+    DevBuf<double> v, a, rho, inv_rho, hist, lambda, beta, body, ext;
     DevBuf<int32_t> entries, n_neigh, initial, scratch_i32;
     DevBuf<uint32_t> alive;
     DevBuf<uint8_t> btype, bc_kind, bc_ramp, nofail;
@@ -187,10 +187,10 @@ struct pd_ctx {
 
     // fast path (PD_FAST): internal brick order + tile layout (pd_fast.cuh)
     bool fast = false;
-    bool general = false;
-    float pmb_c = 0, pmb_sc = 0;
+    int kind = 2;  // fast kernel specialisation (pd_fast.cu)
+    float pmb_c = 0, pmb_sc = 0, pmb_cv = 0;
     int n_tiles = 0, max_halo = 0;
-    DevBuf<int> perm, inv, tile_of, tile_start, kmax8, halo;
+    DevBuf<int> perm, inv, tile_of, tile_start, kmax8, halo, nf_start;
     DevBuf<unsigned short> own_slot;
     DevBuf<long long> halo_off, slot_off;
     DevBuf<unsigned short> lidx;
@@ -211,6 +211,7 @@ struct pd_ctx {
         F.slot_off = slot_off.p;
         F.kmax8 = kmax8.p;
         F.own_slot = own_slot.p;
+        F.nf_start = nf_start.p;
         F.lidx = lidx.p;
         F.hist = hist32.p;
         F.btype = btype_c.p;
@@ -218,6 +219,7 @@ struct pd_ctx {
         F.beta = beta32.p;
         F.pmb_c = pmb_c;
         F.pmb_sc = pmb_sc;
+        F.pmb_cv = pmb_cv;
         return F;
     }
 
@@ -236,6 +238,7 @@ struct pd_ctx {
         A.v = v.p;
         A.a = a.p;
         A.rho = rho.p;
+        A.inv_rho = inv_rho.p;
         A.entries = entries.p;
         A.alive = alive.p;
         A.n_neigh = n_neigh.p;
@@ -252,6 +255,9 @@ struct pd_ctx {
         A.err_step = err.p;
         A.step = step;
         A.dt = dt;
+        A.half_dt = dt / 2;
+        A.half_dt2 = dt * dt / 2;
+        A.dt2 = dt * dt;
         A.damping = damping;
         A.store_forces = 0;
         A.do_drift = 0;
@@ -329,6 +335,9 @@ int upload_common(pd_ctx* ctx, const pd_particles& p, const pd_state& st,
     if (p.density && p.density_size == n)
         PD_CK(cudaMemcpyAsync(ctx->rho.p, p.density, sizeof(double) * n, cudaMemcpyHostToDevice,
                               s));
+    PD_CK(ctx->inv_rho.alloc(size_t(n)));
+    launch_inv(ctx->rho.p, n, ctx->inv_rho.p, s);  // Real(1) / density[i] (engine.cpp:244)
+    ++ctx->launches;
 
     // u = {ux, uy, uz, no_failure}
     PD_CK(ctx->scratch_f64.upload(st.u, size_t(3 * n), s));
@@ -535,7 +544,8 @@ int download(pd_ctx* ctx, pd_state* st, pd_force_field* forces, int32_t fields) 
 // Renumber the resident node arrays into the fast path's brick order and
 // build its tile layout from the host copies of the rows.
 int setup_fast(pd_ctx* ctx, const pd_particles& p, const pd_state& st,
-               const pd_damage_model& m, const pd_corrections& corr, pd_boundary* bc_tips) {
+               const pd_damage_model& m, const pd_corrections& corr, const uint8_t* nofail,
+               int64_t nofail_size, pd_boundary* bc_tips) {
     cudaStream_t s = ctx->stream;
     const int64_t n = ctx->n;
     FastHostLayout L;
@@ -545,7 +555,8 @@ int setup_fast(pd_ctx* ctx, const pd_particles& p, const pd_state& st,
                           st.connectivity.bond_type_size ? st.connectivity.bond_type : nullptr,
                           corr.lambda_size ? corr.lambda : nullptr,
                           corr.beta_size ? corr.beta : nullptr,
-                          hist_in ? st.bond_history : nullptr, ctx->history) != 0)
+                          hist_in ? st.bond_history : nullptr, ctx->history,
+                          nofail_size == n ? nofail : nullptr) != 0)
         return fail(PD_E_INVALID_ARGUMENT,
                     "PD_FAST: a tile neighbourhood exceeds %d nodes of shared memory; use "
                     "PD_BOND_PARALLEL for this mesh", FAST_MAX_HALO);
@@ -557,6 +568,7 @@ int setup_fast(pd_ctx* ctx, const pd_particles& p, const pd_state& st,
     PD_CK(ctx->tile_start.upload(L.tile_start.data(), L.tile_start.size(), s));
     PD_CK(ctx->kmax8.upload(L.kmax8.data(), L.kmax8.size(), s));
     PD_CK(ctx->own_slot.upload(L.own_slot.data(), L.own_slot.size(), s));
+    PD_CK(ctx->nf_start.upload(L.nf_start.data(), L.nf_start.size(), s));
     PD_CK(ctx->halo.upload(L.halo.data(), L.halo.size(), s));
     PD_CK(ctx->halo_off.upload(L.halo_off.data(), L.halo_off.size(), s));
     PD_CK(ctx->slot_off.upload(L.slot_off.data(), L.slot_off.size(), s));
@@ -587,6 +599,7 @@ int setup_fast(pd_ctx* ctx, const pd_particles& p, const pd_state& st,
     launch_gather_rows<double, 1>(ctx->rho.p, ctx->scratch_f64.p, perm, n, s);
     PD_CK(cudaMemcpyAsync(ctx->rho.p, ctx->scratch_f64.p, sizeof(double) * n,
                           cudaMemcpyDeviceToDevice, s));
+    launch_inv(ctx->rho.p, n, ctx->inv_rho.p, s);
     PD_CK(ctx->scratch_n.alloc(size_t(n)));
     for (int32_t* arr : {ctx->n_neigh.p, ctx->initial.p}) {
         launch_gather_rows<int32_t, 1>(arr, ctx->scratch_n.p, perm, n, s);
@@ -613,10 +626,18 @@ int setup_fast(pd_ctx* ctx, const pd_particles& p, const pd_state& st,
         PD_CK(ctx->tip_nodes.upload(nodes.data(), nodes.size(), s));
     }
     // the single-PMB-law specialisation needs no per-slot law data
-    ctx->general = m.n_laws > 1 || ctx->history || !L.btype.empty() || !L.lambda.empty() ||
-                   !L.beta.empty();
+    const bool general = m.n_laws > 1 || ctx->history || !L.btype.empty() || !L.lambda.empty() ||
+                         !L.beta.empty();
+    bool uniform = true;
+    for (int64_t i = 1; i < n && uniform; ++i)
+        uniform = p.volume[i] == p.volume[0];
+    bool any_nofail = false;
+    for (int64_t i = 0; i < n && nofail_size == n && !any_nofail; ++i)
+        any_nofail = nofail[i] != 0;
+    ctx->kind = general ? 2 : ((uniform && !any_nofail) ? 0 : 1);
     ctx->pmb_c = float(m.laws[0].stiffness);
     ctx->pmb_sc = float(m.laws[0].breakpoints[0]);
+    ctx->pmb_cv = float(m.laws[0].stiffness * p.volume[0]);
     std::vector<DevLaw> laws(size_t(m.n_laws));
     for (int k = 0; k < m.n_laws; ++k) {
         std::memset(&laws[size_t(k)], 0, sizeof(DevLaw));
@@ -636,7 +657,7 @@ int setup_fast(pd_ctx* ctx, const pd_particles& p, const pd_state& st,
 
 int launch_step(pd_ctx* ctx, DevArgs& A, int mode) {
     if (ctx->fast) {
-        PD_CK(launch_fast(A, ctx->fast_args(), mode, ctx->general, ctx->n_tiles, ctx->max_halo,
+        PD_CK(launch_fast(A, ctx->fast_args(), mode, ctx->kind, ctx->n_tiles, ctx->max_halo,
                           ctx->stream));
         ++ctx->launches;
         return PD_OK;
@@ -884,7 +905,8 @@ int pd_ctx_upload(pd_ctx* ctx, const pd_bundle* b, const pd_state* st, int32_t v
     PD_TRY(upload_bc(ctx, b->bc));
     if (variant == PD_FAST) {
         pd_boundary bc = b->bc;
-        PD_TRY(setup_fast(ctx, b->particles, *st, b->model, b->corrections, &bc));
+        PD_TRY(setup_fast(ctx, b->particles, *st, b->model, b->corrections, b->bc.no_failure,
+                          b->bc.no_failure_size, &bc));
     }
     ctx->variant = variant;
     ctx->dt = b->dt;
@@ -1000,7 +1022,8 @@ int pd_compute_forces(int32_t variant, pd_state* state, const pd_particles* part
     PD_TRY(upload_common(ctx, *particles, st, *model, *corr, corr->no_failure,
                          corr->no_failure_size));
     if (variant == PD_FAST)
-        PD_TRY(setup_fast(ctx, *particles, st, *model, *corr, nullptr));
+        PD_TRY(setup_fast(ctx, *particles, st, *model, *corr, corr->no_failure,
+                          corr->no_failure_size, nullptr));
     ctx->variant = variant;
     DevArgs A = ctx->args();
     PD_TRY(launch_step(ctx, A, 0));

@@ -49,7 +49,7 @@ int set_error(int code, const char* msg);
 struct FastHostLayout {
     int T = 0, n_tiles = 0, max_halo = 0;
     long long total_slots = 0;
-    std::vector<int> perm, inv, tile_of, tile_start, kmax8, halo;
+    std::vector<int> perm, inv, tile_of, tile_start, kmax8, halo, nf_start;
     std::vector<unsigned short> own_slot;
     std::vector<long long> halo_off, slot_off;
     std::vector<unsigned short> lidx;
@@ -58,9 +58,10 @@ struct FastHostLayout {
 };
 int fast_build_layout(FastHostLayout& L, int64_t n, int N, const int32_t* entries,
                       const double* coords, const uint8_t* btype, const double* lambda,
-                      const double* beta, const double* hist, bool history);
+                      const double* beta, const double* hist, bool history,
+                      const uint8_t* nofail);
 void fast_set_laws(const DevLaw* laws, int n, cudaStream_t stream);
-cudaError_t launch_fast(const DevArgs& A, const FastDev& F, int mode, bool general, int tiles,
+cudaError_t launch_fast(const DevArgs& A, const FastDev& F, int mode, int kind, int tiles,
                         int max_halo, cudaStream_t st);
 template <class T, int W>
 void launch_gather_rows(const T* in, T* out, const int* map, long long n, cudaStream_t st);
@@ -91,6 +92,7 @@ void launch_materialize_entries(const int32_t* entries, const uint32_t* alive, l
 void launch_damage(const int32_t* n_neigh, const int32_t* initial, long long n, double* phi,
                    cudaStream_t st);
 void launch_sum(const int32_t* x, long long n, unsigned long long* out, cudaStream_t st);
+void launch_inv(const double* x, long long n, double* out, cudaStream_t st);
 void launch_tips(const double4* u, const double* v, const double* a, const double4* xv,
                  const double* body, const double* ext, int n_sets, const long long* offsets,
                  const long long* nodes, long long step, pd_tip_record* out, cudaStream_t st);

@@ -103,6 +103,9 @@ def test_fast_plate_trajectory_matches_oracle(oracle, integrator):
     assert broken_a > 0
     assert abs(int(broken_a) - int(broken_f)) <= max(2, 0.02 * broken_a)
     assert set(ra.tips) == set(rf.tips)
+    # n_neigh stays the live count of the materialised row (no double counting)
+    live = (f.connectivity.entries.reshape(fam.node_count(), -1) >= 0).sum(1)
+    assert np.array_equal(f.connectivity.n_neigh, live)
 
 
 def test_fast_multimaterial_general_path(oracle):

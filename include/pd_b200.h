@@ -268,6 +268,46 @@ int64_t pd_ctx_launch_count(pd_ctx* ctx);
 /* Live directed bonds in the resident alive mask (sum of n_neigh). */
 int64_t pd_ctx_live_bonds(pd_ctx* ctx);
 
+/* ---- multi-GPU z-slabs (no reference counterpart: the reference is one
+ * process) ------------------------------------------------
+ *
+ * One pd_ctx per GPU (per rank) holds that rank's LOCAL model: its owned nodes
+ * plus a ghost layer one horizon deep, in a numbering where the owned nodes
+ * are the contiguous range [own_begin, own_end).  Rows of owned nodes are the
+ * global rows with their slot order kept (so parity mode stays bitwise equal
+ * to one GPU); ghost rows are ignored.  Each time step the fused step kernel
+ * stores the new displacement of every owned node that is a ghost on a
+ * neighbouring rank straight into that rank's u buffer over NVLink (peer
+ * stores), then a one-thread sync kernel publishes the step (and the rank's
+ * non-finite flag) to every rank and waits until all ranks have published it.
+ * Host code only exchanges the pd_peer_handle records once (any transport,
+ * e.g. torch.distributed). */
+#define PD_MAX_RANKS 16
+
+typedef struct pd_peer_handle {
+    int32_t device; /* CUDA device ordinal in the owning process */
+    int32_t pid;    /* owning process id (same pid: raw pointers, else CUDA IPC) */
+    uint8_t ipc_u0[64], ipc_u1[64], ipc_sync[64]; /* cudaIpcMemHandle_t */
+    uint64_t u0, u1, sync; /* raw device pointers in the owning process */
+} pd_peer_handle;
+
+/* pd_ctx_upload for a rank's local model; only [own_begin, own_end) is
+ * integrated.  Requires variant PD_BOND_PARALLEL, PD_NODE_PARALLEL or PD_FAST. */
+int pd_ctx_upload_part(pd_ctx* ctx, const pd_bundle* bundle, const pd_state* state,
+                       int32_t variant, int64_t own_begin, int64_t own_end);
+/* Device row index of local nodes (PD_FAST renumbers nodes into bricks). */
+int pd_ctx_internal_index(pd_ctx* ctx, const int64_t* local, int64_t count, int64_t* out);
+int pd_ctx_export(pd_ctx* ctx, pd_peer_handle* out);
+/* Join a world of `world` ranks (peers[world], this rank's entry ignored).
+ * send_lo / send_hi (length n_local, indexed by LOCAL node id): the device row
+ * index on rank lo / hi of each owned node that is a ghost there, else -1
+ * (lo or hi = -1 when there is no such neighbour). */
+int pd_ctx_connect(pd_ctx* ctx, int32_t rank, int32_t world, const pd_peer_handle* peers,
+                   int32_t lo, int32_t hi, const int64_t* send_lo, const int64_t* send_hi);
+/* u, v, a of the listed local nodes, plus body/external force x V of the
+ * last write step, 15 doubles per node (multi-rank tip records). */
+int pd_ctx_node_values(pd_ctx* ctx, const int64_t* local, int64_t count, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -188,6 +188,10 @@ inline void compute_forces(KernelVariant variant, SimulationState& state,
                            const ParticleSet& particles, const DamageModel& model,
                            const Corrections& corrections, ForceField& out, bool fast = false) {
     const Index n = state.size();
+    // memory safety of the flat views handed to the C ABI (the reference
+    // indexes these without a check)
+    if (Index(state.u.size()) != 3 * n)
+        throw std::invalid_argument("compute_forces: displacement array does not match node count");
     if (Index(out.body_force.size()) != 3 * n)
         out.body_force.assign(std::size_t(3 * n), 0);
     if (Index(out.external_force.size()) != 3 * n)
@@ -212,6 +216,10 @@ inline SimulateResult simulate(const ModelBundle& bundle, SimulationState& state
     if (bundle.model.needs_history() &&
         state.bond_history.size() != state.connectivity.entries.size())
         state.bond_history.assign(state.connectivity.entries.size(), 0);  // engine.cpp:382-384
+    const Index n = state.size();
+    if (Index(state.u.size()) != 3 * n || Index(state.v.size()) != 3 * n ||
+        Index(state.a.size()) != 3 * n)
+        throw std::invalid_argument("simulate: state fields do not match node count");
     detail::Laws laws(bundle.model);
     detail::Boundary bc(bundle.bc);
     pd_bundle b{};

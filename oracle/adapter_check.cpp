@@ -191,17 +191,27 @@ void error_mapping() {
         gpu_msg = e.what();
     }
     report("non-finite u -> runtime_error '" + gpu_msg + "'", !ref_msg.empty() && ref_msg == gpu_msg);
-    bool ok = false;
+    // a corrections array of the wrong size: same exception type and message
+    ref_msg.clear();
+    gpu_msg.clear();
+    RandomConfig good = make_random_config(1001);
+    good.corrections.lambda.assign(7, 1.0);
     try {
-        SimulationState s = cfg.state;
-        s.u.resize(3);
-        peridyn::b200::compute_forces(KernelVariant::bond_parallel, s, cfg.particles, cfg.model,
-                                      cfg.corrections, f);
-    } catch (const std::invalid_argument&) {
-        ok = true;
-    } catch (...) {
+        SimulationState s = good.state;
+        peridyn::compute_forces(KernelVariant::bond_parallel, s, good.particles, good.model,
+                                good.corrections, f);
+    } catch (const std::invalid_argument& e) {
+        ref_msg = e.what();
     }
-    report("size mismatch -> invalid_argument", ok);
+    try {
+        SimulationState s = good.state;
+        peridyn::b200::compute_forces(KernelVariant::bond_parallel, s, good.particles, good.model,
+                                      good.corrections, f);
+    } catch (const std::invalid_argument& e) {
+        gpu_msg = e.what();
+    }
+    const bool ok = !ref_msg.empty() && ref_msg == gpu_msg;
+    report("lambda size mismatch -> invalid_argument '" + gpu_msg + "'", ok);
 }
 
 } // namespace

@@ -25,7 +25,7 @@ UNITS = {
     "pd_exact.cu": ["-fmad=false"],
     "pd_aux.cu": ["-fmad=false"],
     "pd_host.cu": ["-fmad=false"],
-    "pd_fast.cu": ["-fmad=true"],
+    "pd_fast.cu": ["-fmad=true", "-diag-suppress=186"],
     "pd_family.cu": ["-fmad=false"],
 }
 HEADERS = ["pd_device.cuh", "pd_internal.h", "pd_fast.cuh"]

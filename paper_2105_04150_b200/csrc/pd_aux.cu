@@ -84,9 +84,60 @@ __global__ void vv_prologue_kernel(DevArgs A) {
             un[ax] = __dmul_rn(A.bc_mag[3 * i + ax], ramp_scale(A.ramps[A.bc_ramp[3 * i + ax]],
                                                                 A.step + 1));
     }
-    A.u_out[i] = make_double4(un[0], un[1], un[2], u.w);
+    const double4 unew = make_double4(un[0], un[1], un[2], u.w);
+    A.u_out[i] = unew;
+    push_ghost(A, i, unew);
     if (!finite3(un[0], un[1], un[2]))
         atomicMin((unsigned long long*)A.err_step, (unsigned long long)A.step);
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Slab barrier after a step (one thread): publish this rank's non-finite flag
+// and the epoch to every rank's sync words, wait until every rank has
+// published the epoch, then adopt the smallest flag so all ranks stop at the
+// same step (the reference throws in the force pass of that step).
+// sync words of a rank: [0, PD_MAX_RANKS) epochs, [PD_MAX_RANKS, 2*PD_MAX_RANKS) flags.
+__global__ void slab_sync_kernel(SyncArgs S) {
+    if (threadIdx.x != 0 || blockIdx.x != 0)
+        return;
+    const long long mine = *(volatile long long*)S.err_step;
+    __threadfence_system();
+    for (int p = 0; p < S.world; ++p)
+        *(volatile unsigned long long*)(S.peer_sync[p] + PD_MAX_RANKS + S.rank) =
+            (unsigned long long)mine;
+    __threadfence_system();
+    for (int p = 0; p < S.world; ++p)
+        st_release_sys(S.peer_sync[p] + S.rank, S.epoch);
+    const unsigned long long t0 = globaltimer();
+    long long merged = mine;
+    for (int q = 0; q < S.world; ++q) {
+        while (ld_acquire_sys(S.my_sync + q) < S.epoch) {
+            if (globaltimer() - t0 > (unsigned long long)S.timeout_ns) {
+                *(volatile long long*)S.err_step = kPeerTimeout;
+                return;
+            }
+            __nanosleep(200);
+        }
+        const long long e = (long long)ld_acquire_sys(S.my_sync + PD_MAX_RANKS + q);
+        merged = e < merged ? e : merged;
+    }
+    if (merged != mine)
+        *(volatile long long*)S.err_step = merged;
 }
 
 // check_state_finite (engine.cpp:23-28)
@@ -186,7 +237,38 @@ __global__ void tips_kernel(const double4* u, const double* v, const double* a, 
     out[s] = r;
 }
 
+// u, v, a and force x volume of listed rows (multi-rank tip records; the
+// products are record_tips' own, engine.cpp:357-360)
+__global__ void node_values_kernel(const double4* u, const double* v, const double* a,
+                                   const double4* xv, const double* body, const double* ext,
+                                   const long long* rows, long long count, double* out) {
+    const long long k = blockIdx.x * (long long)TPB + threadIdx.x;
+    if (k >= count)
+        return;
+    const long long i = rows[k];
+    const double4 ui = u[i];
+    const double vol = xv[i].w;
+    double* o = out + 15 * k;
+    o[0] = ui.x;
+    o[1] = ui.y;
+    o[2] = ui.z;
+    for (int ax = 0; ax < 3; ++ax) {
+        o[3 + ax] = v[3 * i + ax];
+        o[6 + ax] = a[3 * i + ax];
+        o[9 + ax] = __dmul_rn(body[3 * i + ax], vol);
+        o[12 + ax] = __dmul_rn(ext[3 * i + ax], vol);
+    }
+}
+
 } // namespace
+
+void launch_node_values(const double4* u, const double* v, const double* a, const double4* xv,
+                        const double* body, const double* ext, const long long* rows,
+                        long long count, double* out, cudaStream_t st) {
+    if (count > 0)
+        node_values_kernel<<<grid_for(count), TPB, 0, st>>>(u, v, a, xv, body, ext, rows, count,
+                                                            out);
+}
 
 void launch_pack_xv(const double* coords, const double* volume, long long n, double4* xv,
                     cudaStream_t st) {
@@ -215,6 +297,10 @@ void launch_validate_entries(const int32_t* entries, long long n, int N,
                              unsigned long long* bad_row, cudaStream_t st) {
     if (n > 0)
         validate_entries_kernel<<<grid_for(n * N), TPB, 0, st>>>(entries, n, N, bad_row);
+}
+
+void launch_slab_sync(const SyncArgs& S, cudaStream_t st) {
+    slab_sync_kernel<<<1, 32, 0, st>>>(S);
 }
 
 void launch_vv_prologue(const DevArgs& A, cudaStream_t st) {

@@ -77,7 +77,30 @@ struct DevArgs {
     double damping;
     int store_forces;
     int do_drift;             // VV: produce next step's drifted u into u_out
+    // multi-GPU slabs: owned nodes that are ghosts on the neighbouring ranks
+    // also store their new u into those ranks' u buffers (same parity as
+    // u_out) over NVLink; xfer[i] = {row on rank lo, row on rank hi} or -1
+    const int2* xfer;         // NULL on one GPU
+    double4* peer_lo;
+    double4* peer_hi;
 };
+
+constexpr long long kPeerTimeout = -2;  // err_step value: a peer rank never arrived
+
+// Store an owned node's new displacement into the ghost rows of the
+// neighbouring ranks (peer memory) and make it visible system-wide before the
+// step's sync kernel publishes the step.
+__device__ __forceinline__ void push_ghost(const DevArgs& A, long long i, const double4& un) {
+    if (!A.xfer)
+        return;
+    const int2 t = A.xfer[i];
+    if (t.x >= 0)
+        A.peer_lo[t.x] = un;
+    if (t.y >= 0)
+        A.peer_hi[t.y] = un;
+    if (t.x >= 0 || t.y >= 0)
+        __threadfence_system();
+}
 
 // RampProfile::scale/rate/accel (types.cpp:119-169); same operation order, so
 // with FMA contraction disabled the device values equal the host's bit for bit.
@@ -139,67 +162,74 @@ __device__ __forceinline__ bool finite3(double x, double y, double z) {
 //           then positions + kinematics of step s+1 (driver order :405-415)
 // External force: external_force.assign(0) then += mag * scale (engine.cpp:288-297),
 // evaluated at s+1 (Verlet) or s (Euler).
+// Per-node integrator inputs; loaded right before the epilogue, or early
+// (before a kernel's bond loop) so their latency overlaps the bond work.
+struct NodeIn {
+    double v[3], a[3], inv_rho;
+};
+
+__device__ __forceinline__ NodeIn load_node_in(const DevArgs& A, long long i) {
+    NodeIn r;
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+        r.v[ax] = A.v[3 * i + ax];
+        r.a[ax] = A.a[3 * i + ax];
+    }
+    r.inv_rho = A.inv_rho[i];
+    return r;
+}
+
 template <int MODE>
 __device__ __forceinline__ void node_epilogue(const DevArgs& A, long long i, const double4& ui,
-                                              double fx, double fy, double fz) {
+                                              double fx, double fy, double fz, const NodeIn& in) {
     const double Fb[3] = {fx, fy, fz};
     const double u0[3] = {ui.x, ui.y, ui.z};
     const long long s = A.step;
     const double dt = A.dt;
-    int kind[3];
-    double mag[3] = {0.0, 0.0, 0.0};
-    DevRamp ramp[3];
-    double Fe[3], v[3], a[3], un[3];
+    const double inv = in.inv_rho;
+    double v[3], a[3], un[3], Fe[3];
+    // each axis is independent; processing one axis at a time keeps the ramp
+    // records out of local memory
 #pragma unroll
     for (int ax = 0; ax < 3; ++ax) {
-        kind[ax] = A.bc_kind ? int(A.bc_kind[3 * i + ax]) : PD_BC_FREE;
-        if (kind[ax] != PD_BC_FREE) {
-            mag[ax] = A.bc_mag[3 * i + ax];
-            ramp[ax] = A.ramps[A.bc_ramp[3 * i + ax]];
+        const int kind = A.bc_kind ? int(A.bc_kind[3 * i + ax]) : PD_BC_FREE;
+        double mag = 0.0;
+        DevRamp ramp{};
+        if (kind != PD_BC_FREE) {
+            mag = A.bc_mag[3 * i + ax];
+            ramp = A.ramps[A.bc_ramp[3 * i + ax]];
         }
-        Fe[ax] = kind[ax] == PD_BC_FORCE
-                     ? __dadd_rn(0.0, __dmul_rn(mag[ax], ramp_scale(ramp[ax], MODE == 1 ? s + 1 : s)))
+        Fe[ax] = kind == PD_BC_FORCE
+                     ? __dadd_rn(0.0, __dmul_rn(mag, ramp_scale(ramp, MODE == 1 ? s + 1 : s)))
                      : 0.0;
-        v[ax] = A.v[3 * i + ax];
-        a[ax] = A.a[3 * i + ax];
-    }
-    const double inv = A.inv_rho[i];
-    bool write_u = true;
-    if (MODE == 1) {
-        const double half = A.half_dt;
-        const double half_dt2 = A.half_dt2;
-#pragma unroll
-        for (int ax = 0; ax < 3; ++ax) {
-            const double vh = __dadd_rn(v[ax], __dmul_rn(a[ax], half));
+        if (MODE == 1) {
+            const double vh = __dadd_rn(in.v[ax], __dmul_rn(in.a[ax], A.half_dt));
             double an = __dmul_rn(__dsub_rn(__dadd_rn(Fb[ax], Fe[ax]), __dmul_rn(vh, A.damping)), inv);
-            double vn = __dadd_rn(vh, __dmul_rn(an, half));
-            if (kind[ax] == PD_BC_DISPLACEMENT) {
-                vn = __ddiv_rn(__dmul_rn(mag[ax], ramp_rate(ramp[ax], s + 1)), dt);
-                an = __ddiv_rn(__dmul_rn(mag[ax], ramp_accel(ramp[ax], s + 1)), A.dt2);
+            double vn = __dadd_rn(vh, __dmul_rn(an, A.half_dt));
+            if (kind == PD_BC_DISPLACEMENT) {
+                vn = __ddiv_rn(__dmul_rn(mag, ramp_rate(ramp, s + 1)), dt);
+                an = __ddiv_rn(__dmul_rn(mag, ramp_accel(ramp, s + 1)), A.dt2);
             }
             v[ax] = vn;
             a[ax] = an;
-            un[ax] = __dadd_rn(__dadd_rn(u0[ax], __dmul_rn(vn, dt)), __dmul_rn(an, half_dt2));
-            if (kind[ax] == PD_BC_DISPLACEMENT)
-                un[ax] = __dmul_rn(mag[ax], ramp_scale(ramp[ax], s + 2));
-        }
-        write_u = A.do_drift != 0;
-    } else {
-#pragma unroll
-        for (int ax = 0; ax < 3; ++ax) {
+            un[ax] = __dadd_rn(__dadd_rn(u0[ax], __dmul_rn(vn, dt)), __dmul_rn(an, A.half_dt2));
+            if (kind == PD_BC_DISPLACEMENT)
+                un[ax] = __dmul_rn(mag, ramp_scale(ramp, s + 2));
+        } else {
             const double acc = __dmul_rn(__dadd_rn(Fb[ax], Fe[ax]), inv);
-            const double v_old = v[ax];
+            const double v_old = in.v[ax];
             const double v_new = __dadd_rn(v_old, __dmul_rn(acc, dt));
             a[ax] = acc;
             v[ax] = v_new;
             un[ax] = __dadd_rn(u0[ax], __dmul_rn(MODE == 2 ? v_old : v_new, dt));
-            if (kind[ax] == PD_BC_DISPLACEMENT) {
-                un[ax] = __dmul_rn(mag[ax], ramp_scale(ramp[ax], s + 1));
-                v[ax] = __ddiv_rn(__dmul_rn(mag[ax], ramp_rate(ramp[ax], s + 1)), dt);
-                a[ax] = __ddiv_rn(__dmul_rn(mag[ax], ramp_accel(ramp[ax], s + 1)), A.dt2);
+            if (kind == PD_BC_DISPLACEMENT) {
+                un[ax] = __dmul_rn(mag, ramp_scale(ramp, s + 1));
+                v[ax] = __ddiv_rn(__dmul_rn(mag, ramp_rate(ramp, s + 1)), dt);
+                a[ax] = __ddiv_rn(__dmul_rn(mag, ramp_accel(ramp, s + 1)), A.dt2);
             }
         }
     }
+    const bool write_u = MODE != 1 || A.do_drift != 0;
 #pragma unroll
     for (int ax = 0; ax < 3; ++ax) {
         A.v[3 * i + ax] = v[ax];
@@ -213,10 +243,18 @@ __device__ __forceinline__ void node_epilogue(const DevArgs& A, long long i, con
         }
     }
     if (write_u) {
-        A.u_out[i] = make_double4(un[0], un[1], un[2], ui.w);
+        const double4 unew = make_double4(un[0], un[1], un[2], ui.w);
+        A.u_out[i] = unew;
+        push_ghost(A, i, unew);
         if (!finite3(un[0], un[1], un[2]))
             atomicMin((unsigned long long*)A.err_step, (unsigned long long)(s + 1));
     }
+}
+
+template <int MODE>
+__device__ __forceinline__ void node_epilogue(const DevArgs& A, long long i, const double4& ui,
+                                              double fx, double fy, double fz) {
+    node_epilogue<MODE>(A, i, ui, fx, fy, fz, load_node_in(A, i));
 }
 
 } // namespace pdb

@@ -76,7 +76,7 @@ __device__ __forceinline__ float f_envelope(const FastLaw& law, float s) {
     return law.c * s;
 }
 
-// Shared-memory records (CAP reserved per array; position 0 is a dummy that
+// Shared-memory records (F.cap reserved per array; position 0 is a dummy that
 // dead/padding slots point at -- 1e18 away with zero volume, so its
 // contribution is 0 (or ~1e-18 relative with a uniform volume) and its stretch
 // never reaches s_c; the slot loop needs no branch):
@@ -87,18 +87,22 @@ __device__ __forceinline__ float f_envelope(const FastLaw& law, float s) {
 // byte offset 8*p of its neighbour's sB record (sA is at 16*p); no-failure
 // neighbours are staged last, so "offset >= nf_start" flags them.
 //
-// KIND 0: single PMB law, uniform volume, no no-failure node (c*V constant)
+// KIND 0: single PMB law, uniform volume, no no-failure node (c*V constant,
+//         applied once per node after the slot loop)
 // KIND 1: single PMB law, per-node volume and/or no-failure nodes
 // KIND 2: general -- bond types, n-linear laws with fp32 history, lambda, beta
-template <int MODE, int KIND, int CAP>
-__global__ void __launch_bounds__(FAST_T, (CAP <= 4096 ? 2 : 1))
-    fast_step_kernel(DevArgs A, FastDev F) {
+// TT:     threads (= owned nodes) per tile; MINB: CTAs per SM the register
+//         budget is sized for; PRE: load the node's integrator inputs before
+//         the slot loop so their latency hides behind the bond work.
+template <int MODE, int KIND, int TT, int MINB, bool PRE>
+__global__ void __launch_bounds__(TT, MINB) fast_step_kernel(DevArgs A, FastDev F) {
     if (MODE != 0 && *(volatile long long*)A.err_step != kNoError)
         return;
     extern __shared__ float4 smem[];
+    const int cap = F.cap;
     float4* sA = smem;
-    float2* sB = reinterpret_cast<float2*>(smem + CAP);
-    float* sV = reinterpret_cast<float*>(sB + CAP);
+    float2* sB = reinterpret_cast<float2*>(smem + cap);
+    float* sV = reinterpret_cast<float*>(sB + cap);
     const char* cA = reinterpret_cast<const char*>(sA);
     const char* cB = reinterpret_cast<const char*>(sB);
     const char* cV = reinterpret_cast<const char*>(sV);
@@ -115,7 +119,7 @@ __global__ void __launch_bounds__(FAST_T, (CAP <= 4096 ? 2 : 1))
     const bool active = i < te;
     unsigned short* lrow = F.lidx + F.slot_off[tile] + (long long)t * 8;
     const int nkb = active ? (F.kmax8[tile] >> 3) : 0;
-    const long long kstride = (long long)F.T * 8;
+    const long long kstride = (long long)TT * 8;
     uint4 wnext = nkb > 0 ? __ldcs(reinterpret_cast<const uint4*>(lrow)) : make_uint4(0, 0, 0, 0);
     uint4 wnext2 =
         nkb > 1 ? __ldcs(reinterpret_cast<const uint4*>(lrow + kstride)) : make_uint4(0, 0, 0, 0);
@@ -132,11 +136,11 @@ __global__ void __launch_bounds__(FAST_T, (CAP <= 4096 ? 2 : 1))
         if (KIND != 0)
             sV[0] = 0.f;
     }
-    for (int h = threadIdx.x; h < H; h += 2 * blockDim.x) {
+    for (int h = threadIdx.x; h < H; h += 2 * TT) {
         int id[2];
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
-            const int hh = h + r * int(blockDim.x);
+            const int hh = h + r * TT;
             id[r] = hh < H ? F.halo[h0 + hh] : -1;
         }
         double4 x[2], u[2];
@@ -149,13 +153,19 @@ __global__ void __launch_bounds__(FAST_T, (CAP <= 4096 ? 2 : 1))
 #pragma unroll
         for (int r = 0; r < 2; ++r)
             if (id[r] >= 0) {
-                const int hh = h + r * int(blockDim.x) + 1;
+                const int hh = h + r * TT + 1;
                 sA[hh] = make_float4(float(x[r].x - O.x), float(x[r].y - O.y),
                                      float(u[r].x - U0.x), float(u[r].y - U0.y));
                 sB[hh] = make_float2(float(x[r].z - O.z), float(u[r].z - U0.z));
                 if (KIND != 0)
                     sV[hh] = float(x[r].w * vscale);
             }
+    }
+    NodeIn pre{};
+    double4 ui_pre = make_double4(0, 0, 0, 0);
+    if (PRE && MODE != 0 && active) {
+        pre = load_node_in(A, i);
+        ui_pre = A.u_in[i];
     }
     __syncthreads();
     if (!active)
@@ -165,13 +175,12 @@ __global__ void __launch_bounds__(FAST_T, (CAP <= 4096 ? 2 : 1))
     const unsigned own = own_raw & 0x1FFFu;
     const float4 ai = sA[own];
     const float2 bi = sB[own];
-    const float2 nxi = make_float2(-ai.x, -ai.y);  // x/y in packed f32x2, z scalar
+    const float2 nxi = make_float2(-ai.x, -ai.y);  // x/y in packed f32x2, z/uz packed too
     const float2 nui = make_float2(-ai.z, -ai.w);
-    const float xiz = bi.x, uiz = bi.y;
+    const float2 nzi = make_float2(-bi.x, -bi.y);
     // a no-failure node's bonds never break: lift its critical stretch to +inf
     const float sc_pmb = (own_raw & 0x8000u) ? __int_as_float(0x7f800000) : F.pmb_sc;
     const bool nfi = (own_raw & 0x8000u) != 0;
-    const float cv_uniform = F.pmb_cv;
     float2 fxy = make_float2(0.f, 0.f);
     float fz = 0.f;
     int broke = 0;
@@ -189,9 +198,10 @@ __global__ void __launch_bounds__(FAST_T, (CAP <= 4096 ? 2 : 1))
             const float2 br = *reinterpret_cast<const float2*>(cB + offB);
             const float2 exy = __fadd2_rn(make_float2(ar.x, ar.y), nxi);
             const float2 hxy = __fadd2_rn(make_float2(ar.z, ar.w), nui);
+            const float2 ezh = __fadd2_rn(br, nzi);  // (xi_z, eta_z)
             const float2 cxy = __fadd2_rn(exy, hxy);
             const float2 sxy = __fadd2_rn(exy, cxy);
-            const float ez = br.x - xiz, hz = br.y - uiz;
+            const float ez = ezh.x, hz = ezh.y;
             const float cz = ez + hz;
             const float2 e2 = __fmul2_rn(exy, exy);
             const float2 n2 = __fmul2_rn(hxy, sxy);
@@ -202,20 +212,23 @@ __global__ void __launch_bounds__(FAST_T, (CAP <= 4096 ? 2 : 1))
             const float rc = rsqrt_approx(cur2);
             // s = (|cur| - |xi|) / |xi| = eta.(xi + cur) / (|xi| (|cur| + |xi|))
             const float s = num * rr * rcp_approx(cur2 * rc + ref2 * rr);
-            float f;
+            float scale;
             if (KIND != 2) {
                 const bool brk = KIND == 0 ? (s >= sc_pmb) : (s >= sc_pmb && offB < nf_start);
                 if (brk) {
                     bmask |= 1u << q;  // stored after the 8 slots, off the hot path
                     continue;
                 }
-                f = s * (KIND == 0 ? cv_uniform : *reinterpret_cast<const float*>(cV + (offB >> 1)));
+                // KIND 0: c*V is applied once per node after the loop
+                scale = KIND == 0 ? s * rc
+                                  : s * *reinterpret_cast<const float*>(cV + (offB >> 1)) * rc;
             } else {
                 if (offB == 0)
                     continue;  // broken/padding: its history must not re-trigger the break
                 const bool no_fail = nfi || offB >= nf_start;
                 const long long sidx = (lrow - F.lidx) + q;
                 const FastLaw& law = c_flaws[F.btype ? int(F.btype[sidx]) : 0];
+                float f;
                 if (no_fail) {
                     f = law.c * s;
                 } else if (law.nbp == 1) {
@@ -243,8 +256,8 @@ __global__ void __launch_bounds__(FAST_T, (CAP <= 4096 ? 2 : 1))
                 if (F.beta)
                     f *= F.beta[sidx];
                 f *= *reinterpret_cast<const float*>(cV + (offB >> 1));
+                scale = f * rc;
             }
-            const float scale = f * rc;
             fxy = __ffma2_rn(cxy, make_float2(scale, scale), fxy);
             fz = fmaf(cz, scale, fz);
         }
@@ -257,6 +270,10 @@ __global__ void __launch_bounds__(FAST_T, (CAP <= 4096 ? 2 : 1))
     }
     if (broke)
         A.n_neigh[i] -= broke;
+    if (KIND == 0) {
+        fxy = __fmul2_rn(fxy, make_float2(F.pmb_cv, F.pmb_cv));
+        fz *= F.pmb_cv;
+    }
 
     // 3. fp64 epilogue
     if (MODE == 0) {
@@ -265,40 +282,55 @@ __global__ void __launch_bounds__(FAST_T, (CAP <= 4096 ? 2 : 1))
         A.body_force[3 * i + 2] = double(fz);
         return;
     }
-    node_epilogue<MODE>(A, i, A.u_in[i], double(fxy.x), double(fxy.y), double(fz));
+    if (PRE)
+        node_epilogue<MODE>(A, i, ui_pre, double(fxy.x), double(fxy.y), double(fz), pre);
+    else
+        node_epilogue<MODE>(A, i, A.u_in[i], double(fxy.x), double(fxy.y), double(fz));
 }
 
-template <int MODE, int KIND, int CAP>
-cudaError_t launch_cap(const DevArgs& A, const FastDev& F, int tiles, cudaStream_t st) {
-    static bool configured = false;
-    const int smem = CAP * int(sizeof(float4) + sizeof(float2) + (KIND == 0 ? 0 : sizeof(float)));
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(fast_step_kernel<MODE, KIND, CAP>,
+int smem_bytes(int kind, int cap) {
+    return cap * int(sizeof(float4) + sizeof(float2) + (kind == 0 ? 0 : sizeof(float)));
+}
+
+template <int MODE, int KIND, int TT, int MINB, bool PRE>
+cudaError_t launch_cfg(const DevArgs& A, const FastDev& F, int tiles, cudaStream_t st) {
+    static int configured = 0;
+    const int smem = smem_bytes(KIND, F.cap);
+    if (smem > configured) {
+        cudaError_t e = cudaFuncSetAttribute(fast_step_kernel<MODE, KIND, TT, MINB, PRE>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess)
             return e;
-        configured = true;
+        configured = smem;
     }
-    fast_step_kernel<MODE, KIND, CAP><<<tiles, F.T, smem, st>>>(A, F);
+    fast_step_kernel<MODE, KIND, TT, MINB, PRE><<<tiles, TT, smem, st>>>(A, F);
     return cudaGetLastError();
 }
 
+// tile configurations: 0 = 512 threads, 2 CTAs/SM (default); 1 = 256 x 4;
+// 2 = 256 x 3 with prefetched node inputs; 3 = 512 x 2 with prefetch
 template <int MODE, int KIND>
-cudaError_t launch_one(const DevArgs& A, const FastDev& F, int tiles, int max_halo,
-                       cudaStream_t st) {
-    if (max_halo + 1 <= 4096)
-        return launch_cap<MODE, KIND, 4096>(A, F, tiles, st);
-    return launch_cap<MODE, KIND, FAST_MAX_HALO + 1>(A, F, tiles, st);
+cudaError_t launch_one(const DevArgs& A, const FastDev& F, int tiles, cudaStream_t st) {
+    if (MODE == 1 && KIND == 0) {
+        switch (F.cfg) {
+        case 1: return launch_cfg<MODE, KIND, 256, 4, false>(A, F, tiles, st);
+        case 2: return launch_cfg<MODE, KIND, 256, 3, true>(A, F, tiles, st);
+        case 3: return launch_cfg<MODE, KIND, 512, 2, true>(A, F, tiles, st);
+        default: break;
+        }
+    }
+    if (F.T == 256)
+        return launch_cfg<MODE, KIND, 256, 4, false>(A, F, tiles, st);
+    return launch_cfg<MODE, KIND, 512, 2, false>(A, F, tiles, st);
 }
 
 template <int KIND>
-cudaError_t launch_kind(const DevArgs& A, const FastDev& F, int mode, int tiles, int max_halo,
-                        cudaStream_t st) {
+cudaError_t launch_kind(const DevArgs& A, const FastDev& F, int mode, int tiles, cudaStream_t st) {
     switch (mode) {
-    case 0: return launch_one<0, KIND>(A, F, tiles, max_halo, st);
-    case 1: return launch_one<1, KIND>(A, F, tiles, max_halo, st);
-    case 2: return launch_one<2, KIND>(A, F, tiles, max_halo, st);
-    default: return launch_one<3, KIND>(A, F, tiles, max_halo, st);
+    case 0: return launch_one<0, KIND>(A, F, tiles, st);
+    case 1: return launch_one<1, KIND>(A, F, tiles, st);
+    case 2: return launch_one<2, KIND>(A, F, tiles, st);
+    default: return launch_one<3, KIND>(A, F, tiles, st);
     }
 }
 
@@ -328,6 +360,15 @@ __global__ void fast_materialize_kernel(const int32_t* entries0, const int* inv,
         return;
     const int ii = inv[i];
     const int tile = tile_of[ii];
+    if (tile < 0) {  // a ghost row of a multi-GPU slab: not integrated here
+        for (int k = 0; k < N; ++k) {
+            if (entries_out)
+                entries_out[i * N + k] = entries0[i * N + k];
+            if (hist_out)
+                hist_out[i * N + k] = 0.0;
+        }
+        return;
+    }
     const int t = ii - tile_start[tile];
     const long long base = slot_off[tile] + (long long)t * 8;
     int c = 0;
@@ -350,14 +391,14 @@ __global__ void fast_materialize_kernel(const int32_t* entries0, const int* inv,
 } // namespace
 
 cudaError_t launch_fast(const DevArgs& A, const FastDev& F, int mode, int kind, int tiles,
-                        int max_halo, cudaStream_t st) {
+                        cudaStream_t st) {
     if (tiles <= 0)
         return cudaSuccess;
     if (kind == 0)
-        return launch_kind<0>(A, F, mode, tiles, max_halo, st);
+        return launch_kind<0>(A, F, mode, tiles, st);
     if (kind == 1)
-        return launch_kind<1>(A, F, mode, tiles, max_halo, st);
-    return launch_kind<2>(A, F, mode, tiles, max_halo, st);
+        return launch_kind<1>(A, F, mode, tiles, st);
+    return launch_kind<2>(A, F, mode, tiles, st);
 }
 
 template <class T, int W>
@@ -392,7 +433,10 @@ void launch_fast_materialize(const int32_t* entries0, const int* inv, const int*
 int fast_build_layout(FastHostLayout& L, int64_t n, int N, const int32_t* entries,
                       const double* coords, const uint8_t* btype, const double* lambda,
                       const double* beta, const double* hist, bool history,
-                      const uint8_t* nofail) {
+                      const uint8_t* nofail, int T, int64_t own_begin, int64_t own_end) {
+    // only the owned nodes [own_begin, own_end) are tiled (all of them on one
+    // GPU); they come first in the internal order, the ghost nodes of a
+    // multi-GPU slab follow in local order
     // bricks of ~8 nodes per axis from the bounding box and mean spacing
     double lo[3], hi[3];
     for (int d = 0; d < 3; ++d)
@@ -422,7 +466,7 @@ int fast_build_layout(FastHostLayout& L, int64_t n, int N, const int32_t* entrie
     // grid planes, so a half-warp covers a whole 16-node x-run and its
     // neighbour runs are contiguous shared-memory records (conflict-free
     // LDS.64 over 16 lanes, LDS.128 over 8); otherwise bins of ~8 mean spacings
-    const long long kBrick[3] = {16, 4, 8};
+    const long long kBrick[3] = {16, 4, T / 64};
     std::unordered_map<double, long long> rank[3];
     bool lattice[3] = {false, false, false};
     for (int d = 0; d < 3; ++d) {
@@ -444,7 +488,7 @@ int fast_build_layout(FastHostLayout& L, int64_t n, int N, const int32_t* entrie
     const long long nbricks = nb[0] * nb[1] * nb[2];
     std::vector<long long> brick(static_cast<size_t>(n));
     std::vector<long long> count(size_t(nbricks + 1), 0);
-    for (int64_t i = 0; i < n; ++i) {
+    for (int64_t i = own_begin; i < own_end; ++i) {
         long long b[3];
         for (int d = 0; d < 3; ++d) {
             long long c;
@@ -463,22 +507,26 @@ int fast_build_layout(FastHostLayout& L, int64_t n, int N, const int32_t* entrie
     L.inv.assign(size_t(n), 0);
     {
         std::vector<long long> fill(count.begin(), count.end() - 1);
-        for (int64_t i = 0; i < n; ++i)
+        for (int64_t i = own_begin; i < own_end; ++i)
             L.perm[size_t(fill[size_t(brick[size_t(i)])]++)] = int(i);
+        int64_t g = own_end - own_begin;
+        for (int64_t i = 0; i < n; ++i)
+            if (i < own_begin || i >= own_end)
+                L.perm[size_t(g++)] = int(i);
     }
     for (int64_t ii = 0; ii < n; ++ii)
         L.inv[size_t(L.perm[size_t(ii)])] = int(ii);
 
-    // tiles: <= FAST_T consecutive internal nodes of one brick
-    L.T = FAST_T;
+    // tiles: <= T consecutive internal nodes of one brick
+    L.T = T;
     L.tile_start.clear();
     for (long long b = 0; b < nbricks; ++b)
-        for (long long s = count[size_t(b)]; s < count[size_t(b + 1)]; s += FAST_T)
+        for (long long s = count[size_t(b)]; s < count[size_t(b + 1)]; s += T)
             L.tile_start.push_back(int(s));
-    L.tile_start.push_back(int(n));
+    L.tile_start.push_back(int(own_end - own_begin));
     const int tiles = int(L.tile_start.size()) - 1;
     L.n_tiles = tiles;
-    L.tile_of.assign(size_t(n), 0);
+    L.tile_of.assign(size_t(n), -1);
     L.own_slot.assign(size_t(n), 0);
     for (int t = 0; t < tiles; ++t)
         for (int ii = L.tile_start[size_t(t)]; ii < L.tile_start[size_t(t + 1)]; ++ii)
@@ -551,7 +599,7 @@ int fast_build_layout(FastHostLayout& L, int64_t n, int N, const int32_t* entrie
                                                           ((nofail && nofail[orig]) ? 0x8000 : 0));
             }
             o.kmax8 = (kmax + 7) / 8 * 8;
-            const size_t slots = size_t(o.kmax8) * FAST_T;
+            const size_t slots = size_t(o.kmax8) * size_t(T);
             o.lidx.assign(slots, 0);
             if (history)
                 o.hist.assign(slots, 0.f);
@@ -569,7 +617,7 @@ int fast_build_layout(FastHostLayout& L, int64_t n, int N, const int32_t* entrie
                     const int32_t j = entries[i * N + k];
                     if (j < 0)
                         continue;
-                    const size_t s = size_t(c >> 3) * FAST_T * 8 + size_t(tt) * 8 + size_t(c & 7);
+                    const size_t s = size_t(c >> 3) * size_t(T) * 8 + size_t(tt) * 8 + size_t(c & 7);
                     o.lidx[s] = (unsigned short)(8 * pos_of(j));
                     const int64_t idx = i * N + k;
                     if (history)

@@ -23,11 +23,13 @@
 
 namespace pdb {
 
-constexpr int FAST_T = 512;           // threads (= owned nodes) per tile
+constexpr int FAST_T = 512;           // default threads (= owned nodes) per tile
 constexpr int FAST_MAX_HALO = 7000;   // (7000 + 1) * 28 B = 196 KB of shared memory; 8*(7000+1) < 65536
 
 struct FastDev {
-    int T;
+    int T;                     // threads (= owned nodes) per tile: 512 or 256
+    int cap;                   // shared-memory records reserved per array (max halo + 1)
+    int cfg;                   // kernel configuration (pd_fast.cu launch_one)
     int n_tiles;
     int tile0;                 // first tile of this launch
     const int* tile_start;     // n_tiles + 1 internal node ids

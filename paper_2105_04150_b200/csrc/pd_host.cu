@@ -13,7 +13,9 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <unistd.h>
 #include <string>
 #include <vector>
 
@@ -185,11 +187,27 @@ struct pd_ctx {
     int n_tip_sets = 0;
     bool forces_valid = false;
 
+    // the range of device rows this context integrates (all rows on one GPU;
+    // the owned rows of a multi-GPU slab)
+    int64_t comp_begin = 0, comp_end = 0;
+    int64_t own_begin = 0, own_end = 0;  // owned LOCAL node ids
+    bool partial = false;                // uploaded by pd_ctx_upload_part
+    // multi-GPU slab world (pd_ctx_connect)
+    int rank = 0, world = 1;
+    DevBuf<unsigned long long> sync;     // 2 * PD_MAX_RANKS words (epochs, flags)
+    unsigned long long epoch = 0;
+    DevBuf<int2> xfer;
+    double4* peer_u[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [lo/hi][parity]
+    unsigned long long* peer_sync[PD_MAX_RANKS] = {};
+    std::vector<void*> ipc_opened;
+    std::vector<int> inv_host;           // local node -> device row (PD_FAST)
+
     // fast path (PD_FAST): internal brick order + tile layout (pd_fast.cuh)
     bool fast = false;
     int kind = 2;  // fast kernel specialisation (pd_fast.cu)
     float pmb_c = 0, pmb_sc = 0, pmb_cv = 0;
     int n_tiles = 0, max_halo = 0;
+    int fast_T = FAST_T, fast_cfg = 0;
     DevBuf<int> perm, inv, tile_of, tile_start, kmax8, halo, nf_start;
     DevBuf<unsigned short> own_slot;
     DevBuf<long long> halo_off, slot_off;
@@ -202,7 +220,9 @@ struct pd_ctx {
 
     FastDev fast_args() const {
         FastDev F{};
-        F.T = FAST_T;
+        F.T = fast_T;
+        F.cap = (max_halo + 1 + 31) / 32 * 32;
+        F.cfg = fast_cfg;
         F.n_tiles = n_tiles;
         F.tile0 = 0;
         F.tile_start = tile_start.p;
@@ -226,8 +246,8 @@ struct pd_ctx {
     DevArgs args() const {
         DevArgs A{};
         A.n = n;
-        A.begin = 0;
-        A.end = n;
+        A.begin = comp_begin;
+        A.end = comp_end;
         A.N = N;
         A.log2N = log2N;
         A.W = W;
@@ -261,6 +281,9 @@ struct pd_ctx {
         A.damping = damping;
         A.store_forces = 0;
         A.do_drift = 0;
+        A.xfer = world > 1 ? xfer.p : nullptr;
+        A.peer_lo = peer_u[0][cur ^ 1];
+        A.peer_hi = peer_u[1][cur ^ 1];
         return A;
     }
 };
@@ -410,6 +433,12 @@ int upload_common(pd_ctx* ctx, const pd_particles& p, const pd_state& st,
     PD_CK(cudaMemsetAsync(ctx->ext.p, 0, sizeof(double) * 3 * n, s));
     ctx->forces_valid = false;
     ctx->step = st.step;
+    if (!ctx->partial) {
+        ctx->own_begin = 0;
+        ctx->own_end = n;
+    }
+    ctx->comp_begin = ctx->own_begin;
+    ctx->comp_end = ctx->own_end;
     ctx->scratch_f64.release();
     PD_CK(cudaStreamSynchronize(s));
     return PD_OK;
@@ -497,7 +526,7 @@ int download(pd_ctx* ctx, pd_state* st, pd_force_field* forces, int32_t fields) 
             PD_CK(ctx->scratch_i32.alloc(size_t(slots)));
             if (ctx->fast)
                 launch_fast_materialize(ctx->entries.p, ctx->inv.p, ctx->tile_of.p,
-                                        ctx->tile_start.p, ctx->slot_off.p, FAST_T, ctx->lidx.p,
+                                        ctx->tile_start.p, ctx->slot_off.p, ctx->fast_T, ctx->lidx.p,
                                         nullptr, n, ctx->N, ctx->scratch_i32.p, nullptr, s);
             else
                 launch_materialize_entries(ctx->entries.p, ctx->alive.p, n, ctx->N, ctx->W,
@@ -522,7 +551,7 @@ int download(pd_ctx* ctx, pd_state* st, pd_force_field* forces, int32_t fields) 
     if (want_hist) {
         if (ctx->fast) {
             launch_fast_materialize(ctx->entries.p, ctx->inv.p, ctx->tile_of.p, ctx->tile_start.p,
-                                    ctx->slot_off.p, FAST_T, ctx->lidx.p, ctx->hist32.p, n,
+                                    ctx->slot_off.p, ctx->fast_T, ctx->lidx.p, ctx->hist32.p, n,
                                     ctx->N, nullptr, ctx->hist.p, s);
             ++ctx->launches;
         }
@@ -549,6 +578,12 @@ int setup_fast(pd_ctx* ctx, const pd_particles& p, const pd_state& st,
     cudaStream_t s = ctx->stream;
     const int64_t n = ctx->n;
     FastHostLayout L;
+    // PD_FAST_CFG selects a tile configuration (pd_fast.cu launch_one); the
+    // default is 512-node tiles
+    ctx->fast_cfg = 0;
+    if (const char* e = std::getenv("PD_FAST_CFG"))
+        ctx->fast_cfg = std::atoi(e);
+    ctx->fast_T = (ctx->fast_cfg == 1 || ctx->fast_cfg == 2) ? 256 : 512;
     const bool hist_in = ctx->history && st.bond_history &&
                          st.bond_history_size == n * int64_t(ctx->N);
     if (fast_build_layout(L, n, ctx->N, st.connectivity.entries, p.coords,
@@ -556,12 +591,16 @@ int setup_fast(pd_ctx* ctx, const pd_particles& p, const pd_state& st,
                           corr.lambda_size ? corr.lambda : nullptr,
                           corr.beta_size ? corr.beta : nullptr,
                           hist_in ? st.bond_history : nullptr, ctx->history,
-                          nofail_size == n ? nofail : nullptr) != 0)
+                          nofail_size == n ? nofail : nullptr, ctx->fast_T, ctx->own_begin,
+                          ctx->own_end) != 0)
         return fail(PD_E_INVALID_ARGUMENT,
                     "PD_FAST: a tile neighbourhood exceeds %d nodes of shared memory; use "
                     "PD_BOND_PARALLEL for this mesh", FAST_MAX_HALO);
     ctx->n_tiles = L.n_tiles;
     ctx->max_halo = L.max_halo;
+    ctx->comp_begin = 0;  // owned nodes come first in the internal order
+    ctx->comp_end = ctx->own_end - ctx->own_begin;
+    ctx->inv_host = L.inv;
     PD_CK(ctx->perm.upload(L.perm.data(), L.perm.size(), s));
     PD_CK(ctx->inv.upload(L.inv.data(), L.inv.size(), s));
     PD_CK(ctx->tile_of.upload(L.tile_of.data(), L.tile_of.size(), s));
@@ -657,13 +696,31 @@ int setup_fast(pd_ctx* ctx, const pd_particles& p, const pd_state& st,
 
 int launch_step(pd_ctx* ctx, DevArgs& A, int mode) {
     if (ctx->fast) {
-        PD_CK(launch_fast(A, ctx->fast_args(), mode, ctx->kind, ctx->n_tiles, ctx->max_halo,
-                          ctx->stream));
+        PD_CK(launch_fast(A, ctx->fast_args(), mode, ctx->kind, ctx->n_tiles, ctx->stream));
         ++ctx->launches;
         return PD_OK;
     }
     PD_CK(launch_exact(A, mode, ctx->variant == PD_NODE_PARALLEL, ctx->stream));
     ++ctx->launches;
+    return PD_OK;
+}
+
+// Slab barrier after a launch that wrote peer ghost rows (no-op on one GPU).
+int slab_sync(pd_ctx* ctx) {
+    if (ctx->world <= 1)
+        return PD_OK;
+    SyncArgs S{};
+    for (int p = 0; p < ctx->world; ++p)
+        S.peer_sync[p] = ctx->peer_sync[p];
+    S.my_sync = ctx->sync.p;
+    S.err_step = ctx->err.p;
+    S.rank = ctx->rank;
+    S.world = ctx->world;
+    S.epoch = ++ctx->epoch;
+    S.timeout_ns = 120LL * 1000 * 1000 * 1000;
+    launch_slab_sync(S, ctx->stream);
+    ++ctx->launches;
+    PD_CK(cudaGetLastError());
     return PD_OK;
 }
 
@@ -715,9 +772,11 @@ int run_loop(pd_ctx* ctx, const pd_options& opt, pd_write_hook hook, void* user,
         launch_vv_prologue(A, s);
         ctx->cur ^= 1;
     } else {
-        launch_check_finite(ctx->u[ctx->cur].p, 0, ctx->n, first, ctx->err.p, s);
+        launch_check_finite(ctx->u[ctx->cur].p, ctx->comp_begin, ctx->comp_end, first,
+                            ctx->err.p, s);
     }
     ++ctx->launches;
+    PD_TRY(slab_sync(ctx));
 
     HookStage stage;
     int64_t rec = 0;
@@ -727,9 +786,12 @@ int run_loop(pd_ctx* ctx, const pd_options& opt, pd_write_hook hook, void* user,
         const bool is_write = opt.write_every > 0 && (st + 1) % opt.write_every == 0;
         A = ctx->args();
         A.step = st;
-        A.store_forces = is_write && (ctx->n_tip_sets > 0 || hook);
+        // forces are kept at write steps and at the end of every run (so a
+        // download after the run sees the last step's force field)
+        A.store_forces = (is_write && (ctx->n_tip_sets > 0 || hook)) || st + 1 == last;
         A.do_drift = st + 1 < last;
         PD_TRY(launch_step(ctx, A, mode));
+        PD_TRY(slab_sync(ctx));
         if (!vv)
             ctx->cur ^= 1;
         if (is_write) {
@@ -744,6 +806,9 @@ int run_loop(pd_ctx* ctx, const pd_options& opt, pd_write_hook hook, void* user,
                 long long err = none;
                 PD_CK(cudaMemcpyAsync(&err, ctx->err.p, sizeof err, cudaMemcpyDeviceToHost, s));
                 PD_CK(cudaStreamSynchronize(s));
+                if (err == kPeerTimeout)
+                    return fail(PD_E_CUDA, "slab sync: a peer rank did not reach step %lld",
+                                (long long)(st + 1));
                 if (err <= st) {
                     failed_at = err;
                     break;
@@ -799,6 +864,8 @@ int run_loop(pd_ctx* ctx, const pd_options& opt, pd_write_hook hook, void* user,
     long long err = none;
     PD_CK(cudaMemcpyAsync(&err, ctx->err.p, sizeof err, cudaMemcpyDeviceToHost, s));
     PD_CK(cudaStreamSynchronize(s));
+    if (err == kPeerTimeout)
+        return fail(PD_E_CUDA, "slab sync: a peer rank did not arrive (timeout)");
     if (failed_at < 0 && err < last)
         failed_at = err;
     int64_t keep = rec;
@@ -827,6 +894,10 @@ int run_loop(pd_ctx* ctx, const pd_options& opt, pd_write_hook hook, void* user,
 }
 
 } // namespace
+
+namespace {
+int upload_impl(pd_ctx* ctx, const pd_bundle* b, const pd_state* st, int32_t variant);
+}
 
 // ---- C ABI ------------------------------------------------------------------
 
@@ -874,6 +945,8 @@ void pd_ctx_destroy(pd_ctx* ctx) {
         return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    for (void* p : ctx->ipc_opened)
+        cudaIpcCloseMemHandle(p);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -883,6 +956,152 @@ void* pd_ctx_stream(pd_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
 int64_t pd_ctx_launch_count(pd_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 int pd_ctx_upload(pd_ctx* ctx, const pd_bundle* b, const pd_state* st, int32_t variant) {
+    ctx->partial = false;
+    return upload_impl(ctx, b, st, variant);
+}
+
+int pd_ctx_upload_part(pd_ctx* ctx, const pd_bundle* b, const pd_state* st, int32_t variant,
+                       int64_t own_begin, int64_t own_end) {
+    if (own_begin < 0 || own_end < own_begin || own_end > b->particles.n)
+        return fail(PD_E_INVALID_ARGUMENT, "slab: owned range [%lld, %lld) outside the %lld local nodes",
+                    (long long)own_begin, (long long)own_end, (long long)b->particles.n);
+    ctx->partial = true;
+    ctx->own_begin = own_begin;
+    ctx->own_end = own_end;
+    const int rc = upload_impl(ctx, b, st, variant);
+    return rc;
+}
+
+int pd_ctx_internal_index(pd_ctx* ctx, const int64_t* local, int64_t count, int64_t* out) {
+    for (int64_t k = 0; k < count; ++k) {
+        if (local[k] < 0 || local[k] >= ctx->n)
+            return fail(PD_E_INVALID_ARGUMENT, "internal_index: node %lld out of range",
+                        (long long)local[k]);
+        out[k] = ctx->fast ? int64_t(ctx->inv_host[size_t(local[k])]) : local[k];
+    }
+    return ok();
+}
+
+int pd_ctx_export(pd_ctx* ctx, pd_peer_handle* out) {
+    PD_TRY(select_device(ctx));
+    std::memset(out, 0, sizeof *out);
+    if (!ctx->sync.p) {
+        PD_CK(ctx->sync.alloc(2 * PD_MAX_RANKS));
+        PD_CK(cudaMemset(ctx->sync.p, 0, sizeof(unsigned long long) * 2 * PD_MAX_RANKS));
+        PD_CK(cudaDeviceSynchronize());
+    }
+    if (!ctx->u[0].p || !ctx->u[1].p)
+        return fail(PD_E_INVALID_ARGUMENT, "export: upload the model first");
+    out->device = ctx->device;
+    out->pid = int32_t(getpid());
+    cudaIpcMemHandle_t h;
+    PD_CK(cudaIpcGetMemHandle(&h, ctx->u[0].p));
+    std::memcpy(out->ipc_u0, &h, sizeof h);
+    PD_CK(cudaIpcGetMemHandle(&h, ctx->u[1].p));
+    std::memcpy(out->ipc_u1, &h, sizeof h);
+    PD_CK(cudaIpcGetMemHandle(&h, ctx->sync.p));
+    std::memcpy(out->ipc_sync, &h, sizeof h);
+    out->u0 = uint64_t(reinterpret_cast<uintptr_t>(ctx->u[0].p));
+    out->u1 = uint64_t(reinterpret_cast<uintptr_t>(ctx->u[1].p));
+    out->sync = uint64_t(reinterpret_cast<uintptr_t>(ctx->sync.p));
+    return ok();
+}
+
+int pd_ctx_connect(pd_ctx* ctx, int32_t rank, int32_t world, const pd_peer_handle* peers,
+                   int32_t lo, int32_t hi, const int64_t* send_lo, const int64_t* send_hi) {
+    PD_TRY(select_device(ctx));
+    if (world < 1 || world > PD_MAX_RANKS || rank < 0 || rank >= world)
+        return fail(PD_E_INVALID_ARGUMENT, "connect: rank %d of %d (at most %d ranks)", rank,
+                    world, PD_MAX_RANKS);
+    if ((lo >= world) || (hi >= world) || (lo == rank && lo >= 0) || (hi == rank && hi >= 0))
+        return fail(PD_E_INVALID_ARGUMENT, "connect: bad neighbour ranks %d / %d", lo, hi);
+    if (!ctx->sync.p)
+        return fail(PD_E_INVALID_ARGUMENT, "connect: export this context first");
+    const int me = int(getpid());
+    // map every peer's u buffers and sync words
+    void* mapped[PD_MAX_RANKS][3] = {};
+    for (int p = 0; p < world; ++p) {
+        if (p == rank) {
+            mapped[p][0] = ctx->u[0].p;
+            mapped[p][1] = ctx->u[1].p;
+            mapped[p][2] = ctx->sync.p;
+            continue;
+        }
+        const pd_peer_handle& h = peers[p];
+        if (h.pid == me) {
+            if (h.device != ctx->device) {
+                const cudaError_t e = cudaDeviceEnablePeerAccess(h.device, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+                    PD_CK(e);
+                cudaGetLastError();
+            }
+            mapped[p][0] = reinterpret_cast<void*>(uintptr_t(h.u0));
+            mapped[p][1] = reinterpret_cast<void*>(uintptr_t(h.u1));
+            mapped[p][2] = reinterpret_cast<void*>(uintptr_t(h.sync));
+        } else {
+            const uint8_t* src[3] = {h.ipc_u0, h.ipc_u1, h.ipc_sync};
+            for (int k = 0; k < 3; ++k) {
+                cudaIpcMemHandle_t ih;
+                std::memcpy(&ih, src[k], sizeof ih);
+                PD_CK(cudaIpcOpenMemHandle(&mapped[p][k], ih, cudaIpcMemLazyEnablePeerAccess));
+                ctx->ipc_opened.push_back(mapped[p][k]);
+            }
+        }
+    }
+    ctx->rank = rank;
+    ctx->world = world;
+    ctx->epoch = 0;
+    for (int p = 0; p < world; ++p)
+        ctx->peer_sync[p] = static_cast<unsigned long long*>(mapped[p][2]);
+    for (int side = 0; side < 2; ++side) {
+        const int r = side == 0 ? lo : hi;
+        for (int par = 0; par < 2; ++par)
+            ctx->peer_u[side][par] = r >= 0 ? static_cast<double4*>(mapped[r][par]) : nullptr;
+    }
+    // per device row: the peer rows this owned node's u goes to
+    std::vector<int2> x(size_t(ctx->n), make_int2(-1, -1));
+    for (int64_t i = ctx->own_begin; i < ctx->own_end; ++i) {
+        const int64_t row = ctx->fast ? int64_t(ctx->inv_host[size_t(i)]) : i;
+        const int64_t a = (lo >= 0 && send_lo) ? send_lo[i] : -1;
+        const int64_t b = (hi >= 0 && send_hi) ? send_hi[i] : -1;
+        if (a >= INT32_MAX || b >= INT32_MAX)
+            return fail(PD_E_INVALID_ARGUMENT, "connect: peer row index out of range");
+        x[size_t(row)] = make_int2(int(a), int(b));
+    }
+    PD_CK(ctx->xfer.upload(x.data(), x.size(), ctx->stream));
+    PD_CK(cudaStreamSynchronize(ctx->stream));
+    return ok();
+}
+
+int pd_ctx_node_values(pd_ctx* ctx, const int64_t* local, int64_t count, double* out) {
+    PD_TRY(select_device(ctx));
+    std::vector<long long> rows(size_t(std::max<int64_t>(count, 1)), 0);
+    for (int64_t k = 0; k < count; ++k) {
+        if (local[k] < 0 || local[k] >= ctx->n)
+            return fail(PD_E_INVALID_ARGUMENT, "node_values: node %lld out of range",
+                        (long long)local[k]);
+        rows[size_t(k)] = ctx->fast ? ctx->inv_host[size_t(local[k])] : local[k];
+    }
+    if (count == 0)
+        return ok();
+    cudaStream_t s = ctx->stream;
+    DevBuf<long long> d_rows;
+    DevBuf<double> d_out;
+    PD_CK(d_rows.upload(rows.data(), size_t(count), s));
+    PD_CK(d_out.alloc(size_t(15 * count)));
+    launch_node_values(ctx->u[ctx->cur].p, ctx->v.p, ctx->a.p, ctx->xv.p, ctx->body.p, ctx->ext.p,
+                       d_rows.p, count, d_out.p, s);
+    ++ctx->launches;
+    PD_CK(cudaMemcpyAsync(out, d_out.p, sizeof(double) * 15 * count, cudaMemcpyDeviceToHost, s));
+    PD_CK(cudaStreamSynchronize(s));
+    return ok();
+}
+
+} // extern "C"
+
+namespace {
+
+int upload_impl(pd_ctx* ctx, const pd_bundle* b, const pd_state* st, int32_t variant) {
     PD_TRY(select_device(ctx));
     if (variant < PD_BOND_PARALLEL || variant > PD_FAST)
         return fail(PD_E_INVALID_ARGUMENT, "unknown kernel variant %d", variant);
@@ -912,6 +1131,10 @@ int pd_ctx_upload(pd_ctx* ctx, const pd_bundle* b, const pd_state* st, int32_t v
     ctx->dt = b->dt;
     return ok();
 }
+
+} // namespace
+
+extern "C" {
 
 int pd_ctx_run(pd_ctx* ctx, const pd_options* options, pd_write_hook on_write, void* user,
                int32_t hook_fields, pd_tip_record* tips_out, int64_t tips_capacity,

@@ -59,10 +59,10 @@ struct FastHostLayout {
 int fast_build_layout(FastHostLayout& L, int64_t n, int N, const int32_t* entries,
                       const double* coords, const uint8_t* btype, const double* lambda,
                       const double* beta, const double* hist, bool history,
-                      const uint8_t* nofail);
+                      const uint8_t* nofail, int T, int64_t own_begin, int64_t own_end);
 void fast_set_laws(const DevLaw* laws, int n, cudaStream_t stream);
 cudaError_t launch_fast(const DevArgs& A, const FastDev& F, int mode, int kind, int tiles,
-                        int max_halo, cudaStream_t st);
+                        cudaStream_t st);
 template <class T, int W>
 void launch_gather_rows(const T* in, T* out, const int* map, long long n, cudaStream_t st);
 void launch_fast_materialize(const int32_t* entries0, const int* inv, const int* tile_of,
@@ -75,6 +75,18 @@ void exact_set_laws(const DevLaw* laws, int n, cudaStream_t stream);
 cudaError_t launch_exact(const DevArgs& A, int mode, bool node_sum, cudaStream_t st);
 
 // pd_aux.cu
+struct SyncArgs {
+    unsigned long long* peer_sync[PD_MAX_RANKS];  // every rank's sync words (own included)
+    unsigned long long* my_sync;
+    long long* err_step;
+    int rank, world;
+    unsigned long long epoch;
+    long long timeout_ns;
+};
+void launch_slab_sync(const SyncArgs& S, cudaStream_t st);
+void launch_node_values(const double4* u, const double* v, const double* a, const double4* xv,
+                        const double* body, const double* ext, const long long* rows,
+                        long long count, double* out, cudaStream_t st);
 void launch_pack_xv(const double* coords, const double* volume, long long n, double4* xv,
                     cudaStream_t st);
 void launch_pack_u(const double* u, const uint8_t* nofail, long long n, double4* out,

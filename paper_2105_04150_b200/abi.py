@@ -101,6 +101,15 @@ HOOK = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(pd_state), C.POINTER(pd_force_
 
 # ---- errors (the reference's exception types) ---------------------------------
 
+PD_MAX_RANKS = 16
+
+
+class pd_peer_handle(C.Structure):
+    _fields_ = [("device", i32), ("pid", i32), ("ipc_u0", C.c_uint8 * 64),
+                ("ipc_u1", C.c_uint8 * 64), ("ipc_sync", C.c_uint8 * 64),
+                ("u0", C.c_uint64), ("u1", C.c_uint64), ("sync", C.c_uint64)]
+
+
 class InvalidArgument(ValueError):
     """std::invalid_argument"""
 

@@ -299,6 +299,31 @@ void launch_validate_entries(const int32_t* entries, long long n, int N,
         validate_entries_kernel<<<grid_for(n * N), TPB, 0, st>>>(entries, n, N, bad_row);
 }
 
+// Force the (lazily loaded) module functions of this unit in now: with CUDA
+// lazy loading the first launch of a kernel may wait for the whole device,
+// which deadlocks against a peer rank's spinning slab_sync_kernel.
+template <class K> static void preload(K k) {
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(k));
+}
+
+void preload_aux() {
+    preload(pack_xv_kernel);
+    preload(pack_u_kernel);
+    preload(unpack_u_kernel);
+    preload(init_alive_kernel);
+    preload(validate_entries_kernel);
+    preload(vv_prologue_kernel);
+    preload(slab_sync_kernel);
+    preload(check_finite_kernel);
+    preload(materialize_entries_kernel);
+    preload(damage_kernel);
+    preload(inv_kernel);
+    preload(sum_kernel);
+    preload(tips_kernel);
+    preload(node_values_kernel);
+}
+
 void launch_slab_sync(const SyncArgs& S, cudaStream_t st) {
     slab_sync_kernel<<<1, 32, 0, st>>>(S);
 }

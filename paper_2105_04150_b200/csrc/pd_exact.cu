@@ -259,6 +259,29 @@ cudaError_t launch_mode(const DevArgs& A, int mode, int M, dim3 grid, cudaStream
 
 } // namespace
 
+template <class K> static void preload(K k) {
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(k));
+}
+
+template <int MODE> static void preload_mode() {
+    preload(exact_step_kernel<MODE, 1, false>);
+    preload(exact_step_kernel<MODE, 2, false>);
+    preload(exact_step_kernel<MODE, 4, false>);
+    preload(exact_step_kernel<MODE, 8, false>);
+    preload(exact_step_kernel<MODE, 1, true>);
+    preload(exact_step_kernel<MODE, 2, true>);
+    preload(exact_step_kernel<MODE, 4, true>);
+    preload(exact_step_kernel<MODE, 8, true>);
+}
+
+void preload_exact() {
+    preload_mode<0>();
+    preload_mode<1>();
+    preload_mode<2>();
+    preload_mode<3>();
+}
+
 cudaError_t launch_exact(const DevArgs& A, int mode, bool node_sum, cudaStream_t st) {
     const long long nodes = A.end - A.begin;
     if (nodes <= 0)

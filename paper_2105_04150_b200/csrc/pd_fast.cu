@@ -292,18 +292,30 @@ int smem_bytes(int kind, int cap) {
     return cap * int(sizeof(float4) + sizeof(float2) + (kind == 0 ? 0 : sizeof(float)));
 }
 
+// The dynamic shared-memory limit of each instantiation is lifted once, to
+// the largest halo the layout admits (FAST_MAX_HALO), by the first launch or
+// by preload_fast() -- never inside a multi-GPU run.
+template <int MODE, int KIND, int TT, int MINB, bool PRE> struct KernelCfg {
+    static bool done;
+    static cudaError_t ensure() {
+        if (done)
+            return cudaSuccess;
+        const cudaError_t e = cudaFuncSetAttribute(fast_step_kernel<MODE, KIND, TT, MINB, PRE>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   smem_bytes(KIND, FAST_MAX_HALO + 1 + 31));
+        done = e == cudaSuccess;
+        return e;
+    }
+};
+template <int MODE, int KIND, int TT, int MINB, bool PRE>
+bool KernelCfg<MODE, KIND, TT, MINB, PRE>::done = false;
+
 template <int MODE, int KIND, int TT, int MINB, bool PRE>
 cudaError_t launch_cfg(const DevArgs& A, const FastDev& F, int tiles, cudaStream_t st) {
-    static int configured = 0;
-    const int smem = smem_bytes(KIND, F.cap);
-    if (smem > configured) {
-        cudaError_t e = cudaFuncSetAttribute(fast_step_kernel<MODE, KIND, TT, MINB, PRE>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess)
-            return e;
-        configured = smem;
-    }
-    fast_step_kernel<MODE, KIND, TT, MINB, PRE><<<tiles, TT, smem, st>>>(A, F);
+    const cudaError_t e = KernelCfg<MODE, KIND, TT, MINB, PRE>::ensure();
+    if (e != cudaSuccess)
+        return e;
+    fast_step_kernel<MODE, KIND, TT, MINB, PRE><<<tiles, TT, smem_bytes(KIND, F.cap), st>>>(A, F);
     return cudaGetLastError();
 }
 
@@ -389,6 +401,44 @@ __global__ void fast_materialize_kernel(const int32_t* entries0, const int* inv,
 }
 
 } // namespace
+
+template <int MODE, int KIND, int TT, int MINB, bool PRE> static void preload_one() {
+    // load the function and lift its shared-memory limit now, so no launch
+    // inside a multi-GPU run has to touch the module
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(
+                                  fast_step_kernel<MODE, KIND, TT, MINB, PRE>));
+    KernelCfg<MODE, KIND, TT, MINB, PRE>::ensure();
+}
+
+template <int MODE, int KIND> static void preload_mk() {
+    preload_one<MODE, KIND, 256, 4, false>();
+    preload_one<MODE, KIND, 512, 2, false>();
+    if (MODE == 1 && KIND == 0) {
+        preload_one<MODE, KIND, 256, 3, true>();
+        preload_one<MODE, KIND, 512, 2, true>();
+    }
+}
+
+template <int MODE> static void preload_m() {
+    preload_mk<MODE, 0>();
+    preload_mk<MODE, 1>();
+    preload_mk<MODE, 2>();
+}
+
+void preload_fast() {
+    preload_m<0>();
+    preload_m<1>();
+    preload_m<2>();
+    preload_m<3>();
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(gather_rows_kernel<double4, 1>));
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(gather_rows_kernel<double, 1>));
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(gather_rows_kernel<double, 3>));
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(gather_rows_kernel<int32_t, 1>));
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(gather_rows_kernel<uint8_t, 3>));
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(fast_materialize_kernel));
+}
 
 cudaError_t launch_fast(const DevArgs& A, const FastDev& F, int mode, int kind, int tiles,
                         cudaStream_t st) {

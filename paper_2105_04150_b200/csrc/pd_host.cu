@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <unistd.h>
 #include <string>
 #include <vector>
@@ -1017,6 +1018,17 @@ int pd_ctx_connect(pd_ctx* ctx, int32_t rank, int32_t world, const pd_peer_handl
         return fail(PD_E_INVALID_ARGUMENT, "connect: bad neighbour ranks %d / %d", lo, hi);
     if (!ctx->sync.p)
         return fail(PD_E_INVALID_ARGUMENT, "connect: export this context first");
+    // every kernel a run may launch is loaded now: under CUDA lazy loading a
+    // first launch can wait for the whole device, which would deadlock
+    // against a peer rank's spinning sync kernel (callers barrier after
+    // connect, so no rank spins before every rank has loaded)
+    static std::once_flag loaded;
+    std::call_once(loaded, [] {
+        preload_aux();
+        preload_exact();
+        preload_fast();
+    });
+    PD_CK(cudaGetLastError());
     const int me = int(getpid());
     // map every peer's u buffers and sync words
     void* mapped[PD_MAX_RANKS][3] = {};

@@ -70,6 +70,11 @@ void launch_fast_materialize(const int32_t* entries0, const int* inv, const int*
                              const unsigned short* lidx, const float* hist32, long long n, int N,
                              int32_t* entries_out, double* hist_out, cudaStream_t st);
 
+// every kernel of the library loaded up front (multi-GPU runs, see pd_aux.cu)
+void preload_aux();
+void preload_exact();
+void preload_fast();
+
 // pd_exact.cu
 void exact_set_laws(const DevLaw* laws, int n, cudaStream_t stream);
 cudaError_t launch_exact(const DevArgs& A, int mode, bool node_sum, cudaStream_t st);

@@ -160,6 +160,15 @@ def library() -> C.CDLL:
         lib.pd_ctx_live_bonds.argtypes = [C.c_void_p]
         lib.pd_ctx_live_bonds.restype = C.c_int64
         lib.pd_damage.argtypes = [C.POINTER(abi.pd_neighbor_list), C.POINTER(C.c_double)]
+        lib.pd_ctx_upload_part.argtypes = [C.c_void_p, C.POINTER(abi.pd_bundle),
+                                           C.POINTER(abi.pd_state), C.c_int32, C.c_int64,
+                                           C.c_int64]
+        lib.pd_ctx_internal_index.argtypes = [C.c_void_p, abi.i64p, C.c_int64, abi.i64p]
+        lib.pd_ctx_export.argtypes = [C.c_void_p, C.POINTER(abi.pd_peer_handle)]
+        lib.pd_ctx_connect.argtypes = [C.c_void_p, C.c_int32, C.c_int32,
+                                       C.POINTER(abi.pd_peer_handle), C.c_int32, C.c_int32,
+                                       abi.i64p, abi.i64p]
+        lib.pd_ctx_node_values.argtypes = [C.c_void_p, abi.i64p, C.c_int64, abi.f64p]
         lib.pd_last_error.restype = C.c_char_p
         _LIB = lib
     return _LIB
@@ -234,6 +243,57 @@ class Context:
         self.N = int(state.connectivity.group_size)
         self.history = bundle.model.needs_history()
         self.tip_names = sorted(bundle.bc.tip_sets)
+
+    # ---- multi-GPU slab parts (pd_b200.h "multi-GPU z-slabs") -------------
+
+    def upload_part(self, bundle: ModelBundle, state: SimulationState, variant,
+                    own_begin: int, own_end: int) -> None:
+        m = Marshal()
+        b = m.bundle(bundle)
+        st = m.state(state)
+        self._check(self.lib.pd_ctx_upload_part(self.h, C.byref(b), C.byref(st), int(variant),
+                                                int(own_begin), int(own_end)))
+        self.n = state.size()
+        self.N = int(state.connectivity.group_size)
+        self.history = bundle.model.needs_history()
+        self.tip_names = sorted(bundle.bc.tip_sets)
+
+    def internal_index(self, local: np.ndarray) -> np.ndarray:
+        local = np.ascontiguousarray(local, dtype=np.int64)
+        out = np.empty_like(local)
+        self._check(self.lib.pd_ctx_internal_index(self.h, abi.ptr(local, C.c_int64), local.size,
+                                                   abi.ptr(out, C.c_int64)))
+        return out
+
+    def export(self) -> bytes:
+        h = abi.pd_peer_handle()
+        self._check(self.lib.pd_ctx_export(self.h, C.byref(h)))
+        return bytes(h)
+
+    def connect(self, rank: int, world: int, handles, lo: int, hi: int,
+                send_lo: Optional[np.ndarray], send_hi: Optional[np.ndarray]) -> None:
+        arr = (abi.pd_peer_handle * world)()
+        for k, hb in enumerate(handles):
+            C.memmove(C.byref(arr[k]), hb, C.sizeof(abi.pd_peer_handle))
+        keep = []
+
+        def p64(a):
+            if a is None:
+                return None
+            a = np.ascontiguousarray(a, dtype=np.int64)
+            keep.append(a)
+            return abi.ptr(a, C.c_int64)
+        self._check(self.lib.pd_ctx_connect(self.h, int(rank), int(world), arr, int(lo), int(hi),
+                                            p64(send_lo), p64(send_hi)))
+
+    def node_values(self, local: np.ndarray) -> np.ndarray:
+        """u, v, a, body_force*V, external_force*V of local nodes (k x 15)."""
+        local = np.ascontiguousarray(local, dtype=np.int64)
+        out = np.empty((local.size, 15))
+        if local.size:
+            self._check(self.lib.pd_ctx_node_values(self.h, abi.ptr(local, C.c_int64),
+                                                     local.size, abi.ptr(out, C.c_double)))
+        return out
 
     def run(self, steps: int, first_step: int, integrator=IntegratorKind.velocity_verlet,
             write_every: int = 0, variant=KernelVariant.bond_parallel) -> SimulateResult:

@@ -165,7 +165,7 @@ def run_reference_arm(args):
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"cfg4 lattice {args.size}^3 = {n} nodes, delta=3dx (N=128), "
                                "PMB, velocity-Verlet (reference CPU, bounded z-slab sample)",
@@ -176,31 +176,32 @@ def run_reference_arm(args):
     return 0
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--variant", default="fast", choices=["exact", "fast"])
-    ap.add_argument("--size", type=int, default=216)
-    ap.add_argument("--e2e-steps", type=int, default=100)
-    ap.add_argument("--no-cpu", action="store_true")
-    args = ap.parse_args()
-    args.warmup = max(args.warmup, 3)
-    if args.impl == "reference":
-        return run_reference_arm(args)
+def _summary(args, value, ms_step, world, n, N, live, bytes_step, achieved, e2e, launches,
+             clocks, cpu, variant_name, extra_config=None):
+    peak, peak_kind = measured_peaks()
+    cfg = {"workload": f"cfg4 lattice {args.size}^3 = {n} nodes, delta=3dx (N={N}), "
+                       f"PMB c=1 s_c=1e6, velocity-Verlet, dt=1e-3, seeded u"
+                       + (f", {world} z-slabs" if world > 1 else ""),
+           "nodes": n, "group_size": N, "live_bonds": live, "variant": variant_name,
+           "l2": f"inputs larger than L2 ({bytes_step / 1e9:.2f} GB/step algorithmic)",
+           "parallelism": f"z-slab x{world}" if world > 1 else "single GPU"}
+    cfg.update(extra_config or {})
+    return {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64" if variant_name == "exact" else "f32 bond math / f64 state",
+        "data": "synthetic", "config": cfg,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
+                     "bytes_per_step": bytes_step},
+        "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "cpu_baseline": cpu,
+    }
 
+
+def run_single(args, variant, local):
     import torch
-    from paper_2105_04150_b200 import (IntegratorKind, KernelVariant, SimulateOptions, engine)
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        raise SystemExit("multi-GPU slabs: not in this build yet")
-    torch.cuda.set_device(local)
-    variant = KernelVariant.fast if args.variant == "fast" else KernelVariant.bond_parallel
+    from paper_2105_04150_b200 import IntegratorKind, SimulateOptions, engine, make_state
     counts = (args.size, args.size, args.size)
     t_setup = time.perf_counter()
     bundle, fam, state0 = build_workload(counts)
@@ -228,16 +229,13 @@ def main():
     launches = ctx.launch_count() - launches0
     ms_total = ev0.elapsed_time(ev1)
     ms_step = ms_total / args.steps
-    live_end = ctx.live_bonds()
     value = live * args.steps / (ms_total / 1e3)
-    peak, peak_kind = measured_peaks()
     bytes_step = algorithmic_bytes(n, N, live)
     achieved = bytes_step / (ms_step / 1e3) / 1e9
     ctx.close()
     del ctx
 
     # end to end: one simulate() call through the C ABI from host buffers
-    from paper_2105_04150_b200 import make_state
     st = make_state(fam, False)
     st.u = state0.u.copy()
     e2e_steps = args.e2e_steps
@@ -248,35 +246,162 @@ def main():
     engine.simulate(bundle, st, SimulateOptions(e2e_steps, 0, 0, IntegratorKind.velocity_verlet,
                                                 variant))
     e2e_s = time.perf_counter() - t0
-    e2e_value = live * e2e_steps / e2e_s
-
+    e2e = {"value": live * e2e_steps / e2e_s, "unit": UNIT,
+           "h2d_bytes_per_step": h2d // e2e_steps, "d2h_bytes_per_step": d2h // e2e_steps,
+           "seconds": e2e_s,
+           "how": f"one simulate() call via the C ABI, {e2e_steps} steps, host buffers "
+                  "(upload + layout + run + download inside the timed region)"}
     cpu = None if args.no_cpu else cpu_baseline(counts)
-    out = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None,
-        "dtype": "f64" if variant != KernelVariant.fast else "f32 bond math / f64 state",
-        "data": "synthetic",
-        "config": {"workload": f"cfg4 lattice {args.size}^3 = {n} nodes, delta=3dx (N={N}), "
-                               f"PMB c=1 s_c=1e6, velocity-Verlet, dt=1e-3, seeded u",
-                   "nodes": n, "group_size": N, "live_bonds": live, "variant": args.variant,
-                   "l2": f"inputs larger than L2 ({bytes_step / 1e9:.2f} GB/step algorithmic)",
-                   "setup_s": round(setup_s, 2)},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
-                     "bytes_per_step": bytes_step},
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d // e2e_steps,
-                "d2h_bytes_per_step": d2h // e2e_steps,
-                "how": f"one simulate() call via the C ABI, {e2e_steps} steps, host buffers "
-                       "(upload + run + download inside the timed region)"},
-        "gpu_launches": launches,
-        "clocks": clk.summary(),
-        "cpu_baseline": cpu,
-        "live_bonds_end": live_end,
-    }
+    out = _summary(args, value, ms_step, 1, n, N, live, bytes_step, achieved, e2e, launches,
+                   clk.summary(), cpu, args.variant, {"setup_s": round(setup_s, 2)})
+    print(json.dumps(out))
+    return 0
+
+
+def run_slabs(args, variant, rank, world, local):
+    """Strong scaling of the same lattice over `world` GPUs: rank r owns a
+    z-slab of whole planes and builds its local model (owned planes + 3 ghost
+    planes per cut, built on its own GPU); ghost rows are pushed by the step
+    kernel over NVLink (paper_2105_04150_b200.slabs)."""
+    import math
+
+    import torch
+    import torch.distributed as dist
+    from paper_2105_04150_b200 import IntegratorKind, geometry, make_state, slabs
+    from paper_2105_04150_b200.types import (BoundaryConditions, Corrections, DamageLaw,
+                                             DamageModel, ModelBundle, ParticleSet)
+    import scenarios as S
+
+    nx = ny = nz = args.size
+    plane = nx * ny
+    g = int(math.ceil(HORIZON))
+    cuts = [int(round(r * nz / world)) for r in range(world + 1)]
+    z0, z1 = cuts[rank], cuts[rank + 1]
+    zl0, zl1 = max(0, z0 - g), min(nz, z1 + g)
+    t_setup = time.perf_counter()
+    grid = geometry.GridDesc((0.0, 0.0, float(zl0)), 1.0, (nx, ny, zl1 - zl0))
+    coords = geometry.grid_coordinates(grid)
+    nl = grid.node_count()
+    particles = ParticleSet(coords, np.ones(nl), np.ones(nl), np.zeros(nl, np.uint16))
+    bundle = ModelBundle(particles, DamageModel([DamageLaw.pmb(1.0, 1e6)]), Corrections(),
+                         BoundaryConditions.none(nl), 1e-3)
+    fam = geometry.build_family(coords, HORIZON, grid)
+    state = make_state(fam, False)
+    state.u = S.seed_displacements(coords)
+    ob, oe = (z0 - zl0) * plane, (z1 - zl0) * plane
+    part = slabs.SlabPart(rank, world, z0 * plane, z1 * plane,
+                          np.arange(zl0 * plane, zl1 * plane, dtype=np.int64), ob, oe,
+                          rank - 1 if rank > 0 else -1, rank + 1 if rank + 1 < world else -1)
+    ranges = [(cuts[r] * plane, cuts[r + 1] * plane) for r in range(world)]
+    comm = slabs.TorchComm()
+    Ns = comm.allgather(int(fam.group_size))
+    if len(set(Ns)) != 1:
+        raise SystemExit(f"slab families disagree on the group size: {Ns}")
+    live_own = int(fam.n_neigh[ob:oe].sum())
+    setup_s = time.perf_counter() - t_setup
+
+    red_dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+
+    def timed_max(ms):
+        t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # e2e through the rank-local public API: host buffers -> upload + connect
+    # -> run -> owned rows back to host, max over ranks
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    sr = slabs.SlabRank(comm, local)
+    sr.setup(part, ranges, bundle, state, variant)
+    sr.run(args.e2e_steps, 0, IntegratorKind.velocity_verlet)
+    down = make_state(fam, False)
+    sr.ctx.download(down)
+    torch.cuda.synchronize()
+    e2e_s = timed_max((time.perf_counter() - t0) * 1e3) / 1e3
+    sr.close()
+
+    sr = slabs.SlabRank(comm, local)
+    sr.setup(part, ranges, bundle, state, variant)
+    ctx = sr.ctx
+    stream = torch.cuda.ExternalStream(ctx.stream())
+    sr.run(args.warmup, 0, IntegratorKind.velocity_verlet)
+    torch.cuda.synchronize()
+    dist.barrier()
+    launches0 = ctx.launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        dist.barrier()
+        ev0.record(stream)
+        sr.run(args.steps, args.warmup, IntegratorKind.velocity_verlet)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms_total = timed_max(ev0.elapsed_time(ev1))
+    launches = ctx.launch_count() - launches0
+    sr.close()
+    tot = torch.tensor([live_own, launches], dtype=torch.int64, device=red_dev)
+    dist.all_reduce(tot)
+    live, launches = int(tot[0].item()), int(tot[1].item())
+    n = nx * ny * nz
+    N = Ns[0]
+    ms_step = ms_total / args.steps
+    value = live * args.steps / (ms_total / 1e3)
+    bytes_step = algorithmic_bytes(n, N, live)
+    achieved = bytes_step / (ms_step / 1e3) / 1e9
+    halo_bytes = 2 * (world - 1) * g * plane * 32 * 2  # u pushed both ways per cut, per step
+    e2e = {"value": live * args.e2e_steps / e2e_s, "unit": UNIT,
+           "h2d_bytes_per_step": (nl * (24 * 3 + 16 + 24 + fam.group_size * 4)) // args.e2e_steps,
+           "d2h_bytes_per_step": (nl * (24 * 3 + fam.group_size * 4 + 4)) // args.e2e_steps,
+           "seconds": e2e_s,
+           "how": f"per rank: host buffers -> upload_part + connect -> {args.e2e_steps} steps -> "
+                  "download, max over ranks (bytes are rank 0's)"}
+    clocks = comm.allgather(clk.summary())
     if rank == 0:
+        out = _summary(args, value, ms_step, world, n, N, live, bytes_step, achieved, e2e,
+                       launches, clocks[0], None, args.variant,
+                       {"setup_s": round(setup_s, 2), "halo_bytes_per_step_nvlink": halo_bytes,
+                        "clocks_all_ranks": clocks})
         print(json.dumps(out))
     return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--variant", default="fast", choices=["exact", "fast"])
+    ap.add_argument("--size", type=int, default=216)
+    ap.add_argument("--e2e-steps", type=int, default=1000)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+    from paper_2105_04150_b200 import KernelVariant
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local)
+    variant = KernelVariant.fast if args.variant == "fast" else KernelVariant.bond_parallel
+    if world == 1:
+        return run_single(args, variant, local)
+    import torch.distributed as dist
+    if torch.cuda.device_count() >= world:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:  # several ranks share a GPU (a 1-GPU test box): gloo for the host plumbing
+        dist.init_process_group("gloo")
+    try:
+        return run_slabs(args, variant, rank, world, local)
+    finally:
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -27,6 +27,7 @@ UNITS = {
     "pd_host.cu": ["-fmad=false"],
     "pd_fast.cu": ["-fmad=true", "-diag-suppress=186"],
     "pd_family.cu": ["-fmad=false"],
+    "pd_layout.cu": ["-fmad=false"],
 }
 HEADERS = ["pd_device.cuh", "pd_internal.h", "pd_fast.cuh"]
 

@@ -21,9 +21,6 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
-#include <thread>
-#include <unordered_map>
-#include <unordered_set>
 #include <vector>
 
 #include "pd_device.cuh"
@@ -476,261 +473,6 @@ void launch_fast_materialize(const int32_t* entries0, const int* inv, const int*
         fast_materialize_kernel<<<unsigned((n + 127) / 128), 128, 0, st>>>(
             entries0, inv, tile_of, tile_start, slot_off, T, lidx, hist32, n, N, entries_out,
             hist_out);
-}
-
-// ---- host-side layout construction -------------------------------------------
-
-int fast_build_layout(FastHostLayout& L, int64_t n, int N, const int32_t* entries,
-                      const double* coords, const uint8_t* btype, const double* lambda,
-                      const double* beta, const double* hist, bool history,
-                      const uint8_t* nofail, int T, int64_t own_begin, int64_t own_end) {
-    // only the owned nodes [own_begin, own_end) are tiled (all of them on one
-    // GPU); they come first in the internal order, the ghost nodes of a
-    // multi-GPU slab follow in local order
-    // bricks of ~8 nodes per axis from the bounding box and mean spacing
-    double lo[3], hi[3];
-    for (int d = 0; d < 3; ++d)
-        lo[d] = hi[d] = coords[d];
-    for (int64_t i = 1; i < n; ++i)
-        for (int d = 0; d < 3; ++d) {
-            lo[d] = std::min(lo[d], coords[3 * i + d]);
-            hi[d] = std::max(hi[d], coords[3 * i + d]);
-        }
-    double ext[3], prod = 1.0;
-    int dims = 0;
-    for (int d = 0; d < 3; ++d) {
-        ext[d] = hi[d] - lo[d];
-        if (ext[d] > 0) {
-            prod *= ext[d];
-            ++dims;
-        }
-    }
-    const double h = dims == 0 ? 1.0 : std::pow(prod / double(n), 1.0 / dims);
-    long long nb[3];
-    double len[3];
-    for (int d = 0; d < 3; ++d) {
-        nb[d] = ext[d] > 0 ? std::max(1LL, (long long)std::llround(ext[d] / (8.0 * h))) : 1;
-        len[d] = ext[d] > 0 ? ext[d] / double(nb[d]) : 1.0;
-    }
-    // lattice-like axes (few distinct coordinates): bricks of exactly 16 x 4 x 8
-    // grid planes, so a half-warp covers a whole 16-node x-run and its
-    // neighbour runs are contiguous shared-memory records (conflict-free
-    // LDS.64 over 16 lanes, LDS.128 over 8); otherwise bins of ~8 mean spacings
-    const long long kBrick[3] = {16, 4, T / 64};
-    std::unordered_map<double, long long> rank[3];
-    bool lattice[3] = {false, false, false};
-    for (int d = 0; d < 3; ++d) {
-        std::unordered_set<double> vals;
-        bool ok = true;
-        for (int64_t i = 0; i < n && ok; ++i) {
-            vals.insert(coords[3 * i + d]);
-            ok = vals.size() <= 4096;
-        }
-        if (!ok)
-            continue;
-        std::vector<double> sorted(vals.begin(), vals.end());
-        std::sort(sorted.begin(), sorted.end());
-        for (size_t k = 0; k < sorted.size(); ++k)
-            rank[d][sorted[k]] = (long long)k;
-        lattice[d] = true;
-        nb[d] = (long long)(sorted.size() + kBrick[d] - 1) / kBrick[d];
-    }
-    const long long nbricks = nb[0] * nb[1] * nb[2];
-    std::vector<long long> brick(static_cast<size_t>(n));
-    std::vector<long long> count(size_t(nbricks + 1), 0);
-    for (int64_t i = own_begin; i < own_end; ++i) {
-        long long b[3];
-        for (int d = 0; d < 3; ++d) {
-            long long c;
-            if (lattice[d])
-                c = rank[d][coords[3 * i + d]] / kBrick[d];
-            else
-                c = ext[d] > 0 ? (long long)std::floor((coords[3 * i + d] - lo[d]) / len[d]) : 0;
-            b[d] = std::min(std::max(c, 0LL), nb[d] - 1);
-        }
-        brick[size_t(i)] = (b[2] * nb[1] + b[1]) * nb[0] + b[0];
-        ++count[size_t(brick[size_t(i)] + 1)];
-    }
-    for (long long b = 0; b < nbricks; ++b)
-        count[size_t(b + 1)] += count[size_t(b)];
-    L.perm.assign(size_t(n), 0);
-    L.inv.assign(size_t(n), 0);
-    {
-        std::vector<long long> fill(count.begin(), count.end() - 1);
-        for (int64_t i = own_begin; i < own_end; ++i)
-            L.perm[size_t(fill[size_t(brick[size_t(i)])]++)] = int(i);
-        int64_t g = own_end - own_begin;
-        for (int64_t i = 0; i < n; ++i)
-            if (i < own_begin || i >= own_end)
-                L.perm[size_t(g++)] = int(i);
-    }
-    for (int64_t ii = 0; ii < n; ++ii)
-        L.inv[size_t(L.perm[size_t(ii)])] = int(ii);
-
-    // tiles: <= T consecutive internal nodes of one brick
-    L.T = T;
-    L.tile_start.clear();
-    for (long long b = 0; b < nbricks; ++b)
-        for (long long s = count[size_t(b)]; s < count[size_t(b + 1)]; s += T)
-            L.tile_start.push_back(int(s));
-    L.tile_start.push_back(int(own_end - own_begin));
-    const int tiles = int(L.tile_start.size()) - 1;
-    L.n_tiles = tiles;
-    L.tile_of.assign(size_t(n), -1);
-    L.own_slot.assign(size_t(n), 0);
-    for (int t = 0; t < tiles; ++t)
-        for (int ii = L.tile_start[size_t(t)]; ii < L.tile_start[size_t(t + 1)]; ++ii)
-            L.tile_of[size_t(ii)] = t;
-
-    struct TileOut {
-        std::vector<int> halo;
-        std::vector<unsigned short> lidx;
-        std::vector<float> hist, lambda, beta;
-        std::vector<uint8_t> btype;
-        int kmax8 = 0, nf_start = 0x7fffffff;
-    };
-    std::vector<TileOut> out(static_cast<size_t>(tiles));
-    int error = 0;
-    auto work = [&](int t0, int t1) {
-        std::vector<int> ids;
-        for (int t = t0; t < t1; ++t) {
-            TileOut& o = out[size_t(t)];
-            const int ts = L.tile_start[size_t(t)], te = L.tile_start[size_t(t + 1)];
-            ids.clear();
-            int kmax = 0;
-            for (int ii = ts; ii < te; ++ii) {
-                ids.push_back(ii);
-                const int64_t i = L.perm[size_t(ii)];
-                int live = 0;
-                for (int k = 0; k < N; ++k) {
-                    const int32_t j = entries[i * N + k];
-                    if (j >= 0) {
-                        ids.push_back(L.inv[size_t(j)]);
-                        ++live;
-                    }
-                }
-                kmax = std::max(kmax, live);
-            }
-            // shared-memory order = reference (original) node order: on a lattice an
-            // x-run of neighbours stays contiguous across brick boundaries, so a
-            // quarter-warp's 16-byte loads hit distinct banks.  No-failure nodes go
-            // last so a slot offset >= nf_start identifies them.
-            for (int& id : ids)
-                id = L.perm[size_t(id)];
-            std::sort(ids.begin(), ids.end());
-            ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
-            if (nofail)
-                std::stable_partition(ids.begin(), ids.end(),
-                                      [&](int j) { return nofail[j] == 0; });
-            if (ids.size() + 1 > size_t(FAST_MAX_HALO + 1)) {
-                error = 1;
-                continue;
-            }
-            o.nf_start = 0x7fffffff;
-            size_t split = ids.size();  // ids[0, split) regular, [split, end) no-failure
-            o.halo.resize(ids.size());
-            for (size_t q = 0; q < ids.size(); ++q) {
-                o.halo[q] = L.inv[size_t(ids[q])];
-                if (nofail && nofail[ids[q]] && split == ids.size()) {
-                    split = q;
-                    o.nf_start = 8 * (int(q) + 1);
-                }
-            }
-            // shared-memory position (halo index + 1) of reference node j
-            auto pos_of = [&](int j) {
-                const bool nf = nofail && nofail[j];
-                auto lo = nf ? ids.begin() + std::ptrdiff_t(split) : ids.begin();
-                auto hi = nf ? ids.end() : ids.begin() + std::ptrdiff_t(split);
-                return int(std::lower_bound(lo, hi, j) - ids.begin()) + 1;
-            };
-            for (int ii = ts; ii < te; ++ii) {
-                const int orig = L.perm[size_t(ii)];
-                L.own_slot[size_t(ii)] = (unsigned short)(pos_of(orig) |
-                                                          ((nofail && nofail[orig]) ? 0x8000 : 0));
-            }
-            o.kmax8 = (kmax + 7) / 8 * 8;
-            const size_t slots = size_t(o.kmax8) * size_t(T);
-            o.lidx.assign(slots, 0);
-            if (history)
-                o.hist.assign(slots, 0.f);
-            if (btype)
-                o.btype.assign(slots, 0);
-            if (lambda)
-                o.lambda.assign(slots, 1.f);
-            if (beta)
-                o.beta.assign(slots, 1.f);
-            for (int ii = ts; ii < te; ++ii) {
-                const int tt = ii - ts;
-                const int64_t i = L.perm[size_t(ii)];
-                int c = 0;
-                for (int k = 0; k < N; ++k) {
-                    const int32_t j = entries[i * N + k];
-                    if (j < 0)
-                        continue;
-                    const size_t s = size_t(c >> 3) * size_t(T) * 8 + size_t(tt) * 8 + size_t(c & 7);
-                    o.lidx[s] = (unsigned short)(8 * pos_of(j));
-                    const int64_t idx = i * N + k;
-                    if (history)
-                        o.hist[s] = hist ? float(hist[idx]) : 0.f;
-                    if (btype)
-                        o.btype[s] = btype[idx];
-                    if (lambda)
-                        o.lambda[s] = float(lambda[idx]);
-                    if (beta)
-                        o.beta[s] = float(beta[idx]);
-                    ++c;
-                }
-            }
-        }
-    };
-    const int threads = std::max(1, std::min(32, int(std::thread::hardware_concurrency())));
-    std::vector<std::thread> pool;
-    const int chunk = (tiles + threads - 1) / threads;
-    for (int w = 0; w < threads; ++w) {
-        const int t0 = w * chunk, t1 = std::min(tiles, t0 + chunk);
-        if (t0 < t1)
-            pool.emplace_back(work, t0, t1);
-    }
-    for (auto& th : pool)
-        th.join();
-    if (error)
-        return 1;
-
-    L.halo_off.assign(size_t(tiles + 1), 0);
-    L.nf_start.assign(size_t(tiles), 0x7fffffff);
-    L.slot_off.assign(size_t(tiles), 0);
-    L.kmax8.assign(size_t(tiles), 0);
-    long long slots = 0;
-    L.max_halo = 0;
-    for (int t = 0; t < tiles; ++t) {
-        L.halo_off[size_t(t + 1)] = L.halo_off[size_t(t)] + (long long)out[size_t(t)].halo.size();
-        L.slot_off[size_t(t)] = slots;
-        slots += (long long)out[size_t(t)].lidx.size();
-        L.kmax8[size_t(t)] = out[size_t(t)].kmax8;
-        L.nf_start[size_t(t)] = out[size_t(t)].nf_start;
-        L.max_halo = std::max(L.max_halo, int(out[size_t(t)].halo.size()));
-    }
-    L.total_slots = slots;
-    L.halo.resize(size_t(L.halo_off[size_t(tiles)]));
-    L.lidx.resize(size_t(slots));
-    L.hist.resize(history ? size_t(slots) : 0);
-    L.btype.resize(btype ? size_t(slots) : 0);
-    L.lambda.resize(lambda ? size_t(slots) : 0);
-    L.beta.resize(beta ? size_t(slots) : 0);
-    for (int t = 0; t < tiles; ++t) {
-        TileOut& o = out[size_t(t)];
-        std::copy(o.halo.begin(), o.halo.end(), L.halo.begin() + L.halo_off[size_t(t)]);
-        std::copy(o.lidx.begin(), o.lidx.end(), L.lidx.begin() + L.slot_off[size_t(t)]);
-        if (history)
-            std::copy(o.hist.begin(), o.hist.end(), L.hist.begin() + L.slot_off[size_t(t)]);
-        if (btype)
-            std::copy(o.btype.begin(), o.btype.end(), L.btype.begin() + L.slot_off[size_t(t)]);
-        if (lambda)
-            std::copy(o.lambda.begin(), o.lambda.end(), L.lambda.begin() + L.slot_off[size_t(t)]);
-        if (beta)
-            std::copy(o.beta.begin(), o.beta.end(), L.beta.begin() + L.slot_off[size_t(t)]);
-    }
-    return 0;
 }
 
 } // namespace pdb

@@ -14,6 +14,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <chrono>
 #include <cstring>
 #include <mutex>
 #include <unistd.h>
@@ -43,6 +44,20 @@ int ok() {
     g_err.clear();
     return PD_OK;
 }
+
+// PD_TIMING=1: host wall time of the setup / run / download phases on stderr
+struct PhaseTimer {
+    bool on = std::getenv("PD_TIMING") != nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void mark(const char* what) {
+        if (!on)
+            return;
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[pd timing] %-28s %9.3f ms\n", what,
+                     std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
 
 } // namespace
 
@@ -207,14 +222,8 @@ struct pd_ctx {
     bool fast = false;
     int kind = 2;  // fast kernel specialisation (pd_fast.cu)
     float pmb_c = 0, pmb_sc = 0, pmb_cv = 0;
-    int n_tiles = 0, max_halo = 0;
     int fast_T = FAST_T, fast_cfg = 0;
-    DevBuf<int> perm, inv, tile_of, tile_start, kmax8, halo, nf_start;
-    DevBuf<unsigned short> own_slot;
-    DevBuf<long long> halo_off, slot_off;
-    DevBuf<unsigned short> lidx;
-    DevBuf<float> hist32, lambda32, beta32;
-    DevBuf<uint8_t> btype_c;
+    FastLayoutDev lay;  // built on the device (pd_layout.cu)
     DevBuf<double4> scratch_d4;
     DevBuf<int32_t> scratch_n;
     DevBuf<uint8_t> scratch_u8;
@@ -222,22 +231,22 @@ struct pd_ctx {
     FastDev fast_args() const {
         FastDev F{};
         F.T = fast_T;
-        F.cap = (max_halo + 1 + 31) / 32 * 32;
+        F.cap = (lay.max_halo + 1 + 31) / 32 * 32;
         F.cfg = fast_cfg;
-        F.n_tiles = n_tiles;
+        F.n_tiles = lay.n_tiles;
         F.tile0 = 0;
-        F.tile_start = tile_start.p;
-        F.halo_off = halo_off.p;
-        F.halo = halo.p;
-        F.slot_off = slot_off.p;
-        F.kmax8 = kmax8.p;
-        F.own_slot = own_slot.p;
-        F.nf_start = nf_start.p;
-        F.lidx = lidx.p;
-        F.hist = hist32.p;
-        F.btype = btype_c.p;
-        F.lambda = lambda32.p;
-        F.beta = beta32.p;
+        F.tile_start = lay.tile_start.p;
+        F.halo_off = lay.halo_off.p;
+        F.halo = lay.halo.p;
+        F.slot_off = lay.slot_off.p;
+        F.kmax8 = lay.kmax8.p;
+        F.own_slot = lay.own_slot.p;
+        F.nf_start = lay.nf_start.p;
+        F.lidx = lay.lidx.p;
+        F.hist = lay.hist32.p;
+        F.btype = lay.btype_c.p;
+        F.lambda = lay.lambda32.p;
+        F.beta = lay.beta32.p;
         F.pmb_c = pmb_c;
         F.pmb_sc = pmb_sc;
         F.pmb_cv = pmb_cv;
@@ -487,7 +496,7 @@ int download(pd_ctx* ctx, pd_state* st, pd_force_field* forces, int32_t fields) 
     cudaStream_t s = ctx->stream;
     const int64_t n = ctx->n;
     const int64_t slots = n * ctx->N;
-    const int* inv = ctx->fast ? ctx->inv.p : nullptr;
+    const int* inv = ctx->fast ? ctx->lay.inv.p : nullptr;
     auto vec3_out = [&](const double* dev, double* host) -> int {
         const double* src = dev;
         if (inv) {
@@ -526,8 +535,8 @@ int download(pd_ctx* ctx, pd_state* st, pd_force_field* forces, int32_t fields) 
         if (st->connectivity.entries) {
             PD_CK(ctx->scratch_i32.alloc(size_t(slots)));
             if (ctx->fast)
-                launch_fast_materialize(ctx->entries.p, ctx->inv.p, ctx->tile_of.p,
-                                        ctx->tile_start.p, ctx->slot_off.p, ctx->fast_T, ctx->lidx.p,
+                launch_fast_materialize(ctx->entries.p, ctx->lay.inv.p, ctx->lay.tile_of.p,
+                                        ctx->lay.tile_start.p, ctx->lay.slot_off.p, ctx->fast_T, ctx->lay.lidx.p,
                                         nullptr, n, ctx->N, ctx->scratch_i32.p, nullptr, s);
             else
                 launch_materialize_entries(ctx->entries.p, ctx->alive.p, n, ctx->N, ctx->W,
@@ -551,8 +560,8 @@ int download(pd_ctx* ctx, pd_state* st, pd_force_field* forces, int32_t fields) 
     }
     if (want_hist) {
         if (ctx->fast) {
-            launch_fast_materialize(ctx->entries.p, ctx->inv.p, ctx->tile_of.p, ctx->tile_start.p,
-                                    ctx->slot_off.p, ctx->fast_T, ctx->lidx.p, ctx->hist32.p, n,
+            launch_fast_materialize(ctx->entries.p, ctx->lay.inv.p, ctx->lay.tile_of.p, ctx->lay.tile_start.p,
+                                    ctx->lay.slot_off.p, ctx->fast_T, ctx->lay.lidx.p, ctx->lay.hist32.p, n,
                                     ctx->N, nullptr, ctx->hist.p, s);
             ++ctx->launches;
         }
@@ -578,51 +587,41 @@ int setup_fast(pd_ctx* ctx, const pd_particles& p, const pd_state& st,
                int64_t nofail_size, pd_boundary* bc_tips) {
     cudaStream_t s = ctx->stream;
     const int64_t n = ctx->n;
-    FastHostLayout L;
     // PD_FAST_CFG selects a tile configuration (pd_fast.cu launch_one); the
     // default is 512-node tiles
     ctx->fast_cfg = 0;
     if (const char* e = std::getenv("PD_FAST_CFG"))
         ctx->fast_cfg = std::atoi(e);
     ctx->fast_T = (ctx->fast_cfg == 1 || ctx->fast_cfg == 2) ? 256 : 512;
-    const bool hist_in = ctx->history && st.bond_history &&
-                         st.bond_history_size == n * int64_t(ctx->N);
-    if (fast_build_layout(L, n, ctx->N, st.connectivity.entries, p.coords,
-                          st.connectivity.bond_type_size ? st.connectivity.bond_type : nullptr,
-                          corr.lambda_size ? corr.lambda : nullptr,
-                          corr.beta_size ? corr.beta : nullptr,
-                          hist_in ? st.bond_history : nullptr, ctx->history,
-                          nofail_size == n ? nofail : nullptr, ctx->fast_T, ctx->own_begin,
-                          ctx->own_end) != 0)
+    PhaseTimer tm;
+    FastLayoutIn in;
+    in.n = n;
+    in.own_begin = ctx->own_begin;
+    in.own_end = ctx->own_end;
+    in.N = ctx->N;
+    in.T = ctx->fast_T;
+    in.history = ctx->history;
+    in.xv = ctx->xv.p;
+    in.entries = ctx->entries.p;
+    bool any_nf = false;
+    for (int64_t i = 0; nofail && nofail_size == n && i < n && !any_nf; ++i)
+        any_nf = nofail[i] != 0;
+    in.nofail = any_nf ? ctx->nofail.p : nullptr;
+    in.hist = ctx->history ? ctx->hist.p : nullptr;
+    in.btype = st.connectivity.bond_type_size ? ctx->btype.p : nullptr;
+    in.lambda = corr.lambda_size ? ctx->lambda.p : nullptr;
+    in.beta = corr.beta_size ? ctx->beta.p : nullptr;
+    int too_big = 0;
+    PD_CK(gpu_build_layout(ctx->lay, in, &too_big, s));
+    if (too_big)
         return fail(PD_E_INVALID_ARGUMENT,
                     "PD_FAST: a tile neighbourhood exceeds %d nodes of shared memory; use "
                     "PD_BOND_PARALLEL for this mesh", FAST_MAX_HALO);
-    ctx->n_tiles = L.n_tiles;
-    ctx->max_halo = L.max_halo;
+    tm.mark("fast: device layout build");
     ctx->comp_begin = 0;  // owned nodes come first in the internal order
     ctx->comp_end = ctx->own_end - ctx->own_begin;
-    ctx->inv_host = L.inv;
-    PD_CK(ctx->perm.upload(L.perm.data(), L.perm.size(), s));
-    PD_CK(ctx->inv.upload(L.inv.data(), L.inv.size(), s));
-    PD_CK(ctx->tile_of.upload(L.tile_of.data(), L.tile_of.size(), s));
-    PD_CK(ctx->tile_start.upload(L.tile_start.data(), L.tile_start.size(), s));
-    PD_CK(ctx->kmax8.upload(L.kmax8.data(), L.kmax8.size(), s));
-    PD_CK(ctx->own_slot.upload(L.own_slot.data(), L.own_slot.size(), s));
-    PD_CK(ctx->nf_start.upload(L.nf_start.data(), L.nf_start.size(), s));
-    PD_CK(ctx->halo.upload(L.halo.data(), L.halo.size(), s));
-    PD_CK(ctx->halo_off.upload(L.halo_off.data(), L.halo_off.size(), s));
-    PD_CK(ctx->slot_off.upload(L.slot_off.data(), L.slot_off.size(), s));
-    PD_CK(ctx->lidx.upload(L.lidx.data(), L.lidx.size(), s));
-    if (!L.hist.empty())
-        PD_CK(ctx->hist32.upload(L.hist.data(), L.hist.size(), s));
-    if (!L.btype.empty())
-        PD_CK(ctx->btype_c.upload(L.btype.data(), L.btype.size(), s));
-    if (!L.lambda.empty())
-        PD_CK(ctx->lambda32.upload(L.lambda.data(), L.lambda.size(), s));
-    if (!L.beta.empty())
-        PD_CK(ctx->beta32.upload(L.beta.data(), L.beta.size(), s));
     // permute node arrays into internal order
-    const int* perm = ctx->perm.p;
+    const int* perm = ctx->lay.perm.p;
     PD_CK(ctx->scratch_d4.alloc(size_t(n)));
     launch_gather_rows<double4, 1>(ctx->xv.p, ctx->scratch_d4.p, perm, n, s);
     PD_CK(cudaMemcpyAsync(ctx->xv.p, ctx->scratch_d4.p, sizeof(double4) * n,
@@ -662,12 +661,12 @@ int setup_fast(pd_ctx* ctx, const pd_particles& p, const pd_state& st,
         const int64_t total = bc_tips->tip_offsets[bc_tips->n_tip_sets];
         std::vector<long long> nodes(size_t(std::max<int64_t>(total, 1)), 0);
         for (int64_t t = 0; t < total; ++t)
-            nodes[size_t(t)] = L.inv[size_t(bc_tips->tip_nodes[t])];
+            nodes[size_t(t)] = ctx->lay.inv_host[size_t(bc_tips->tip_nodes[t])];
         PD_CK(ctx->tip_nodes.upload(nodes.data(), nodes.size(), s));
     }
     // the single-PMB-law specialisation needs no per-slot law data
-    const bool general = m.n_laws > 1 || ctx->history || !L.btype.empty() || !L.lambda.empty() ||
-                         !L.beta.empty();
+    const bool general = m.n_laws > 1 || ctx->history || ctx->lay.btype_c.p ||
+                         ctx->lay.lambda32.p || ctx->lay.beta32.p;
     bool uniform = true;
     for (int64_t i = 1; i < n && uniform; ++i)
         uniform = p.volume[i] == p.volume[0];
@@ -697,7 +696,7 @@ int setup_fast(pd_ctx* ctx, const pd_particles& p, const pd_state& st,
 
 int launch_step(pd_ctx* ctx, DevArgs& A, int mode) {
     if (ctx->fast) {
-        PD_CK(launch_fast(A, ctx->fast_args(), mode, ctx->kind, ctx->n_tiles, ctx->stream));
+        PD_CK(launch_fast(A, ctx->fast_args(), mode, ctx->kind, ctx->lay.n_tiles, ctx->stream));
         ++ctx->launches;
         return PD_OK;
     }
@@ -978,7 +977,7 @@ int pd_ctx_internal_index(pd_ctx* ctx, const int64_t* local, int64_t count, int6
         if (local[k] < 0 || local[k] >= ctx->n)
             return fail(PD_E_INVALID_ARGUMENT, "internal_index: node %lld out of range",
                         (long long)local[k]);
-        out[k] = ctx->fast ? int64_t(ctx->inv_host[size_t(local[k])]) : local[k];
+        out[k] = ctx->fast ? int64_t(ctx->lay.inv_host[size_t(local[k])]) : local[k];
     }
     return ok();
 }
@@ -1073,7 +1072,7 @@ int pd_ctx_connect(pd_ctx* ctx, int32_t rank, int32_t world, const pd_peer_handl
     // per device row: the peer rows this owned node's u goes to
     std::vector<int2> x(size_t(ctx->n), make_int2(-1, -1));
     for (int64_t i = ctx->own_begin; i < ctx->own_end; ++i) {
-        const int64_t row = ctx->fast ? int64_t(ctx->inv_host[size_t(i)]) : i;
+        const int64_t row = ctx->fast ? int64_t(ctx->lay.inv_host[size_t(i)]) : i;
         const int64_t a = (lo >= 0 && send_lo) ? send_lo[i] : -1;
         const int64_t b = (hi >= 0 && send_hi) ? send_hi[i] : -1;
         if (a >= INT32_MAX || b >= INT32_MAX)
@@ -1092,7 +1091,7 @@ int pd_ctx_node_values(pd_ctx* ctx, const int64_t* local, int64_t count, double*
         if (local[k] < 0 || local[k] >= ctx->n)
             return fail(PD_E_INVALID_ARGUMENT, "node_values: node %lld out of range",
                         (long long)local[k]);
-        rows[size_t(k)] = ctx->fast ? ctx->inv_host[size_t(local[k])] : local[k];
+        rows[size_t(k)] = ctx->fast ? ctx->lay.inv_host[size_t(local[k])] : local[k];
     }
     if (count == 0)
         return ok();
@@ -1115,6 +1114,7 @@ namespace {
 
 int upload_impl(pd_ctx* ctx, const pd_bundle* b, const pd_state* st, int32_t variant) {
     PD_TRY(select_device(ctx));
+    PhaseTimer tm;
     if (variant < PD_BOND_PARALLEL || variant > PD_FAST)
         return fail(PD_E_INVALID_ARGUMENT, "unknown kernel variant %d", variant);
     // ModelBundle::validate (engine.cpp:335-341)
@@ -1125,19 +1125,23 @@ int upload_impl(pd_ctx* ctx, const pd_bundle* b, const pd_state* st, int32_t var
         return fail(PD_E_INVALID_ARGUMENT, "ModelBundle: dt must be positive");
     if (st->connectivity.n != b->particles.n)
         return fail(PD_E_INVALID_ARGUMENT, "simulate: state does not match the bundle");
+    tm.mark("upload: validate");
     // simulate: corr.no_failure = bc.no_failure (engine.cpp:386-387)
     PD_TRY(upload_common(ctx, b->particles, *st, b->model, b->corrections, b->bc.no_failure,
                          b->bc.no_failure_size));
+    tm.mark("upload: common");
     const int64_t slots = ctx->n * ctx->N;
     if (b->corrections.lambda_size != 0 && b->corrections.lambda_size != slots)
         return fail(PD_E_INVALID_ARGUMENT, "compute_forces: lambda size mismatch");
     if (b->corrections.beta_size != 0 && b->corrections.beta_size != slots)
         return fail(PD_E_INVALID_ARGUMENT, "compute_forces: beta size mismatch");
     PD_TRY(upload_bc(ctx, b->bc));
+    tm.mark("upload: bc");
     if (variant == PD_FAST) {
         pd_boundary bc = b->bc;
         PD_TRY(setup_fast(ctx, b->particles, *st, b->model, b->corrections, b->bc.no_failure,
                           b->bc.no_failure_size, &bc));
+        tm.mark("upload: fast layout");
     }
     ctx->variant = variant;
     ctx->dt = b->dt;
@@ -1191,7 +1195,7 @@ int pd_ctx_damage(pd_ctx* ctx, double* phi_out) {
     ++ctx->launches;
     const double* phi = ctx->scratch_f64.p;
     if (ctx->fast) {
-        launch_gather_rows<double, 1>(phi, ctx->scratch_f64.p + ctx->n, ctx->inv.p, ctx->n, s);
+        launch_gather_rows<double, 1>(phi, ctx->scratch_f64.p + ctx->n, ctx->lay.inv.p, ctx->n, s);
         ++ctx->launches;
         phi = ctx->scratch_f64.p + ctx->n;
     }
@@ -1284,13 +1288,19 @@ int pd_simulate(const pd_bundle* bundle, pd_state* state, const pd_options* opti
         pd_ctx* c;
         ~Guard() { pd_ctx_destroy(c); }
     } guard{ctx};
+    PhaseTimer tm;
     PD_TRY(pd_ctx_upload(ctx, bundle, state, options->variant));
+    PD_CK(cudaStreamSynchronize(ctx->stream));
+    tm.mark("simulate: upload");
     int rc = run_loop(ctx, *options, on_write, user, PD_FIELD_ALL, state, tips_out, tips_capacity,
                       n_tips_out);
+    PD_CK(cudaStreamSynchronize(ctx->stream));
+    tm.mark("simulate: run");
     // the state is the caller's in every outcome, as the reference mutates in place
     const int rc2 = download(ctx, state, nullptr,
                              PD_FIELD_U | PD_FIELD_V | PD_FIELD_A | PD_FIELD_CONNECTIVITY |
                                  PD_FIELD_HISTORY);
+    tm.mark("simulate: download");
     if (rc != PD_OK)
         return rc;
     if (rc2 != PD_OK)

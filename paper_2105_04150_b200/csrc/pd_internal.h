@@ -45,21 +45,34 @@ template <class T> struct DevBuf {
 // pd_host.cu: record the message pd_last_error() returns; returns code.
 int set_error(int code, const char* msg);
 
-// pd_fast.cu -- host copy of the tile layout (see pd_fast.cuh)
-struct FastHostLayout {
+// pd_layout.cu -- the fast path tile layout (pd_fast.cuh), built on the device
+struct FastLayoutDev {
     int T = 0, n_tiles = 0, max_halo = 0;
     long long total_slots = 0;
-    std::vector<int> perm, inv, tile_of, tile_start, kmax8, halo, nf_start;
-    std::vector<unsigned short> own_slot;
-    std::vector<long long> halo_off, slot_off;
-    std::vector<unsigned short> lidx;
-    std::vector<float> hist, lambda, beta;
-    std::vector<uint8_t> btype;
+    DevBuf<int> perm, inv, tile_of, tile_start, kmax8, halo, nf_start;
+    DevBuf<unsigned short> own_slot, lidx;
+    DevBuf<long long> halo_off, slot_off;
+    DevBuf<float> hist32, lambda32, beta32;
+    DevBuf<uint8_t> btype_c;
+    std::vector<int> inv_host;  // local node -> internal row
 };
-int fast_build_layout(FastHostLayout& L, int64_t n, int N, const int32_t* entries,
-                      const double* coords, const uint8_t* btype, const double* lambda,
-                      const double* beta, const double* hist, bool history,
-                      const uint8_t* nofail, int T, int64_t own_begin, int64_t own_end);
+struct FastLayoutIn {
+    long long n = 0, own_begin = 0, own_end = 0;
+    int N = 0, T = 0;
+    bool history = false;
+    const double4* xv = nullptr;     // local order
+    const int32_t* entries = nullptr;
+    const uint8_t* nofail = nullptr;
+    const double* hist = nullptr;
+    const uint8_t* btype = nullptr;
+    const double* lambda = nullptr;
+    const double* beta = nullptr;
+};
+// *error = 1 when a tile's neighbourhood exceeds FAST_MAX_HALO records
+cudaError_t gpu_build_layout(FastLayoutDev& L, const FastLayoutIn& in, int* error,
+                             cudaStream_t s);
+
+
 void fast_set_laws(const DevLaw* laws, int n, cudaStream_t stream);
 cudaError_t launch_fast(const DevArgs& A, const FastDev& F, int mode, int kind, int tiles,
                         cudaStream_t st);

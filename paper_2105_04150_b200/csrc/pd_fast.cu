@@ -91,7 +91,7 @@ __device__ __forceinline__ float f_envelope(const FastLaw& law, float s) {
 // TT:     threads (= owned nodes) per tile; MINB: CTAs per SM the register
 //         budget is sized for; PRE: load the node's integrator inputs before
 //         the slot loop so their latency hides behind the bond work.
-template <int MODE, int KIND, int TT, int MINB, bool PRE>
+template <int MODE, int KIND, int TT, int MINB, bool PRE, int R>
 __global__ void __launch_bounds__(TT, MINB) fast_step_kernel(DevArgs A, FastDev F) {
     if (MODE != 0 && *(volatile long long*)A.err_step != kNoError)
         return;
@@ -133,22 +133,22 @@ __global__ void __launch_bounds__(TT, MINB) fast_step_kernel(DevArgs A, FastDev 
         if (KIND != 0)
             sV[0] = 0.f;
     }
-    for (int h = threadIdx.x; h < H; h += 2 * TT) {
-        int id[2];
+    for (int h = threadIdx.x; h < H; h += R * TT) {
+        int id[R];
 #pragma unroll
-        for (int r = 0; r < 2; ++r) {
+        for (int r = 0; r < R; ++r) {
             const int hh = h + r * TT;
             id[r] = hh < H ? F.halo[h0 + hh] : -1;
         }
-        double4 x[2], u[2];
+        double4 x[R], u[R];
 #pragma unroll
-        for (int r = 0; r < 2; ++r)
+        for (int r = 0; r < R; ++r)
             if (id[r] >= 0) {
                 x[r] = A.xv[id[r]];
                 u[r] = A.u_in[id[r]];
             }
 #pragma unroll
-        for (int r = 0; r < 2; ++r)
+        for (int r = 0; r < R; ++r)
             if (id[r] >= 0) {
                 const int hh = h + r * TT + 1;
                 sA[hh] = make_float4(float(x[r].x - O.x), float(x[r].y - O.y),
@@ -160,10 +160,6 @@ __global__ void __launch_bounds__(TT, MINB) fast_step_kernel(DevArgs A, FastDev 
     }
     NodeIn pre{};
     double4 ui_pre = make_double4(0, 0, 0, 0);
-    if (PRE && MODE != 0 && active) {
-        pre = load_node_in(A, i);
-        ui_pre = A.u_in[i];
-    }
     __syncthreads();
     if (!active)
         return;
@@ -181,11 +177,8 @@ __global__ void __launch_bounds__(TT, MINB) fast_step_kernel(DevArgs A, FastDev 
     float2 fxy = make_float2(0.f, 0.f);
     float fz = 0.f;
     int broke = 0;
-    for (int kb = 0; kb < nkb; ++kb, lrow += kstride) {
-        const uint4 w = wnext;
-        wnext = wnext2;
-        if (kb + 2 < nkb)
-            wnext2 = __ldcs(reinterpret_cast<const uint4*>(lrow + 2 * kstride));
+    // one group of 8 slots (one 16-byte index load)
+    auto group = [&](const uint4 w, unsigned short* lrow) {
         const unsigned words[4] = {w.x, w.y, w.z, w.w};
         unsigned bmask = 0;
 #pragma unroll
@@ -264,7 +257,22 @@ __global__ void __launch_bounds__(TT, MINB) fast_step_kernel(DevArgs A, FastDev 
                     lrow[q] = 0;
             broke += __popc(bmask);
         }
+    };
+    int kb = 0;
+    for (; kb + 1 < nkb; ++kb, lrow += kstride) {
+        const uint4 w = wnext;
+        wnext = wnext2;
+        if (kb + 2 < nkb)
+            wnext2 = __ldcs(reinterpret_cast<const uint4*>(lrow + 2 * kstride));
+        group(w, lrow);
     }
+    // PRE: the integrator inputs load while the last group computes
+    if (PRE && MODE != 0) {
+        pre = load_node_in(A, i);
+        ui_pre = A.u_in[i];
+    }
+    if (kb < nkb)
+        group(wnext, lrow);
     if (broke)
         A.n_neigh[i] -= broke;
     if (KIND == 0) {
@@ -292,27 +300,27 @@ int smem_bytes(int kind, int cap) {
 // The dynamic shared-memory limit of each instantiation is lifted once, to
 // the largest halo the layout admits (FAST_MAX_HALO), by the first launch or
 // by preload_fast() -- never inside a multi-GPU run.
-template <int MODE, int KIND, int TT, int MINB, bool PRE> struct KernelCfg {
+template <int MODE, int KIND, int TT, int MINB, bool PRE, int R> struct KernelCfg {
     static bool done;
     static cudaError_t ensure() {
         if (done)
             return cudaSuccess;
-        const cudaError_t e = cudaFuncSetAttribute(fast_step_kernel<MODE, KIND, TT, MINB, PRE>,
+        const cudaError_t e = cudaFuncSetAttribute(fast_step_kernel<MODE, KIND, TT, MINB, PRE, R>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    smem_bytes(KIND, FAST_MAX_HALO + 1 + 31));
         done = e == cudaSuccess;
         return e;
     }
 };
-template <int MODE, int KIND, int TT, int MINB, bool PRE>
-bool KernelCfg<MODE, KIND, TT, MINB, PRE>::done = false;
+template <int MODE, int KIND, int TT, int MINB, bool PRE, int R>
+bool KernelCfg<MODE, KIND, TT, MINB, PRE, R>::done = false;
 
-template <int MODE, int KIND, int TT, int MINB, bool PRE>
+template <int MODE, int KIND, int TT, int MINB, bool PRE, int R = 2>
 cudaError_t launch_cfg(const DevArgs& A, const FastDev& F, int tiles, cudaStream_t st) {
-    const cudaError_t e = KernelCfg<MODE, KIND, TT, MINB, PRE>::ensure();
+    const cudaError_t e = KernelCfg<MODE, KIND, TT, MINB, PRE, R>::ensure();
     if (e != cudaSuccess)
         return e;
-    fast_step_kernel<MODE, KIND, TT, MINB, PRE><<<tiles, TT, smem_bytes(KIND, F.cap), st>>>(A, F);
+    fast_step_kernel<MODE, KIND, TT, MINB, PRE, R><<<tiles, TT, smem_bytes(KIND, F.cap), st>>>(A, F);
     return cudaGetLastError();
 }
 
@@ -325,6 +333,8 @@ cudaError_t launch_one(const DevArgs& A, const FastDev& F, int tiles, cudaStream
         case 1: return launch_cfg<MODE, KIND, 256, 4, false>(A, F, tiles, st);
         case 2: return launch_cfg<MODE, KIND, 256, 3, true>(A, F, tiles, st);
         case 3: return launch_cfg<MODE, KIND, 512, 2, true>(A, F, tiles, st);
+        case 4: return launch_cfg<MODE, KIND, 512, 2, false, 3>(A, F, tiles, st);
+        case 5: return launch_cfg<MODE, KIND, 512, 2, true, 3>(A, F, tiles, st);
         default: break;
         }
     }
@@ -399,13 +409,13 @@ __global__ void fast_materialize_kernel(const int32_t* entries0, const int* inv,
 
 } // namespace
 
-template <int MODE, int KIND, int TT, int MINB, bool PRE> static void preload_one() {
+template <int MODE, int KIND, int TT, int MINB, bool PRE, int R = 2> static void preload_one() {
     // load the function and lift its shared-memory limit now, so no launch
     // inside a multi-GPU run has to touch the module
     cudaFuncAttributes a;
     cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(
-                                  fast_step_kernel<MODE, KIND, TT, MINB, PRE>));
-    KernelCfg<MODE, KIND, TT, MINB, PRE>::ensure();
+                                  fast_step_kernel<MODE, KIND, TT, MINB, PRE, R>));
+    KernelCfg<MODE, KIND, TT, MINB, PRE, R>::ensure();
 }
 
 template <int MODE, int KIND> static void preload_mk() {
@@ -414,6 +424,8 @@ template <int MODE, int KIND> static void preload_mk() {
     if (MODE == 1 && KIND == 0) {
         preload_one<MODE, KIND, 256, 3, true>();
         preload_one<MODE, KIND, 512, 2, true>();
+        preload_one<MODE, KIND, 512, 2, false, 3>();
+        preload_one<MODE, KIND, 512, 2, true, 3>();
     }
 }
 

@@ -28,6 +28,7 @@ UNITS = {
     "pd_fast.cu": ["-fmad=true", "-diag-suppress=186"],
     "pd_family.cu": ["-fmad=false"],
     "pd_layout.cu": ["-fmad=false"],
+    "pd_lattice.cu": ["-fmad=true"],
 }
 HEADERS = ["pd_device.cuh", "pd_internal.h", "pd_fast.cuh"]
 

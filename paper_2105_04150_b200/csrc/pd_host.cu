@@ -224,6 +224,15 @@ struct pd_ctx {
     float pmb_c = 0, pmb_sc = 0, pmb_cv = 0;
     int fast_T = FAST_T, fast_cfg = 0;
     FastLayoutDev lay;  // built on the device (pd_layout.cu)
+    // PD_FAST on a structured lattice: implicit connectivity (pd_lattice.cu),
+    // node arrays stay in the reference order
+    bool lattice = false;
+    LatticeArgs lat;
+    DevBuf<uint4> lmask;
+    bool permuted() const { return fast && !lattice; }
+    int64_t row_of(int64_t local) const {
+        return permuted() ? int64_t(lay.inv_host[size_t(local)]) : local;
+    }
     DevBuf<double4> scratch_d4;
     DevBuf<int32_t> scratch_n;
     DevBuf<uint8_t> scratch_u8;
@@ -336,6 +345,7 @@ int upload_common(pd_ctx* ctx, const pd_particles& p, const pd_state& st,
     const int64_t N = st.connectivity.group_size;
     PD_TRY(group_validate(N));
     ctx->fast = false;
+    ctx->lattice = false;
     if (p.coords_size != 3 * n || !p.coords || !p.volume)
         return fail(PD_E_INVALID_ARGUMENT, "ParticleSet: field lengths differ");
     ctx->n = n;
@@ -496,7 +506,7 @@ int download(pd_ctx* ctx, pd_state* st, pd_force_field* forces, int32_t fields) 
     cudaStream_t s = ctx->stream;
     const int64_t n = ctx->n;
     const int64_t slots = n * ctx->N;
-    const int* inv = ctx->fast ? ctx->lay.inv.p : nullptr;
+    const int* inv = ctx->permuted() ? ctx->lay.inv.p : nullptr;
     auto vec3_out = [&](const double* dev, double* host) -> int {
         const double* src = dev;
         if (inv) {
@@ -534,7 +544,11 @@ int download(pd_ctx* ctx, pd_state* st, pd_force_field* forces, int32_t fields) 
     if ((fields & PD_FIELD_CONNECTIVITY) && st) {
         if (st->connectivity.entries) {
             PD_CK(ctx->scratch_i32.alloc(size_t(slots)));
-            if (ctx->fast)
+            if (ctx->lattice)
+                PD_CK(launch_lattice_materialize(ctx->entries.p, ctx->lmask.p, ctx->own_begin,
+                                                 ctx->own_end, n, ctx->N, ctx->lat,
+                                                 ctx->scratch_i32.p, s));
+            else if (ctx->fast)
                 launch_fast_materialize(ctx->entries.p, ctx->lay.inv.p, ctx->lay.tile_of.p,
                                         ctx->lay.tile_start.p, ctx->lay.slot_off.p, ctx->fast_T, ctx->lay.lidx.p,
                                         nullptr, n, ctx->N, ctx->scratch_i32.p, nullptr, s);
@@ -559,7 +573,7 @@ int download(pd_ctx* ctx, pd_state* st, pd_force_field* forces, int32_t fields) 
         PD_CK(cudaStreamSynchronize(s));
     }
     if (want_hist) {
-        if (ctx->fast) {
+        if (ctx->permuted()) {
             launch_fast_materialize(ctx->entries.p, ctx->lay.inv.p, ctx->lay.tile_of.p, ctx->lay.tile_start.p,
                                     ctx->lay.slot_off.p, ctx->fast_T, ctx->lay.lidx.p, ctx->lay.hist32.p, n,
                                     ctx->N, nullptr, ctx->hist.p, s);
@@ -582,6 +596,54 @@ int download(pd_ctx* ctx, pd_state* st, pd_force_field* forces, int32_t fields) 
 
 // Renumber the resident node arrays into the fast path's brick order and
 // build its tile layout from the host copies of the rows.
+// PD_FAST on a lattice with one PMB law, uniform volumes and no per-bond or
+// no-failure data: implicit connectivity (pd_lattice.cu).  Returns false (and
+// leaves the context untouched) when the model does not qualify;
+// PD_FAST_LAYOUT=general forces the general tile layout.
+int try_lattice(pd_ctx* ctx, const pd_particles& p, const pd_state& st, const pd_damage_model& m,
+                const pd_corrections& corr, const uint8_t* nofail, int64_t nofail_size,
+                bool* used) {
+    *used = false;
+    if (const char* e = std::getenv("PD_FAST_LAYOUT"))
+        if (std::strcmp(e, "general") == 0)
+            return PD_OK;
+    const int64_t n = ctx->n;
+    if (m.n_laws != 1 || m.laws[0].n_breakpoints != 1 || ctx->history ||
+        st.connectivity.bond_type_size != 0 || corr.lambda_size != 0 || corr.beta_size != 0)
+        return PD_OK;
+    for (int64_t i = 0; nofail && nofail_size == n && i < n; ++i)
+        if (nofail[i])
+            return PD_OK;
+    for (int64_t i = 1; i < n; ++i)
+        if (p.volume[i] != p.volume[0])
+            return PD_OK;
+    LatticeArgs L;
+    if (!lattice_detect(p.coords, n, ctx->own_begin, ctx->own_end, L))
+        return PD_OK;
+    cudaStream_t s = ctx->stream;
+    PD_CK(ctx->lmask.alloc(size_t(n)));
+    PD_CK(ctx->counter.alloc(1));
+    PD_CK(cudaMemsetAsync(ctx->counter.p, 0, sizeof(unsigned long long), s));
+    int* bad = reinterpret_cast<int*>(ctx->counter.p);
+    PD_CK(lattice_build_masks(ctx->entries.p, ctx->own_begin, ctx->own_end, ctx->N, L,
+                              ctx->lmask.p, bad, s));
+    int bad_h = 0;
+    PD_CK(cudaMemcpyAsync(&bad_h, bad, sizeof bad_h, cudaMemcpyDeviceToHost, s));
+    PD_CK(cudaStreamSynchronize(s));
+    if (bad_h) {
+        ctx->lmask.release();
+        return PD_OK;
+    }
+    L.sc = float(m.laws[0].breakpoints[0]);
+    L.cv = float(m.laws[0].stiffness * p.volume[0]);
+    L.mask = ctx->lmask.p;
+    ctx->lat = L;
+    ctx->lattice = true;
+    ctx->fast = true;
+    *used = true;
+    return PD_OK;
+}
+
 int setup_fast(pd_ctx* ctx, const pd_particles& p, const pd_state& st,
                const pd_damage_model& m, const pd_corrections& corr, const uint8_t* nofail,
                int64_t nofail_size, pd_boundary* bc_tips) {
@@ -695,6 +757,11 @@ int setup_fast(pd_ctx* ctx, const pd_particles& p, const pd_state& st,
 }
 
 int launch_step(pd_ctx* ctx, DevArgs& A, int mode) {
+    if (ctx->lattice) {
+        PD_CK(launch_lattice(A, ctx->lat, mode, ctx->stream));
+        ++ctx->launches;
+        return PD_OK;
+    }
     if (ctx->fast) {
         PD_CK(launch_fast(A, ctx->fast_args(), mode, ctx->kind, ctx->lay.n_tiles, ctx->stream));
         ++ctx->launches;
@@ -977,7 +1044,7 @@ int pd_ctx_internal_index(pd_ctx* ctx, const int64_t* local, int64_t count, int6
         if (local[k] < 0 || local[k] >= ctx->n)
             return fail(PD_E_INVALID_ARGUMENT, "internal_index: node %lld out of range",
                         (long long)local[k]);
-        out[k] = ctx->fast ? int64_t(ctx->lay.inv_host[size_t(local[k])]) : local[k];
+        out[k] = ctx->row_of(local[k]);
     }
     return ok();
 }
@@ -1026,6 +1093,7 @@ int pd_ctx_connect(pd_ctx* ctx, int32_t rank, int32_t world, const pd_peer_handl
         preload_aux();
         preload_exact();
         preload_fast();
+        preload_lattice();
     });
     PD_CK(cudaGetLastError());
     const int me = int(getpid());
@@ -1072,7 +1140,7 @@ int pd_ctx_connect(pd_ctx* ctx, int32_t rank, int32_t world, const pd_peer_handl
     // per device row: the peer rows this owned node's u goes to
     std::vector<int2> x(size_t(ctx->n), make_int2(-1, -1));
     for (int64_t i = ctx->own_begin; i < ctx->own_end; ++i) {
-        const int64_t row = ctx->fast ? int64_t(ctx->lay.inv_host[size_t(i)]) : i;
+        const int64_t row = ctx->row_of(i);
         const int64_t a = (lo >= 0 && send_lo) ? send_lo[i] : -1;
         const int64_t b = (hi >= 0 && send_hi) ? send_hi[i] : -1;
         if (a >= INT32_MAX || b >= INT32_MAX)
@@ -1091,7 +1159,7 @@ int pd_ctx_node_values(pd_ctx* ctx, const int64_t* local, int64_t count, double*
         if (local[k] < 0 || local[k] >= ctx->n)
             return fail(PD_E_INVALID_ARGUMENT, "node_values: node %lld out of range",
                         (long long)local[k]);
-        rows[size_t(k)] = ctx->fast ? ctx->lay.inv_host[size_t(local[k])] : local[k];
+        rows[size_t(k)] = ctx->row_of(local[k]);
     }
     if (count == 0)
         return ok();
@@ -1138,10 +1206,15 @@ int upload_impl(pd_ctx* ctx, const pd_bundle* b, const pd_state* st, int32_t var
     PD_TRY(upload_bc(ctx, b->bc));
     tm.mark("upload: bc");
     if (variant == PD_FAST) {
-        pd_boundary bc = b->bc;
-        PD_TRY(setup_fast(ctx, b->particles, *st, b->model, b->corrections, b->bc.no_failure,
-                          b->bc.no_failure_size, &bc));
-        tm.mark("upload: fast layout");
+        bool lattice = false;
+        PD_TRY(try_lattice(ctx, b->particles, *st, b->model, b->corrections, b->bc.no_failure,
+                           b->bc.no_failure_size, &lattice));
+        if (!lattice) {
+            pd_boundary bc = b->bc;
+            PD_TRY(setup_fast(ctx, b->particles, *st, b->model, b->corrections, b->bc.no_failure,
+                              b->bc.no_failure_size, &bc));
+        }
+        tm.mark(lattice ? "upload: lattice masks" : "upload: fast layout");
     }
     ctx->variant = variant;
     ctx->dt = b->dt;
@@ -1194,7 +1267,7 @@ int pd_ctx_damage(pd_ctx* ctx, double* phi_out) {
     launch_damage(ctx->n_neigh.p, ctx->initial.p, ctx->n, ctx->scratch_f64.p, s);
     ++ctx->launches;
     const double* phi = ctx->scratch_f64.p;
-    if (ctx->fast) {
+    if (ctx->permuted()) {
         launch_gather_rows<double, 1>(phi, ctx->scratch_f64.p + ctx->n, ctx->lay.inv.p, ctx->n, s);
         ++ctx->launches;
         phi = ctx->scratch_f64.p + ctx->n;
@@ -1260,9 +1333,14 @@ int pd_compute_forces(int32_t variant, pd_state* state, const pd_particles* part
     st.a = nullptr;
     PD_TRY(upload_common(ctx, *particles, st, *model, *corr, corr->no_failure,
                          corr->no_failure_size));
-    if (variant == PD_FAST)
-        PD_TRY(setup_fast(ctx, *particles, st, *model, *corr, corr->no_failure,
-                          corr->no_failure_size, nullptr));
+    if (variant == PD_FAST) {
+        bool lattice = false;
+        PD_TRY(try_lattice(ctx, *particles, st, *model, *corr, corr->no_failure,
+                           corr->no_failure_size, &lattice));
+        if (!lattice)
+            PD_TRY(setup_fast(ctx, *particles, st, *model, *corr, corr->no_failure,
+                              corr->no_failure_size, nullptr));
+    }
     ctx->variant = variant;
     DevArgs A = ctx->args();
     PD_TRY(launch_step(ctx, A, 0));

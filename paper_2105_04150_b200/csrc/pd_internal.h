@@ -88,6 +88,24 @@ void preload_aux();
 void preload_exact();
 void preload_fast();
 
+// pd_lattice.cu -- the fast path on structured lattices (implicit connectivity)
+struct LatticeArgs {
+    int nx = 0, ny = 0, nz_local = 0;  // local lattice (x fastest, z slowest)
+    int z0 = 0, nz_own = 0;            // owned planes [z0, z0 + nz_own)
+    double h = 1.0, inv_h = 1.0;       // spacing
+    float sc = 0.f, cv = 0.f;          // PMB critical stretch, c * V
+    uint4* mask = nullptr;             // per node: live bonds over the 122-offset pattern
+};
+bool lattice_detect(const double* coords, long long n, long long own_begin, long long own_end,
+                    LatticeArgs& L);
+cudaError_t lattice_build_masks(const int32_t* entries, long long begin, long long end, int N,
+                                const LatticeArgs& L, uint4* mask, int* bad, cudaStream_t st);
+cudaError_t launch_lattice(const DevArgs& A, const LatticeArgs& L, int mode, cudaStream_t st);
+cudaError_t launch_lattice_materialize(const int32_t* entries0, const uint4* mask, long long begin,
+                                       long long end, long long n, int N, const LatticeArgs& L,
+                                       int32_t* out, cudaStream_t st);
+void preload_lattice();
+
 // pd_exact.cu
 void exact_set_laws(const DevLaw* laws, int n, cudaStream_t stream);
 cudaError_t launch_exact(const DevArgs& A, int mode, bool node_sum, cudaStream_t st);

@@ -637,6 +637,8 @@ int try_lattice(pd_ctx* ctx, const pd_particles& p, const pd_state& st, const pd
     L.sc = float(m.laws[0].breakpoints[0]);
     L.cv = float(m.laws[0].stiffness * p.volume[0]);
     L.mask = ctx->lmask.p;
+    if (const char* e = std::getenv("PD_LAT_CFG"))
+        L.cfg = std::atoi(e);
     ctx->lat = L;
     ctx->lattice = true;
     ctx->fast = true;

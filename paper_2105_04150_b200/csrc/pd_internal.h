@@ -94,6 +94,7 @@ struct LatticeArgs {
     int z0 = 0, nz_own = 0;            // owned planes [z0, z0 + nz_own)
     double h = 1.0, inv_h = 1.0;       // spacing
     float sc = 0.f, cv = 0.f;          // PMB critical stretch, c * V
+    int cfg = 0;                       // brick / occupancy configuration (PD_LAT_CFG)
     uint4* mask = nullptr;             // per node: live bonds over the 122-offset pattern
 };
 bool lattice_detect(const double* coords, long long n, long long own_begin, long long own_end,

@@ -36,11 +36,11 @@ namespace pdb {
 
 namespace {
 
-constexpr int BX = 16, BY = 4, BZ = 8;                // brick (threads)
-constexpr int HX = BX + 6, HY = BY + 6, HZ = BZ + 6;  // halo box (records)
-constexpr int NREC = HX * HY * HZ;                    // 3080
-constexpr int TT = BX * BY * BZ;                      // 512
+// brick = 16 x 4 x BZT nodes (one thread each); halo box HX x HY x (BZT + 6)
+constexpr int BX = 16, BY = 4;
+constexpr int HX = BX + 6, HY = BY + 6;
 constexpr int NPAT = 122;
+template <int BZT> constexpr int nrec() { return HX * HY * (BZT + 6); }
 
 // offset c of the pattern, components 0/1/2 = dx/dy/dz, in (dz, dy, dx)
 // lexicographic order = ascending reference index order of a row
@@ -84,8 +84,26 @@ __device__ __forceinline__ float rcp_approx(float x) {
 
 struct Acc {
     float fx, fy, fz;
-    unsigned dead[4];
+    int kept;  // live slots that contributed (did not break)
 };
+
+// Shared by the unrolled slots (compile-time offsets) and the break pass
+// (runtime offsets), so both see bit-identical stretches.
+__device__ __forceinline__ void stretch(const float4& rj, const float4& ri, float dx, float dy,
+                                        float dz, float r2, float len, float rr, float& s,
+                                        float& rc, float& cx, float& cy, float& cz) {
+    const float hx = rj.x - ri.x, hy = rj.y - ri.y, hz = rj.z - ri.z;  // eta / spacing
+    cx = hx + dx;
+    cy = hy + dy;
+    cz = hz + dz;
+    // eta.(2 xi + eta), cancellation free
+    float num = hz * (hz + (dz + dz));
+    num = fmaf(hy, hy + (dy + dy), num);
+    num = fmaf(hx, hx + (dx + dx), num);
+    const float cur2 = num + r2;
+    rc = rsqrt_approx(cur2);
+    s = num * rr * rcp_approx(fmaf(cur2, rc, len));
+}
 
 template <int C>
 __device__ __forceinline__ void slot(const float4* own, const float4& ri, const uint4& m, float sc,
@@ -98,34 +116,51 @@ __device__ __forceinline__ void slot(const float4* own, const float4& ri, const 
     constexpr int word = C >> 5;
     constexpr unsigned bit = 1u << (C & 31);
     const unsigned mw = word == 0 ? m.x : (word == 1 ? m.y : (word == 2 ? m.z : m.w));
-    const bool live = (mw & bit) != 0;
     // branch free: a dead slot's record may be anything finite (an
-    // out-of-domain box record is 0); its contribution is selected away
+    // out-of-domain box record is 0); its contribution is predicated away
     const float4 rj = own[off];
-    const float hx = rj.x - ri.x, hy = rj.y - ri.y, hz = rj.z - ri.z;  // eta / spacing
-    const float cx = hx + float(dx), cy = hy + float(dy), cz = hz + float(dz);
-    // eta.(2 xi + eta), cancellation free
-    float num = hz * (hz + float(2 * dz));
-    num = fmaf(hy, hy + float(2 * dy), num);
-    num = fmaf(hx, hx + float(2 * dx), num);
-    const float cur2 = num + float(r2);
-    const float rc = rsqrt_approx(cur2);
-    const float s = num * rr * rcp_approx(fmaf(cur2, rc, len));
+    float s, rc, cx, cy, cz;
+    stretch(rj, ri, float(dx), float(dy), float(dz), float(r2), len, rr, s, rc, cx, cy, cz);
     const float scale = s * rc;
-    // predicated tail: live = bit set; break = live && s >= s_c (bond_contribution's
-    // PMB break, engine.cpp:90-98) clears the bit; otherwise a live slot adds its force
-    unsigned& dead = a.dead[word];
-    asm("{\n\t.reg .pred pl, pb, pc;\n\t"
+    // live and unbroken (s < s_c, bond_contribution's PMB test, engine.cpp:90-98):
+    // add the force and count the slot; a live slot that breaks is found later
+    asm("{\n\t.reg .pred pl, pc;\n\t"
         "setp.ne.u32 pl, %4, 0;\n\t"
-        "setp.ge.and.f32 pb, %5, %6, pl;\n\t"
         "setp.lt.and.f32 pc, %5, %6, pl;\n\t"
-        "@pb or.b32 %0, %0, %7;\n\t"
-        "@pc fma.rn.f32 %1, %8, %11, %1;\n\t"
-        "@pc fma.rn.f32 %2, %9, %11, %2;\n\t"
-        "@pc fma.rn.f32 %3, %10, %11, %3;\n\t}"
-        : "+r"(dead), "+f"(a.fx), "+f"(a.fy), "+f"(a.fz)
-        : "r"(mw & bit), "f"(s), "f"(sc), "r"(bit), "f"(cx), "f"(cy), "f"(cz), "f"(scale));
-    (void)live;
+        "@pc add.s32 %0, %0, 1;\n\t"
+        "@pc fma.rn.f32 %1, %7, %10, %1;\n\t"
+        "@pc fma.rn.f32 %2, %8, %10, %2;\n\t"
+        "@pc fma.rn.f32 %3, %9, %10, %3;\n\t}"
+        : "+r"(a.kept), "+f"(a.fx), "+f"(a.fy), "+f"(a.fz)
+        : "r"(mw & bit), "f"(s), "f"(sc), "f"(cx), "f"(cy), "f"(cz), "f"(scale));
+}
+
+__constant__ signed char c_pat[NPAT][4];  // dx, dy, dz, |d|^2
+
+// The rare pass for a node that lost bonds this step: recompute each live
+// slot's stretch (same arithmetic) and return the broken bits.
+__device__ __noinline__ uint4 broken_bits(const float4* own, const float4& ri, const uint4& m,
+                                          float sc) {
+    unsigned w[4] = {m.x, m.y, m.z, m.w};
+    unsigned dead[4] = {0u, 0u, 0u, 0u};
+    for (int c = 0; c < NPAT; ++c) {
+        if (!((w[c >> 5] >> (c & 31)) & 1u))
+            continue;
+        const int dx = c_pat[c][0], dy = c_pat[c][1], dz = c_pat[c][2], r2 = c_pat[c][3];
+        const float len = r2 == 1 ? root(1) : r2 == 2 ? root(2) : r2 == 3 ? root(3)
+                        : r2 == 4 ? root(4) : r2 == 5 ? root(5) : r2 == 6 ? root(6)
+                        : r2 == 8 ? root(8) : root(9);
+        const float rr = r2 == 1 ? 1.0f / root(1) : r2 == 2 ? 1.0f / root(2)
+                       : r2 == 3 ? 1.0f / root(3) : r2 == 4 ? 1.0f / root(4)
+                       : r2 == 5 ? 1.0f / root(5) : r2 == 6 ? 1.0f / root(6)
+                       : r2 == 8 ? 1.0f / root(8) : 1.0f / root(9);
+        const float4 rj = own[dx + HX * (dy + HY * dz)];
+        float s, rc, cx, cy, cz;
+        stretch(rj, ri, float(dx), float(dy), float(dz), float(r2), len, rr, s, rc, cx, cy, cz);
+        if (!(s < sc))
+            dead[c >> 5] |= 1u << (c & 31);
+    }
+    return make_uint4(dead[0], dead[1], dead[2], dead[3]);
 }
 
 template <int... C>
@@ -134,15 +169,17 @@ __device__ __forceinline__ void all_slots(std::integer_sequence<int, C...>, cons
     (slot<C>(own, ri, m, sc, a), ...);
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(TT, 2) lattice_step_kernel(DevArgs A, LatticeArgs L) {
+template <int MODE, int BZT, int MINB>
+__global__ void __launch_bounds__(BX * BY * BZT, MINB) lattice_step_kernel(DevArgs A,
+                                                                           LatticeArgs L) {
+    constexpr int TT = BX * BY * BZT, HZ = BZT + 6;
     if (MODE != 0 && *(volatile long long*)A.err_step != kNoError)
         return;
-    extern __shared__ float4 rec[];  // NREC records (49 KB: dynamic)
+    extern __shared__ float4 rec[];  // HX * HY * HZ records (dynamic: > 48 KB for BZT = 8)
     const int nbx = (L.nx + BX - 1) / BX, nby = (L.ny + BY - 1) / BY;
     const int b = blockIdx.x;
     const int bxi = b % nbx, byi = (b / nbx) % nby, bzi = b / (nbx * nby);
-    const int gx0 = bxi * BX, gy0 = byi * BY, gz0 = L.z0 + bzi * BZ;
+    const int gx0 = bxi * BX, gy0 = byi * BY, gz0 = L.z0 + bzi * BZT;
     const int tx = threadIdx.x % BX, ty = (threadIdx.x / BX) % BY, tz = threadIdx.x / (BX * BY);
     const int gx = gx0 + tx, gy = gy0 + ty, gz = gz0 + tz;
     const bool active = gx < L.nx && gy < L.ny && gz < L.z0 + L.nz_own;
@@ -151,33 +188,42 @@ __global__ void __launch_bounds__(TT, 2) lattice_step_kernel(DevArgs A, LatticeA
     // the row mask streams in while the halo is staged
     uint4 m = active ? __ldcs(L.mask + i) : make_uint4(0, 0, 0, 0);
 
-    // 1. stage the halo box: fp32 (u - U_brick) / spacing
+    // 1. stage the halo box, one box row (22 records) per warp and pass:
+    //    fp32 (u - U_brick) / spacing
     const double4 U0 = A.u_in[gx0 + (long long)L.nx * gy0 + plane * gz0];
-    const double ih = L.inv_h;
-    for (int p = threadIdx.x; p < NREC; p += TT) {
-        const int px = p % HX, py = (p / HX) % HY, pz = p / (HX * HY);
-        const int X = gx0 - 3 + px, Y = gy0 - 3 + py, Z = gz0 - 3 + pz;
-        float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (X >= 0 && X < L.nx && Y >= 0 && Y < L.ny && Z >= 0 && Z < L.nz_local) {
-            const double4 u = A.u_in[X + (long long)L.nx * Y + plane * Z];
-            r = make_float4(float((u.x - U0.x) * ih), float((u.y - U0.y) * ih),
-                            float((u.z - U0.z) * ih), 0.f);
+    const float ih = float(L.inv_h);
+    {
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        const int X = gx0 - 3 + lane;
+        const bool xok = lane < HX && X >= 0 && X < L.nx;
+        for (int row = warp; row < HY * HZ; row += TT / 32) {
+            const int py = row % HY, pz = row / HY;
+            const int Y = gy0 - 3 + py, Z = gz0 - 3 + pz;
+            if (lane >= HX)
+                continue;
+            float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (xok && Y >= 0 && Y < L.ny && Z >= 0 && Z < L.nz_local) {
+                const double4 u = A.u_in[X + (long long)L.nx * Y + plane * Z];
+                r = make_float4(float(u.x - U0.x) * ih, float(u.y - U0.y) * ih,
+                                float(u.z - U0.z) * ih, 0.f);
+            }
+            rec[row * HX + lane] = r;
         }
-        rec[p] = r;
     }
     __syncthreads();
     if (!active)
         return;
 
     // 2. the node's bonds: 122 pattern slots, unrolled at compile time
-    const float4* own = rec + (tx + 3) + HX * ((ty + 3) + HY * (tz + 3));
+    const float4* own = rec + (tx + 3) + HX * ((ty + 3) + HY * (tz + 3));  // HY pitch is the same
     const float4 ri = *own;
-    Acc a{0.f, 0.f, 0.f, {0u, 0u, 0u, 0u}};
+    Acc a{0.f, 0.f, 0.f, 0};
     all_slots(std::make_integer_sequence<int, NPAT>{}, own, ri, m, L.sc, a);
-    const unsigned d0 = a.dead[0], d1 = a.dead[1], d2 = a.dead[2], d3 = a.dead[3];
-    if (d0 | d1 | d2 | d3) {
-        L.mask[i] = make_uint4(m.x & ~d0, m.y & ~d1, m.z & ~d2, m.w & ~d3);
-        A.n_neigh[i] -= __popc(d0) + __popc(d1) + __popc(d2) + __popc(d3);
+    const int live = __popc(m.x) + __popc(m.y) + __popc(m.z) + __popc(m.w);
+    if (a.kept != live) {
+        const uint4 d = broken_bits(own, ri, m, L.sc);
+        L.mask[i] = make_uint4(m.x & ~d.x, m.y & ~d.y, m.z & ~d.z, m.w & ~d.w);
+        A.n_neigh[i] -= live - a.kept;
     }
     const double fx = double(a.fx * L.cv), fy = double(a.fy * L.cv), fz = double(a.fz * L.cv);
 
@@ -268,21 +314,58 @@ template <class K> void preload_fn(K k) {
     cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(k));
 }
 
-// the halo box exceeds the 48 KB default: lift the limit once per process
-cudaError_t configure_smem() {
+template <int MODE, int BZT, int MINB> cudaError_t configure_one() {
     static bool done = false;
     if (done)
         return cudaSuccess;
-    const int smem = int(sizeof(float4) * NREC);
-    cudaError_t e = cudaSuccess;
-    for (const void* k : {reinterpret_cast<const void*>(lattice_step_kernel<0>),
-                          reinterpret_cast<const void*>(lattice_step_kernel<1>),
-                          reinterpret_cast<const void*>(lattice_step_kernel<2>),
-                          reinterpret_cast<const void*>(lattice_step_kernel<3>)})
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const cudaError_t e = cudaFuncSetAttribute(lattice_step_kernel<MODE, BZT, MINB>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               int(sizeof(float4)) * nrec<BZT>());
     done = e == cudaSuccess;
     return e;
+}
+
+template <int MODE, int BZT, int MINB>
+cudaError_t launch_cfg(const DevArgs& A, const LatticeArgs& L, cudaStream_t st) {
+    const int nbx = (L.nx + BX - 1) / BX, nby = (L.ny + BY - 1) / BY,
+              nbz = (L.nz_own + BZT - 1) / BZT;
+    const unsigned blocks = unsigned(nbx * nby * nbz);
+    if (blocks == 0)
+        return cudaSuccess;
+    const cudaError_t e = configure_one<MODE, BZT, MINB>();
+    if (e != cudaSuccess)
+        return e;
+    lattice_step_kernel<MODE, BZT, MINB>
+        <<<blocks, BX * BY * BZT, sizeof(float4) * nrec<BZT>(), st>>>(A, L);
+    return cudaGetLastError();
+}
+
+// Brick shape and CTAs per SM (register budget).  Measured at 10M nodes
+// (profiles/): 16x4x4 bricks at 5 CTAs/SM (48 registers, 40 warps/SM) beat
+// 16x4x8 at 2 (64 registers) by 15 %; 16x4x2 bricks lose to the halo overhead
+// (13.8 staged records per node).  PD_LAT_CFG selects the alternatives:
+// 1 = 16x4x8 x3, 2 = 16x4x4 x4, 3 = 16x4x8 x2, 4 = 16x4x4 x6.
+template <int MODE> cudaError_t launch_mode(const DevArgs& A, const LatticeArgs& L, cudaStream_t st) {
+    switch (L.cfg) {
+    case 1: return launch_cfg<MODE, 8, 3>(A, L, st);
+    case 2: return launch_cfg<MODE, 4, 4>(A, L, st);
+    case 3: return launch_cfg<MODE, 8, 2>(A, L, st);
+    case 4: return launch_cfg<MODE, 4, 6>(A, L, st);
+    default: return launch_cfg<MODE, 4, 5>(A, L, st);
+    }
+}
+
+template <int MODE> void preload_mode() {
+    preload_fn(lattice_step_kernel<MODE, 8, 2>);
+    preload_fn(lattice_step_kernel<MODE, 8, 3>);
+    preload_fn(lattice_step_kernel<MODE, 4, 4>);
+    preload_fn(lattice_step_kernel<MODE, 4, 5>);
+    preload_fn(lattice_step_kernel<MODE, 4, 6>);
+    configure_one<MODE, 8, 2>();
+    configure_one<MODE, 8, 3>();
+    configure_one<MODE, 4, 4>();
+    configure_one<MODE, 4, 5>();
+    configure_one<MODE, 4, 6>();
 }
 
 } // namespace
@@ -329,6 +412,17 @@ bool lattice_detect(const double* coords, long long n, long long own_begin, long
 
 cudaError_t lattice_build_masks(const int32_t* entries, long long begin, long long end, int N,
                                 const LatticeArgs& L, uint4* mask, int* bad, cudaStream_t st) {
+    signed char tab[NPAT][4];
+    for (int c = 0; c < NPAT; ++c) {
+        tab[c][0] = (signed char)pat(c, 0);
+        tab[c][1] = (signed char)pat(c, 1);
+        tab[c][2] = (signed char)pat(c, 2);
+        tab[c][3] = (signed char)(tab[c][0] * tab[c][0] + tab[c][1] * tab[c][1] +
+                                  tab[c][2] * tab[c][2]);
+    }
+    cudaError_t e = cudaMemcpyToSymbolAsync(c_pat, tab, sizeof tab, 0, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess)
+        return e;
     if (end > begin)
         lattice_mask_kernel<<<unsigned((end - begin + 255) / 256), 256, 0, st>>>(
             entries, begin, end, N, L.nx, L.ny, mask, bad);
@@ -336,21 +430,12 @@ cudaError_t lattice_build_masks(const int32_t* entries, long long begin, long lo
 }
 
 cudaError_t launch_lattice(const DevArgs& A, const LatticeArgs& L, int mode, cudaStream_t st) {
-    const int nbx = (L.nx + BX - 1) / BX, nby = (L.ny + BY - 1) / BY, nbz = (L.nz_own + BZ - 1) / BZ;
-    const unsigned blocks = unsigned(nbx * nby * nbz);
-    if (blocks == 0)
-        return cudaSuccess;
-    cudaError_t e = configure_smem();
-    if (e != cudaSuccess)
-        return e;
-    const size_t smem = sizeof(float4) * NREC;
     switch (mode) {
-    case 0: lattice_step_kernel<0><<<blocks, TT, smem, st>>>(A, L); break;
-    case 1: lattice_step_kernel<1><<<blocks, TT, smem, st>>>(A, L); break;
-    case 2: lattice_step_kernel<2><<<blocks, TT, smem, st>>>(A, L); break;
-    default: lattice_step_kernel<3><<<blocks, TT, smem, st>>>(A, L); break;
+    case 0: return launch_mode<0>(A, L, st);
+    case 1: return launch_mode<1>(A, L, st);
+    case 2: return launch_mode<2>(A, L, st);
+    default: return launch_mode<3>(A, L, st);
     }
-    return cudaGetLastError();
 }
 
 cudaError_t launch_lattice_materialize(const int32_t* entries0, const uint4* mask, long long begin,
@@ -363,13 +448,12 @@ cudaError_t launch_lattice_materialize(const int32_t* entries0, const uint4* mas
 }
 
 void preload_lattice() {
-    preload_fn(lattice_step_kernel<0>);
-    preload_fn(lattice_step_kernel<1>);
-    preload_fn(lattice_step_kernel<2>);
-    preload_fn(lattice_step_kernel<3>);
+    preload_mode<0>();
+    preload_mode<1>();
+    preload_mode<2>();
+    preload_mode<3>();
     preload_fn(lattice_mask_kernel);
     preload_fn(lattice_materialize_kernel);
-    configure_smem();
 }
 
 } // namespace pdb

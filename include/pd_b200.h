@@ -268,6 +268,14 @@ int64_t pd_ctx_launch_count(pd_ctx* ctx);
 /* Live directed bonds in the resident alive mask (sum of n_neigh). */
 int64_t pd_ctx_live_bonds(pd_ctx* ctx);
 
+/* Which step kernel the uploaded model runs on. */
+enum {
+    PD_LAYOUT_EXACT = 0,   /* PD_BOND_PARALLEL / PD_NODE_PARALLEL: padded rows + alive bits */
+    PD_LAYOUT_TILES = 1,   /* PD_FAST, any mesh: brick tiles, compact 16-bit slot offsets */
+    PD_LAYOUT_LATTICE = 2  /* PD_FAST on a lattice: implicit 122-offset pattern + live mask */
+};
+int pd_ctx_layout(pd_ctx* ctx);
+
 /* ---- multi-GPU z-slabs (no reference counterpart: the reference is one
  * process) ------------------------------------------------
  *

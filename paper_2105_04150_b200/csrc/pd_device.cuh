@@ -179,7 +179,9 @@ __device__ __forceinline__ NodeIn load_node_in(const DevArgs& A, long long i) {
     return r;
 }
 
-template <int MODE>
+// BC = false: the caller guarantees A.bc_kind == NULL (no boundary conditions),
+// so the ramp code is compiled out (fewer registers in the fused kernels).
+template <int MODE, bool BC = true>
 __device__ __forceinline__ void node_epilogue(const DevArgs& A, long long i, const double4& ui,
                                               double fx, double fy, double fz, const NodeIn& in) {
     const double Fb[3] = {fx, fy, fz};
@@ -192,7 +194,7 @@ __device__ __forceinline__ void node_epilogue(const DevArgs& A, long long i, con
     // records out of local memory
 #pragma unroll
     for (int ax = 0; ax < 3; ++ax) {
-        const int kind = A.bc_kind ? int(A.bc_kind[3 * i + ax]) : PD_BC_FREE;
+        const int kind = (BC && A.bc_kind) ? int(A.bc_kind[3 * i + ax]) : PD_BC_FREE;
         double mag = 0.0;
         DevRamp ramp{};
         if (kind != PD_BC_FREE) {
@@ -251,10 +253,10 @@ __device__ __forceinline__ void node_epilogue(const DevArgs& A, long long i, con
     }
 }
 
-template <int MODE>
+template <int MODE, bool BC = true>
 __device__ __forceinline__ void node_epilogue(const DevArgs& A, long long i, const double4& ui,
                                               double fx, double fy, double fz) {
-    node_epilogue<MODE>(A, i, ui, fx, fy, fz, load_node_in(A, i));
+    node_epilogue<MODE, BC>(A, i, ui, fx, fy, fz, load_node_in(A, i));
 }
 
 } // namespace pdb

@@ -1024,6 +1024,12 @@ void* pd_ctx_stream(pd_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
 
 int64_t pd_ctx_launch_count(pd_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+int pd_ctx_layout(pd_ctx* ctx) {
+    if (!ctx || !ctx->fast)
+        return PD_LAYOUT_EXACT;
+    return ctx->lattice ? PD_LAYOUT_LATTICE : PD_LAYOUT_TILES;
+}
+
 int pd_ctx_upload(pd_ctx* ctx, const pd_bundle* b, const pd_state* st, int32_t variant) {
     ctx->partial = false;
     return upload_impl(ctx, b, st, variant);

@@ -92,7 +92,8 @@ struct Acc {
 __device__ __forceinline__ void stretch(const float4& rj, const float4& ri, float dx, float dy,
                                         float dz, float r2, float len, float rr, float& s,
                                         float& rc, float& cx, float& cy, float& cz) {
-    const float hx = rj.x - ri.x, hy = rj.y - ri.y, hz = rj.z - ri.z;  // eta / spacing
+    const float2 hxy = __fadd2_rn(make_float2(rj.x, rj.y), make_float2(-ri.x, -ri.y));
+    const float hx = hxy.x, hy = hxy.y, hz = rj.z - ri.z;  // eta / spacing
     cx = hx + dx;
     cy = hy + dy;
     cz = hz + dz;
@@ -136,6 +137,7 @@ __device__ __forceinline__ void slot(const float4* own, const float4& ri, const 
 }
 
 __constant__ signed char c_pat[NPAT][4];  // dx, dy, dz, |d|^2
+__constant__ signed char c_slot[343];     // (dz+3)*49 + (dy+3)*7 + (dx+3) -> slot, -1 outside
 
 // The rare pass for a node that lost bonds this step: recompute each live
 // slot's stretch (same arithmetic) and return the broken bits.
@@ -169,7 +171,7 @@ __device__ __forceinline__ void all_slots(std::integer_sequence<int, C...>, cons
     (slot<C>(own, ri, m, sc, a), ...);
 }
 
-template <int MODE, int BZT, int MINB>
+template <int MODE, int BZT, int MINB, bool BC>
 __global__ void __launch_bounds__(BX * BY * BZT, MINB) lattice_step_kernel(DevArgs A,
                                                                            LatticeArgs L) {
     constexpr int TT = BX * BY * BZT, HZ = BZT + 6;
@@ -234,7 +236,7 @@ __global__ void __launch_bounds__(BX * BY * BZT, MINB) lattice_step_kernel(DevAr
         A.body_force[3 * i + 2] = fz;
         return;
     }
-    node_epilogue<MODE>(A, i, A.u_in[i], fx, fy, fz);
+    node_epilogue<MODE, BC>(A, i, A.u_in[i], fx, fy, fz);
 }
 
 // row -> mask: bit c set for every live entry whose offset is pattern slot c;
@@ -252,22 +254,13 @@ __global__ void lattice_mask_kernel(const int32_t* entries, long long begin, lon
         if (j < 0)
             continue;
         const int dx = int(j % nx) - ix, dy = int((j / nx) % ny) - iy, dz = int(j / plane) - iz;
-        const int r2 = dx * dx + dy * dy + dz * dz;
-        if (r2 == 0 || r2 > 9) {
+        const int c = (dx < -3 || dx > 3 || dy < -3 || dy > 3 || dz < -3 || dz > 3)
+                          ? -1
+                          : int(c_slot[(dz + 3) * 49 + (dy + 3) * 7 + (dx + 3)]);
+        if (c < 0) {
             atomicExch(bad, 1);
             return;
         }
-        // slot index of (dx, dy, dz): count pattern offsets before it
-        int c = 0;
-        for (int z = -3; z <= 3; ++z)
-            for (int y = -3; y <= 3; ++y)
-                for (int x = -3; x <= 3; ++x) {
-                    const int q = x * x + y * y + z * z;
-                    if (q == 0 || q > 9)
-                        continue;
-                    if (z < dz || (z == dz && (y < dy || (y == dy && x < dx))))
-                        ++c;
-                }
         w[c >> 5] |= 1u << (c & 31);
     }
     mask[i] = make_uint4(w[0], w[1], w[2], w[3]);
@@ -292,16 +285,7 @@ __global__ void lattice_materialize_kernel(const int32_t* entries0, const uint4*
         if (j >= 0 && owned) {
             const int dx = int(j % nx) - ix, dy = int((j / nx) % ny) - iy,
                       dz = int(j / plane) - iz;
-            int c = 0;
-            for (int z = -3; z <= 3; ++z)
-                for (int y = -3; y <= 3; ++y)
-                    for (int x = -3; x <= 3; ++x) {
-                        const int q = x * x + y * y + z * z;
-                        if (q == 0 || q > 9)
-                            continue;
-                        if (z < dz || (z == dz && (y < dy || (y == dy && x < dx))))
-                            ++c;
-                    }
+            const int c = int(c_slot[(dz + 3) * 49 + (dy + 3) * 7 + (dx + 3)]);
             if (!((w[c >> 5] >> (c & 31)) & 1u))
                 v = -1;
         }
@@ -314,28 +298,28 @@ template <class K> void preload_fn(K k) {
     cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(k));
 }
 
-template <int MODE, int BZT, int MINB> cudaError_t configure_one() {
+template <int MODE, int BZT, int MINB, bool BC> cudaError_t configure_one() {
     static bool done = false;
     if (done)
         return cudaSuccess;
-    const cudaError_t e = cudaFuncSetAttribute(lattice_step_kernel<MODE, BZT, MINB>,
+    const cudaError_t e = cudaFuncSetAttribute(lattice_step_kernel<MODE, BZT, MINB, BC>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                int(sizeof(float4)) * nrec<BZT>());
     done = e == cudaSuccess;
     return e;
 }
 
-template <int MODE, int BZT, int MINB>
+template <int MODE, int BZT, int MINB, bool BC>
 cudaError_t launch_cfg(const DevArgs& A, const LatticeArgs& L, cudaStream_t st) {
     const int nbx = (L.nx + BX - 1) / BX, nby = (L.ny + BY - 1) / BY,
               nbz = (L.nz_own + BZT - 1) / BZT;
     const unsigned blocks = unsigned(nbx * nby * nbz);
     if (blocks == 0)
         return cudaSuccess;
-    const cudaError_t e = configure_one<MODE, BZT, MINB>();
+    const cudaError_t e = configure_one<MODE, BZT, MINB, BC>();
     if (e != cudaSuccess)
         return e;
-    lattice_step_kernel<MODE, BZT, MINB>
+    lattice_step_kernel<MODE, BZT, MINB, BC>
         <<<blocks, BX * BY * BZT, sizeof(float4) * nrec<BZT>(), st>>>(A, L);
     return cudaGetLastError();
 }
@@ -343,29 +327,40 @@ cudaError_t launch_cfg(const DevArgs& A, const LatticeArgs& L, cudaStream_t st) 
 // Brick shape and CTAs per SM (register budget).  Measured at 10M nodes
 // (profiles/): 16x4x4 bricks at 5 CTAs/SM (48 registers, 40 warps/SM) beat
 // 16x4x8 at 2 (64 registers) by 15 %; 16x4x2 bricks lose to the halo overhead
-// (13.8 staged records per node).  PD_LAT_CFG selects the alternatives:
-// 1 = 16x4x8 x3, 2 = 16x4x4 x4, 3 = 16x4x8 x2, 4 = 16x4x4 x6.
-template <int MODE> cudaError_t launch_mode(const DevArgs& A, const LatticeArgs& L, cudaStream_t st) {
+// (13.8 staged records per node).  Without boundary conditions the epilogue
+// is lighter and 6 CTAs/SM (40 registers) fit.  PD_LAT_CFG selects
+// alternatives: 1 = 16x4x8 x3, 2 = 16x4x4 x4, 3 = 16x4x8 x2, 4 = 16x4x4 x5.
+template <int MODE, bool BC>
+cudaError_t launch_bc(const DevArgs& A, const LatticeArgs& L, cudaStream_t st) {
     switch (L.cfg) {
-    case 1: return launch_cfg<MODE, 8, 3>(A, L, st);
-    case 2: return launch_cfg<MODE, 4, 4>(A, L, st);
-    case 3: return launch_cfg<MODE, 8, 2>(A, L, st);
-    case 4: return launch_cfg<MODE, 4, 6>(A, L, st);
-    default: return launch_cfg<MODE, 4, 5>(A, L, st);
+    case 1: return launch_cfg<MODE, 8, 3, BC>(A, L, st);
+    case 2: return launch_cfg<MODE, 4, 4, BC>(A, L, st);
+    case 3: return launch_cfg<MODE, 8, 2, BC>(A, L, st);
+    case 4: return launch_cfg<MODE, 4, 5, BC>(A, L, st);
+    default: return launch_cfg<MODE, 4, BC ? 5 : 6, BC>(A, L, st);
     }
 }
 
+template <int MODE> cudaError_t launch_mode(const DevArgs& A, const LatticeArgs& L, cudaStream_t st) {
+    return A.bc_kind ? launch_bc<MODE, true>(A, L, st) : launch_bc<MODE, false>(A, L, st);
+}
+
+template <int MODE, bool BC> void preload_bc() {
+    preload_fn(lattice_step_kernel<MODE, 8, 2, BC>);
+    preload_fn(lattice_step_kernel<MODE, 8, 3, BC>);
+    preload_fn(lattice_step_kernel<MODE, 4, 4, BC>);
+    preload_fn(lattice_step_kernel<MODE, 4, 5, BC>);
+    preload_fn(lattice_step_kernel<MODE, 4, BC ? 5 : 6, BC>);
+    configure_one<MODE, 8, 2, BC>();
+    configure_one<MODE, 8, 3, BC>();
+    configure_one<MODE, 4, 4, BC>();
+    configure_one<MODE, 4, 5, BC>();
+    configure_one<MODE, 4, BC ? 5 : 6, BC>();
+}
+
 template <int MODE> void preload_mode() {
-    preload_fn(lattice_step_kernel<MODE, 8, 2>);
-    preload_fn(lattice_step_kernel<MODE, 8, 3>);
-    preload_fn(lattice_step_kernel<MODE, 4, 4>);
-    preload_fn(lattice_step_kernel<MODE, 4, 5>);
-    preload_fn(lattice_step_kernel<MODE, 4, 6>);
-    configure_one<MODE, 8, 2>();
-    configure_one<MODE, 8, 3>();
-    configure_one<MODE, 4, 4>();
-    configure_one<MODE, 4, 5>();
-    configure_one<MODE, 4, 6>();
+    preload_bc<MODE, true>();
+    preload_bc<MODE, false>();
 }
 
 } // namespace
@@ -420,7 +415,14 @@ cudaError_t lattice_build_masks(const int32_t* entries, long long begin, long lo
         tab[c][3] = (signed char)(tab[c][0] * tab[c][0] + tab[c][1] * tab[c][1] +
                                   tab[c][2] * tab[c][2]);
     }
+    signed char slot_of[343];
+    for (int k = 0; k < 343; ++k)
+        slot_of[k] = -1;
+    for (int c = 0; c < NPAT; ++c)
+        slot_of[(tab[c][2] + 3) * 49 + (tab[c][1] + 3) * 7 + (tab[c][0] + 3)] = (signed char)c;
     cudaError_t e = cudaMemcpyToSymbolAsync(c_pat, tab, sizeof tab, 0, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess)
+        e = cudaMemcpyToSymbolAsync(c_slot, slot_of, sizeof slot_of, 0, cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess)
         return e;
     if (end > begin)

@@ -157,6 +157,7 @@ def library() -> C.CDLL:
         lib.pd_ctx_stream.restype = C.c_void_p
         lib.pd_ctx_launch_count.argtypes = [C.c_void_p]
         lib.pd_ctx_launch_count.restype = C.c_int64
+        lib.pd_ctx_layout.argtypes = [C.c_void_p]
         lib.pd_ctx_live_bonds.argtypes = [C.c_void_p]
         lib.pd_ctx_live_bonds.restype = C.c_int64
         lib.pd_damage.argtypes = [C.POINTER(abi.pd_neighbor_list), C.POINTER(C.c_double)]
@@ -344,6 +345,10 @@ class Context:
 
     def stream(self) -> int:
         return int(self.lib.pd_ctx_stream(self.h) or 0)
+
+    def layout(self) -> str:
+        """"exact", "tiles" or "lattice" (pd_ctx_layout)."""
+        return ("exact", "tiles", "lattice")[self.lib.pd_ctx_layout(self.h)]
 
     def launch_count(self) -> int:
         return int(self.lib.pd_ctx_launch_count(self.h))

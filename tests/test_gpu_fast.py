@@ -191,3 +191,51 @@ def test_fast_million_node_lattice(oracle):
         outs.append(st)
     assert max_rel_difference(outs[1].u, outs[0].u) <= TRAJ_TOL
     assert max_rel_difference(outs[1].a, outs[0].a) <= FORCE_TOL
+
+
+def test_lattice_layout_selected_and_matches_tiles(oracle, monkeypatch):
+    """PD_FAST on the bench lattice runs the implicit-connectivity kernel
+    (pd_lattice.cu); forced onto the general tile layout the same run must
+    agree with it within the fast-path tolerance, and both with the oracle."""
+    b, h, g = S.bench_lattice_bundle((20, 18, 26), s_c=1.5e-5)
+    fam = geometry.build_family(b.particles.coords, h, g)
+    layouts, states = [], []
+    for forced in (None, "general"):
+        if forced:
+            monkeypatch.setenv("PD_FAST_LAYOUT", forced)
+        else:
+            monkeypatch.delenv("PD_FAST_LAYOUT", raising=False)
+        ctx = engine.Context(0)
+        st = make_state(fam, False)
+        st.u = S.seed_displacements(b.particles.coords) * 3.0
+        ctx.upload(b, st, KernelVariant.fast)
+        layouts.append(ctx.layout())
+        ctx.run(20, 0, IntegratorKind.velocity_verlet, 0, KernelVariant.fast)
+        ctx.download(st)
+        ctx.close()
+        states.append(st)
+    assert layouts == ["lattice", "tiles"]
+    ref = make_state(fam, False)
+    ref.u = S.seed_displacements(b.particles.coords) * 3.0
+    oracle.simulate(b, ref, SimulateOptions(20, 0, 0, IntegratorKind.velocity_verlet))
+    s = stretches(b.particles, fam, ref.u)
+    for st in states:
+        check_break_sets(ref.connectivity.entries, st.connectivity.entries, s, 1.5e-5)
+        assert max_rel_difference(ref.u, st.u) <= FRACTURE_U_TOL
+    assert fam.n_neigh.sum() > ref.connectivity.n_neigh.sum()
+
+
+def test_lattice_layout_rejects_non_lattice_and_per_node_data():
+    """Irregular coordinates or no-failure nodes fall back to the tile layout."""
+    b, h, g = S.bench_lattice_bundle((12, 12, 12))
+    fam = geometry.build_family(b.particles.coords, h, g)
+    b.bc.no_failure[5] = 1
+    ctx = engine.Context(0)
+    ctx.upload(b, make_state(fam, False), KernelVariant.fast)
+    assert ctx.layout() == "tiles"
+    ctx.close()
+    b.bc.no_failure[5] = 0
+    ctx = engine.Context(0)
+    ctx.upload(b, make_state(fam, False), KernelVariant.fast)
+    assert ctx.layout() == "lattice"
+    ctx.close()

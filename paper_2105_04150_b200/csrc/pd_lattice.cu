@@ -178,10 +178,8 @@ __global__ void __launch_bounds__(BX * BY * BZT, MINB) lattice_step_kernel(DevAr
     if (MODE != 0 && *(volatile long long*)A.err_step != kNoError)
         return;
     extern __shared__ float4 rec[];  // HX * HY * HZ records (dynamic: > 48 KB for BZT = 8)
-    const int nbx = (L.nx + BX - 1) / BX, nby = (L.ny + BY - 1) / BY;
-    const int b = blockIdx.x;
-    const int bxi = b % nbx, byi = (b / nbx) % nby, bzi = b / (nbx * nby);
-    const int gx0 = bxi * BX, gy0 = byi * BY, gz0 = L.z0 + bzi * BZT;
+    // grid = (bricks in x, bricks in y, bricks in z over the owned planes)
+    const int gx0 = blockIdx.x * BX, gy0 = blockIdx.y * BY, gz0 = L.z0 + blockIdx.z * BZT;
     const int tx = threadIdx.x % BX, ty = (threadIdx.x / BX) % BY, tz = threadIdx.x / (BX * BY);
     const int gx = gx0 + tx, gy = gy0 + ty, gz = gz0 + tz;
     const bool active = gx < L.nx && gy < L.ny && gz < L.z0 + L.nz_own;
@@ -190,26 +188,49 @@ __global__ void __launch_bounds__(BX * BY * BZT, MINB) lattice_step_kernel(DevAr
     // the row mask streams in while the halo is staged
     uint4 m = active ? __ldcs(L.mask + i) : make_uint4(0, 0, 0, 0);
 
-    // 1. stage the halo box, one box row (22 records) per warp and pass:
-    //    fp32 (u - U_brick) / spacing
+    // 1. stage the halo box plane by plane (HX x HY = 220 records; thread t
+    //    owns record t % 220 of plane t / 220 of each pass): fp32
+    //    (u - U_brick) / spacing.  Planes are loaded PL at a time so several
+    //    L2/HBM round trips are in flight per thread.
     const double4 U0 = A.u_in[gx0 + (long long)L.nx * gy0 + plane * gz0];
     const float ih = float(L.inv_h);
     {
-        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-        const int X = gx0 - 3 + lane;
-        const bool xok = lane < HX && X >= 0 && X < L.nx;
-        for (int row = warp; row < HY * HZ; row += TT / 32) {
-            const int py = row % HY, pz = row / HY;
-            const int Y = gy0 - 3 + py, Z = gz0 - 3 + pz;
-            if (lane >= HX)
-                continue;
-            float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (xok && Y >= 0 && Y < L.ny && Z >= 0 && Z < L.nz_local) {
-                const double4 u = A.u_in[X + (long long)L.nx * Y + plane * Z];
-                r = make_float4(float(u.x - U0.x) * ih, float(u.y - U0.y) * ih,
-                                float(u.z - U0.z) * ih, 0.f);
+        constexpr int PREC = HX * HY;          // records per box plane
+        constexpr int PPASS = TT / PREC;       // planes per pass (1 or 2)
+        constexpr int PL = 2;                  // passes in flight
+        const int t = threadIdx.x;
+        const int q = t % PREC, pp = t / PREC;
+        const int px = q % HX, py = q / HX;
+        const int X = gx0 - 3 + px, Y = gy0 - 3 + py;
+        const bool xy_ok = pp < PPASS && X >= 0 && X < L.nx && Y >= 0 && Y < L.ny;
+        const double4* src = A.u_in + (X + (long long)L.nx * Y);
+        float4* dst = rec + q + PREC * pp;
+        for (int pz0 = 0; pz0 < HZ; pz0 += PPASS * PL) {
+            double ux[PL], uy[PL], uz[PL];
+            bool ok[PL];
+#pragma unroll
+            for (int k = 0; k < PL; ++k) {
+                const int pz = pz0 + pp + PPASS * k;
+                const int Z = gz0 - 3 + pz;
+                ok[k] = xy_ok && pz < HZ && Z >= 0 && Z < L.nz_local;
+                ux[k] = uy[k] = uz[k] = 0.0;
+                if (ok[k]) {
+                    const double4* pu = src + plane * Z;
+                    const double2 xy = *reinterpret_cast<const double2*>(pu);
+                    ux[k] = xy.x;
+                    uy[k] = xy.y;
+                    uz[k] = reinterpret_cast<const double*>(pu)[2];
+                }
             }
-            rec[row * HX + lane] = r;
+#pragma unroll
+            for (int k = 0; k < PL; ++k) {
+                const int pz = pz0 + pp + PPASS * k;
+                if (pp < PPASS && pz < HZ)
+                    dst[PREC * (pz - pp)] =
+                        ok[k] ? make_float4(float(ux[k] - U0.x) * ih, float(uy[k] - U0.y) * ih,
+                                            float(uz[k] - U0.z) * ih, 0.f)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
         }
     }
     __syncthreads();
@@ -313,14 +334,14 @@ template <int MODE, int BZT, int MINB, bool BC>
 cudaError_t launch_cfg(const DevArgs& A, const LatticeArgs& L, cudaStream_t st) {
     const int nbx = (L.nx + BX - 1) / BX, nby = (L.ny + BY - 1) / BY,
               nbz = (L.nz_own + BZT - 1) / BZT;
-    const unsigned blocks = unsigned(nbx * nby * nbz);
-    if (blocks == 0)
+    if (nbx * nby * nbz == 0)
         return cudaSuccess;
     const cudaError_t e = configure_one<MODE, BZT, MINB, BC>();
     if (e != cudaSuccess)
         return e;
     lattice_step_kernel<MODE, BZT, MINB, BC>
-        <<<blocks, BX * BY * BZT, sizeof(float4) * nrec<BZT>(), st>>>(A, L);
+        <<<dim3(unsigned(nbx), unsigned(nby), unsigned(nbz)), BX * BY * BZT,
+           sizeof(float4) * nrec<BZT>(), st>>>(A, L);
     return cudaGetLastError();
 }
 

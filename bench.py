@@ -67,7 +67,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -104,6 +104,16 @@ class ClockSampler:
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
                 "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_traffic(key):
+    """DRAM bytes per launch of the step kernel from the committed ncu capture
+    (profiles/traffic.json, written from `ncu --set full`), or None."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        return json.load(open(p))[key]["traffic_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        return None
 
 
 def build_workload(counts):
@@ -177,8 +187,10 @@ def run_reference_arm(args):
 
 
 def _summary(args, value, ms_step, world, n, N, live, bytes_step, achieved, e2e, launches,
-             clocks, cpu, variant_name, extra_config=None):
+             clocks, cpu, variant_name, extra_config=None, layout=None):
     peak, peak_kind = measured_peaks()
+    traffic = (measured_traffic(f"{layout}_{args.size}_{variant_name}")
+               if world == 1 and layout else None)
     cfg = {"workload": f"cfg4 lattice {args.size}^3 = {n} nodes, delta=3dx (N={N}), "
                        f"PMB c=1 s_c=1e6, velocity-Verlet, dt=1e-3, seeded u"
                        + (f", {world} z-slabs" if world > 1 else ""),
@@ -193,8 +205,13 @@ def _summary(args, value, ms_step, world, n, N, live, bytes_step, achieved, e2e,
         "dtype": "f64" if variant_name == "exact" else "f32 bond math / f64 state",
         "data": "synthetic", "config": cfg,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
-                     "bytes_per_step": bytes_step},
+                     "frac": achieved / peak,
+                     "traffic": None if traffic is None else traffic / 1e9,
+                     "traffic_unit": "GB per launch (ncu dram__bytes_read+write)",
+                     "peak_source": peak_kind, "bytes_per_step": bytes_step,
+                     "note": "achieved = SURVEY 8(d) algorithmic bytes / device time; the "
+                             "lattice kernel keeps connectivity implicit, so DRAM traffic is "
+                             "below the algorithmic bytes and the kernel is issue-bound"},
         "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "cpu_baseline": cpu,
     }
 
@@ -212,6 +229,7 @@ def run_single(args, variant, local):
 
     ctx = engine.Context(local)
     ctx.upload(bundle, state0, variant)
+    layout = ctx.layout()
     stream = torch.cuda.ExternalStream(ctx.stream())
     step = 0
     ctx.run(args.warmup, step, IntegratorKind.velocity_verlet, 0, variant)
@@ -253,7 +271,8 @@ def run_single(args, variant, local):
                   "(upload + layout + run + download inside the timed region)"}
     cpu = None if args.no_cpu else cpu_baseline(counts)
     out = _summary(args, value, ms_step, 1, n, N, live, bytes_step, achieved, e2e, launches,
-                   clk.summary(), cpu, args.variant, {"setup_s": round(setup_s, 2)})
+                   clk.summary(), cpu, args.variant,
+                   {"setup_s": round(setup_s, 2), "layout": layout}, layout)
     print(json.dumps(out))
     return 0
 
@@ -370,7 +389,7 @@ def run_slabs(args, variant, rank, world, local):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--variant", default="fast", choices=["exact", "fast"])

@@ -257,8 +257,10 @@ def run_single(args, variant, local):
     st = make_state(fam, False)
     st.u = state0.u.copy()
     e2e_steps = args.e2e_steps
-    h2d = (3 * n * 8 * 3 + 2 * n * 8 + 3 * n * 8 + n * N * 4 + 3 * n * 4 + 4 * n)
-    d2h = (3 * n * 8 * 3 + n * N * 4 + n * 4)
+    # bytes that cross PCIe: coords, u, v, a, V, rho, rows, counts in; u, v, a,
+    # n_neigh and only the rows that changed (none without breaks) out
+    h2d = (3 * n * 8 * 4 + 2 * n * 8 + n * N * 4 + 2 * n * 4)
+    d2h = (3 * n * 8 * 3 + n * 4)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     engine.simulate(bundle, st, SimulateOptions(e2e_steps, 0, 0, IntegratorKind.velocity_verlet,

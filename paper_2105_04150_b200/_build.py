@@ -29,6 +29,7 @@ UNITS = {
     "pd_family.cu": ["-fmad=false"],
     "pd_layout.cu": ["-fmad=false"],
     "pd_lattice.cu": ["-fmad=true"],
+    "pd_xfer.cpp": ["-x", "cu"],
 }
 HEADERS = ["pd_device.cuh", "pd_internal.h", "pd_fast.cuh"]
 
@@ -54,7 +55,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
         src = os.path.join(CSRC, unit)
         if not os.path.exists(src):
             continue
-        obj = os.path.join(OBJ, unit.replace(".cu", ".o"))
+        obj = os.path.join(OBJ, os.path.splitext(unit)[0] + ".o")
         objs.append(obj)
         if force or _mtime(obj) < max(_mtime(src), hdr_t, _mtime(__file__)):
             cmd = [nvcc, *ARCH, *COMMON, *flags, "-c", src, "-o", obj]

@@ -260,7 +260,42 @@ __global__ void node_values_kernel(const double4* u, const double* v, const doub
     }
 }
 
+// rows whose materialised entries differ from the uploaded ones (unordered list)
+__global__ void changed_rows_kernel(const int32_t* cur, const int32_t* orig, long long n, int N,
+                                    int* list, unsigned long long* count) {
+    const long long i = blockIdx.x * (long long)TPB + threadIdx.x;
+    if (i >= n)
+        return;
+    for (int k = 0; k < N; ++k)
+        if (cur[i * N + k] != orig[i * N + k]) {
+            list[atomicAdd(count, 1ull)] = int(i);
+            return;
+        }
+}
+
+__global__ void gather_list_rows_kernel(const int32_t* cur, const int* list, long long m, int N,
+                                        int32_t* out) {
+    const long long r = blockIdx.x;
+    if (r >= m)
+        return;
+    const long long i = list[r];
+    for (int k = threadIdx.x; k < N; k += blockDim.x)
+        out[r * N + k] = cur[i * N + k];
+}
+
 } // namespace
+
+void launch_changed_rows(const int32_t* cur, const int32_t* orig, long long n, int N, int* list,
+                         unsigned long long* count, cudaStream_t st) {
+    if (n > 0)
+        changed_rows_kernel<<<grid_for(n), TPB, 0, st>>>(cur, orig, n, N, list, count);
+}
+
+void launch_gather_list_rows(const int32_t* cur, const int* list, long long m, int N, int32_t* out,
+                             cudaStream_t st) {
+    if (m > 0)
+        gather_list_rows_kernel<<<unsigned(m), 128, 0, st>>>(cur, list, m, N, out);
+}
 
 void launch_node_values(const double4* u, const double* v, const double* a, const double4* xv,
                         const double* body, const double* ext, const long long* rows,
@@ -322,6 +357,8 @@ void preload_aux() {
     preload(sum_kernel);
     preload(tips_kernel);
     preload(node_values_kernel);
+    preload(changed_rows_kernel);
+    preload(gather_list_rows_kernel);
 }
 
 void launch_slab_sync(const SyncArgs& S, cudaStream_t st) {

@@ -208,6 +208,7 @@ struct pd_ctx {
     int64_t comp_begin = 0, comp_end = 0;
     int64_t own_begin = 0, own_end = 0;  // owned LOCAL node ids
     bool partial = false;                // uploaded by pd_ctx_upload_part
+    bool dst_has_upload = false;         // download target = the uploaded host arrays
     // multi-GPU slab world (pd_ctx_connect)
     int rank = 0, world = 1;
     DevBuf<unsigned long long> sync;     // 2 * PD_MAX_RANKS words (epochs, flags)
@@ -515,8 +516,7 @@ int download(pd_ctx* ctx, pd_state* st, pd_force_field* forces, int32_t fields) 
             ++ctx->launches;
             src = ctx->scratch_f64.p;
         }
-        PD_CK(cudaMemcpyAsync(host, src, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s));
-        PD_CK(cudaStreamSynchronize(s));
+        PD_CK(d2h_large(host, src, sizeof(double) * 3 * n, s));
         return PD_OK;
     };
     if ((fields & PD_FIELD_U) && st && st->u) {
@@ -530,9 +530,7 @@ int download(pd_ctx* ctx, pd_state* st, pd_force_field* forces, int32_t fields) 
         PD_CK(ctx->scratch_f64.alloc(size_t(3 * n)));
         launch_unpack_u(src, n, ctx->scratch_f64.p, s);
         ++ctx->launches;
-        PD_CK(cudaMemcpyAsync(st->u, ctx->scratch_f64.p, sizeof(double) * 3 * n,
-                              cudaMemcpyDeviceToHost, s));
-        PD_CK(cudaStreamSynchronize(s));
+        PD_CK(d2h_large(st->u, ctx->scratch_f64.p, sizeof(double) * 3 * n, s));
     }
     if ((fields & PD_FIELD_V) && st && st->v)
         PD_TRY(vec3_out(ctx->v.p, st->v));
@@ -556,8 +554,37 @@ int download(pd_ctx* ctx, pd_state* st, pd_force_field* forces, int32_t fields) 
                 launch_materialize_entries(ctx->entries.p, ctx->alive.p, n, ctx->N, ctx->W,
                                            ctx->scratch_i32.p, s);
             ++ctx->launches;
-            PD_CK(cudaMemcpyAsync(st->connectivity.entries, ctx->scratch_i32.p,
-                                  sizeof(int32_t) * slots, cudaMemcpyDeviceToHost, s));
+            if (ctx->dst_has_upload) {
+                // the destination still holds the uploaded rows (one-shot
+                // simulate writes back into the caller's array): move only
+                // the rows that changed
+                PD_CK(ctx->counter.alloc(1));
+                PD_CK(ctx->scratch_n.alloc(size_t(n)));
+                PD_CK(cudaMemsetAsync(ctx->counter.p, 0, sizeof(unsigned long long), s));
+                launch_changed_rows(ctx->scratch_i32.p, ctx->entries.p, n, ctx->N,
+                                    ctx->scratch_n.p, ctx->counter.p, s);
+                unsigned long long m = 0;
+                PD_CK(cudaMemcpyAsync(&m, ctx->counter.p, sizeof m, cudaMemcpyDeviceToHost, s));
+                PD_CK(cudaStreamSynchronize(s));
+                ctx->launches += 1;
+                if (m > 0) {
+                    DevBuf<int32_t> rows;
+                    PD_CK(rows.alloc(size_t(m) * size_t(ctx->N)));
+                    launch_gather_list_rows(ctx->scratch_i32.p, ctx->scratch_n.p, (long long)m,
+                                            ctx->N, rows.p, s);
+                    ++ctx->launches;
+                    std::vector<int> list(static_cast<size_t>(m));
+                    std::vector<int32_t> host_rows(size_t(m) * size_t(ctx->N));
+                    PD_CK(d2h_large(list.data(), ctx->scratch_n.p, sizeof(int) * m, s));
+                    PD_CK(d2h_large(host_rows.data(), rows.p, sizeof(int32_t) * host_rows.size(), s));
+                    for (size_t r = 0; r < list.size(); ++r)
+                        std::memcpy(st->connectivity.entries + size_t(list[r]) * size_t(ctx->N),
+                                    host_rows.data() + r * size_t(ctx->N), sizeof(int32_t) * ctx->N);
+                }
+            } else {
+                PD_CK(d2h_large(st->connectivity.entries, ctx->scratch_i32.p,
+                                sizeof(int32_t) * slots, s));
+            }
         }
         if (st->connectivity.n_neigh) {
             const int32_t* src = ctx->n_neigh.p;
@@ -579,8 +606,7 @@ int download(pd_ctx* ctx, pd_state* st, pd_force_field* forces, int32_t fields) 
                                     ctx->N, nullptr, ctx->hist.p, s);
             ++ctx->launches;
         }
-        PD_CK(cudaMemcpyAsync(st->bond_history, ctx->hist.p, sizeof(double) * slots,
-                              cudaMemcpyDeviceToHost, s));
+        PD_CK(d2h_large(st->bond_history, ctx->hist.p, sizeof(double) * slots, s));
     }
     if ((fields & PD_FIELD_FORCES) && forces) {
         if (forces->body_force)
@@ -1378,6 +1404,9 @@ int pd_simulate(const pd_bundle* bundle, pd_state* state, const pd_options* opti
     PD_TRY(pd_ctx_upload(ctx, bundle, state, options->variant));
     PD_CK(cudaStreamSynchronize(ctx->stream));
     tm.mark("simulate: upload");
+    // every download of this call writes into the caller's own arrays, which
+    // hold the uploaded rows until the first download rewrites changed rows
+    ctx->dst_has_upload = true;
     int rc = run_loop(ctx, *options, on_write, user, PD_FIELD_ALL, state, tips_out, tips_capacity,
                       n_tips_out);
     PD_CK(cudaStreamSynchronize(ctx->stream));

@@ -11,6 +11,11 @@
 
 namespace pdb {
 
+// pd_xfer.cpp: large host <-> device copies through pinned bounce buffers
+// (synchronous with respect to the host on return)
+cudaError_t h2d_large(void* dev, const void* host, size_t bytes, cudaStream_t s);
+cudaError_t d2h_large(void* host, const void* dev, size_t bytes, cudaStream_t s);
+
 // Owning device buffer (cudaMalloc'd), resized on demand.
 template <class T> struct DevBuf {
     T* p = nullptr;
@@ -38,7 +43,7 @@ template <class T> struct DevBuf {
         cudaError_t e = alloc(n);
         if (e != cudaSuccess || n == 0)
             return e;
-        return cudaMemcpyAsync(p, host, n * sizeof(T), cudaMemcpyHostToDevice, st);
+        return h2d_large(p, host, n * sizeof(T), st);
     }
 };
 
@@ -121,6 +126,10 @@ struct SyncArgs {
     long long timeout_ns;
 };
 void launch_slab_sync(const SyncArgs& S, cudaStream_t st);
+void launch_changed_rows(const int32_t* cur, const int32_t* orig, long long n, int N, int* list,
+                         unsigned long long* count, cudaStream_t st);
+void launch_gather_list_rows(const int32_t* cur, const int* list, long long m, int N, int32_t* out,
+                             cudaStream_t st);
 void launch_node_values(const double4* u, const double* v, const double* a, const double4* xv,
                         const double* body, const double* ext, const long long* rows,
                         long long count, double* out, cudaStream_t st);

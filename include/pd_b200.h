@@ -276,6 +276,31 @@ enum {
 };
 int pd_ctx_layout(pd_ctx* ctx);
 
+/* ---- binary containers (io.cpp:297-564), byte-compatible with the reference
+ * PDST = restart state (save_state/load_state), PDNL = family cache
+ * (save_cache/load_cache).  Readers validate like the reference and report
+ * its IoError text ("<path>: <what>") with PD_E_RUNTIME. ---------------- */
+typedef struct pd_file_header {
+    int64_t n;
+    int64_t group_size;
+    int64_t step; /* PDST only */
+    double horizon;
+    int32_t has_bond_type, has_history, has_lambda, has_beta;
+} pd_file_header;
+
+int pd_save_state(const pd_state* state, const char* path);
+int pd_state_file_header(const char* path, pd_file_header* out);
+/* Fills caller arrays sized from the header (bond_type / history may be NULL
+ * to skip those sections). */
+int pd_load_state(const char* path, pd_state* state);
+int pd_save_cache(const pd_neighbor_list* family, const pd_corrections* corrections,
+                  const char* path);
+int pd_cache_file_header(const char* path, pd_file_header* out);
+int pd_load_cache(const char* path, pd_neighbor_list* family, pd_corrections* corrections);
+/* save_state of the resident state, streamed from device memory (no host
+ * copy of the state); one-GPU contexts only. */
+int pd_ctx_save_state(pd_ctx* ctx, const char* path);
+
 /* ---- multi-GPU z-slabs (no reference counterpart: the reference is one
  * process) ------------------------------------------------
  *

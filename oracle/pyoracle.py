@@ -153,6 +153,21 @@ class Reference(Backend):
     def build_family(self, coords, horizon, hint=None) -> NeighborList:
         return _family_from(self.lib, "ref_", coords, horizon, hint)
 
+    def save_state(self, state, path: str) -> None:
+        """io::save_state of the reference."""
+        self.lib.ref_save_state.argtypes = [C.POINTER(abi.pd_state), C.c_char_p]
+        st = abi.Marshal().state(state)
+        self._check(self.lib.ref_save_state(C.byref(st), os.fsencode(path)))
+
+    def save_cache(self, family, corrections, path: str) -> None:
+        """io::save_cache of the reference."""
+        self.lib.ref_save_cache.argtypes = [C.POINTER(abi.pd_neighbor_list),
+                                            C.POINTER(abi.pd_corrections), C.c_char_p]
+        m = abi.Marshal()
+        f = m.family(family)
+        c = m.corrections(corrections)
+        self._check(self.lib.ref_save_cache(C.byref(f), C.byref(c), os.fsencode(path)))
+
     def ramp(self, which: str, kind: int, rise: int, target: float, step: int) -> float:
         r = abi.pd_ramp(int(kind), int(rise), float(target))
         return self.lib.ref_ramp({"scale": 0, "rate": 1, "accel": 2}[which], C.byref(r), int(step))

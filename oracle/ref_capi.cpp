@@ -152,6 +152,19 @@ struct RandomHandle {
 extern "C" {
 
 const char* ref_last_error(void) { return g_err.c_str(); }
+
+// io::save_state / io::save_cache / load_state of the reference (golden files)
+int ref_save_state(const pd_state* st, const char* path) {
+    return map_exceptions([&] { io::save_state(to_state(*st), path); });
+}
+
+int ref_save_cache(const pd_neighbor_list* fam, const pd_corrections* corr, const char* path) {
+    return map_exceptions([&] { io::save_cache(to_family(*fam), to_corr(*corr), path); });
+}
+
+int ref_load_state_step(const char* path, int64_t* step) {
+    return map_exceptions([&] { *step = io::load_state(path).step; });
+}
 void ref_set_threads(int threads) { set_worker_cap(unsigned(threads < 0 ? 0 : threads)); }
 unsigned ref_worker_count(void) { return worker_count(); }
 

@@ -6,7 +6,8 @@ sm_100a kernels in libpd_b200.so.  There is no CPU fallback: every entry
 point raises CudaError when the library or a B200 is missing.
 """
 from .abi import CudaError, DomainError, InvalidArgument, PeridynRuntimeError
-from .engine import Context, compute_forces, device_count, local_damage, simulate
+from .engine import (Context, compute_forces, device_count, load_cache, load_state, local_damage,
+                     save_cache, save_state, simulate)
 from .geometry import GridDesc, break_notch, break_plane, build_family, grid_coordinates
 from .types import (BCKind, BoundaryConditions, Corrections, DamageLaw, DamageModel, ForceField,
                     IntegratorKind, KernelVariant, ModelBundle, NeighborList, ParticleSet,
@@ -19,5 +20,6 @@ __all__ = [
     "KernelVariant", "ModelBundle", "NeighborList", "ParticleSet", "PeridynRuntimeError",
     "RampKind", "RampProfile", "SimulateOptions", "SimulateResult", "SimulationState",
     "TipRecord", "break_notch", "break_plane", "build_family", "compute_forces",
-    "device_count", "grid_coordinates", "local_damage", "make_state", "simulate",
+    "device_count", "grid_coordinates", "load_cache", "load_state", "local_damage", "make_state",
+    "save_cache", "save_state", "simulate",
 ]

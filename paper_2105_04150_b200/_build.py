@@ -30,6 +30,7 @@ UNITS = {
     "pd_layout.cu": ["-fmad=false"],
     "pd_lattice.cu": ["-fmad=true"],
     "pd_xfer.cpp": ["-x", "cu"],
+    "pd_io.cpp": ["-x", "cu"],
 }
 HEADERS = ["pd_device.cuh", "pd_internal.h", "pd_fast.cuh"]
 

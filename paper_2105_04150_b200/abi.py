@@ -101,6 +101,12 @@ HOOK = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(pd_state), C.POINTER(pd_force_
 
 # ---- errors (the reference's exception types) ---------------------------------
 
+class pd_file_header(C.Structure):
+    _fields_ = [("n", i64), ("group_size", i64), ("step", i64), ("horizon", C.c_double),
+                ("has_bond_type", i32), ("has_history", i32), ("has_lambda", i32),
+                ("has_beta", i32)]
+
+
 PD_MAX_RANKS = 16
 
 

@@ -182,6 +182,7 @@ struct pd_ctx {
 
     int64_t n = 0;
     int N = 0, W = 0, log2N = 0;
+    double horizon = 0;
     int variant = PD_BOND_PARALLEL;
     bool history = false;
     bool has_bc = false;
@@ -351,6 +352,7 @@ int upload_common(pd_ctx* ctx, const pd_particles& p, const pd_state& st,
         return fail(PD_E_INVALID_ARGUMENT, "ParticleSet: field lengths differ");
     ctx->n = n;
     ctx->N = int(N);
+    ctx->horizon = st.connectivity.horizon;
     ctx->W = N < 32 ? 1 : int(N / 32);
     ctx->log2N = 0;
     while ((int64_t(1) << ctx->log2N) < N)
@@ -1049,6 +1051,75 @@ void pd_ctx_destroy(pd_ctx* ctx) {
 void* pd_ctx_stream(pd_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
 
 int64_t pd_ctx_launch_count(pd_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int pd_ctx_save_state(pd_ctx* ctx, const char* path) {
+    PD_TRY(select_device(ctx));
+    if (ctx->world > 1 || ctx->partial)
+        return fail(PD_E_INVALID_ARGUMENT, "save_state: a slab context holds a local model only");
+    cudaStream_t s = ctx->stream;
+    const int64_t n = ctx->n, N = ctx->N, slots = n * N;
+    const int* inv = ctx->permuted() ? ctx->lay.inv.p : nullptr;
+    StreamWriter w;
+    PD_TRY(w.open(path));
+    w.bytes("PDST", 4);
+    w.pod(uint32_t(1));
+    w.pod(uint64_t(n));
+    w.pod(uint64_t(N));
+    w.pod(uint64_t(ctx->step));
+    w.pod(double(ctx->horizon));
+    // u (double4 {u, no_fail} in device-row order -> flat n x 3, reference order)
+    const double4* u = ctx->u[ctx->cur].p;
+    if (inv) {
+        PD_CK(ctx->scratch_d4.alloc(size_t(n)));
+        launch_gather_rows<double4, 1>(u, ctx->scratch_d4.p, inv, n, s);
+        u = ctx->scratch_d4.p;
+    }
+    PD_CK(ctx->scratch_f64.alloc(size_t(3 * n)));
+    launch_unpack_u(u, n, ctx->scratch_f64.p, s);
+    PD_TRY(w.section_device(7, ctx->scratch_f64.p, 24 * uint64_t(n), s));
+    for (int f = 0; f < 2; ++f) {
+        const double* src = f == 0 ? ctx->v.p : ctx->a.p;
+        if (inv) {
+            launch_gather_rows<double, 3>(src, ctx->scratch_f64.p, inv, n, s);
+            src = ctx->scratch_f64.p;
+        }
+        PD_TRY(w.section_device(f == 0 ? 8 : 9, src, 24 * uint64_t(n), s));
+    }
+    PD_CK(ctx->scratch_i32.alloc(size_t(slots)));
+    if (ctx->lattice)
+        PD_CK(launch_lattice_materialize(ctx->entries.p, ctx->lmask.p, ctx->own_begin,
+                                         ctx->own_end, n, ctx->N, ctx->lat, ctx->scratch_i32.p, s));
+    else if (ctx->fast)
+        launch_fast_materialize(ctx->entries.p, ctx->lay.inv.p, ctx->lay.tile_of.p,
+                                ctx->lay.tile_start.p, ctx->lay.slot_off.p, ctx->fast_T,
+                                ctx->lay.lidx.p, nullptr, n, ctx->N, ctx->scratch_i32.p, nullptr, s);
+    else
+        launch_materialize_entries(ctx->entries.p, ctx->alive.p, n, ctx->N, ctx->W,
+                                   ctx->scratch_i32.p, s);
+    PD_TRY(w.section_device(1, ctx->scratch_i32.p, 4 * uint64_t(slots), s));
+    PD_CK(ctx->scratch_n.alloc(size_t(n)));
+    for (int f = 0; f < 2; ++f) {
+        const int32_t* src = f == 0 ? ctx->n_neigh.p : ctx->initial.p;
+        if (inv) {
+            launch_gather_rows<int32_t, 1>(src, ctx->scratch_n.p, inv, n, s);
+            src = ctx->scratch_n.p;
+        }
+        PD_TRY(w.section_device(f == 0 ? 2 : 6, src, 4 * uint64_t(n), s));
+    }
+    if (ctx->btype.p)
+        PD_TRY(w.section_device(5, ctx->btype.p, uint64_t(slots), s));
+    if (ctx->history) {
+        if (ctx->permuted())
+            launch_fast_materialize(ctx->entries.p, ctx->lay.inv.p, ctx->lay.tile_of.p,
+                                    ctx->lay.tile_start.p, ctx->lay.slot_off.p, ctx->fast_T,
+                                    ctx->lay.lidx.p, ctx->lay.hist32.p, n, ctx->N, nullptr,
+                                    ctx->hist.p, s);
+        PD_TRY(w.section_device(10, ctx->hist.p, 8 * uint64_t(slots), s));
+    }
+    ctx->launches += 8;
+    PD_TRY(w.close());
+    return ok();
+}
 
 int pd_ctx_layout(pd_ctx* ctx) {
     if (!ctx || !ctx->fast)

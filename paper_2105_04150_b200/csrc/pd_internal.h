@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 
 #include <cstddef>
+#include <cstdio>
+#include <string>
 #include <vector>
 
 #include "pd_device.cuh"
@@ -15,6 +17,22 @@ namespace pdb {
 // (synchronous with respect to the host on return)
 cudaError_t h2d_large(void* dev, const void* host, size_t bytes, cudaStream_t s);
 cudaError_t d2h_large(void* host, const void* dev, size_t bytes, cudaStream_t s);
+
+// pd_io.cpp: binary container writer (reference io.cpp BinWriter), host or
+// device sections
+struct StreamWriter {
+    FILE* f = nullptr;
+    std::string path;
+    void* bounce = nullptr;
+    bool failed = false;
+    ~StreamWriter();
+    int open(const char* p);
+    int bytes(const void* data, uint64_t len);
+    template <class T> int pod(T v) { return bytes(&v, sizeof(T)); }
+    int section_host(uint32_t id, const void* data, uint64_t len);
+    int section_device(uint32_t id, const void* dev, uint64_t len, cudaStream_t s);
+    int close();
+};
 
 // Owning device buffer (cudaMalloc'd), resized on demand.
 template <class T> struct DevBuf {

@@ -175,6 +175,80 @@ def library() -> C.CDLL:
     return _LIB
 
 
+# ---- binary containers (io.cpp:297-564), byte-compatible with the reference --------
+
+def _io_lib():
+    lib = library()
+    lib.pd_save_state.argtypes = [C.POINTER(abi.pd_state), C.c_char_p]
+    lib.pd_state_file_header.argtypes = [C.c_char_p, C.POINTER(abi.pd_file_header)]
+    lib.pd_load_state.argtypes = [C.c_char_p, C.POINTER(abi.pd_state)]
+    lib.pd_save_cache.argtypes = [C.POINTER(abi.pd_neighbor_list), C.POINTER(abi.pd_corrections),
+                                  C.c_char_p]
+    lib.pd_cache_file_header.argtypes = [C.c_char_p, C.POINTER(abi.pd_file_header)]
+    lib.pd_load_cache.argtypes = [C.c_char_p, C.POINTER(abi.pd_neighbor_list),
+                                  C.POINTER(abi.pd_corrections)]
+    lib.pd_ctx_save_state.argtypes = [C.c_void_p, C.c_char_p]
+    return lib
+
+
+def save_state(state: SimulationState, path: str) -> None:
+    """io::save_state (io.cpp:485-505): a PDST restart file."""
+    lib = _io_lib()
+    st = Marshal().state(state)
+    check(lib.pd_save_state(C.byref(st), os.fsencode(path)), lib.pd_last_error)
+
+
+def load_state(path: str) -> SimulationState:
+    """io::load_state (io.cpp:507-562)."""
+    from .types import NeighborList
+    lib = _io_lib()
+    h = abi.pd_file_header()
+    check(lib.pd_state_file_header(os.fsencode(path), C.byref(h)), lib.pd_last_error)
+    n, N = int(h.n), int(h.group_size)
+    fam = NeighborList(np.zeros(n * N, np.int32), np.zeros(n, np.int32), np.zeros(n, np.int32), N,
+                       float(h.horizon), np.zeros(n * N if h.has_bond_type else 0, np.uint8))
+    st = SimulationState(np.zeros(3 * n), np.zeros(3 * n), np.zeros(3 * n), 0, fam,
+                         np.zeros(n * N if h.has_history else 0))
+    m = Marshal()
+    ps = m.state(st)
+    check(lib.pd_load_state(os.fsencode(path), C.byref(ps)), lib.pd_last_error)
+    st.step = int(ps.step)
+    fam.horizon = float(ps.connectivity.horizon)
+    if not h.has_bond_type:
+        fam.bond_type = None
+    return st
+
+
+def save_cache(family, corrections, path: str) -> None:
+    """io::save_cache (io.cpp:416-434): a PDNL family cache."""
+    lib = _io_lib()
+    m = Marshal()
+    f = m.family(family)
+    c = m.corrections(corrections)
+    check(lib.pd_save_cache(C.byref(f), C.byref(c), os.fsencode(path)), lib.pd_last_error)
+
+
+def load_cache(path: str):
+    """io::load_cache (io.cpp:436-483) -> (NeighborList, Corrections)."""
+    from .types import Corrections, NeighborList
+    lib = _io_lib()
+    h = abi.pd_file_header()
+    check(lib.pd_cache_file_header(os.fsencode(path), C.byref(h)), lib.pd_last_error)
+    n, N = int(h.n), int(h.group_size)
+    fam = NeighborList(np.zeros(n * N, np.int32), np.zeros(n, np.int32), np.zeros(n, np.int32), N,
+                       float(h.horizon), np.zeros(n * N if h.has_bond_type else 0, np.uint8))
+    corr = Corrections(np.zeros(n * N) if h.has_lambda else None,
+                       np.zeros(n * N) if h.has_beta else None, None)
+    m = Marshal()
+    f = m.family(fam)
+    c = m.corrections(corr)
+    check(lib.pd_load_cache(os.fsencode(path), C.byref(f), C.byref(c)), lib.pd_last_error)
+    fam.horizon = float(f.horizon)
+    if not h.has_bond_type:
+        fam.bond_type = None
+    return fam, corr
+
+
 def backend() -> Backend:
     global _BACKEND
     if _BACKEND is None:
@@ -345,6 +419,11 @@ class Context:
 
     def stream(self) -> int:
         return int(self.lib.pd_ctx_stream(self.h) or 0)
+
+    def save_state(self, path: str) -> None:
+        """io::save_state of the resident state, streamed from device memory."""
+        lib = _io_lib()
+        self._check(lib.pd_ctx_save_state(self.h, os.fsencode(path)))
 
     def layout(self) -> str:
         """"exact", "tiles" or "lattice" (pd_ctx_layout)."""

@@ -261,6 +261,11 @@ def run_single(args, variant, local):
     # n_neigh and only the rows that changed (none without breaks) out
     h2d = (3 * n * 8 * 4 + 2 * n * 8 + n * N * 4 + 2 * n * 4)
     d2h = (3 * n * 8 * 3 + n * 4)
+    # one untimed call first (driver/pinned-buffer first-use costs), then the timed one
+    warm = make_state(fam, False)
+    warm.u = state0.u.copy()
+    engine.simulate(bundle, warm, SimulateOptions(2, 0, 0, IntegratorKind.velocity_verlet, variant))
+    del warm
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     engine.simulate(bundle, st, SimulateOptions(e2e_steps, 0, 0, IntegratorKind.velocity_verlet,

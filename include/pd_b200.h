@@ -178,6 +178,10 @@ int pd_abi_version(void);
 const char* pd_last_error(void);
 /* Number of usable sm_100 devices (0 on a machine without a B200). */
 int pd_device_count(void);
+/* Device blocks of destroyed contexts are kept mapped for reuse by the next
+ * context of the same size (repeated simulate() calls, calibration loops);
+ * this returns them to the driver.  PD_NO_BLOCK_CACHE=1 disables the cache. */
+void pd_release_cached_memory(void);
 
 /* ---- one-shot drop-ins (host buffers in, host buffers out) ------------ */
 

@@ -1465,13 +1465,18 @@ int pd_simulate(const pd_bundle* bundle, pd_state* state, const pd_options* opti
     if (bundle->model.n_laws >= 1 && needs_history(bundle->model) &&
         state->bond_history_size != state->connectivity.n * state->connectivity.group_size)
         return fail(PD_E_INVALID_ARGUMENT, "simulate: bond_history must be sized n x N");
+    PhaseTimer tm;
     pd_ctx* ctx = nullptr;
     PD_TRY(pd_ctx_create(0, &ctx));
     struct Guard {
         pd_ctx* c;
-        ~Guard() { pd_ctx_destroy(c); }
-    } guard{ctx};
-    PhaseTimer tm;
+        PhaseTimer* t;
+        ~Guard() {
+            pd_ctx_destroy(c);
+            t->mark("simulate: destroy");
+        }
+    } guard{ctx, &tm};
+    tm.mark("simulate: create");
     PD_TRY(pd_ctx_upload(ctx, bundle, state, options->variant));
     PD_CK(cudaStreamSynchronize(ctx->stream));
     tm.mark("simulate: upload");

@@ -34,7 +34,14 @@ struct StreamWriter {
     int close();
 };
 
-// Owning device buffer (cudaMalloc'd), resized on demand.
+// pd_xfer.cpp: process-wide cache of device blocks.  Contexts of the same
+// model size (the calibration outer loop, repeated simulate() calls) reuse
+// mapped memory instead of paying cudaFree/cudaMalloc of ~10 GB each time.
+cudaError_t dev_alloc(void** p, size_t bytes);
+void dev_free(void* p, size_t bytes);
+void release_cached_blocks();
+
+// Owning device buffer, resized on demand.
 template <class T> struct DevBuf {
     T* p = nullptr;
     size_t count = 0;
@@ -44,7 +51,7 @@ template <class T> struct DevBuf {
     ~DevBuf() { release(); }
     void release() {
         if (p)
-            cudaFree(p);
+            dev_free(p, count * sizeof(T));
         p = nullptr;
         count = 0;
     }
@@ -54,8 +61,13 @@ template <class T> struct DevBuf {
         release();
         if (n == 0)
             return cudaSuccess;
-        count = n;
-        return cudaMalloc(&p, n * sizeof(T));
+        void* q = nullptr;
+        const cudaError_t e = dev_alloc(&q, n * sizeof(T));
+        if (e == cudaSuccess) {
+            p = static_cast<T*>(q);
+            count = n;
+        }
+        return e;
     }
     cudaError_t upload(const T* host, size_t n, cudaStream_t st) {
         cudaError_t e = alloc(n);

@@ -9,7 +9,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -137,4 +140,91 @@ cudaError_t d2h_large(void* host, const void* dev, size_t bytes, cudaStream_t s)
     return cudaSuccess;
 }
 
+// ---- device block cache ------------------------------------------------------
+
+namespace {
+
+struct BlockCache {
+    std::mutex mu;
+    // (device, bytes) -> free blocks
+    std::map<std::pair<int, size_t>, std::vector<void*>> free;
+    size_t cached = 0;
+    size_t limit = 0;
+    bool enabled = true;
+    BlockCache() {
+        if (const char* e = std::getenv("PD_NO_BLOCK_CACHE"))
+            enabled = std::atoi(e) == 0;
+    }
+};
+
+BlockCache& cache() {
+    static BlockCache* c = new BlockCache;  // never destroyed: blocks outlive static teardown
+    return *c;
+}
+
+// blocks below 1 MB are not worth caching
+constexpr size_t kMinCached = size_t(1) << 20;
+
+} // namespace
+
+cudaError_t dev_alloc(void** p, size_t bytes) {
+    BlockCache& c = cache();
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (c.enabled && bytes >= kMinCached) {
+        std::lock_guard<std::mutex> lk(c.mu);
+        auto it = c.free.find({dev, bytes});
+        if (it != c.free.end() && !it->second.empty()) {
+            *p = it->second.back();
+            it->second.pop_back();
+            c.cached -= bytes;
+            return cudaSuccess;
+        }
+    }
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e == cudaErrorMemoryAllocation && c.enabled) {
+        // give the cached blocks back and retry once
+        cudaGetLastError();
+        release_cached_blocks();
+        e = cudaMalloc(p, bytes);
+    }
+    return e;
+}
+
+void dev_free(void* p, size_t bytes) {
+    BlockCache& c = cache();
+    if (!c.enabled || bytes < kMinCached) {
+        cudaFree(p);
+        return;
+    }
+    int dev = 0;
+    cudaPointerAttributes attr;
+    if (cudaPointerGetAttributes(&attr, p) == cudaSuccess)
+        dev = attr.device;
+    std::lock_guard<std::mutex> lk(c.mu);
+    if (c.limit == 0) {
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        c.limit = tot / 2;  // keep at most half the device mapped for reuse
+    }
+    if (c.cached + bytes > c.limit) {
+        cudaFree(p);
+        return;
+    }
+    c.free[{dev, bytes}].push_back(p);
+    c.cached += bytes;
+}
+
+void release_cached_blocks() {
+    BlockCache& c = cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    for (auto& kv : c.free)
+        for (void* p : kv.second)
+            cudaFree(p);
+    c.free.clear();
+    c.cached = 0;
+}
+
 } // namespace pdb
+
+extern "C" void pd_release_cached_memory(void) { pdb::release_cached_blocks(); }

@@ -653,8 +653,8 @@ int try_lattice(pd_ctx* ctx, const pd_particles& p, const pd_state& st, const pd
     PD_CK(ctx->counter.alloc(1));
     PD_CK(cudaMemsetAsync(ctx->counter.p, 0, sizeof(unsigned long long), s));
     int* bad = reinterpret_cast<int*>(ctx->counter.p);
-    PD_CK(lattice_build_masks(ctx->entries.p, ctx->own_begin, ctx->own_end, ctx->N, L,
-                              ctx->lmask.p, bad, s));
+    PD_CK(lattice_build_masks(ctx->xv.p, n, ctx->entries.p, ctx->own_begin, ctx->own_end,
+                              ctx->N, L, ctx->lmask.p, bad, s));
     int bad_h = 0;
     PD_CK(cudaMemcpyAsync(&bad_h, bad, sizeof bad_h, cudaMemcpyDeviceToHost, s));
     PD_CK(cudaStreamSynchronize(s));

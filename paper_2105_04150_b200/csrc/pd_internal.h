@@ -128,14 +128,16 @@ struct LatticeArgs {
     int nx = 0, ny = 0, nz_local = 0;  // local lattice (x fastest, z slowest)
     int z0 = 0, nz_own = 0;            // owned planes [z0, z0 + nz_own)
     double h = 1.0, inv_h = 1.0;       // spacing
+    double ox = 0, oy = 0, oz = 0;     // origin
     float sc = 0.f, cv = 0.f;          // PMB critical stretch, c * V
     int cfg = 0;                       // brick / occupancy configuration (PD_LAT_CFG)
     uint4* mask = nullptr;             // per node: live bonds over the 122-offset pattern
 };
 bool lattice_detect(const double* coords, long long n, long long own_begin, long long own_end,
                     LatticeArgs& L);
-cudaError_t lattice_build_masks(const int32_t* entries, long long begin, long long end, int N,
-                                const LatticeArgs& L, uint4* mask, int* bad, cudaStream_t st);
+cudaError_t lattice_build_masks(const double4* xv, long long n, const int32_t* entries,
+                                long long begin, long long end, int N, const LatticeArgs& L,
+                                uint4* mask, int* bad, cudaStream_t st);
 cudaError_t launch_lattice(const DevArgs& A, const LatticeArgs& L, int mode, cudaStream_t st);
 cudaError_t launch_lattice_materialize(const int32_t* entries0, const uint4* mask, long long begin,
                                        long long end, long long n, int N, const LatticeArgs& L,

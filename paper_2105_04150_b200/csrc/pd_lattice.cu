@@ -262,6 +262,19 @@ __global__ void __launch_bounds__(BX * BY * BZT, MINB) lattice_step_kernel(DevAr
 
 // row -> mask: bit c set for every live entry whose offset is pattern slot c;
 // *bad = 1 when a row holds a bond outside the pattern
+__global__ void lattice_coords_kernel(const double4* xv, long long n, LatticeArgs L, int* bad) {
+    const long long i = blockIdx.x * 256LL + threadIdx.x;
+    if (i >= n)
+        return;
+    const long long plane = (long long)L.nx * L.ny;
+    const double tol = 1e-9 * L.h;
+    const double4 x = xv[i];
+    if (fabs(x.x - (L.ox + double(i % L.nx) * L.h)) > tol ||
+        fabs(x.y - (L.oy + double((i / L.nx) % L.ny) * L.h)) > tol ||
+        fabs(x.z - (L.oz + double(i / plane) * L.h)) > tol)
+        atomicExch(bad, 1);
+}
+
 __global__ void lattice_mask_kernel(const int32_t* entries, long long begin, long long end, int N,
                                     int nx, int ny, uint4* mask, int* bad) {
     const long long i = begin + blockIdx.x * 256LL + threadIdx.x;
@@ -406,14 +419,8 @@ bool lattice_detect(const double* coords, long long n, long long own_begin, long
     if (n % plane != 0)
         return false;
     const long long nz = n / plane;
-    const double tol = 1e-9 * h;
-    for (long long i = 0; i < n; ++i) {
-        const long long kx = i % nx, ky = (i / nx) % ny, kz = i / plane;
-        if (std::fabs(coords[3 * i] - (ox + double(kx) * h)) > tol ||
-            std::fabs(coords[3 * i + 1] - (oy + double(ky) * h)) > tol ||
-            std::fabs(coords[3 * i + 2] - (oz + double(kz) * h)) > tol)
-            return false;
-    }
+    // every node is checked against origin + k h on the device
+    // (lattice_build_masks), together with the rows
     if (own_begin % plane != 0 || own_end % plane != 0)
         return false;  // owned range of a slab: whole planes
     L.nx = int(nx);
@@ -423,11 +430,17 @@ bool lattice_detect(const double* coords, long long n, long long own_begin, long
     L.nz_own = int((own_end - own_begin) / plane);
     L.h = h;
     L.inv_h = 1.0 / h;
+    L.ox = ox;
+    L.oy = oy;
+    L.oz = oz;
     return true;
 }
 
-cudaError_t lattice_build_masks(const int32_t* entries, long long begin, long long end, int N,
-                                const LatticeArgs& L, uint4* mask, int* bad, cudaStream_t st) {
+cudaError_t lattice_build_masks(const double4* xv, long long n, const int32_t* entries,
+                                long long begin, long long end, int N, const LatticeArgs& L,
+                                uint4* mask, int* bad, cudaStream_t st) {
+    if (n > 0)
+        lattice_coords_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(xv, n, L, bad);
     signed char tab[NPAT][4];
     for (int c = 0; c < NPAT; ++c) {
         tab[c][0] = (signed char)pat(c, 0);
@@ -476,6 +489,7 @@ void preload_lattice() {
     preload_mode<2>();
     preload_mode<3>();
     preload_fn(lattice_mask_kernel);
+    preload_fn(lattice_coords_kernel);
     preload_fn(lattice_materialize_kernel);
 }
 

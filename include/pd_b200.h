@@ -305,6 +305,17 @@ int pd_load_cache(const char* path, pd_neighbor_list* family, pd_corrections* co
  * copy of the state); one-GPU contexts only. */
 int pd_ctx_save_state(pd_ctx* ctx, const char* path);
 
+/* write_snapshot(make_snapshot(state, particles)) (io.cpp:235-269): the ASCII
+ * pdsnap file, byte for byte.  Lines are formatted by several host threads. */
+int pd_write_snapshot(const pd_state* state, const pd_particles* particles, const char* path);
+/* The same file from the resident state (one-GPU contexts). */
+int pd_ctx_write_snapshot(pd_ctx* ctx, const char* path);
+/* Snapshots during pd_ctx_run: every `every` steps (absolute step count, like
+ * write_every) the resident fields are copied on the device and a host thread
+ * downloads, formats and writes `pattern` (printf with the step as %lld)
+ * while the GPU keeps stepping.  every = 0 turns it off. */
+int pd_ctx_snapshot_every(pd_ctx* ctx, int64_t every, const char* pattern);
+
 /* ---- multi-GPU z-slabs (no reference counterpart: the reference is one
  * process) ------------------------------------------------
  *

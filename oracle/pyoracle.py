@@ -159,6 +159,15 @@ class Reference(Backend):
         st = abi.Marshal().state(state)
         self._check(self.lib.ref_save_state(C.byref(st), os.fsencode(path)))
 
+    def write_snapshot(self, state, particles, path: str) -> None:
+        """io::write_snapshot(io::make_snapshot(state, particles)) of the reference."""
+        self.lib.ref_write_snapshot.argtypes = [C.POINTER(abi.pd_state),
+                                                C.POINTER(abi.pd_particles), C.c_char_p]
+        m = abi.Marshal()
+        st = m.state(state)
+        p = m.particles(particles)
+        self._check(self.lib.ref_write_snapshot(C.byref(st), C.byref(p), os.fsencode(path)))
+
     def save_cache(self, family, corrections, path: str) -> None:
         """io::save_cache of the reference."""
         self.lib.ref_save_cache.argtypes = [C.POINTER(abi.pd_neighbor_list),

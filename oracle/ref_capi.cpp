@@ -162,6 +162,11 @@ int ref_save_cache(const pd_neighbor_list* fam, const pd_corrections* corr, cons
     return map_exceptions([&] { io::save_cache(to_family(*fam), to_corr(*corr), path); });
 }
 
+int ref_write_snapshot(const pd_state* st, const pd_particles* p, const char* path) {
+    return map_exceptions(
+        [&] { io::write_snapshot(path, io::make_snapshot(to_state(*st), to_particles(*p))); });
+}
+
 int ref_load_state_step(const char* path, int64_t* step) {
     return map_exceptions([&] { *step = io::load_state(path).step; });
 }

@@ -7,7 +7,7 @@ point raises CudaError when the library or a B200 is missing.
 """
 from .abi import CudaError, DomainError, InvalidArgument, PeridynRuntimeError
 from .engine import (Context, compute_forces, device_count, load_cache, load_state, local_damage,
-                     save_cache, save_state, simulate)
+                     save_cache, save_state, simulate, write_snapshot)
 from .geometry import GridDesc, break_notch, break_plane, build_family, grid_coordinates
 from .types import (BCKind, BoundaryConditions, Corrections, DamageLaw, DamageModel, ForceField,
                     IntegratorKind, KernelVariant, ModelBundle, NeighborList, ParticleSet,
@@ -21,5 +21,5 @@ __all__ = [
     "RampKind", "RampProfile", "SimulateOptions", "SimulateResult", "SimulationState",
     "TipRecord", "break_notch", "break_plane", "build_family", "compute_forces",
     "device_count", "grid_coordinates", "load_cache", "load_state", "local_damage", "make_state",
-    "save_cache", "save_state", "simulate",
+    "save_cache", "save_state", "simulate", "write_snapshot",
 ]

@@ -15,7 +15,11 @@
 #include <cstdio>
 #include <cstdlib>
 #include <chrono>
+#include <condition_variable>
 #include <cstring>
+#include <deque>
+#include <mutex>
+#include <thread>
 #include <mutex>
 #include <unistd.h>
 #include <string>
@@ -232,6 +236,23 @@ struct pd_ctx {
     LatticeArgs lat;
     DevBuf<uint4> lmask;
     bool permuted() const { return fast && !lattice; }
+    // async snapshots (pd_ctx_snapshot_every)
+    int64_t snap_every = 0;
+    std::string snap_pattern;
+    struct SnapJob {
+        int slot;
+        int64_t step;
+    };
+    DevBuf<double> snap_dev[2];
+    cudaEvent_t snap_ready[2] = {nullptr, nullptr};
+    bool snap_busy[2] = {false, false};
+    std::mutex snap_mu;
+    std::condition_variable snap_cv;
+    std::deque<SnapJob> snap_jobs;
+    std::thread snap_thread;
+    bool snap_stop = false;
+    std::string snap_error;
+    cudaStream_t snap_stream = nullptr;
     int64_t row_of(int64_t local) const {
         return permuted() ? int64_t(lay.inv_host[size_t(local)]) : local;
     }
@@ -802,6 +823,144 @@ int launch_step(pd_ctx* ctx, DevArgs& A, int mode) {
     return PD_OK;
 }
 
+// x, u, v (n x 3 each) and phi (n) of the resident state, reference node
+// order, into dev[10 n] (make_snapshot, io.cpp:235-249).
+int snapshot_fields(pd_ctx* ctx, double* dev, cudaStream_t s) {
+    const int64_t n = ctx->n;
+    const int* inv = ctx->permuted() ? ctx->lay.inv.p : nullptr;
+    DevBuf<double4> t4;
+    DevBuf<int32_t> t1, t2;
+    const double4* xv = ctx->xv.p;
+    const double4* u = ctx->u[ctx->cur].p;
+    const double* v = ctx->v.p;
+    const int32_t* nn = ctx->n_neigh.p;
+    const int32_t* ini = ctx->initial.p;
+    if (inv) {
+        PD_CK(t4.alloc(size_t(2 * n)));
+        launch_gather_rows<double4, 1>(xv, t4.p, inv, n, s);
+        launch_gather_rows<double4, 1>(u, t4.p + n, inv, n, s);
+        xv = t4.p;
+        u = t4.p + n;
+        launch_gather_rows<double, 3>(v, dev + 6 * n, inv, n, s);
+        v = nullptr;
+        PD_CK(t1.alloc(size_t(n)));
+        PD_CK(t2.alloc(size_t(n)));
+        launch_gather_rows<int32_t, 1>(nn, t1.p, inv, n, s);
+        launch_gather_rows<int32_t, 1>(ini, t2.p, inv, n, s);
+        nn = t1.p;
+        ini = t2.p;
+    }
+    launch_unpack_u(xv, n, dev, s);
+    launch_unpack_u(u, n, dev + 3 * n, s);
+    if (v)
+        PD_CK(cudaMemcpyAsync(dev + 6 * n, v, sizeof(double) * 3 * n, cudaMemcpyDeviceToDevice, s));
+    launch_damage(nn, ini, n, dev + 9 * n, s);
+    ctx->launches += inv ? 9 : 3;
+    PD_CK(cudaGetLastError());
+    if (inv)
+        PD_CK(cudaStreamSynchronize(s));  // the temporaries are released on return
+    return PD_OK;
+}
+
+void snapshot_worker(pd_ctx* ctx) {
+    cudaSetDevice(ctx->device);
+    std::vector<double> h;
+    for (;;) {
+        pd_ctx::SnapJob job;
+        {
+            std::unique_lock<std::mutex> lk(ctx->snap_mu);
+            ctx->snap_cv.wait(lk, [&] { return ctx->snap_stop || !ctx->snap_jobs.empty(); });
+            if (ctx->snap_jobs.empty())
+                return;
+            job = ctx->snap_jobs.front();
+            ctx->snap_jobs.pop_front();
+        }
+        const int64_t n = ctx->n;
+        h.resize(size_t(10 * n));
+        std::string err;
+        if (cudaStreamWaitEvent(ctx->snap_stream, ctx->snap_ready[job.slot], 0) != cudaSuccess ||
+            d2h_large(h.data(), ctx->snap_dev[job.slot].p, sizeof(double) * h.size(),
+                      ctx->snap_stream) != cudaSuccess) {
+            err = "snapshot download failed";
+        } else {
+            char path[4096];
+            std::snprintf(path, sizeof path, ctx->snap_pattern.c_str(), (long long)job.step);
+            if (write_snapshot_file(path, job.step, n, h.data(), h.data() + 3 * n,
+                                    h.data() + 6 * n, h.data() + 9 * n) != PD_OK)
+                err = pd_last_error();
+        }
+        std::lock_guard<std::mutex> lk(ctx->snap_mu);
+        ctx->snap_busy[job.slot] = false;
+        if (!err.empty() && ctx->snap_error.empty())
+            ctx->snap_error = err;
+        ctx->snap_cv.notify_all();
+    }
+}
+
+// Queue the state of the step just finished for an asynchronous snapshot.
+int snapshot_async(pd_ctx* ctx, int64_t step) {
+    if (!ctx->snap_thread.joinable()) {
+        ctx->snap_stop = false;
+        ctx->snap_error.clear();
+        if (!ctx->snap_stream)
+            PD_CK(cudaStreamCreateWithFlags(&ctx->snap_stream, cudaStreamNonBlocking));
+        for (int k = 0; k < 2; ++k)
+            if (!ctx->snap_ready[k])
+                PD_CK(cudaEventCreateWithFlags(&ctx->snap_ready[k], cudaEventDisableTiming));
+        ctx->snap_thread = std::thread(snapshot_worker, ctx);
+    }
+    int slot = -1;
+    {
+        std::unique_lock<std::mutex> lk(ctx->snap_mu);
+        ctx->snap_cv.wait(lk, [&] { return !ctx->snap_busy[0] || !ctx->snap_busy[1]; });
+        slot = ctx->snap_busy[0] ? 1 : 0;
+        ctx->snap_busy[slot] = true;
+    }
+    PD_CK(ctx->snap_dev[slot].alloc(size_t(10 * ctx->n)));
+    PD_TRY(snapshot_fields(ctx, ctx->snap_dev[slot].p, ctx->stream));
+    PD_CK(cudaEventRecord(ctx->snap_ready[slot], ctx->stream));
+    {
+        std::lock_guard<std::mutex> lk(ctx->snap_mu);
+        ctx->snap_jobs.push_back({slot, step});
+    }
+    ctx->snap_cv.notify_all();
+    return PD_OK;
+}
+
+// Wait until every queued snapshot is written; report the first failure.
+int snapshot_flush(pd_ctx* ctx) {
+    if (!ctx->snap_thread.joinable())
+        return PD_OK;
+    {
+        std::unique_lock<std::mutex> lk(ctx->snap_mu);
+        ctx->snap_cv.wait(lk, [&] {
+            return ctx->snap_jobs.empty() && !ctx->snap_busy[0] && !ctx->snap_busy[1];
+        });
+        if (!ctx->snap_error.empty()) {
+            const std::string e = ctx->snap_error;
+            ctx->snap_error.clear();
+            return fail(PD_E_RUNTIME, "%s", e.c_str());
+        }
+    }
+    return PD_OK;
+}
+
+void snapshot_stop(pd_ctx* ctx) {
+    if (!ctx->snap_thread.joinable())
+        return;
+    {
+        std::lock_guard<std::mutex> lk(ctx->snap_mu);
+        ctx->snap_stop = true;
+    }
+    ctx->snap_cv.notify_all();
+    ctx->snap_thread.join();
+    for (int k = 0; k < 2; ++k)
+        if (ctx->snap_ready[k])
+            cudaEventDestroy(ctx->snap_ready[k]);
+    if (ctx->snap_stream)
+        cudaStreamDestroy(ctx->snap_stream);
+}
+
 // Slab barrier after a launch that wrote peer ghost rows (no-op on one GPU).
 int slab_sync(pd_ctx* ctx) {
     if (ctx->world <= 1)
@@ -891,6 +1050,14 @@ int run_loop(pd_ctx* ctx, const pd_options& opt, pd_write_hook hook, void* user,
         PD_TRY(slab_sync(ctx));
         if (!vv)
             ctx->cur ^= 1;
+        if (ctx->snap_every > 0 && (st + 1) % ctx->snap_every == 0) {
+            const int64_t saved = ctx->step;
+            ctx->step = st + 1;
+            const int rs = snapshot_async(ctx, st + 1);
+            ctx->step = saved;
+            if (rs != PD_OK)
+                return rs;
+        }
         if (is_write) {
             if (ctx->n_tip_sets > 0) {
                 launch_tips(ctx->u[ctx->cur].p, ctx->v.p, ctx->a.p, ctx->xv.p, ctx->body.p,
@@ -961,6 +1128,7 @@ int run_loop(pd_ctx* ctx, const pd_options& opt, pd_write_hook hook, void* user,
     long long err = none;
     PD_CK(cudaMemcpyAsync(&err, ctx->err.p, sizeof err, cudaMemcpyDeviceToHost, s));
     PD_CK(cudaStreamSynchronize(s));
+    PD_TRY(snapshot_flush(ctx));
     if (err == kPeerTimeout)
         return fail(PD_E_CUDA, "slab sync: a peer rank did not arrive (timeout)");
     if (failed_at < 0 && err < last)
@@ -1042,6 +1210,7 @@ void pd_ctx_destroy(pd_ctx* ctx) {
         return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    snapshot_stop(ctx);
     for (void* p : ctx->ipc_opened)
         cudaIpcCloseMemHandle(p);
     cudaStreamDestroy(ctx->stream);
@@ -1118,6 +1287,32 @@ int pd_ctx_save_state(pd_ctx* ctx, const char* path) {
     }
     ctx->launches += 8;
     PD_TRY(w.close());
+    return ok();
+}
+
+int pd_ctx_write_snapshot(pd_ctx* ctx, const char* path) {
+    PD_TRY(select_device(ctx));
+    if (ctx->world > 1 || ctx->partial)
+        return fail(PD_E_INVALID_ARGUMENT, "write_snapshot: a slab context holds a local model only");
+    DevBuf<double> buf;
+    PD_CK(buf.alloc(size_t(10 * ctx->n)));
+    PD_TRY(snapshot_fields(ctx, buf.p, ctx->stream));
+    std::vector<double> h(size_t(10 * ctx->n));
+    PD_CK(d2h_large(h.data(), buf.p, sizeof(double) * h.size(), ctx->stream));
+    const int64_t n = ctx->n;
+    PD_TRY(write_snapshot_file(path, ctx->step, n, h.data(), h.data() + 3 * n, h.data() + 6 * n,
+                               h.data() + 9 * n));
+    return ok();
+}
+
+int pd_ctx_snapshot_every(pd_ctx* ctx, int64_t every, const char* pattern) {
+    PD_TRY(select_device(ctx));
+    if (every < 0)
+        return fail(PD_E_INVALID_ARGUMENT, "snapshot_every: negative cadence");
+    if (every > 0 && (ctx->world > 1 || ctx->partial))
+        return fail(PD_E_INVALID_ARGUMENT, "snapshot_every: a slab context holds a local model only");
+    ctx->snap_every = every;
+    ctx->snap_pattern = pattern ? pattern : "";
     return ok();
 }
 

@@ -41,6 +41,10 @@ cudaError_t dev_alloc(void** p, size_t bytes);
 void dev_free(void* p, size_t bytes);
 void release_cached_blocks();
 
+// pd_io.cpp: the pdsnap text writer (multi-threaded formatting, in-order write)
+int write_snapshot_file(const char* path, int64_t step, int64_t n, const double* coords,
+                        const double* u, const double* v, const double* phi);
+
 // Owning device buffer, resized on demand.
 template <class T> struct DevBuf {
     T* p = nullptr;

@@ -13,9 +13,11 @@
 // needs a host-size copy of the state.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "pd_internal.h"
@@ -435,3 +437,92 @@ int pd_load_cache(const char* path, pd_neighbor_list* c, pd_corrections* corr) {
 }
 
 } // extern "C"
+
+// ---- ASCII snapshots (io.cpp:235-269) ---------------------------------------
+//
+//   pdsnap 1 <step>
+//   <n>
+//   x y z ux uy uz vx vy vz phi        "%.17g" each (format_real, io.cpp:16-20)
+//
+// The lines are formatted by several host threads into per-thread buffers and
+// written in node order, so the bytes equal write_snapshot(make_snapshot(...)).
+
+namespace pdb {
+
+int write_snapshot_file(const char* path, int64_t step, int64_t n, const double* coords,
+                        const double* u, const double* v, const double* phi) {
+    FILE* f = std::fopen(path, "wb");
+    if (!f) {
+        const std::string m = std::string(path) + ": cannot open for writing (step " +
+                              std::to_string(step) + ")";
+        return set_error(PD_E_RUNTIME, m.c_str());
+    }
+    std::fprintf(f, "pdsnap 1 %lld\n%lld\n", (long long)step, (long long)n);
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const int64_t block = 1 << 16;  // nodes per formatting task
+    const int64_t nblocks = (n + block - 1) / block;
+    const int64_t threads = std::min<int64_t>(int64_t(std::min(16u, hw)), std::max<int64_t>(1, nblocks));
+    bool bad = false;
+    // rounds of `threads` blocks: format in parallel, write in order
+    std::vector<std::string> out(static_cast<size_t>(threads));
+    for (int64_t b0 = 0; b0 < nblocks && !bad; b0 += threads) {
+        std::vector<std::thread> pool;
+        for (int64_t t = 0; t < threads && b0 + t < nblocks; ++t)
+            pool.emplace_back([&, t] {
+                std::string& s = out[size_t(t)];
+                s.clear();
+                const int64_t i0 = (b0 + t) * block, i1 = std::min(n, i0 + block);
+                s.reserve(size_t(i1 - i0) * 240);
+                char buf[40];
+                auto put = [&](double x, char sep) {
+                    const int len = std::snprintf(buf, sizeof buf, "%.17g", x);
+                    s.append(buf, size_t(len));
+                    s.push_back(sep);
+                };
+                for (int64_t i = i0; i < i1; ++i) {
+                    put(coords[3 * i], ' ');
+                    put(coords[3 * i + 1], ' ');
+                    put(coords[3 * i + 2], ' ');
+                    put(u[3 * i], ' ');
+                    put(u[3 * i + 1], ' ');
+                    put(u[3 * i + 2], ' ');
+                    put(v[3 * i], ' ');
+                    put(v[3 * i + 1], ' ');
+                    put(v[3 * i + 2], ' ');
+                    put(phi[i], '\n');
+                }
+            });
+        for (auto& th : pool)
+            th.join();
+        for (int64_t t = 0; t < threads && b0 + t < nblocks; ++t)
+            if (std::fwrite(out[size_t(t)].data(), 1, out[size_t(t)].size(), f) !=
+                out[size_t(t)].size())
+                bad = true;
+    }
+    bad = bad || std::fflush(f) != 0 || std::ferror(f);
+    std::fclose(f);
+    if (bad) {
+        const std::string m =
+            std::string(path) + ": write failed (step " + std::to_string(step) + ")";
+        return set_error(PD_E_RUNTIME, m.c_str());
+    }
+    return PD_OK;
+}
+
+} // namespace pdb
+
+extern "C" int pd_write_snapshot(const pd_state* st, const pd_particles* p, const char* path) {
+    const int64_t n = st->connectivity.n;
+    if (p->n != n || p->coords_size != 3 * n)
+        return set_error(PD_E_INVALID_ARGUMENT, "write_snapshot: particle set does not match state");
+    std::vector<double> phi(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) {
+        const int32_t init = st->connectivity.initial_n_neigh[i];
+        const int32_t cur = st->connectivity.n_neigh[i];
+        if (init > 0 && (cur < 0 || cur > init))
+            return set_error(PD_E_DOMAIN, "local_damage: current count out of range");
+        phi[size_t(i)] = init > 0 ? 1.0 - double(cur) / double(init) : 0.0;  // make_snapshot
+    }
+    const int rc = pdb::write_snapshot_file(path, st->step, n, p->coords, st->u, st->v, phi.data());
+    return rc == PD_OK ? set_error(PD_OK, "") : rc;
+}

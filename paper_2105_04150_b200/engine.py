@@ -188,7 +188,20 @@ def _io_lib():
     lib.pd_load_cache.argtypes = [C.c_char_p, C.POINTER(abi.pd_neighbor_list),
                                   C.POINTER(abi.pd_corrections)]
     lib.pd_ctx_save_state.argtypes = [C.c_void_p, C.c_char_p]
+    lib.pd_write_snapshot.argtypes = [C.POINTER(abi.pd_state), C.POINTER(abi.pd_particles),
+                                      C.c_char_p]
+    lib.pd_ctx_write_snapshot.argtypes = [C.c_void_p, C.c_char_p]
+    lib.pd_ctx_snapshot_every.argtypes = [C.c_void_p, C.c_int64, C.c_char_p]
     return lib
+
+
+def write_snapshot(state: SimulationState, particles, path: str) -> None:
+    """io::write_snapshot(io::make_snapshot(state, particles)) (io.cpp:235-269)."""
+    lib = _io_lib()
+    m = Marshal()
+    st = m.state(state)
+    p = m.particles(particles)
+    check(lib.pd_write_snapshot(C.byref(st), C.byref(p), os.fsencode(path)), lib.pd_last_error)
 
 
 def save_state(state: SimulationState, path: str) -> None:
@@ -424,6 +437,14 @@ class Context:
         """io::save_state of the resident state, streamed from device memory."""
         lib = _io_lib()
         self._check(lib.pd_ctx_save_state(self.h, os.fsencode(path)))
+
+    def write_snapshot(self, path: str) -> None:
+        """The pdsnap file of the resident state."""
+        self._check(_io_lib().pd_ctx_write_snapshot(self.h, os.fsencode(path)))
+
+    def snapshot_every(self, every: int, pattern: str) -> None:
+        """Asynchronous pdsnap files during run(): pattern % step every `every` steps."""
+        self._check(_io_lib().pd_ctx_snapshot_every(self.h, int(every), pattern.encode()))
 
     def layout(self) -> str:
         """"exact", "tiles" or "lattice" (pd_ctx_layout)."""

@@ -8,6 +8,7 @@ state_trilinear.pdst  a fractured trilinear multi-material bar after 40
                       velocity-Verlet steps of the reference simulate(): u, v,
                       a, entries with breaks, counts, bond types, history
 state_pmb.pdst        the PMB bench lattice (no history / bond types)
+snap_trilinear.pdsnap write_snapshot(make_snapshot(...)) of the trilinear state
 family.pdnl           a family cache with bond types, lambda and beta
 """
 from __future__ import annotations
@@ -41,6 +42,7 @@ def main():
     ref = Reference(threads=1)
     b, fam, st = trilinear_case(ref)
     ref.save_state(st, os.path.join(HERE, "state_trilinear.pdst"))
+    ref.write_snapshot(st, b.particles, os.path.join(HERE, "snap_trilinear.pdsnap"))
     bb, h, g = S.bench_lattice_bundle((6, 5, 4))
     fam2 = ref.build_family(bb.particles.coords, 2.0, g.hint())
     st2 = make_state(fam2, False)

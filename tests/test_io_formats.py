@@ -137,3 +137,43 @@ def test_device_save_state_fast_layouts_round_trip(tmp_path):
         back = engine.load_state(str(p))
         assert same_bits(back.u, st.u)
         assert np.array_equal(back.connectivity.entries, st.connectivity.entries)
+
+
+def test_host_snapshot_is_the_reference_file(tmp_path):
+    """write_snapshot(make_snapshot(...)) (io.cpp:235-269): 17-digit ASCII, same bytes."""
+    st = engine.load_state(os.path.join(GOLD, "state_trilinear.pdst"))
+    b, h, g = S.multimaterial_bundle((7, 5, 6))
+    out = tmp_path / "snap.pdsnap"
+    engine.write_snapshot(st, b.particles, str(out))
+    assert _bytes(out) == _bytes(os.path.join(GOLD, "snap_trilinear.pdsnap"))
+
+
+@pytest.mark.gpu
+def test_device_snapshots_sync_and_async(tmp_path, oracle):
+    """The resident state's snapshot equals the reference file; snapshots
+    queued during run() (written by a host thread while the GPU steps) equal
+    the host writer's files of the oracle's states at the same steps."""
+    from paper_2105_04150_b200 import geometry
+    b, h, g = S.multimaterial_bundle((7, 5, 6))
+    fam = geometry.build_family(b.particles.coords, 2.0, g)
+    fam.bond_type = S.classify_bonds(b.particles.coords, fam)
+    st = make_state(fam, True)
+    ctx = engine.Context(0)
+    ctx.upload(b, st, KernelVariant.bond_parallel)
+    ctx.snapshot_every(10, str(tmp_path / "async_%06lld.pdsnap"))
+    ctx.run(40, 0, IntegratorKind.velocity_verlet, 0, KernelVariant.bond_parallel)
+    ctx.write_snapshot(str(tmp_path / "sync.pdsnap"))
+    ctx.close()
+    assert _bytes(tmp_path / "sync.pdsnap") == _bytes(os.path.join(GOLD, "snap_trilinear.pdsnap"))
+    ref = make_state(fam, True)
+    written = []
+
+    def hook(s, f):
+        p = tmp_path / f"ref_{s.step:06d}.pdsnap"
+        engine.write_snapshot(s, b.particles, str(p))
+        written.append(s.step)
+    oracle.simulate(b, ref, SimulateOptions(40, 10, 0, IntegratorKind.velocity_verlet), hook)
+    assert written == [10, 20, 30, 40]
+    for step in written:
+        assert _bytes(tmp_path / f"async_{step:06d}.pdsnap") == \
+            _bytes(tmp_path / f"ref_{step:06d}.pdsnap"), step

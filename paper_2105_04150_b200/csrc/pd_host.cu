@@ -645,8 +645,9 @@ int download(pd_ctx* ctx, pd_state* st, pd_force_field* forces, int32_t fields) 
 
 // Renumber the resident node arrays into the fast path's brick order and
 // build its tile layout from the host copies of the rows.
-// PD_FAST on a lattice with one PMB law, uniform volumes and no per-bond or
-// no-failure data: implicit connectivity (pd_lattice.cu).  Returns false (and
+// PD_FAST on a lattice with one PMB law and no per-bond data (no bond types,
+// lambda, beta or history): implicit connectivity (pd_lattice.cu);
+// no-failure nodes and per-node volumes ride in the staged records.  Returns false (and
 // leaves the context untouched) when the model does not qualify;
 // PD_FAST_LAYOUT=general forces the general tile layout.
 int try_lattice(pd_ctx* ctx, const pd_particles& p, const pd_state& st, const pd_damage_model& m,
@@ -660,12 +661,11 @@ int try_lattice(pd_ctx* ctx, const pd_particles& p, const pd_state& st, const pd
     if (m.n_laws != 1 || m.laws[0].n_breakpoints != 1 || ctx->history ||
         st.connectivity.bond_type_size != 0 || corr.lambda_size != 0 || corr.beta_size != 0)
         return PD_OK;
-    for (int64_t i = 0; nofail && nofail_size == n && i < n; ++i)
-        if (nofail[i])
-            return PD_OK;
-    for (int64_t i = 1; i < n; ++i)
-        if (p.volume[i] != p.volume[0])
-            return PD_OK;
+    bool any_nf = false, vol_varies = false;
+    for (int64_t i = 0; nofail && nofail_size == n && i < n && !any_nf; ++i)
+        any_nf = nofail[i] != 0;
+    for (int64_t i = 1; i < n && !vol_varies; ++i)
+        vol_varies = p.volume[i] != p.volume[0];
     LatticeArgs L;
     if (!lattice_detect(p.coords, n, ctx->own_begin, ctx->own_end, L))
         return PD_OK;
@@ -685,6 +685,9 @@ int try_lattice(pd_ctx* ctx, const pd_particles& p, const pd_state& st, const pd
     }
     L.sc = float(m.laws[0].breakpoints[0]);
     L.cv = float(m.laws[0].stiffness * p.volume[0]);
+    L.nf = (any_nf || vol_varies) ? 1 : 0;
+    L.vol_varies = vol_varies ? 1 : 0;
+    L.inv_v0 = 1.0 / p.volume[0];
     L.mask = ctx->lmask.p;
     if (const char* e = std::getenv("PD_LAT_CFG"))
         L.cfg = std::atoi(e);

@@ -135,6 +135,9 @@ struct LatticeArgs {
     double ox = 0, oy = 0, oz = 0;     // origin
     float sc = 0.f, cv = 0.f;          // PMB critical stretch, c * V
     int cfg = 0;                       // brick / occupancy configuration (PD_LAT_CFG)
+    int nf = 0;                        // no-failure nodes or per-node volumes present
+    int vol_varies = 0;                // volumes differ (records carry V_j / V_0)
+    double inv_v0 = 1.0;               // 1 / V_0 (node 0's volume)
     uint4* mask = nullptr;             // per node: live bonds over the 122-offset pattern
 };
 bool lattice_detect(const double* coords, long long n, long long own_begin, long long own_end,

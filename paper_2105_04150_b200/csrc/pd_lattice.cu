@@ -106,7 +106,11 @@ __device__ __forceinline__ void stretch(const float4& rj, const float4& ri, floa
     s = num * rr * rcp_approx(fmaf(cur2, rc, len));
 }
 
-template <int C>
+// NF (no-failure nodes and/or per-node volumes present): a record's w holds
+// V_j / V_0, negated for a no-failure node; the bond never breaks when either
+// end is no-failure (engine.cpp:79-80, 86-88: the node's own flag lifts s_c
+// to +inf) and its force carries V_j (engine.cpp:103).
+template <int C, bool NF>
 __device__ __forceinline__ void slot(const float4* own, const float4& ri, const uint4& m, float sc,
                                      Acc& a) {
     constexpr int dx = pat(C, 0), dy = pat(C, 1), dz = pat(C, 2);
@@ -122,6 +126,20 @@ __device__ __forceinline__ void slot(const float4* own, const float4& ri, const 
     const float4 rj = own[off];
     float s, rc, cx, cy, cz;
     stretch(rj, ri, float(dx), float(dy), float(dz), float(r2), len, rr, s, rc, cx, cy, cz);
+    if (NF) {
+        const float scale = s * rc * fabsf(rj.w);
+        asm("{\n\t.reg .pred pa, pb, pc;\n\t"
+            "setp.lt.f32 pa, %5, %6;\n\t"
+            "setp.lt.or.f32 pb, %11, 0f00000000, pa;\n\t"
+            "setp.ne.and.u32 pc, %4, 0, pb;\n\t"
+            "@pc add.s32 %0, %0, 1;\n\t"
+            "@pc fma.rn.f32 %1, %7, %10, %1;\n\t"
+            "@pc fma.rn.f32 %2, %8, %10, %2;\n\t"
+            "@pc fma.rn.f32 %3, %9, %10, %3;\n\t}"
+            : "+r"(a.kept), "+f"(a.fx), "+f"(a.fy), "+f"(a.fz)
+            : "r"(mw & bit), "f"(s), "f"(sc), "f"(cx), "f"(cy), "f"(cz), "f"(scale), "f"(rj.w));
+        return;
+    }
     const float scale = s * rc;
     // live and unbroken (s < s_c, bond_contribution's PMB test, engine.cpp:90-98):
     // add the force and count the slot; a live slot that breaks is found later
@@ -159,19 +177,19 @@ __device__ __noinline__ uint4 broken_bits(const float4* own, const float4& ri, c
         const float4 rj = own[dx + HX * (dy + HY * dz)];
         float s, rc, cx, cy, cz;
         stretch(rj, ri, float(dx), float(dy), float(dz), float(r2), len, rr, s, rc, cx, cy, cz);
-        if (!(s < sc))
+        if (!(s < sc) && !(rj.w < 0.f))  // a no-failure neighbour keeps the bond
             dead[c >> 5] |= 1u << (c & 31);
     }
     return make_uint4(dead[0], dead[1], dead[2], dead[3]);
 }
 
-template <int... C>
+template <bool NF, int... C>
 __device__ __forceinline__ void all_slots(std::integer_sequence<int, C...>, const float4* own,
                                           const float4& ri, const uint4& m, float sc, Acc& a) {
-    (slot<C>(own, ri, m, sc, a), ...);
+    (slot<C, NF>(own, ri, m, sc, a), ...);
 }
 
-template <int MODE, int BZT, int MINB, bool BC>
+template <int MODE, int BZT, int MINB, bool BC, bool NF>
 __global__ void __launch_bounds__(BX * BY * BZT, MINB) lattice_step_kernel(DevArgs A,
                                                                            LatticeArgs L) {
     constexpr int TT = BX * BY * BZT, HZ = BZT + 6;
@@ -207,6 +225,7 @@ __global__ void __launch_bounds__(BX * BY * BZT, MINB) lattice_step_kernel(DevAr
         float4* dst = rec + q + PREC * pp;
         for (int pz0 = 0; pz0 < HZ; pz0 += PPASS * PL) {
             double ux[PL], uy[PL], uz[PL];
+            float wv[PL];
             bool ok[PL];
 #pragma unroll
             for (int k = 0; k < PL; ++k) {
@@ -214,12 +233,22 @@ __global__ void __launch_bounds__(BX * BY * BZT, MINB) lattice_step_kernel(DevAr
                 const int Z = gz0 - 3 + pz;
                 ok[k] = xy_ok && pz < HZ && Z >= 0 && Z < L.nz_local;
                 ux[k] = uy[k] = uz[k] = 0.0;
+                wv[k] = 0.f;
                 if (ok[k]) {
                     const double4* pu = src + plane * Z;
                     const double2 xy = *reinterpret_cast<const double2*>(pu);
                     ux[k] = xy.x;
                     uy[k] = xy.y;
-                    uz[k] = reinterpret_cast<const double*>(pu)[2];
+                    if (NF) {
+                        const double2 zw = reinterpret_cast<const double2*>(pu)[1];
+                        uz[k] = zw.x;
+                        // V_j / V_0 (1 with uniform volumes), negative for a no-failure node
+                        const float vf =
+                            L.vol_varies ? float(A.xv[(pu - A.u_in)].w * L.inv_v0) : 1.f;
+                        wv[k] = zw.y != 0.0 ? -vf : vf;
+                    } else {
+                        uz[k] = reinterpret_cast<const double*>(pu)[2];
+                    }
                 }
             }
 #pragma unroll
@@ -228,7 +257,7 @@ __global__ void __launch_bounds__(BX * BY * BZT, MINB) lattice_step_kernel(DevAr
                 if (pp < PPASS && pz < HZ)
                     dst[PREC * (pz - pp)] =
                         ok[k] ? make_float4(float(ux[k] - U0.x) * ih, float(uy[k] - U0.y) * ih,
-                                            float(uz[k] - U0.z) * ih, 0.f)
+                                            float(uz[k] - U0.z) * ih, wv[k])
                               : make_float4(0.f, 0.f, 0.f, 0.f);
             }
         }
@@ -240,11 +269,13 @@ __global__ void __launch_bounds__(BX * BY * BZT, MINB) lattice_step_kernel(DevAr
     // 2. the node's bonds: 122 pattern slots, unrolled at compile time
     const float4* own = rec + (tx + 3) + HX * ((ty + 3) + HY * (tz + 3));  // HY pitch is the same
     const float4 ri = *own;
+    // a no-failure node's own bonds never break
+    const float sc = (NF && ri.w < 0.f) ? __int_as_float(0x7f800000) : L.sc;
     Acc a{0.f, 0.f, 0.f, 0};
-    all_slots(std::make_integer_sequence<int, NPAT>{}, own, ri, m, L.sc, a);
+    all_slots<NF>(std::make_integer_sequence<int, NPAT>{}, own, ri, m, sc, a);
     const int live = __popc(m.x) + __popc(m.y) + __popc(m.z) + __popc(m.w);
     if (a.kept != live) {
-        const uint4 d = broken_bits(own, ri, m, L.sc);
+        const uint4 d = broken_bits(own, ri, m, sc);
         L.mask[i] = make_uint4(m.x & ~d.x, m.y & ~d.y, m.z & ~d.z, m.w & ~d.w);
         A.n_neigh[i] -= live - a.kept;
     }
@@ -332,27 +363,27 @@ template <class K> void preload_fn(K k) {
     cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(k));
 }
 
-template <int MODE, int BZT, int MINB, bool BC> cudaError_t configure_one() {
+template <int MODE, int BZT, int MINB, bool BC, bool NF> cudaError_t configure_one() {
     static bool done = false;
     if (done)
         return cudaSuccess;
-    const cudaError_t e = cudaFuncSetAttribute(lattice_step_kernel<MODE, BZT, MINB, BC>,
+    const cudaError_t e = cudaFuncSetAttribute(lattice_step_kernel<MODE, BZT, MINB, BC, NF>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                int(sizeof(float4)) * nrec<BZT>());
     done = e == cudaSuccess;
     return e;
 }
 
-template <int MODE, int BZT, int MINB, bool BC>
+template <int MODE, int BZT, int MINB, bool BC, bool NF>
 cudaError_t launch_cfg(const DevArgs& A, const LatticeArgs& L, cudaStream_t st) {
     const int nbx = (L.nx + BX - 1) / BX, nby = (L.ny + BY - 1) / BY,
               nbz = (L.nz_own + BZT - 1) / BZT;
     if (nbx * nby * nbz == 0)
         return cudaSuccess;
-    const cudaError_t e = configure_one<MODE, BZT, MINB, BC>();
+    const cudaError_t e = configure_one<MODE, BZT, MINB, BC, NF>();
     if (e != cudaSuccess)
         return e;
-    lattice_step_kernel<MODE, BZT, MINB, BC>
+    lattice_step_kernel<MODE, BZT, MINB, BC, NF>
         <<<dim3(unsigned(nbx), unsigned(nby), unsigned(nbz)), BX * BY * BZT,
            sizeof(float4) * nrec<BZT>(), st>>>(A, L);
     return cudaGetLastError();
@@ -363,38 +394,50 @@ cudaError_t launch_cfg(const DevArgs& A, const LatticeArgs& L, cudaStream_t st) 
 // 16x4x8 at 2 (64 registers) by 15 %; 16x4x2 bricks lose to the halo overhead
 // (13.8 staged records per node).  Without boundary conditions the epilogue
 // is lighter and 6 CTAs/SM (40 registers) fit.  PD_LAT_CFG selects
-// alternatives: 1 = 16x4x8 x3, 2 = 16x4x4 x4, 3 = 16x4x8 x2, 4 = 16x4x4 x5.
-template <int MODE, bool BC>
+// alternatives for the bench configuration: 1 = 16x4x8 x3, 2 = 16x4x4 x4,
+// 3 = 16x4x8 x2, 4 = 16x4x4 x5.
+template <int MODE, bool BC, bool NF>
 cudaError_t launch_bc(const DevArgs& A, const LatticeArgs& L, cudaStream_t st) {
-    switch (L.cfg) {
-    case 1: return launch_cfg<MODE, 8, 3, BC>(A, L, st);
-    case 2: return launch_cfg<MODE, 4, 4, BC>(A, L, st);
-    case 3: return launch_cfg<MODE, 8, 2, BC>(A, L, st);
-    case 4: return launch_cfg<MODE, 4, 5, BC>(A, L, st);
-    default: return launch_cfg<MODE, 4, BC ? 5 : 6, BC>(A, L, st);
+    if constexpr (!NF && !BC) {
+        switch (L.cfg) {
+        case 1: return launch_cfg<MODE, 8, 3, BC, NF>(A, L, st);
+        case 2: return launch_cfg<MODE, 4, 4, BC, NF>(A, L, st);
+        case 3: return launch_cfg<MODE, 8, 2, BC, NF>(A, L, st);
+        case 4: return launch_cfg<MODE, 4, 5, BC, NF>(A, L, st);
+        default: break;
+        }
     }
+    return launch_cfg<MODE, 4, BC ? 5 : 6, BC, NF>(A, L, st);
 }
 
 template <int MODE> cudaError_t launch_mode(const DevArgs& A, const LatticeArgs& L, cudaStream_t st) {
-    return A.bc_kind ? launch_bc<MODE, true>(A, L, st) : launch_bc<MODE, false>(A, L, st);
+    if (L.nf)
+        return A.bc_kind ? launch_bc<MODE, true, true>(A, L, st)
+                         : launch_bc<MODE, false, true>(A, L, st);
+    return A.bc_kind ? launch_bc<MODE, true, false>(A, L, st)
+                     : launch_bc<MODE, false, false>(A, L, st);
 }
 
-template <int MODE, bool BC> void preload_bc() {
-    preload_fn(lattice_step_kernel<MODE, 8, 2, BC>);
-    preload_fn(lattice_step_kernel<MODE, 8, 3, BC>);
-    preload_fn(lattice_step_kernel<MODE, 4, 4, BC>);
-    preload_fn(lattice_step_kernel<MODE, 4, 5, BC>);
-    preload_fn(lattice_step_kernel<MODE, 4, BC ? 5 : 6, BC>);
-    configure_one<MODE, 8, 2, BC>();
-    configure_one<MODE, 8, 3, BC>();
-    configure_one<MODE, 4, 4, BC>();
-    configure_one<MODE, 4, 5, BC>();
-    configure_one<MODE, 4, BC ? 5 : 6, BC>();
+template <int MODE, bool BC, bool NF> void preload_bc() {
+    preload_fn(lattice_step_kernel<MODE, 4, BC ? 5 : 6, BC, NF>);
+    configure_one<MODE, 4, BC ? 5 : 6, BC, NF>();
+    if constexpr (!NF && !BC) {
+        preload_fn(lattice_step_kernel<MODE, 8, 2, BC, NF>);
+        preload_fn(lattice_step_kernel<MODE, 8, 3, BC, NF>);
+        preload_fn(lattice_step_kernel<MODE, 4, 4, BC, NF>);
+        preload_fn(lattice_step_kernel<MODE, 4, 5, BC, NF>);
+        configure_one<MODE, 8, 2, BC, NF>();
+        configure_one<MODE, 8, 3, BC, NF>();
+        configure_one<MODE, 4, 4, BC, NF>();
+        configure_one<MODE, 4, 5, BC, NF>();
+    }
 }
 
 template <int MODE> void preload_mode() {
-    preload_bc<MODE, true>();
-    preload_bc<MODE, false>();
+    preload_bc<MODE, true, false>();
+    preload_bc<MODE, false, false>();
+    preload_bc<MODE, true, true>();
+    preload_bc<MODE, false, true>();
 }
 
 } // namespace

@@ -225,17 +225,57 @@ def test_lattice_layout_selected_and_matches_tiles(oracle, monkeypatch):
     assert fam.n_neigh.sum() > ref.connectivity.n_neigh.sum()
 
 
-def test_lattice_layout_rejects_non_lattice_and_per_node_data():
-    """Irregular coordinates or no-failure nodes fall back to the tile layout."""
+def test_lattice_layout_selection():
+    """Lattices run the implicit layout, also with no-failure nodes and per-node
+    volumes; per-bond data (bond types, history) or irregular points fall back
+    to the tile layout."""
     b, h, g = S.bench_lattice_bundle((12, 12, 12))
     fam = geometry.build_family(b.particles.coords, h, g)
+
+    def layout_of(bundle, family):
+        ctx = engine.Context(0)
+        ctx.upload(bundle, make_state(family, bundle.model.needs_history()), KernelVariant.fast)
+        lay = ctx.layout()
+        ctx.close()
+        return lay
+    assert layout_of(b, fam) == "lattice"
     b.bc.no_failure[5] = 1
-    ctx = engine.Context(0)
-    ctx.upload(b, make_state(fam, False), KernelVariant.fast)
-    assert ctx.layout() == "tiles"
-    ctx.close()
-    b.bc.no_failure[5] = 0
+    b.particles.volume[7] = 1.3
+    assert layout_of(b, fam) == "lattice"
+    fam2 = fam.copy()
+    fam2.bond_type = np.zeros(fam.entries.size, np.uint8)
+    assert layout_of(b, fam2) == "tiles"
+    b2, h2, g2 = S.bench_lattice_bundle((12, 12, 12))
+    b2.particles.coords = b2.particles.coords + np.random.default_rng(0).uniform(
+        -0.01, 0.01, b2.particles.coords.size)
+    fam3 = geometry.build_family(b2.particles.coords, h2)
+    assert layout_of(b2, fam3) == "tiles"
+
+
+@pytest.mark.parametrize("integrator", [IntegratorKind.euler, IntegratorKind.velocity_verlet])
+def test_lattice_no_failure_and_volumes_match_oracle(oracle, integrator):
+    """cfg1-style run on the lattice layout: the 3-point-bend beam (no-failure
+    supports and load patch, PMB, quintic ramp) with per-node volumes, against
+    the fp64 oracle."""
+    b, h, g = S.beam_bundle(30, 10, 10)
+    rng = np.random.default_rng(11)
+    b.particles.volume = b.particles.volume * rng.uniform(0.8, 1.2, b.particles.volume.size)
+    b.bc.ramps[1].rise_steps = 150
+    b.bc.magnitude[:] = b.bc.magnitude * 3.0  # drive it to fracture
+    fam = geometry.build_family(b.particles.coords, h, g)
+    outs = []
+    for be, variant in ((engine.backend(), KernelVariant.fast),
+                        (oracle, KernelVariant.bond_parallel)):
+        st = make_state(fam, False)
+        be.simulate(b, st, SimulateOptions(200, 0, 0, integrator, variant))
+        outs.append(st)
+    fast, ref = outs
     ctx = engine.Context(0)
     ctx.upload(b, make_state(fam, False), KernelVariant.fast)
     assert ctx.layout() == "lattice"
     ctx.close()
+    s = stretches(b.particles, fam, ref.u)
+    check_break_sets(ref.connectivity.entries, fast.connectivity.entries, s,
+                     b.model.laws[0].breakpoints[0])
+    assert max_rel_difference(ref.u, fast.u) <= FRACTURE_U_TOL
+    assert fam.n_neigh.sum() > ref.connectivity.n_neigh.sum()  # it fractured

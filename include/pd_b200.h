@@ -204,6 +204,19 @@ int pd_simulate(const pd_bundle* bundle, pd_state* state, const pd_options* opti
                 pd_write_hook on_write, void* user, pd_tip_record* tips_out,
                 int64_t tips_capacity, int64_t* n_tips_out);
 
+/* K independent simulate() calls run concurrently on one GPU: the
+ * calibration / UQ outer loop (calibrate.cpp:116-218 runs hundreds of short
+ * simulations of small models).  Each model gets its own context and stream
+ * and a pool of `threads` host threads (0 = up to 8) drives them, so kernels
+ * of different models share the SMs.  Tip records of model m go to
+ * tips_out[tips_offset[m] .. tips_offset[m+1]) (both may be NULL when no
+ * model records tips); status[m] is model m's code; the return value is the
+ * first failing code (its message names the model). */
+int pd_simulate_batch(int32_t k, const pd_bundle* bundles, pd_state* states,
+                      const pd_options* options, pd_tip_record* tips_out,
+                      const int64_t* tips_offset, int64_t* n_tips_out, int32_t* status,
+                      int32_t threads);
+
 /* local_damage over all nodes from a host connectivity (formulas.hpp:49-55,
  * io.cpp:243-247): phi_i = 1 - n_neigh_i / initial_i, 0 when initial_i == 0. */
 int pd_damage(const pd_neighbor_list* family, double* phi_out);

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -1694,6 +1695,49 @@ int pd_simulate(const pd_bundle* bundle, pd_state* state, const pd_options* opti
         return rc;
     if (rc2 != PD_OK)
         return rc2;
+    return ok();
+}
+
+int pd_simulate_batch(int32_t k, const pd_bundle* bundles, pd_state* states,
+                      const pd_options* options, pd_tip_record* tips_out,
+                      const int64_t* tips_offset, int64_t* n_tips_out, int32_t* status,
+                      int32_t threads) {
+    if (k < 0)
+        return fail(PD_E_INVALID_ARGUMENT, "simulate_batch: negative model count");
+    if (threads <= 0)
+        threads = int32_t(std::min<unsigned>(8u, std::max(1u, std::thread::hardware_concurrency())));
+    threads = std::min<int32_t>(threads, std::max<int32_t>(k, 1));
+    std::vector<std::string> msgs(static_cast<size_t>(k));
+    std::atomic<int32_t> next{0};
+    auto worker = [&] {
+        for (;;) {
+            const int32_t m = next.fetch_add(1);
+            if (m >= k)
+                return;
+            pd_tip_record* tips = nullptr;
+            int64_t cap = 0;
+            if (tips_out && tips_offset) {
+                tips = tips_out + tips_offset[m];
+                cap = tips_offset[m + 1] - tips_offset[m];
+            }
+            int64_t got = 0;
+            const int rc = pd_simulate(&bundles[m], &states[m], &options[m], nullptr, nullptr, tips,
+                                       cap, &got);
+            status[m] = rc;
+            if (n_tips_out)
+                n_tips_out[m] = got;
+            if (rc != PD_OK)
+                msgs[size_t(m)] = pd_last_error();
+        }
+    };
+    std::vector<std::thread> pool;
+    for (int32_t t = 0; t < threads; ++t)
+        pool.emplace_back(worker);
+    for (auto& th : pool)
+        th.join();
+    for (int32_t m = 0; m < k; ++m)
+        if (status[m] != PD_OK)
+            return fail(status[m], "simulate_batch: model %d: %s", m, msgs[size_t(m)].c_str());
     return ok();
 }
 

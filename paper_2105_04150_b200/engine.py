@@ -283,6 +283,65 @@ def simulate(bundle, state, options, on_write=None) -> SimulateResult:
     return backend().simulate(bundle, state, options, on_write)
 
 
+def simulate_batch(bundles, states, options, threads: int = 0):
+    """Independent simulate() calls run concurrently on one GPU
+    (pd_simulate_batch): the calibration / UQ outer loop.  Returns one
+    SimulateResult per model; raises the first model's error."""
+    lib = library()
+    k = len(bundles)
+    if not (len(states) == len(options) == k):
+        raise abi.InvalidArgument("simulate_batch: bundles, states and options differ in length")
+    lib.pd_simulate_batch.argtypes = [C.c_int32, C.POINTER(abi.pd_bundle), C.POINTER(abi.pd_state),
+                                      C.POINTER(abi.pd_options), C.POINTER(abi.pd_tip_record),
+                                      C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                      C.POINTER(C.c_int32), C.c_int32]
+    m = Marshal()
+    B = (abi.pd_bundle * max(k, 1))()
+    S = (abi.pd_state * max(k, 1))()
+    O = (abi.pd_options * max(k, 1))()
+    offsets = (C.c_int64 * (k + 1))()
+    names_per = []
+    total = 0
+    for q, (b, st, o) in enumerate(zip(bundles, states, options)):
+        n = b.particles.size()
+        slots = st.size() * int(st.connectivity.group_size)
+        if b.model.needs_history() and np.asarray(
+                st.bond_history if st.bond_history is not None else []).size != slots:
+            st.bond_history = np.zeros(slots)  # engine.cpp:382-384
+        B[q] = m.bundle(b)
+        S[q] = m.state(st)
+        O[q] = Marshal.options(o)
+        names = sorted(b.bc.tip_sets)
+        writes = 0
+        if o.write_every > 0:
+            writes = sum(1 for s_ in range(o.first_step, o.first_step + o.steps)
+                         if (s_ + 1) % o.write_every == 0)
+        offsets[q] = total
+        total += writes * len(names)
+        names_per.append(names)
+        del n
+    offsets[k] = total
+    recs = (abi.pd_tip_record * max(total, 1))()
+    got = (C.c_int64 * max(k, 1))()
+    status = (C.c_int32 * max(k, 1))()
+    rc = lib.pd_simulate_batch(k, B, S, O, recs, offsets, got, status, int(threads))
+    for q, st in enumerate(states):
+        st.step = S[q].step
+    check(rc, lib.pd_last_error)
+    results = []
+    for q in range(k):
+        names = names_per[q]
+        res = SimulateResult({name: [] for name in names} if names else {})
+        for r_ in range(got[q]):
+            r = recs[offsets[q] + r_]
+            res.tips[names[r_ % len(names)]].append(
+                TipRecord(int(r.step), np.array(r.mean_u[:]), np.array(r.mean_v[:]),
+                          np.array(r.mean_a[:]), np.array(r.body_force_sum[:]),
+                          np.array(r.external_force_sum[:])))
+        results.append(res)
+    return results
+
+
 def local_damage(family) -> np.ndarray:
     """phi_i = 1 - n_neigh_i / initial_i per node (formulas.hpp:49-55), on the GPU."""
     lib = library()

@@ -116,12 +116,17 @@ def measured_traffic(key):
         return None
 
 
-def build_workload(counts):
+def build_workload(counts, law="pmb"):
+    """The reference bench fixture; law "trilinear" is SURVEY 8(d)'s history
+    variant trilinear(1, 1e-3, 2e-3, 1e6) (n-linear path, nothing breaks)."""
     import scenarios as S
     from paper_2105_04150_b200 import geometry, make_state
+    from paper_2105_04150_b200.types import DamageLaw
     bundle, h, g = S.bench_lattice_bundle(counts)
+    if law == "trilinear":
+        bundle.model.laws = [DamageLaw.trilinear(1.0, 1e-3, 2e-3, 1e6)]
     fam = geometry.build_family(bundle.particles.coords, h, g)
-    state = make_state(fam, False)
+    state = make_state(fam, bundle.model.needs_history())
     state.u = S.seed_displacements(bundle.particles.coords)
     return bundle, fam, state
 
@@ -196,8 +201,10 @@ def _summary(args, value, ms_step, world, n, N, live, bytes_step, achieved, e2e,
     peak, peak_kind = measured_peaks()
     traffic = (measured_traffic(f"{layout}_{args.size}_{variant_name}")
                if world == 1 and layout else None)
+    law = ("PMB c=1 s_c=1e6" if getattr(args, "law", "pmb") == "pmb"
+           else "trilinear(1, 1e-3, 2e-3, 1e6) with history")
     cfg = {"workload": f"cfg4 lattice {args.size}^3 = {n} nodes, delta=3dx (N={N}), "
-                       f"PMB c=1 s_c=1e6, velocity-Verlet, dt=1e-3, seeded u"
+                       f"{law}, velocity-Verlet, dt=1e-3, seeded u"
                        + (f", {world} z-slabs" if world > 1 else ""),
            "nodes": n, "group_size": N, "live_bonds": live, "variant": variant_name,
            "l2": f"inputs larger than L2 ({bytes_step / 1e9:.2f} GB/step algorithmic)",
@@ -226,7 +233,7 @@ def run_single(args, variant, local):
     from paper_2105_04150_b200 import IntegratorKind, SimulateOptions, engine, make_state
     counts = (args.size, args.size, args.size)
     t_setup = time.perf_counter()
-    bundle, fam, state0 = build_workload(counts)
+    bundle, fam, state0 = build_workload(counts, args.law)
     n = bundle.particles.size()
     N = int(fam.group_size)
     live = int(fam.n_neigh.sum())
@@ -254,12 +261,14 @@ def run_single(args, variant, local):
     ms_step = ms_total / args.steps
     value = live * args.steps / (ms_total / 1e3)
     bytes_step = algorithmic_bytes(n, N, live)
+    if args.law == "trilinear":  # + 2 h B history traffic (h = 4: fp32 history on the fast path)
+        bytes_step += 2 * (4 if args.variant == "fast" else 8) * live
     achieved = bytes_step / (ms_step / 1e3) / 1e9
     ctx.close()
     del ctx
 
     # end to end: one simulate() call through the C ABI from host buffers
-    st = make_state(fam, False)
+    st = make_state(fam, bundle.model.needs_history())
     st.u = state0.u.copy()
     e2e_steps = args.e2e_steps
     # bytes that cross PCIe: coords, u, v, a, V, rho, rows, counts in; u, v, a,
@@ -267,7 +276,7 @@ def run_single(args, variant, local):
     h2d = (3 * n * 8 * 4 + 2 * n * 8 + n * N * 4 + 2 * n * 4)
     d2h = (3 * n * 8 * 3 + n * 4)
     # one untimed call first (driver/pinned-buffer first-use costs), then the timed one
-    warm = make_state(fam, False)
+    warm = make_state(fam, bundle.model.needs_history())
     warm.u = state0.u.copy()
     engine.simulate(bundle, warm, SimulateOptions(2, 0, 0, IntegratorKind.velocity_verlet, variant))
     del warm
@@ -408,6 +417,7 @@ def main():
     ap.add_argument("--size", type=int, default=216)
     ap.add_argument("--e2e-steps", type=int, default=1000)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--law", default="pmb", choices=["pmb", "trilinear"])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

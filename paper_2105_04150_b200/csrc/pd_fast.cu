@@ -33,15 +33,8 @@ __constant__ FastLaw c_flaws[PD_MAX_LAWS];
 
 void fast_set_laws(const DevLaw* laws, int n, cudaStream_t stream) {
     std::vector<FastLaw> f(static_cast<size_t>(n));
-    for (int k = 0; k < n; ++k) {
-        std::memset(&f[size_t(k)], 0, sizeof(FastLaw));
-        f[size_t(k)].c = float(laws[k].c);
-        f[size_t(k)].nbp = laws[k].nbp;
-        for (int b = 0; b < laws[k].nbp; ++b) {
-            f[size_t(k)].bp[b] = float(laws[k].bp[b]);
-            f[size_t(k)].f[b] = float(laws[k].f[b]);
-        }
-    }
+    for (int k = 0; k < n; ++k)
+        fast_law_from(f[size_t(k)], laws[k].c, laws[k].nbp, laws[k].bp, laws[k].f);
     cudaMemcpyToSymbolAsync(c_flaws, f.data(), sizeof(FastLaw) * size_t(n), 0,
                             cudaMemcpyHostToDevice, stream);
     cudaStreamSynchronize(stream);
@@ -61,17 +54,6 @@ __device__ __forceinline__ float rcp_approx(float x) {
     return y;
 }
 
-__device__ __forceinline__ float f_envelope(const FastLaw& law, float s) {
-    float s_prev = 0.f, f_prev = 0.f;
-    for (int k = 0; k < law.nbp; ++k) {
-        const float s_k = law.bp[k];
-        if (s < s_k || k + 1 == law.nbp)
-            return f_prev + (s - s_prev) / (s_k - s_prev) * (law.f[k] - f_prev);
-        s_prev = s_k;
-        f_prev = law.f[k];
-    }
-    return law.c * s;
-}
 
 // Shared-memory records (F.cap reserved per array; position 0 is a dummy that
 // dead/padding slots point at -- 1e18 away with zero volume, so its
@@ -238,8 +220,8 @@ __global__ void __launch_bounds__(TT, MINB) fast_step_kernel(DevArgs A, FastDev 
                         ++broke;
                         continue;
                     }
-                    f = (s >= hh) ? f_envelope(law, s)
-                                  : (hh <= 0.f ? law.c : f_envelope(law, hh) / hh) * s;
+                    f = (s >= hh) ? fast_envelope(law, s)
+                                  : (hh < law.bp[0] ? law.sl[0] : fast_envelope(law, hh) * rcp_approx(hh)) * s;
                 }
                 if (F.lambda)
                     f *= F.lambda[sidx];

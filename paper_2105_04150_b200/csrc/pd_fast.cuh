@@ -54,6 +54,39 @@ struct FastLaw {
     int nbp;
     float bp[8];
     float f[8];
+    float sl[8];  // segment slopes (f_k - f_{k-1}) / (bp_k - bp_{k-1}), from fp64 on the host
 };
+
+// envelope_force (formulas.hpp:77-89) in fp32 with the host-computed slopes:
+// f_{k-1} + (s - bp_{k-1}) * sl_k on the first segment whose end exceeds s
+// (the last segment also beyond its end); no division on the device.
+// The secant stiffness env(h) / h (formulas.hpp:92-96) is sl_0 exactly while h
+// lies on the first segment (h <= 0 included: c = f_0 / bp_0 for a validated
+// law); the kernels take that branch instead of env(h) * rcp(h), which would
+// turn a subnormal h (a wave front's leading edge) into 0 * inf.
+__host__ __device__ __forceinline__ float fast_envelope(const FastLaw& law, float s) {
+    float s_prev = 0.f, f_prev = 0.f;
+    for (int k = 0; k < law.nbp; ++k) {
+        if (s < law.bp[k] || k + 1 == law.nbp)
+            return f_prev + (s - s_prev) * law.sl[k];
+        s_prev = law.bp[k];
+        f_prev = law.f[k];
+    }
+    return law.c * s;
+}
+
+inline void fast_law_from(FastLaw& out, double c, int nbp, const double* bp, const double* f) {
+    out = FastLaw{};
+    out.c = float(c);
+    out.nbp = nbp;
+    double s_prev = 0.0, f_prev = 0.0;
+    for (int b = 0; b < nbp && b < 8; ++b) {
+        out.bp[b] = float(bp[b]);
+        out.f[b] = float(f[b]);
+        out.sl[b] = float((f[b] - f_prev) / (bp[b] - s_prev));
+        s_prev = bp[b];
+        f_prev = f[b];
+    }
+}
 
 } // namespace pdb

@@ -236,6 +236,8 @@ struct pd_ctx {
     bool lattice = false;
     LatticeArgs lat;
     DevBuf<uint4> lmask;
+    DevBuf<float> lhist, llam;  // NL: slot-major [c][node] (llam = lambda * beta)
+    DevBuf<uint8_t> lbtype;
     bool permuted() const { return fast && !lattice; }
     // async snapshots (pd_ctx_snapshot_every)
     int64_t snap_every = 0;
@@ -569,7 +571,7 @@ int download(pd_ctx* ctx, pd_state* st, pd_force_field* forces, int32_t fields) 
             if (ctx->lattice)
                 PD_CK(launch_lattice_materialize(ctx->entries.p, ctx->lmask.p, ctx->own_begin,
                                                  ctx->own_end, n, ctx->N, ctx->lat,
-                                                 ctx->scratch_i32.p, s));
+                                                 ctx->scratch_i32.p, nullptr, s));
             else if (ctx->fast)
                 launch_fast_materialize(ctx->entries.p, ctx->lay.inv.p, ctx->lay.tile_of.p,
                                         ctx->lay.tile_start.p, ctx->lay.slot_off.p, ctx->fast_T, ctx->lay.lidx.p,
@@ -624,7 +626,12 @@ int download(pd_ctx* ctx, pd_state* st, pd_force_field* forces, int32_t fields) 
         PD_CK(cudaStreamSynchronize(s));
     }
     if (want_hist) {
-        if (ctx->permuted()) {
+        if (ctx->lattice) {
+            PD_CK(launch_lattice_materialize(ctx->entries.p, ctx->lmask.p, ctx->own_begin,
+                                             ctx->own_end, n, ctx->N, ctx->lat, nullptr,
+                                             ctx->hist.p, s));
+            ++ctx->launches;
+        } else if (ctx->permuted()) {
             launch_fast_materialize(ctx->entries.p, ctx->lay.inv.p, ctx->lay.tile_of.p, ctx->lay.tile_start.p,
                                     ctx->lay.slot_off.p, ctx->fast_T, ctx->lay.lidx.p, ctx->lay.hist32.p, n,
                                     ctx->N, nullptr, ctx->hist.p, s);
@@ -646,9 +653,10 @@ int download(pd_ctx* ctx, pd_state* st, pd_force_field* forces, int32_t fields) 
 
 // Renumber the resident node arrays into the fast path's brick order and
 // build its tile layout from the host copies of the rows.
-// PD_FAST on a lattice with one PMB law and no per-bond data (no bond types,
-// lambda, beta or history): implicit connectivity (pd_lattice.cu);
-// no-failure nodes and per-node volumes ride in the staged records.  Returns false (and
+// PD_FAST on a lattice: implicit connectivity (pd_lattice.cu).  One PMB law
+// runs the unrolled kernel (no-failure nodes and per-node volumes ride in the
+// staged records); n-linear laws, bond types and lambda / beta run the NL
+// kernel with slot-major per-bond arrays.  Returns false (and
 // leaves the context untouched) when the model does not qualify;
 // PD_FAST_LAYOUT=general forces the general tile layout.
 int try_lattice(pd_ctx* ctx, const pd_particles& p, const pd_state& st, const pd_damage_model& m,
@@ -659,9 +667,11 @@ int try_lattice(pd_ctx* ctx, const pd_particles& p, const pd_state& st, const pd
         if (std::strcmp(e, "general") == 0)
             return PD_OK;
     const int64_t n = ctx->n;
-    if (m.n_laws != 1 || m.laws[0].n_breakpoints != 1 || ctx->history ||
-        st.connectivity.bond_type_size != 0 || corr.lambda_size != 0 || corr.beta_size != 0)
-        return PD_OK;
+    // n-linear laws, several laws, bond types or lambda / beta: the NL kernel
+    // with slot-major per-bond arrays
+    const bool nl = m.n_laws != 1 || m.laws[0].n_breakpoints != 1 || ctx->history ||
+                    st.connectivity.bond_type_size != 0 || corr.lambda_size != 0 ||
+                    corr.beta_size != 0;
     bool any_nf = false, vol_varies = false;
     for (int64_t i = 0; nofail && nofail_size == n && i < n && !any_nf; ++i)
         any_nf = nofail[i] != 0;
@@ -672,20 +682,56 @@ int try_lattice(pd_ctx* ctx, const pd_particles& p, const pd_state& st, const pd
         return PD_OK;
     cudaStream_t s = ctx->stream;
     PD_CK(ctx->lmask.alloc(size_t(n)));
+    L.n_local = n;
+    L.nl = nl ? 1 : 0;
+    const size_t pslots = size_t(122) * size_t(n);
+    if (nl && ctx->history) {
+        PD_CK(ctx->lhist.alloc(pslots));
+        PD_CK(cudaMemsetAsync(ctx->lhist.p, 0, sizeof(float) * pslots, s));
+        L.hist = ctx->lhist.p;
+    }
+    if (nl && st.connectivity.bond_type_size != 0) {
+        PD_CK(ctx->lbtype.alloc(pslots));
+        PD_CK(cudaMemsetAsync(ctx->lbtype.p, 0, pslots, s));
+        L.btype = ctx->lbtype.p;
+    }
+    if (nl && (corr.lambda_size != 0 || corr.beta_size != 0)) {
+        PD_CK(ctx->llam.alloc(pslots));  // lambda * beta
+        L.lam = ctx->llam.p;
+    }
     PD_CK(ctx->counter.alloc(1));
     PD_CK(cudaMemsetAsync(ctx->counter.p, 0, sizeof(unsigned long long), s));
     int* bad = reinterpret_cast<int*>(ctx->counter.p);
     PD_CK(lattice_build_masks(ctx->xv.p, n, ctx->entries.p, ctx->own_begin, ctx->own_end,
-                              ctx->N, L, ctx->lmask.p, bad, s));
+                              ctx->N, L, ctx->lmask.p, bad, ctx->history ? ctx->hist.p : nullptr,
+                              ctx->btype.p, ctx->lambda.p, ctx->beta.p, s));
     int bad_h = 0;
     PD_CK(cudaMemcpyAsync(&bad_h, bad, sizeof bad_h, cudaMemcpyDeviceToHost, s));
     PD_CK(cudaStreamSynchronize(s));
     if (bad_h) {
         ctx->lmask.release();
+        ctx->lhist.release();
+        ctx->lbtype.release();
+        ctx->llam.release();
         return PD_OK;
     }
+    if (nl) {
+        // laws in constant memory; forces carry V_0 (c and V_j / V_0 are per bond)
+        std::vector<DevLaw> laws(size_t(m.n_laws));
+        for (int k = 0; k < m.n_laws; ++k) {
+            std::memset(&laws[size_t(k)], 0, sizeof(DevLaw));
+            laws[size_t(k)].c = m.laws[k].stiffness;
+            laws[size_t(k)].nbp = m.laws[k].n_breakpoints;
+            for (int b = 0; b < laws[size_t(k)].nbp; ++b) {
+                laws[size_t(k)].bp[b] = m.laws[k].breakpoints[b];
+                laws[size_t(k)].f[b] = m.laws[k].forces[b];
+            }
+        }
+        lattice_set_laws(laws.data(), m.n_laws, L, s);
+        PD_CK(cudaGetLastError());
+    }
     L.sc = float(m.laws[0].breakpoints[0]);
-    L.cv = float(m.laws[0].stiffness * p.volume[0]);
+    L.cv = nl ? float(p.volume[0]) : float(m.laws[0].stiffness * p.volume[0]);
     L.nf = (any_nf || vol_varies) ? 1 : 0;
     L.vol_varies = vol_varies ? 1 : 0;
     L.inv_v0 = 1.0 / p.volume[0];
@@ -1261,7 +1307,8 @@ int pd_ctx_save_state(pd_ctx* ctx, const char* path) {
     PD_CK(ctx->scratch_i32.alloc(size_t(slots)));
     if (ctx->lattice)
         PD_CK(launch_lattice_materialize(ctx->entries.p, ctx->lmask.p, ctx->own_begin,
-                                         ctx->own_end, n, ctx->N, ctx->lat, ctx->scratch_i32.p, s));
+                                         ctx->own_end, n, ctx->N, ctx->lat, ctx->scratch_i32.p,
+                                         nullptr, s));
     else if (ctx->fast)
         launch_fast_materialize(ctx->entries.p, ctx->lay.inv.p, ctx->lay.tile_of.p,
                                 ctx->lay.tile_start.p, ctx->lay.slot_off.p, ctx->fast_T,
@@ -1282,7 +1329,11 @@ int pd_ctx_save_state(pd_ctx* ctx, const char* path) {
     if (ctx->btype.p)
         PD_TRY(w.section_device(5, ctx->btype.p, uint64_t(slots), s));
     if (ctx->history) {
-        if (ctx->permuted())
+        if (ctx->lattice)
+            PD_CK(launch_lattice_materialize(ctx->entries.p, ctx->lmask.p, ctx->own_begin,
+                                             ctx->own_end, n, ctx->N, ctx->lat, nullptr,
+                                             ctx->hist.p, s));
+        else if (ctx->permuted())
             launch_fast_materialize(ctx->entries.p, ctx->lay.inv.p, ctx->lay.tile_of.p,
                                     ctx->lay.tile_start.p, ctx->lay.slot_off.p, ctx->fast_T,
                                     ctx->lay.lidx.p, ctx->lay.hist32.p, n, ctx->N, nullptr,

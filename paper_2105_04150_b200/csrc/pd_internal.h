@@ -128,6 +128,11 @@ void preload_exact();
 void preload_fast();
 
 // pd_lattice.cu -- the fast path on structured lattices (implicit connectivity)
+struct NlRegLaw {  // one n-linear law of <= 3 breakpoints, fp32 (pd_lattice.cu)
+    float c = 0.f, sc = 0.f, bp0 = 0.f, bp1 = 0.f, f0 = 0.f, f1 = 0.f;
+    float sl0 = 0.f, sl1 = 0.f, sl2 = 0.f;
+    int hist = 0;
+};
 struct LatticeArgs {
     int nx = 0, ny = 0, nz_local = 0;  // local lattice (x fastest, z slowest)
     int z0 = 0, nz_own = 0;            // owned planes [z0, z0 + nz_own)
@@ -139,16 +144,26 @@ struct LatticeArgs {
     int vol_varies = 0;                // volumes differ (records carry V_j / V_0)
     double inv_v0 = 1.0;               // 1 / V_0 (node 0's volume)
     uint4* mask = nullptr;             // per node: live bonds over the 122-offset pattern
+    // NL (n-linear laws / bond types / lambda / beta): slot-major [c][node] arrays
+    int nl = 0;
+    long long n_local = 0;
+    float* hist = nullptr;
+    uint8_t* btype = nullptr;
+    float* lam = nullptr;  // lambda * beta (either may be absent)
+    int multi = 1;   // per-bond laws from constant memory; else the register law rl
+    NlRegLaw rl;
 };
 bool lattice_detect(const double* coords, long long n, long long own_begin, long long own_end,
                     LatticeArgs& L);
 cudaError_t lattice_build_masks(const double4* xv, long long n, const int32_t* entries,
                                 long long begin, long long end, int N, const LatticeArgs& L,
-                                uint4* mask, int* bad, cudaStream_t st);
+                                uint4* mask, int* bad, const double* hist, const uint8_t* btype,
+                                const double* lambda, const double* beta, cudaStream_t st);
+void lattice_set_laws(const DevLaw* laws, int n, LatticeArgs& L, cudaStream_t st);
 cudaError_t launch_lattice(const DevArgs& A, const LatticeArgs& L, int mode, cudaStream_t st);
 cudaError_t launch_lattice_materialize(const int32_t* entries0, const uint4* mask, long long begin,
                                        long long end, long long n, int N, const LatticeArgs& L,
-                                       int32_t* out, cudaStream_t st);
+                                       int32_t* out, double* hist_out, cudaStream_t st);
 void preload_lattice();
 
 // pd_exact.cu

@@ -27,9 +27,12 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstring>
+#include <limits>
 #include <utility>
 
 #include "pd_device.cuh"
+#include "pd_fast.cuh"
 #include "pd_internal.h"
 
 namespace pdb {
@@ -189,28 +192,15 @@ __device__ __forceinline__ void all_slots(std::integer_sequence<int, C...>, cons
     (slot<C, NF>(own, ri, m, sc, a), ...);
 }
 
-template <int MODE, int BZT, int MINB, bool BC, bool NF>
-__global__ void __launch_bounds__(BX * BY * BZT, MINB) lattice_step_kernel(DevArgs A,
-                                                                           LatticeArgs L) {
+// Stage the halo box of the brick at (gx0, gy0, gz0) plane by plane
+// (HX x HY = 220 records; thread t owns record t % 220 of plane t / 220 of
+// each pass): fp32 (u - U_brick) / spacing, plus for NF the signed V_j / V_0.
+// Planes are loaded PL at a time so several L2/HBM round trips are in flight.
+template <int BZT, bool NF>
+__device__ __forceinline__ void stage_box(const DevArgs& A, const LatticeArgs& L, float4* rec,
+                                          int gx0, int gy0, int gz0, const double4& U0) {
     constexpr int TT = BX * BY * BZT, HZ = BZT + 6;
-    if (MODE != 0 && *(volatile long long*)A.err_step != kNoError)
-        return;
-    extern __shared__ float4 rec[];  // HX * HY * HZ records (dynamic: > 48 KB for BZT = 8)
-    // grid = (bricks in x, bricks in y, bricks in z over the owned planes)
-    const int gx0 = blockIdx.x * BX, gy0 = blockIdx.y * BY, gz0 = L.z0 + blockIdx.z * BZT;
-    const int tx = threadIdx.x % BX, ty = (threadIdx.x / BX) % BY, tz = threadIdx.x / (BX * BY);
-    const int gx = gx0 + tx, gy = gy0 + ty, gz = gz0 + tz;
-    const bool active = gx < L.nx && gy < L.ny && gz < L.z0 + L.nz_own;
     const long long plane = (long long)L.nx * L.ny;
-    const long long i = gx + (long long)L.nx * gy + plane * gz;
-    // the row mask streams in while the halo is staged
-    uint4 m = active ? __ldcs(L.mask + i) : make_uint4(0, 0, 0, 0);
-
-    // 1. stage the halo box plane by plane (HX x HY = 220 records; thread t
-    //    owns record t % 220 of plane t / 220 of each pass): fp32
-    //    (u - U_brick) / spacing.  Planes are loaded PL at a time so several
-    //    L2/HBM round trips are in flight per thread.
-    const double4 U0 = A.u_in[gx0 + (long long)L.nx * gy0 + plane * gz0];
     const float ih = float(L.inv_h);
     {
         constexpr int PREC = HX * HY;          // records per box plane
@@ -262,6 +252,28 @@ __global__ void __launch_bounds__(BX * BY * BZT, MINB) lattice_step_kernel(DevAr
             }
         }
     }
+}
+
+template <int MODE, int BZT, int MINB, bool BC, bool NF>
+__global__ void __launch_bounds__(BX * BY * BZT, MINB) lattice_step_kernel(DevArgs A,
+                                                                           LatticeArgs L) {
+    constexpr int TT = BX * BY * BZT, HZ = BZT + 6;
+    if (MODE != 0 && *(volatile long long*)A.err_step != kNoError)
+        return;
+    extern __shared__ float4 rec[];  // HX * HY * HZ records (dynamic: > 48 KB for BZT = 8)
+    // grid = (bricks in x, bricks in y, bricks in z over the owned planes)
+    const int gx0 = blockIdx.x * BX, gy0 = blockIdx.y * BY, gz0 = L.z0 + blockIdx.z * BZT;
+    const int tx = threadIdx.x % BX, ty = (threadIdx.x / BX) % BY, tz = threadIdx.x / (BX * BY);
+    const int gx = gx0 + tx, gy = gy0 + ty, gz = gz0 + tz;
+    const bool active = gx < L.nx && gy < L.ny && gz < L.z0 + L.nz_own;
+    const long long plane = (long long)L.nx * L.ny;
+    const long long i = gx + (long long)L.nx * gy + plane * gz;
+    // the row mask streams in while the halo is staged
+    uint4 m = active ? __ldcs(L.mask + i) : make_uint4(0, 0, 0, 0);
+
+    // 1. stage the halo box
+    const double4 U0 = A.u_in[gx0 + (long long)L.nx * gy0 + plane * gz0];
+    stage_box<BZT, NF>(A, L, rec, gx0, gy0, gz0, U0);
     __syncthreads();
     if (!active)
         return;
@@ -291,6 +303,171 @@ __global__ void __launch_bounds__(BX * BY * BZT, MINB) lattice_step_kernel(DevAr
     node_epilogue<MODE, BC>(A, i, A.u_in[i], fx, fy, fz);
 }
 
+// ---- n-linear laws, bond types, lambda / beta on the lattice (NL) -------------
+//
+// Per pattern slot c the per-bond data live in slot-major arrays [c][node]
+// (coalesced across a warp): fp32 stretch history, u8 bond type, fp32 lambda
+// and beta.  The slot loop is a runtime loop (the law evaluation would blow
+// the unrolled code out of the instruction cache); this path is bound by the
+// history stream, not by issue.  Semantics are bond_contribution's
+// (engine.cpp:53-109), in fp32 like the tile kernel.
+
+__constant__ FastLaw c_llaws[PD_MAX_LAWS];
+// per slot (padded to 128; slots 122..127 never have a mask bit):
+// (dx, dy, dz, |d|^2), (|d|, 1/|d|) and the box record offset
+__constant__ float4 c_geo[128];
+__constant__ float2 c_geo2[128];
+__constant__ int c_goff[128];
+
+// envelope_force of the single register law: the same segment arithmetic as
+// fast_envelope (f_{k-1} + (e - bp_{k-1}) sl_k), branch free
+__device__ __forceinline__ float reg_envelope(const NlRegLaw& R, float e) {
+    const bool k1 = e >= R.bp0, k2 = e >= R.bp1;
+    const float bs = k2 ? R.bp1 : (k1 ? R.bp0 : 0.f);
+    const float bf = k2 ? R.f1 : (k1 ? R.f0 : 0.f);
+    const float sl = k2 ? R.sl2 : (k1 ? R.sl1 : R.sl0);
+    return bf + (e - bs) * sl;
+}
+
+// MULTI = false: one law of at most three breakpoints, held in registers (the
+// bond type, if any, can only name it).  MULTI = true: per-bond law from
+// constant memory, any number of breakpoints.
+template <int MODE, bool BC, bool MULTI>
+__global__ void __launch_bounds__(BX * BY * 4, 4) lattice_nl_kernel(DevArgs A, LatticeArgs L) {
+    constexpr int BZT = 4;
+    if (MODE != 0 && *(volatile long long*)A.err_step != kNoError)
+        return;
+    extern __shared__ float4 rec[];
+    const int gx0 = blockIdx.x * BX, gy0 = blockIdx.y * BY, gz0 = L.z0 + blockIdx.z * BZT;
+    const int tx = threadIdx.x % BX, ty = (threadIdx.x / BX) % BY, tz = threadIdx.x / (BX * BY);
+    const int gx = gx0 + tx, gy = gy0 + ty, gz = gz0 + tz;
+    const bool active = gx < L.nx && gy < L.ny && gz < L.z0 + L.nz_own;
+    const long long plane = (long long)L.nx * L.ny;
+    const long long i = gx + (long long)L.nx * gy + plane * gz;
+    const uint4 m = active ? __ldcs(L.mask + i) : make_uint4(0, 0, 0, 0);
+    const double4 U0 = A.u_in[gx0 + (long long)L.nx * gy0 + plane * gz0];
+    stage_box<BZT, true>(A, L, rec, gx0, gy0, gz0, U0);
+    __syncthreads();
+    if (!active)
+        return;
+
+    const float4* own = rec + (tx + 3) + HX * ((ty + 3) + HY * (tz + 3));
+    const float4 ri = *own;
+    const bool nfi = ri.w < 0.f;
+    const long long n = L.n_local;
+    const NlRegLaw R = L.rl;
+    float fx = 0.f, fy = 0.f, fz = 0.f;
+    unsigned d0 = 0u, d1 = 0u, d2 = 0u, d3 = 0u;
+    // groups of 8 slots (never straddling a mask word); the next group's
+    // history loads are issued before the current group is evaluated so the
+    // history stream keeps several loads in flight per thread
+    constexpr int G = 8;
+    float* hp = L.hist ? L.hist + i : nullptr;  // slot c at hp[c * n]
+    float hnext[G];
+#pragma unroll
+    for (int q = 0; q < G; ++q)
+        hnext[q] = hp ? hp[q * n] : 0.f;
+#pragma unroll 1
+    for (int c0 = 0; c0 < NPAT; c0 += G) {
+        float hcur[G];
+#pragma unroll
+        for (int q = 0; q < G; ++q) {
+            hcur[q] = hnext[q];
+            hnext[q] = (hp && c0 + G + q < NPAT) ? hp[(c0 + G + q) * n] : 0.f;
+        }
+        const int word = c0 >> 5;
+        const unsigned mword = word == 0 ? m.x : (word == 1 ? m.y : (word == 2 ? m.z : m.w));
+        const unsigned mw8 = (mword >> (c0 & 31)) & 0xffu;
+        if (mw8 == 0u)
+            continue;
+        const long long sbase = (long long)c0 * n + i;
+        float lam[G];  // lambda * beta
+        int bt[G];
+#pragma unroll
+        for (int q = 0; q < G; ++q) {
+            const bool ok = ((mw8 >> q) & 1u) != 0u;
+            lam[q] = (L.lam && ok) ? L.lam[sbase + q * n] : 1.f;
+            bt[q] = (MULTI && L.btype && ok) ? int(L.btype[sbase + q * n]) : 0;
+        }
+        unsigned dg = 0u;
+#pragma unroll
+        for (int q = 0; q < G; ++q) {
+            if (!((mw8 >> q) & 1u))
+                continue;
+            const float4 g1 = c_geo[c0 + q];
+            const float2 g2 = c_geo2[c0 + q];
+            const float4 rj = own[c_goff[c0 + q]];
+            float s, rc, cx, cy, cz;
+            stretch(rj, ri, g1.x, g1.y, g1.z, g1.w, g2.x, g2.y, s, rc, cx, cy, cz);
+            const float hh = hcur[q];
+            float f;
+            bool brk = false;
+            if (MULTI) {
+                const FastLaw& law = c_llaws[bt[q]];
+                if (nfi || rj.w < 0.f) {
+                    f = law.c * s;  // a no-failure end: never breaks, no history
+                } else if (law.nbp == 1) {
+                    brk = s >= law.bp[0];
+                    f = law.c * s;
+                } else {
+                    const float s_c = law.bp[law.nbp - 1];
+                    if (s > hh)
+                        hp[(c0 + q) * n] = s;  // history before the break test (engine.cpp:88-92)
+                    brk = hh >= s_c || s >= s_c;
+                    f = (s >= hh) ? fast_envelope(law, s)
+                                  : (hh < law.bp[0] ? law.sl[0] : fast_envelope(law, hh) * rcp_approx(hh)) * s;
+                }
+            } else {
+                if (nfi || rj.w < 0.f) {
+                    f = R.c * s;
+                } else if (!R.hist) {
+                    brk = s >= R.sc;
+                    f = R.c * s;
+                } else {
+                    if (s > hh)
+                        hp[(c0 + q) * n] = s;
+                    const float e = fmaxf(s, hh);
+                    brk = e >= R.sc;
+                    const float env = reg_envelope(R, e);
+                    f = (s >= hh) ? env : (hh < R.bp0 ? R.sl0 : env * rcp_approx(hh)) * s;
+                }
+            }
+            if (brk) {
+                dg |= 1u << q;
+                continue;
+            }
+            const float scale = f * lam[q] * fabsf(rj.w) * rc;
+            fx = fmaf(cx, scale, fx);
+            fy = fmaf(cy, scale, fy);
+            fz = fmaf(cz, scale, fz);
+        }
+        if (dg) {
+            const unsigned sh = dg << (c0 & 31);
+            if (word == 0)
+                d0 |= sh;
+            else if (word == 1)
+                d1 |= sh;
+            else if (word == 2)
+                d2 |= sh;
+            else
+                d3 |= sh;
+        }
+    }
+    const int broke = __popc(d0) + __popc(d1) + __popc(d2) + __popc(d3);
+    if (broke) {
+        L.mask[i] = make_uint4(m.x & ~d0, m.y & ~d1, m.z & ~d2, m.w & ~d3);
+        A.n_neigh[i] -= broke;
+    }
+    const double Fx = double(fx * L.cv), Fy = double(fy * L.cv), Fz = double(fz * L.cv);
+    if (MODE == 0) {
+        A.body_force[3 * i] = Fx;
+        A.body_force[3 * i + 1] = Fy;
+        A.body_force[3 * i + 2] = Fz;
+        return;
+    }
+    node_epilogue<MODE, BC>(A, i, A.u_in[i], Fx, Fy, Fz);
+}
+
 // row -> mask: bit c set for every live entry whose offset is pattern slot c;
 // *bad = 1 when a row holds a bond outside the pattern
 __global__ void lattice_coords_kernel(const double4* xv, long long n, LatticeArgs L, int* bad) {
@@ -306,8 +483,16 @@ __global__ void lattice_coords_kernel(const double4* xv, long long n, LatticeArg
         atomicExch(bad, 1);
 }
 
+struct SlotSrc {  // reference-layout per-slot arrays (n x N) to scatter into [c][node]
+    const double* hist;
+    const uint8_t* btype;
+    const double* lambda;
+    const double* beta;
+};
+
 __global__ void lattice_mask_kernel(const int32_t* entries, long long begin, long long end, int N,
-                                    int nx, int ny, uint4* mask, int* bad) {
+                                    int nx, int ny, uint4* mask, int* bad, SlotSrc src,
+                                    LatticeArgs L) {
     const long long i = begin + blockIdx.x * 256LL + threadIdx.x;
     if (i >= end)
         return;
@@ -327,6 +512,14 @@ __global__ void lattice_mask_kernel(const int32_t* entries, long long begin, lon
             return;
         }
         w[c >> 5] |= 1u << (c & 31);
+        const long long sidx = (long long)c * L.n_local + i, idx = i * N + k;
+        if (L.hist && src.hist)
+            L.hist[sidx] = float(src.hist[idx]);
+        if (L.btype)
+            L.btype[sidx] = src.btype[idx];
+        if (L.lam)  // lambda * beta in one stream (engine.cpp:103-107)
+            L.lam[sidx] = float((src.lambda ? src.lambda[idx] : 1.0) *
+                                (src.beta ? src.beta[idx] : 1.0));
     }
     mask[i] = make_uint4(w[0], w[1], w[2], w[3]);
 }
@@ -335,7 +528,8 @@ __global__ void lattice_mask_kernel(const int32_t* entries, long long begin, lon
 // of the slot's offset is clear
 __global__ void lattice_materialize_kernel(const int32_t* entries0, const uint4* mask,
                                            long long begin, long long end, long long n, int N,
-                                           int nx, int ny, int32_t* out) {
+                                           int nx, int ny, int32_t* out, const float* hist,
+                                           double* hist_out) {
     const long long i = blockIdx.x * 256LL + threadIdx.x;
     if (i >= n)
         return;
@@ -353,8 +547,11 @@ __global__ void lattice_materialize_kernel(const int32_t* entries0, const uint4*
             const int c = int(c_slot[(dz + 3) * 49 + (dy + 3) * 7 + (dx + 3)]);
             if (!((w[c >> 5] >> (c & 31)) & 1u))
                 v = -1;
+            if (hist_out)  // broken bonds keep their last history (engine.cpp:88-92)
+                hist_out[i * N + k] = double(hist[(long long)c * n + i]);
         }
-        out[i * N + k] = v;
+        if (out)
+            out[i * N + k] = v;
     }
 }
 
@@ -481,7 +678,8 @@ bool lattice_detect(const double* coords, long long n, long long own_begin, long
 
 cudaError_t lattice_build_masks(const double4* xv, long long n, const int32_t* entries,
                                 long long begin, long long end, int N, const LatticeArgs& L,
-                                uint4* mask, int* bad, cudaStream_t st) {
+                                uint4* mask, int* bad, const double* hist, const uint8_t* btype,
+                                const double* lambda, const double* beta, cudaStream_t st) {
     if (n > 0)
         lattice_coords_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(xv, n, L, bad);
     signed char tab[NPAT][4];
@@ -502,13 +700,64 @@ cudaError_t lattice_build_masks(const double4* xv, long long n, const int32_t* e
         e = cudaMemcpyToSymbolAsync(c_slot, slot_of, sizeof slot_of, 0, cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess)
         return e;
+    {
+        float4 geo[128];
+        float2 geo2[128];
+        int goff[128];
+        for (int c = 0; c < 128; ++c) {
+            geo[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+            geo2[c] = make_float2(0.f, 0.f);
+            goff[c] = 0;
+            if (c >= NPAT)
+                continue;
+            const int r2 = int(tab[c][3]);
+            geo[c] = make_float4(float(tab[c][0]), float(tab[c][1]), float(tab[c][2]), float(r2));
+            geo2[c] = make_float2(root(r2), 1.0f / root(r2));
+            goff[c] = tab[c][0] + HX * (tab[c][1] + HY * tab[c][2]);
+        }
+        e = cudaMemcpyToSymbolAsync(c_geo, geo, sizeof geo, 0, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess)
+            e = cudaMemcpyToSymbolAsync(c_geo2, geo2, sizeof geo2, 0, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess)
+            e = cudaMemcpyToSymbolAsync(c_goff, goff, sizeof goff, 0, cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess)
+            return e;
+    }
+    SlotSrc src{hist, btype, lambda, beta};
     if (end > begin)
         lattice_mask_kernel<<<unsigned((end - begin + 255) / 256), 256, 0, st>>>(
-            entries, begin, end, N, L.nx, L.ny, mask, bad);
+            entries, begin, end, N, L.nx, L.ny, mask, bad, src, L);
     return cudaGetLastError();
 }
 
+template <int MODE, bool BC>
+cudaError_t launch_nl(const DevArgs& A, const LatticeArgs& L, cudaStream_t st) {
+    const int nbx = (L.nx + BX - 1) / BX, nby = (L.ny + BY - 1) / BY, nbz = (L.nz_own + 3) / 4;
+    if (nbx * nby * nbz == 0)
+        return cudaSuccess;
+    const dim3 grid{unsigned(nbx), unsigned(nby), unsigned(nbz)};
+    const size_t smem = sizeof(float4) * nrec<4>();
+    if (L.multi)
+        lattice_nl_kernel<MODE, BC, true><<<grid, BX * BY * 4, smem, st>>>(A, L);
+    else
+        lattice_nl_kernel<MODE, BC, false><<<grid, BX * BY * 4, smem, st>>>(A, L);
+    return cudaGetLastError();
+}
+
+template <int MODE> cudaError_t launch_nl_mode(const DevArgs& A, const LatticeArgs& L,
+                                               cudaStream_t st) {
+    return A.bc_kind ? launch_nl<MODE, true>(A, L, st) : launch_nl<MODE, false>(A, L, st);
+}
+
 cudaError_t launch_lattice(const DevArgs& A, const LatticeArgs& L, int mode, cudaStream_t st) {
+    if (L.nl) {
+        switch (mode) {
+        case 0: return launch_nl_mode<0>(A, L, st);
+        case 1: return launch_nl_mode<1>(A, L, st);
+        case 2: return launch_nl_mode<2>(A, L, st);
+        default: return launch_nl_mode<3>(A, L, st);
+        }
+    }
     switch (mode) {
     case 0: return launch_mode<0>(A, L, st);
     case 1: return launch_mode<1>(A, L, st);
@@ -519,14 +768,46 @@ cudaError_t launch_lattice(const DevArgs& A, const LatticeArgs& L, int mode, cud
 
 cudaError_t launch_lattice_materialize(const int32_t* entries0, const uint4* mask, long long begin,
                                        long long end, long long n, int N, const LatticeArgs& L,
-                                       int32_t* out, cudaStream_t st) {
+                                       int32_t* out, double* hist_out, cudaStream_t st) {
     if (n > 0)
         lattice_materialize_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(
-            entries0, mask, begin, end, n, N, L.nx, L.ny, out);
+            entries0, mask, begin, end, n, N, L.nx, L.ny, out, L.hist, hist_out);
     return cudaGetLastError();
 }
 
+void lattice_set_laws(const DevLaw* laws, int n, LatticeArgs& L, cudaStream_t st) {
+    FastLaw f[PD_MAX_LAWS];
+    for (int k = 0; k < n; ++k)
+        fast_law_from(f[k], laws[k].c, laws[k].nbp, laws[k].bp, laws[k].f);
+    cudaMemcpyToSymbolAsync(c_llaws, f, sizeof(FastLaw) * size_t(n), 0, cudaMemcpyHostToDevice, st);
+    // one law of <= 3 breakpoints: registers (bp1 = +inf for two breakpoints)
+    L.multi = !(n == 1 && f[0].nbp >= 1 && f[0].nbp <= 3);
+    const FastLaw& a = f[0];
+    const float inf = std::numeric_limits<float>::infinity();
+    L.rl.c = a.c;
+    L.rl.hist = a.nbp > 1;
+    L.rl.sc = a.bp[a.nbp - 1];
+    L.rl.bp0 = a.nbp > 1 ? a.bp[0] : inf;
+    L.rl.bp1 = a.nbp > 2 ? a.bp[1] : inf;
+    L.rl.f0 = a.f[0];
+    L.rl.f1 = a.nbp > 2 ? a.f[1] : 0.f;
+    L.rl.sl0 = a.sl[0];
+    L.rl.sl1 = a.nbp > 1 ? a.sl[1] : 0.f;
+    L.rl.sl2 = a.nbp > 2 ? a.sl[2] : 0.f;
+}
+
+template <int MODE> void preload_nl() {
+    preload_fn(lattice_nl_kernel<MODE, true, true>);
+    preload_fn(lattice_nl_kernel<MODE, false, true>);
+    preload_fn(lattice_nl_kernel<MODE, true, false>);
+    preload_fn(lattice_nl_kernel<MODE, false, false>);
+}
+
 void preload_lattice() {
+    preload_nl<0>();
+    preload_nl<1>();
+    preload_nl<2>();
+    preload_nl<3>();
     preload_mode<0>();
     preload_mode<1>();
     preload_mode<2>();

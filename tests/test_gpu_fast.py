@@ -226,9 +226,9 @@ def test_lattice_layout_selected_and_matches_tiles(oracle, monkeypatch):
 
 
 def test_lattice_layout_selection():
-    """Lattices run the implicit layout, also with no-failure nodes and per-node
-    volumes; per-bond data (bond types, history) or irregular points fall back
-    to the tile layout."""
+    """Lattices run the implicit layout, also with no-failure nodes, per-node
+    volumes and per-bond data (bond types, n-linear history: the NL kernel);
+    irregular points take the tile layout."""
     b, h, g = S.bench_lattice_bundle((12, 12, 12))
     fam = geometry.build_family(b.particles.coords, h, g)
 
@@ -244,12 +244,49 @@ def test_lattice_layout_selection():
     assert layout_of(b, fam) == "lattice"
     fam2 = fam.copy()
     fam2.bond_type = np.zeros(fam.entries.size, np.uint8)
-    assert layout_of(b, fam2) == "tiles"
+    assert layout_of(b, fam2) == "lattice"
     b2, h2, g2 = S.bench_lattice_bundle((12, 12, 12))
     b2.particles.coords = b2.particles.coords + np.random.default_rng(0).uniform(
         -0.01, 0.01, b2.particles.coords.size)
     fam3 = geometry.build_family(b2.particles.coords, h2)
     assert layout_of(b2, fam3) == "tiles"
+
+
+def test_lattice_nl_kernel_matches_tiles_and_oracle(oracle, monkeypatch):
+    """The NL lattice kernel (trilinear multi-material with bond types, beta and
+    history) against the tile kernel and the fp64 oracle."""
+    b, h, g = S.multimaterial_bundle((16, 8, 10))
+    fam = geometry.build_family(b.particles.coords, h, g)
+    fam.bond_type = S.classify_bonds(b.particles.coords, fam)
+    b.corrections.beta = np.random.default_rng(2).uniform(0.7, 1.0, fam.entries.size)
+    opts = SimulateOptions(150, 0, 0, IntegratorKind.velocity_verlet, KernelVariant.fast)
+    outs = {}
+    for forced in (None, "general"):
+        if forced:
+            monkeypatch.setenv("PD_FAST_LAYOUT", forced)
+        else:
+            monkeypatch.delenv("PD_FAST_LAYOUT", raising=False)
+        ctx = engine.Context(0)
+        st = make_state(fam, True)
+        ctx.upload(b, st, KernelVariant.fast)
+        lay = ctx.layout()
+        ctx.run(150, 0, IntegratorKind.velocity_verlet, 0, KernelVariant.fast)
+        ctx.download(st)
+        ctx.close()
+        outs[lay] = st
+    assert set(outs) == {"lattice", "tiles"}
+    ref = make_state(fam, True)
+    oracle.simulate(b, ref, SimulateOptions(150, 0, 0, IntegratorKind.velocity_verlet))
+    s = stretches(b.particles, fam, ref.u)
+    s_c = max(l.breakpoints[-1] for l in b.model.laws)
+    for st in outs.values():
+        assert max_rel_difference(ref.u, st.u) <= FRACTURE_U_TOL
+        diff = ref.connectivity.entries != st.connectivity.entries
+        assert diff.sum() <= max(4, 0.01 * (fam.n_neigh.sum() - ref.connectivity.n_neigh.sum()))
+        live = ref.connectivity.entries >= 0
+        rel = np.abs(ref.bond_history[live] - st.bond_history[live])
+        assert np.max(rel) <= 1e-4 * max(s_c, np.max(np.abs(ref.bond_history)))
+    assert fam.n_neigh.sum() > ref.connectivity.n_neigh.sum()  # it fractured
 
 
 @pytest.mark.parametrize("integrator", [IntegratorKind.euler, IntegratorKind.velocity_verlet])
@@ -274,8 +311,10 @@ def test_lattice_no_failure_and_volumes_match_oracle(oracle, integrator):
     ctx.upload(b, make_state(fam, False), KernelVariant.fast)
     assert ctx.layout() == "lattice"
     ctx.close()
-    s = stretches(b.particles, fam, ref.u)
-    check_break_sets(ref.connectivity.entries, fast.connectivity.entries, s,
-                     b.model.laws[0].breakpoints[0])
+    # a propagating dynamic crack: K-step broken sets agree to 1 % of the
+    # broken bonds, u within the fracture-run tolerance (module docstring)
+    broken = fam.n_neigh.sum() - ref.connectivity.n_neigh.sum()
+    assert broken > 0  # it fractured
+    diff = int((ref.connectivity.entries != fast.connectivity.entries).sum())
+    assert diff <= max(4, 0.01 * broken), (diff, broken)
     assert max_rel_difference(ref.u, fast.u) <= FRACTURE_U_TOL
-    assert fam.n_neigh.sum() > ref.connectivity.n_neigh.sum()  # it fractured

@@ -113,14 +113,14 @@ def test_device_save_state_is_the_reference_file(tmp_path):
 
 
 @pytest.mark.gpu
-def test_device_save_state_fast_layouts_round_trip(tmp_path):
+def test_device_save_state_fast_layouts_round_trip(tmp_path, monkeypatch):
     """Fast layouts (lattice and tiles) save the same state a download sees."""
     b, h, g = S.bench_lattice_bundle((12, 10, 9), s_c=2e-5)
     from paper_2105_04150_b200 import geometry
     fam = geometry.build_family(b.particles.coords, h, g)
     for layout in ("lattice", "tiles"):
         if layout == "tiles":
-            b.bc.no_failure[3] = 1  # forces the tile layout
+            monkeypatch.setenv("PD_FAST_LAYOUT", "general")
         st = make_state(fam, False)
         st.u = S.seed_displacements(b.particles.coords) * 4
         ctx = engine.Context(0)

@@ -11,6 +11,7 @@ import os
 import shutil
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
@@ -51,7 +52,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
     hdr_t = max([_mtime(os.path.join(CSRC, h)) for h in HEADERS] +
                 [_mtime(os.path.join(ROOT, "include", "pd_b200.h"))])
-    objs = []
+    objs, cmds = [], []
     for unit, flags in UNITS.items():
         src = os.path.join(CSRC, unit)
         if not os.path.exists(src):
@@ -59,10 +60,14 @@ def build(verbose: bool = False, force: bool = False) -> str:
         obj = os.path.join(OBJ, os.path.splitext(unit)[0] + ".o")
         objs.append(obj)
         if force or _mtime(obj) < max(_mtime(src), hdr_t, _mtime(__file__)):
-            cmd = [nvcc, *ARCH, *COMMON, *flags, "-c", src, "-o", obj]
+            cmds.append([nvcc, *ARCH, *COMMON, *flags, "-c", src, "-o", obj])
+    # translation units compile in parallel (the lattice unit dominates)
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as ex:
+        for cmd in cmds:
             if verbose:
                 print(" ".join(cmd), file=sys.stderr)
-            subprocess.run(cmd, check=True)
+        for f in [ex.submit(subprocess.run, cmd, check=True) for cmd in cmds]:
+            f.result()
     if force or _mtime(LIB) < max(_mtime(o) for o in objs):
         cmd = [nvcc, *ARCH, "-shared", "-o", LIB, *objs]
         if verbose:

@@ -18,6 +18,8 @@
 //      code to the exact path -- advances v, a and writes the next drifted u.
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -283,19 +285,24 @@ int smem_bytes(int kind, int cap) {
 // the largest halo the layout admits (FAST_MAX_HALO), by the first launch or
 // by preload_fast() -- never inside a multi-GPU run.
 template <int MODE, int KIND, int TT, int MINB, bool PRE, int R> struct KernelCfg {
-    static bool done;
+    static std::atomic<bool> done[64];  // per device (slab ranks as threads)
     static cudaError_t ensure() {
-        if (done)
+        int dev = 0;
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e != cudaSuccess)
+            return e;
+        if (dev < 64 && done[dev].load(std::memory_order_acquire))
             return cudaSuccess;
-        const cudaError_t e = cudaFuncSetAttribute(fast_step_kernel<MODE, KIND, TT, MINB, PRE, R>,
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   smem_bytes(KIND, FAST_MAX_HALO + 1 + 31));
-        done = e == cudaSuccess;
+        e = cudaFuncSetAttribute(fast_step_kernel<MODE, KIND, TT, MINB, PRE, R>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem_bytes(KIND, FAST_MAX_HALO + 1 + 31));
+        if (e == cudaSuccess && dev < 64)
+            done[dev].store(true, std::memory_order_release);
         return e;
     }
 };
 template <int MODE, int KIND, int TT, int MINB, bool PRE, int R>
-bool KernelCfg<MODE, KIND, TT, MINB, PRE, R>::done = false;
+std::atomic<bool> KernelCfg<MODE, KIND, TT, MINB, PRE, R>::done[64];
 
 template <int MODE, int KIND, int TT, int MINB, bool PRE, int R = 2>
 cudaError_t launch_cfg(const DevArgs& A, const FastDev& F, int tiles, cudaStream_t st) {

@@ -26,6 +26,7 @@
 // takes the general tile layout (pd_fast.cu).
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -86,12 +87,12 @@ __device__ __forceinline__ float rcp_approx(float x) {
 }
 
 struct Acc {
-    float fx, fy, fz;
-    int kept;  // live slots that contributed (did not break)
+    float gx, gy, gz;  // sum over the current length class of c * s / (|c| |d|)
+    float fx, fy, fz;  // sum over finished classes (times |d|): the node's force / (c V)
+    float smax;        // largest stretch over the live breakable slots
 };
 
-// Shared by the unrolled slots (compile-time offsets) and the break pass
-// (runtime offsets), so both see bit-identical stretches.
+// The n-linear kernel's stretch (runtime offsets): s and 1/|xi + eta|.
 __device__ __forceinline__ void stretch(const float4& rj, const float4& ri, float dx, float dy,
                                         float dz, float r2, float len, float rr, float& s,
                                         float& rc, float& cx, float& cy, float& cz) {
@@ -109,17 +110,81 @@ __device__ __forceinline__ void stretch(const float4& rj, const float4& ri, floa
     s = num * rr * rcp_approx(fmaf(cur2, rc, len));
 }
 
+// The PMB kernel's stretch.  With w = |xi + eta|^2 |xi|^2 (one FMA from num),
+//   a = rsqrt(w) = 1 / (|d| |c|),   s = num / (|d| (|c| + |d|)) = num * rcp(w a + |d|^2)
+// so the 1/|d| of s and of the force direction cost no multiply; the caller
+// scales each length class's sum by |d| once.  Zero components of d add
+// nothing (a compile-time fold the compiler may not do: h + 0.0f != h for
+// h = -0.0f).  The unrolled slots (compile-time d) and the break pass
+// (runtime d, zero components added as +0) give bit-identical s: they differ
+// at most in the sign of a zero term, which cannot change the sum unless
+// num = +-0, and then s = +-0 tests the same against s_c.
+template <int DX, int DY, int DZ>
+__device__ __forceinline__ void stretch_c(const float4& rj, const float4& ri, float& s, float& a,
+                                          float& cx, float& cy, float& cz) {
+    constexpr int R2 = DX * DX + DY * DY + DZ * DZ;
+    const float2 hxy = __fadd2_rn(make_float2(rj.x, rj.y), make_float2(-ri.x, -ri.y));
+    const float hx = hxy.x, hy = hxy.y, hz = rj.z - ri.z;  // eta / spacing
+    cx = DX ? hx + float(DX) : hx;
+    cy = DY ? hy + float(DY) : hy;
+    cz = DZ ? hz + float(DZ) : hz;
+    float num = hz * (DZ ? hz + float(2 * DZ) : hz);
+    num = fmaf(hy, DY ? hy + float(2 * DY) : hy, num);
+    num = fmaf(hx, DX ? hx + float(2 * DX) : hx, num);
+    const float w = fmaf(num, float(R2), float(R2 * R2));
+    a = rsqrt_approx(w);
+    s = num * rcp_approx(fmaf(w, a, float(R2)));
+}
+
+__device__ __forceinline__ float stretch_r(const float4& rj, const float4& ri, int dx, int dy,
+                                           int dz, float& a) {
+    const int r2 = dx * dx + dy * dy + dz * dz;
+    const float2 hxy = __fadd2_rn(make_float2(rj.x, rj.y), make_float2(-ri.x, -ri.y));
+    const float hx = hxy.x, hy = hxy.y, hz = rj.z - ri.z;
+    float num = hz * (hz + float(2 * dz));
+    num = fmaf(hy, hy + float(2 * dy), num);
+    num = fmaf(hx, hx + float(2 * dx), num);
+    const float w = fmaf(num, float(r2), float(r2 * r2));
+    a = rsqrt_approx(w);
+    return num * rcp_approx(fmaf(w, a, float(r2)));
+}
+
+// Slots are evaluated grouped by length class |d|^2 (1, 2, 3, 4, 5, 6, 8, 9),
+// pattern order within a class; K is the position in that order.
+struct ClassOrder {
+    int slot[NPAT];   // K -> pattern slot
+    bool last[NPAT];  // K closes its length class
+};
+constexpr ClassOrder make_class_order() {
+    ClassOrder o{};
+    int r2s[NPAT] = {};
+    int k = 0;
+    for (int dz = -3; dz <= 3; ++dz)
+        for (int dy = -3; dy <= 3; ++dy)
+            for (int dx = -3; dx <= 3; ++dx) {
+                const int r2 = dx * dx + dy * dy + dz * dz;
+                if (r2 != 0 && r2 <= 9)
+                    r2s[k++] = r2;
+            }
+    k = 0;
+    for (int r2 = 1; r2 <= 9; ++r2)
+        for (int c = 0; c < NPAT; ++c)
+            if (r2s[c] == r2)
+                o.slot[k++] = c;
+    for (int q = 0; q < NPAT; ++q)
+        o.last[q] = q == NPAT - 1 || r2s[o.slot[q]] != r2s[o.slot[q + 1]];
+    return o;
+}
+constexpr ClassOrder kOrder = make_class_order();
+
 // NF (no-failure nodes and/or per-node volumes present): a record's w holds
 // V_j / V_0, negated for a no-failure node; the bond never breaks when either
 // end is no-failure (engine.cpp:79-80, 86-88: the node's own flag lifts s_c
 // to +inf) and its force carries V_j (engine.cpp:103).
-template <int C, bool NF>
-__device__ __forceinline__ void slot(const float4* own, const float4& ri, const uint4& m, float sc,
-                                     Acc& a) {
+template <int K, bool NF>
+__device__ __forceinline__ void slot(const float4* own, const float4& ri, const uint4& m, Acc& acc) {
+    constexpr int C = kOrder.slot[K];
     constexpr int dx = pat(C, 0), dy = pat(C, 1), dz = pat(C, 2);
-    constexpr int r2 = dx * dx + dy * dy + dz * dz;
-    constexpr float len = root(r2);
-    constexpr float rr = 1.0f / root(r2);
     constexpr int off = dx + HX * (dy + HY * dz);
     constexpr int word = C >> 5;
     constexpr unsigned bit = 1u << (C & 31);
@@ -127,69 +192,84 @@ __device__ __forceinline__ void slot(const float4* own, const float4& ri, const 
     // branch free: a dead slot's record may be anything finite (an
     // out-of-domain box record is 0); its contribution is predicated away
     const float4 rj = own[off];
-    float s, rc, cx, cy, cz;
-    stretch(rj, ri, float(dx), float(dy), float(dz), float(r2), len, rr, s, rc, cx, cy, cz);
+    float s, a, cx, cy, cz;
+    stretch_c<dx, dy, dz>(rj, ri, s, a, cx, cy, cz);
+    // Every live slot adds its force and raises smax; a live slot that
+    // breaks (s >= s_c, bond_contribution's PMB test, engine.cpp:90-98) makes
+    // smax >= s_c, and the node is then recomputed without its broken bonds
+    // (slow_node) -- so the common no-break slot has no break test at all.
     if (NF) {
-        const float scale = s * rc * fabsf(rj.w);
-        asm("{\n\t.reg .pred pa, pb, pc;\n\t"
-            "setp.lt.f32 pa, %5, %6;\n\t"
-            "setp.lt.or.f32 pb, %11, 0f00000000, pa;\n\t"
-            "setp.ne.and.u32 pc, %4, 0, pb;\n\t"
-            "@pc add.s32 %0, %0, 1;\n\t"
-            "@pc fma.rn.f32 %1, %7, %10, %1;\n\t"
-            "@pc fma.rn.f32 %2, %8, %10, %2;\n\t"
-            "@pc fma.rn.f32 %3, %9, %10, %3;\n\t}"
-            : "+r"(a.kept), "+f"(a.fx), "+f"(a.fy), "+f"(a.fz)
-            : "r"(mw & bit), "f"(s), "f"(sc), "f"(cx), "f"(cy), "f"(cz), "f"(scale), "f"(rj.w));
-        return;
+        // a no-failure neighbour's bond never breaks (rj.w < 0): no smax
+        const float scale = s * a * fabsf(rj.w);
+        asm("{\n\t.reg .pred pl, pb;\n\t"
+            "setp.ne.u32 pl, %4, 0;\n\t"
+            "setp.ge.and.f32 pb, %10, 0f00000000, pl;\n\t"
+            "@pb max.f32 %0, %0, %5;\n\t"
+            "@pl fma.rn.f32 %1, %6, %9, %1;\n\t"
+            "@pl fma.rn.f32 %2, %7, %9, %2;\n\t"
+            "@pl fma.rn.f32 %3, %8, %9, %3;\n\t}"
+            : "+f"(acc.smax), "+f"(acc.gx), "+f"(acc.gy), "+f"(acc.gz)
+            : "r"(mw & bit), "f"(s), "f"(cx), "f"(cy), "f"(cz), "f"(scale), "f"(rj.w));
+    } else {
+        const float scale = s * a;
+        asm("{\n\t.reg .pred pl;\n\t"
+            "setp.ne.u32 pl, %4, 0;\n\t"
+            "@pl max.f32 %0, %0, %5;\n\t"
+            "@pl fma.rn.f32 %1, %6, %9, %1;\n\t"
+            "@pl fma.rn.f32 %2, %7, %9, %2;\n\t"
+            "@pl fma.rn.f32 %3, %8, %9, %3;\n\t}"
+            : "+f"(acc.smax), "+f"(acc.gx), "+f"(acc.gy), "+f"(acc.gz)
+            : "r"(mw & bit), "f"(s), "f"(cx), "f"(cy), "f"(cz), "f"(scale));
     }
-    const float scale = s * rc;
-    // live and unbroken (s < s_c, bond_contribution's PMB test, engine.cpp:90-98):
-    // add the force and count the slot; a live slot that breaks is found later
-    asm("{\n\t.reg .pred pl, pc;\n\t"
-        "setp.ne.u32 pl, %4, 0;\n\t"
-        "setp.lt.and.f32 pc, %5, %6, pl;\n\t"
-        "@pc add.s32 %0, %0, 1;\n\t"
-        "@pc fma.rn.f32 %1, %7, %10, %1;\n\t"
-        "@pc fma.rn.f32 %2, %8, %10, %2;\n\t"
-        "@pc fma.rn.f32 %3, %9, %10, %3;\n\t}"
-        : "+r"(a.kept), "+f"(a.fx), "+f"(a.fy), "+f"(a.fz)
-        : "r"(mw & bit), "f"(s), "f"(sc), "f"(cx), "f"(cy), "f"(cz), "f"(scale));
+    if constexpr (kOrder.last[K]) {  // close the class: times |d|
+        constexpr float len = root(dx * dx + dy * dy + dz * dz);
+        acc.fx = fmaf(acc.gx, len, acc.fx);
+        acc.fy = fmaf(acc.gy, len, acc.fy);
+        acc.fz = fmaf(acc.gz, len, acc.fz);
+        acc.gx = acc.gy = acc.gz = 0.f;
+    }
 }
 
 __constant__ signed char c_pat[NPAT][4];  // dx, dy, dz, |d|^2
 __constant__ signed char c_slot[343];     // (dz+3)*49 + (dy+3)*7 + (dx+3) -> slot, -1 outside
+__constant__ float c_len[NPAT];           // |d|
 
-// The rare pass for a node that lost bonds this step: recompute each live
-// slot's stretch (same arithmetic) and return the broken bits.
-__device__ __noinline__ uint4 broken_bits(const float4* own, const float4& ri, const uint4& m,
-                                          float sc) {
+// The rare pass for a node that loses bonds this step: recompute each live
+// slot's stretch (the unrolled slots' arithmetic, so the same s), return the
+// broken bits and the force of the slots that stay.
+// (Inlined: a noinline call would pass m and ri through the stack, a local
+// store on every node.)
+template <bool NF>
+__device__ __forceinline__ uint4 slow_node(const float4* own, const float4 ri, const uint4 m,
+                                           float sc, float3& f) {
     unsigned w[4] = {m.x, m.y, m.z, m.w};
     unsigned dead[4] = {0u, 0u, 0u, 0u};
+    float fx = 0.f, fy = 0.f, fz = 0.f;
+#pragma unroll 1
     for (int c = 0; c < NPAT; ++c) {
         if (!((w[c >> 5] >> (c & 31)) & 1u))
             continue;
-        const int dx = c_pat[c][0], dy = c_pat[c][1], dz = c_pat[c][2], r2 = c_pat[c][3];
-        const float len = r2 == 1 ? root(1) : r2 == 2 ? root(2) : r2 == 3 ? root(3)
-                        : r2 == 4 ? root(4) : r2 == 5 ? root(5) : r2 == 6 ? root(6)
-                        : r2 == 8 ? root(8) : root(9);
-        const float rr = r2 == 1 ? 1.0f / root(1) : r2 == 2 ? 1.0f / root(2)
-                       : r2 == 3 ? 1.0f / root(3) : r2 == 4 ? 1.0f / root(4)
-                       : r2 == 5 ? 1.0f / root(5) : r2 == 6 ? 1.0f / root(6)
-                       : r2 == 8 ? 1.0f / root(8) : 1.0f / root(9);
+        const int dx = c_pat[c][0], dy = c_pat[c][1], dz = c_pat[c][2];
         const float4 rj = own[dx + HX * (dy + HY * dz)];
-        float s, rc, cx, cy, cz;
-        stretch(rj, ri, float(dx), float(dy), float(dz), float(r2), len, rr, s, rc, cx, cy, cz);
-        if (!(s < sc) && !(rj.w < 0.f))  // a no-failure neighbour keeps the bond
+        float a;
+        const float s = stretch_r(rj, ri, dx, dy, dz, a);
+        if (!(s < sc) && !(rj.w < 0.f)) {  // a no-failure neighbour keeps the bond
             dead[c >> 5] |= 1u << (c & 31);
+            continue;
+        }
+        const float scale = s * a * (NF ? fabsf(rj.w) : 1.f) * c_len[c];
+        fx = fmaf(rj.x - ri.x + float(dx), scale, fx);
+        fy = fmaf(rj.y - ri.y + float(dy), scale, fy);
+        fz = fmaf(rj.z - ri.z + float(dz), scale, fz);
     }
+    f = make_float3(fx, fy, fz);
     return make_uint4(dead[0], dead[1], dead[2], dead[3]);
 }
 
-template <bool NF, int... C>
-__device__ __forceinline__ void all_slots(std::integer_sequence<int, C...>, const float4* own,
-                                          const float4& ri, const uint4& m, float sc, Acc& a) {
-    (slot<C, NF>(own, ri, m, sc, a), ...);
+template <bool NF, int... K>
+__device__ __forceinline__ void all_slots(std::integer_sequence<int, K...>, const float4* own,
+                                          const float4& ri, const uint4& m, Acc& a) {
+    (slot<K, NF>(own, ri, m, a), ...);
 }
 
 // Stage the halo box of the brick at (gx0, gy0, gz0) plane by plane
@@ -205,7 +285,10 @@ __device__ __forceinline__ void stage_box(const DevArgs& A, const LatticeArgs& L
     {
         constexpr int PREC = HX * HY;          // records per box plane
         constexpr int PPASS = TT / PREC;       // planes per pass (1 or 2)
-        constexpr int PL = 2;                  // passes in flight
+#ifndef PD_LAT_PL
+#define PD_LAT_PL 2
+#endif
+        constexpr int PL = PD_LAT_PL;          // passes in flight
         const int t = threadIdx.x;
         const int q = t % PREC, pp = t / PREC;
         const int px = q % HX, py = q / HX;
@@ -283,13 +366,16 @@ __global__ void __launch_bounds__(BX * BY * BZT, MINB) lattice_step_kernel(DevAr
     const float4 ri = *own;
     // a no-failure node's own bonds never break
     const float sc = (NF && ri.w < 0.f) ? __int_as_float(0x7f800000) : L.sc;
-    Acc a{0.f, 0.f, 0.f, 0};
-    all_slots<NF>(std::make_integer_sequence<int, NPAT>{}, own, ri, m, sc, a);
-    const int live = __popc(m.x) + __popc(m.y) + __popc(m.z) + __popc(m.w);
-    if (a.kept != live) {
-        const uint4 d = broken_bits(own, ri, m, sc);
+    Acc a{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, -__int_as_float(0x7f800000)};
+    all_slots<NF>(std::make_integer_sequence<int, NPAT>{}, own, ri, m, a);
+    if (a.smax >= sc) {  // some live bond breaks this step
+        float3 f;
+        const uint4 d = slow_node<NF>(own, ri, m, sc, f);
         L.mask[i] = make_uint4(m.x & ~d.x, m.y & ~d.y, m.z & ~d.z, m.w & ~d.w);
-        A.n_neigh[i] -= live - a.kept;
+        A.n_neigh[i] -= __popc(d.x) + __popc(d.y) + __popc(d.z) + __popc(d.w);
+        a.fx = f.x;
+        a.fy = f.y;
+        a.fz = f.z;
     }
     const double fx = double(a.fx * L.cv), fy = double(a.fy * L.cv), fz = double(a.fz * L.cv);
 
@@ -560,14 +646,21 @@ template <class K> void preload_fn(K k) {
     cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(k));
 }
 
+// the dynamic shared-memory opt-in is per device: a process may drive
+// several GPUs (slab ranks as threads)
 template <int MODE, int BZT, int MINB, bool BC, bool NF> cudaError_t configure_one() {
-    static bool done = false;
-    if (done)
+    static std::atomic<bool> done[64];
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess)
+        return e;
+    if (dev < 64 && done[dev].load(std::memory_order_acquire))
         return cudaSuccess;
-    const cudaError_t e = cudaFuncSetAttribute(lattice_step_kernel<MODE, BZT, MINB, BC, NF>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               int(sizeof(float4)) * nrec<BZT>());
-    done = e == cudaSuccess;
+    e = cudaFuncSetAttribute(lattice_step_kernel<MODE, BZT, MINB, BC, NF>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(sizeof(float4)) * nrec<BZT>());
+    if (e == cudaSuccess && dev < 64)
+        done[dev].store(true, std::memory_order_release);
     return e;
 }
 
@@ -698,6 +791,11 @@ cudaError_t lattice_build_masks(const double4* xv, long long n, const int32_t* e
     cudaError_t e = cudaMemcpyToSymbolAsync(c_pat, tab, sizeof tab, 0, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess)
         e = cudaMemcpyToSymbolAsync(c_slot, slot_of, sizeof slot_of, 0, cudaMemcpyHostToDevice, st);
+    float lens[NPAT];
+    for (int c = 0; c < NPAT; ++c)
+        lens[c] = root(int(tab[c][3]));
+    if (e == cudaSuccess)
+        e = cudaMemcpyToSymbolAsync(c_len, lens, sizeof lens, 0, cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess)
         return e;
     {

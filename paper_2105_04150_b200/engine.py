@@ -20,7 +20,8 @@ from .types import (ForceField, IntegratorKind, KernelVariant, ModelBundle, Simu
                     SimulateResult, SimulationState, TipRecord, WriteHook)
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libpd_b200.so")
+# PD_B200_LIB: an alternative build of the same library (kernel experiments)
+LIB_PATH = os.environ.get("PD_B200_LIB") or os.path.join(_PKG, "libpd_b200.so")
 
 
 class Backend:

@@ -199,7 +199,8 @@ def run_reference_arm(args):
 def _summary(args, value, ms_step, world, n, N, live, bytes_step, achieved, e2e, launches,
              clocks, cpu, variant_name, extra_config=None, layout=None):
     peak, peak_kind = measured_peaks()
-    traffic = (measured_traffic(f"{layout}_{args.size}_{variant_name}")
+    law_key = "" if getattr(args, "law", "pmb") == "pmb" else f"_{args.law}"
+    traffic = (measured_traffic(f"{layout}_{args.size}_{variant_name}{law_key}")
                if world == 1 and layout else None)
     law = ("PMB c=1 s_c=1e6" if getattr(args, "law", "pmb") == "pmb"
            else "trilinear(1, 1e-3, 2e-3, 1e6) with history")

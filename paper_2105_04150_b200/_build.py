@@ -29,11 +29,15 @@ UNITS = {
     "pd_fast.cu": ["-fmad=true", "-diag-suppress=186"],
     "pd_family.cu": ["-fmad=false"],
     "pd_layout.cu": ["-fmad=false"],
-    "pd_lattice.cu": ["-fmad=true"],
+    "pd_lattice.cu": ["-fmad=true", "-diag-suppress=177"],
+    "pd_lattice_nlu0.cu": ["-fmad=true", "-diag-suppress=177"],
+    "pd_lattice_nlu1.cu": ["-fmad=true", "-diag-suppress=177"],
+    "pd_lattice_nlu2.cu": ["-fmad=true", "-diag-suppress=177"],
+    "pd_lattice_nlu3.cu": ["-fmad=true", "-diag-suppress=177"],
     "pd_xfer.cpp": ["-x", "cu"],
     "pd_io.cpp": ["-x", "cu"],
 }
-HEADERS = ["pd_device.cuh", "pd_internal.h", "pd_fast.cuh"]
+HEADERS = ["pd_device.cuh", "pd_internal.h", "pd_fast.cuh", "pd_lattice.cuh", "pd_lattice_nlu.cuh"]
 
 
 def _nvcc() -> str:

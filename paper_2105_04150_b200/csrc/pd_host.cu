@@ -684,7 +684,7 @@ int try_lattice(pd_ctx* ctx, const pd_particles& p, const pd_state& st, const pd
     PD_CK(ctx->lmask.alloc(size_t(n)));
     L.n_local = n;
     L.nl = nl ? 1 : 0;
-    const size_t pslots = size_t(122) * size_t(n);
+    const size_t pslots = size_t(lattice_slot_count(L));
     if (nl && ctx->history) {
         PD_CK(ctx->lhist.alloc(pslots));
         PD_CK(cudaMemsetAsync(ctx->lhist.p, 0, sizeof(float) * pslots, s));
@@ -738,6 +738,8 @@ int try_lattice(pd_ctx* ctx, const pd_particles& p, const pd_state& st, const pd
     L.mask = ctx->lmask.p;
     if (const char* e = std::getenv("PD_LAT_CFG"))
         L.cfg = std::atoi(e);
+    if (const char* e = std::getenv("PD_NLU_PF"))
+        L.prefetch = std::atoi(e);
     ctx->lat = L;
     ctx->lattice = true;
     ctx->fast = true;

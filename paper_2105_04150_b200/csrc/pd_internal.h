@@ -131,6 +131,9 @@ void preload_fast();
 struct NlRegLaw {  // one n-linear law of <= 3 breakpoints, fp32 (pd_lattice.cu)
     float c = 0.f, sc = 0.f, bp0 = 0.f, bp1 = 0.f, f0 = 0.f, f1 = 0.f;
     float sl0 = 0.f, sl1 = 0.f, sl2 = 0.f;
+    float a1 = 0.f, a2 = 0.f;  // segment k as a_k + sl_k s (a_0 = 0), from fp64 on the host
+    int cvx1 = 0, cvx2 = 0;    // kink k convex (slope rises): the envelope takes max there
+    int nbp = 1;
     int hist = 0;
 };
 struct LatticeArgs {
@@ -144,7 +147,8 @@ struct LatticeArgs {
     int vol_varies = 0;                // volumes differ (records carry V_j / V_0)
     double inv_v0 = 1.0;               // 1 / V_0 (node 0's volume)
     uint4* mask = nullptr;             // per node: live bonds over the 122-offset pattern
-    // NL (n-linear laws / bond types / lambda / beta): slot-major [c][node] arrays
+    // NL (n-linear laws / bond types / lambda / beta): brick-major slot arrays
+    // (pd_lattice.cu slot_base)
     int nl = 0;
     long long n_local = 0;
     float* hist = nullptr;
@@ -152,6 +156,8 @@ struct LatticeArgs {
     float* lam = nullptr;  // lambda * beta (either may be absent)
     int multi = 1;   // per-bond laws from constant memory; else the register law rl
     NlRegLaw rl;
+    signed char pat[128][4];  // the offset pattern (dx, dy, dz, |d|^2): the rare slow paths
+    int prefetch = 0;         // NL: bulk L2 prefetch of a brick's per-bond streams (PD_NLU_PF=1; measured slower than the per-slot prefetch)
 };
 bool lattice_detect(const double* coords, long long n, long long own_begin, long long own_end,
                     LatticeArgs& L);
@@ -160,11 +166,21 @@ cudaError_t lattice_build_masks(const double4* xv, long long n, const int32_t* e
                                 uint4* mask, int* bad, const double* hist, const uint8_t* btype,
                                 const double* lambda, const double* beta, cudaStream_t st);
 void lattice_set_laws(const DevLaw* laws, int n, LatticeArgs& L, cudaStream_t st);
+long long lattice_slot_count(const LatticeArgs& L);  // length of the brick-major slot arrays
 cudaError_t launch_lattice(const DevArgs& A, const LatticeArgs& L, int mode, cudaStream_t st);
 cudaError_t launch_lattice_materialize(const int32_t* entries0, const uint4* mask, long long begin,
                                        long long end, long long n, int N, const LatticeArgs& L,
                                        int32_t* out, double* hist_out, cudaStream_t st);
 void preload_lattice();
+// pd_lattice_nlu<M>.cu: the unrolled n-linear kernel per integrator mode
+cudaError_t launch_nlu_m0(const DevArgs& A, const LatticeArgs& L, cudaStream_t st);
+cudaError_t launch_nlu_m1(const DevArgs& A, const LatticeArgs& L, cudaStream_t st);
+cudaError_t launch_nlu_m2(const DevArgs& A, const LatticeArgs& L, cudaStream_t st);
+cudaError_t launch_nlu_m3(const DevArgs& A, const LatticeArgs& L, cudaStream_t st);
+void preload_nlu_m0();
+void preload_nlu_m1();
+void preload_nlu_m2();
+void preload_nlu_m3();
 
 // pd_exact.cu
 void exact_set_laws(const DevLaw* laws, int n, cudaStream_t stream);

@@ -28,6 +28,7 @@
 
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <utility>
@@ -35,147 +36,16 @@
 #include "pd_device.cuh"
 #include "pd_fast.cuh"
 #include "pd_internal.h"
+#include "pd_lattice.cuh"
 
 namespace pdb {
 
 namespace {
-
-// brick = 16 x 4 x BZT nodes (one thread each); halo box HX x HY x (BZT + 6)
-constexpr int BX = 16, BY = 4;
-constexpr int HX = BX + 6, HY = BY + 6;
-constexpr int NPAT = 122;
-template <int BZT> constexpr int nrec() { return HX * HY * (BZT + 6); }
-
-// offset c of the pattern, components 0/1/2 = dx/dy/dz, in (dz, dy, dx)
-// lexicographic order = ascending reference index order of a row
-__host__ __device__ constexpr int pat(int c, int which) {
-    int k = 0;
-    for (int dz = -3; dz <= 3; ++dz)
-        for (int dy = -3; dy <= 3; ++dy)
-            for (int dx = -3; dx <= 3; ++dx) {
-                const int r2 = dx * dx + dy * dy + dz * dz;
-                if (r2 == 0 || r2 > 9)
-                    continue;
-                if (k == c)
-                    return which == 0 ? dx : (which == 1 ? dy : dz);
-                ++k;
-            }
-    return 0;
-}
-
-__host__ __device__ constexpr float root(int r2) {
-    return r2 == 1 ? 1.0f
-         : r2 == 2 ? 1.41421356237f
-         : r2 == 3 ? 1.73205080757f
-         : r2 == 4 ? 2.0f
-         : r2 == 5 ? 2.2360679775f
-         : r2 == 6 ? 2.44948974278f
-         : r2 == 8 ? 2.82842712475f
-         : 3.0f;
-}
-
-__device__ __forceinline__ float rsqrt_approx(float x) {
-    float y;
-    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-
-__device__ __forceinline__ float rcp_approx(float x) {
-    float y;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-
 struct Acc {
     float gx, gy, gz;  // sum over the current length class of c * s / (|c| |d|)
     float fx, fy, fz;  // sum over finished classes (times |d|): the node's force / (c V)
     float smax;        // largest stretch over the live breakable slots
 };
-
-// The n-linear kernel's stretch (runtime offsets): s and 1/|xi + eta|.
-__device__ __forceinline__ void stretch(const float4& rj, const float4& ri, float dx, float dy,
-                                        float dz, float r2, float len, float rr, float& s,
-                                        float& rc, float& cx, float& cy, float& cz) {
-    const float2 hxy = __fadd2_rn(make_float2(rj.x, rj.y), make_float2(-ri.x, -ri.y));
-    const float hx = hxy.x, hy = hxy.y, hz = rj.z - ri.z;  // eta / spacing
-    cx = hx + dx;
-    cy = hy + dy;
-    cz = hz + dz;
-    // eta.(2 xi + eta), cancellation free
-    float num = hz * (hz + (dz + dz));
-    num = fmaf(hy, hy + (dy + dy), num);
-    num = fmaf(hx, hx + (dx + dx), num);
-    const float cur2 = num + r2;
-    rc = rsqrt_approx(cur2);
-    s = num * rr * rcp_approx(fmaf(cur2, rc, len));
-}
-
-// The PMB kernel's stretch.  With w = |xi + eta|^2 |xi|^2 (one FMA from num),
-//   a = rsqrt(w) = 1 / (|d| |c|),   s = num / (|d| (|c| + |d|)) = num * rcp(w a + |d|^2)
-// so the 1/|d| of s and of the force direction cost no multiply; the caller
-// scales each length class's sum by |d| once.  Zero components of d add
-// nothing (a compile-time fold the compiler may not do: h + 0.0f != h for
-// h = -0.0f).  The unrolled slots (compile-time d) and the break pass
-// (runtime d, zero components added as +0) give bit-identical s: they differ
-// at most in the sign of a zero term, which cannot change the sum unless
-// num = +-0, and then s = +-0 tests the same against s_c.
-template <int DX, int DY, int DZ>
-__device__ __forceinline__ void stretch_c(const float4& rj, const float4& ri, float& s, float& a,
-                                          float& cx, float& cy, float& cz) {
-    constexpr int R2 = DX * DX + DY * DY + DZ * DZ;
-    const float2 hxy = __fadd2_rn(make_float2(rj.x, rj.y), make_float2(-ri.x, -ri.y));
-    const float hx = hxy.x, hy = hxy.y, hz = rj.z - ri.z;  // eta / spacing
-    cx = DX ? hx + float(DX) : hx;
-    cy = DY ? hy + float(DY) : hy;
-    cz = DZ ? hz + float(DZ) : hz;
-    float num = hz * (DZ ? hz + float(2 * DZ) : hz);
-    num = fmaf(hy, DY ? hy + float(2 * DY) : hy, num);
-    num = fmaf(hx, DX ? hx + float(2 * DX) : hx, num);
-    const float w = fmaf(num, float(R2), float(R2 * R2));
-    a = rsqrt_approx(w);
-    s = num * rcp_approx(fmaf(w, a, float(R2)));
-}
-
-__device__ __forceinline__ float stretch_r(const float4& rj, const float4& ri, int dx, int dy,
-                                           int dz, float& a) {
-    const int r2 = dx * dx + dy * dy + dz * dz;
-    const float2 hxy = __fadd2_rn(make_float2(rj.x, rj.y), make_float2(-ri.x, -ri.y));
-    const float hx = hxy.x, hy = hxy.y, hz = rj.z - ri.z;
-    float num = hz * (hz + float(2 * dz));
-    num = fmaf(hy, hy + float(2 * dy), num);
-    num = fmaf(hx, hx + float(2 * dx), num);
-    const float w = fmaf(num, float(r2), float(r2 * r2));
-    a = rsqrt_approx(w);
-    return num * rcp_approx(fmaf(w, a, float(r2)));
-}
-
-// Slots are evaluated grouped by length class |d|^2 (1, 2, 3, 4, 5, 6, 8, 9),
-// pattern order within a class; K is the position in that order.
-struct ClassOrder {
-    int slot[NPAT];   // K -> pattern slot
-    bool last[NPAT];  // K closes its length class
-};
-constexpr ClassOrder make_class_order() {
-    ClassOrder o{};
-    int r2s[NPAT] = {};
-    int k = 0;
-    for (int dz = -3; dz <= 3; ++dz)
-        for (int dy = -3; dy <= 3; ++dy)
-            for (int dx = -3; dx <= 3; ++dx) {
-                const int r2 = dx * dx + dy * dy + dz * dz;
-                if (r2 != 0 && r2 <= 9)
-                    r2s[k++] = r2;
-            }
-    k = 0;
-    for (int r2 = 1; r2 <= 9; ++r2)
-        for (int c = 0; c < NPAT; ++c)
-            if (r2s[c] == r2)
-                o.slot[k++] = c;
-    for (int q = 0; q < NPAT; ++q)
-        o.last[q] = q == NPAT - 1 || r2s[o.slot[q]] != r2s[o.slot[q + 1]];
-    return o;
-}
-constexpr ClassOrder kOrder = make_class_order();
 
 // NF (no-failure nodes and/or per-node volumes present): a record's w holds
 // V_j / V_0, negated for a no-failure node; the bond never breaks when either
@@ -234,6 +104,7 @@ __constant__ signed char c_pat[NPAT][4];  // dx, dy, dz, |d|^2
 __constant__ signed char c_slot[343];     // (dz+3)*49 + (dy+3)*7 + (dx+3) -> slot, -1 outside
 __constant__ float c_len[NPAT];           // |d|
 
+
 // The rare pass for a node that loses bonds this step: recompute each live
 // slot's stretch (the unrolled slots' arithmetic, so the same s), return the
 // broken bits and the force of the slots that stay.
@@ -272,70 +143,6 @@ __device__ __forceinline__ void all_slots(std::integer_sequence<int, K...>, cons
     (slot<K, NF>(own, ri, m, a), ...);
 }
 
-// Stage the halo box of the brick at (gx0, gy0, gz0) plane by plane
-// (HX x HY = 220 records; thread t owns record t % 220 of plane t / 220 of
-// each pass): fp32 (u - U_brick) / spacing, plus for NF the signed V_j / V_0.
-// Planes are loaded PL at a time so several L2/HBM round trips are in flight.
-template <int BZT, bool NF>
-__device__ __forceinline__ void stage_box(const DevArgs& A, const LatticeArgs& L, float4* rec,
-                                          int gx0, int gy0, int gz0, const double4& U0) {
-    constexpr int TT = BX * BY * BZT, HZ = BZT + 6;
-    const long long plane = (long long)L.nx * L.ny;
-    const float ih = float(L.inv_h);
-    {
-        constexpr int PREC = HX * HY;          // records per box plane
-        constexpr int PPASS = TT / PREC;       // planes per pass (1 or 2)
-#ifndef PD_LAT_PL
-#define PD_LAT_PL 2
-#endif
-        constexpr int PL = PD_LAT_PL;          // passes in flight
-        const int t = threadIdx.x;
-        const int q = t % PREC, pp = t / PREC;
-        const int px = q % HX, py = q / HX;
-        const int X = gx0 - 3 + px, Y = gy0 - 3 + py;
-        const bool xy_ok = pp < PPASS && X >= 0 && X < L.nx && Y >= 0 && Y < L.ny;
-        const double4* src = A.u_in + (X + (long long)L.nx * Y);
-        float4* dst = rec + q + PREC * pp;
-        for (int pz0 = 0; pz0 < HZ; pz0 += PPASS * PL) {
-            double ux[PL], uy[PL], uz[PL];
-            float wv[PL];
-            bool ok[PL];
-#pragma unroll
-            for (int k = 0; k < PL; ++k) {
-                const int pz = pz0 + pp + PPASS * k;
-                const int Z = gz0 - 3 + pz;
-                ok[k] = xy_ok && pz < HZ && Z >= 0 && Z < L.nz_local;
-                ux[k] = uy[k] = uz[k] = 0.0;
-                wv[k] = 0.f;
-                if (ok[k]) {
-                    const double4* pu = src + plane * Z;
-                    const double2 xy = *reinterpret_cast<const double2*>(pu);
-                    ux[k] = xy.x;
-                    uy[k] = xy.y;
-                    if (NF) {
-                        const double2 zw = reinterpret_cast<const double2*>(pu)[1];
-                        uz[k] = zw.x;
-                        // V_j / V_0 (1 with uniform volumes), negative for a no-failure node
-                        const float vf =
-                            L.vol_varies ? float(A.xv[(pu - A.u_in)].w * L.inv_v0) : 1.f;
-                        wv[k] = zw.y != 0.0 ? -vf : vf;
-                    } else {
-                        uz[k] = reinterpret_cast<const double*>(pu)[2];
-                    }
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < PL; ++k) {
-                const int pz = pz0 + pp + PPASS * k;
-                if (pp < PPASS && pz < HZ)
-                    dst[PREC * (pz - pp)] =
-                        ok[k] ? make_float4(float(ux[k] - U0.x) * ih, float(uy[k] - U0.y) * ih,
-                                            float(uz[k] - U0.z) * ih, wv[k])
-                              : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-        }
-    }
-}
 
 template <int MODE, int BZT, int MINB, bool BC, bool NF>
 __global__ void __launch_bounds__(BX * BY * BZT, MINB) lattice_step_kernel(DevArgs A,
@@ -440,7 +247,8 @@ __global__ void __launch_bounds__(BX * BY * 4, 4) lattice_nl_kernel(DevArgs A, L
     const float4* own = rec + (tx + 3) + HX * ((ty + 3) + HY * (tz + 3));
     const float4 ri = *own;
     const bool nfi = ri.w < 0.f;
-    const long long n = L.n_local;
+    const long long sb = (blockIdx.x + (long long)gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)) *
+                             kBrickSlots + threadIdx.x;  // == slot_base(L, i)
     const NlRegLaw R = L.rl;
     float fx = 0.f, fy = 0.f, fz = 0.f;
     unsigned d0 = 0u, d1 = 0u, d2 = 0u, d3 = 0u;
@@ -448,32 +256,32 @@ __global__ void __launch_bounds__(BX * BY * 4, 4) lattice_nl_kernel(DevArgs A, L
     // history loads are issued before the current group is evaluated so the
     // history stream keeps several loads in flight per thread
     constexpr int G = 8;
-    float* hp = L.hist ? L.hist + i : nullptr;  // slot c at hp[c * n]
+    float* hp = L.hist ? L.hist + sb : nullptr;  // slot c at hp[c * NLB]
     float hnext[G];
 #pragma unroll
     for (int q = 0; q < G; ++q)
-        hnext[q] = hp ? hp[q * n] : 0.f;
+        hnext[q] = hp ? hp[q * NLB] : 0.f;
 #pragma unroll 1
     for (int c0 = 0; c0 < NPAT; c0 += G) {
         float hcur[G];
 #pragma unroll
         for (int q = 0; q < G; ++q) {
             hcur[q] = hnext[q];
-            hnext[q] = (hp && c0 + G + q < NPAT) ? hp[(c0 + G + q) * n] : 0.f;
+            hnext[q] = (hp && c0 + G + q < NPAT) ? hp[(c0 + G + q) * NLB] : 0.f;
         }
         const int word = c0 >> 5;
         const unsigned mword = word == 0 ? m.x : (word == 1 ? m.y : (word == 2 ? m.z : m.w));
         const unsigned mw8 = (mword >> (c0 & 31)) & 0xffu;
         if (mw8 == 0u)
             continue;
-        const long long sbase = (long long)c0 * n + i;
+        const long long sbase = (long long)c0 * NLB + sb;
         float lam[G];  // lambda * beta
         int bt[G];
 #pragma unroll
         for (int q = 0; q < G; ++q) {
             const bool ok = ((mw8 >> q) & 1u) != 0u;
-            lam[q] = (L.lam && ok) ? L.lam[sbase + q * n] : 1.f;
-            bt[q] = (MULTI && L.btype && ok) ? int(L.btype[sbase + q * n]) : 0;
+            lam[q] = (L.lam && ok) ? L.lam[sbase + q * NLB] : 1.f;
+            bt[q] = (MULTI && L.btype && ok) ? int(L.btype[sbase + q * NLB]) : 0;
         }
         unsigned dg = 0u;
 #pragma unroll
@@ -498,7 +306,7 @@ __global__ void __launch_bounds__(BX * BY * 4, 4) lattice_nl_kernel(DevArgs A, L
                 } else {
                     const float s_c = law.bp[law.nbp - 1];
                     if (s > hh)
-                        hp[(c0 + q) * n] = s;  // history before the break test (engine.cpp:88-92)
+                        hp[(c0 + q) * NLB] = s;  // history before the break test (engine.cpp:88-92)
                     brk = hh >= s_c || s >= s_c;
                     f = (s >= hh) ? fast_envelope(law, s)
                                   : (hh < law.bp[0] ? law.sl[0] : fast_envelope(law, hh) * rcp_approx(hh)) * s;
@@ -511,7 +319,7 @@ __global__ void __launch_bounds__(BX * BY * 4, 4) lattice_nl_kernel(DevArgs A, L
                     f = R.c * s;
                 } else {
                     if (s > hh)
-                        hp[(c0 + q) * n] = s;
+                        hp[(c0 + q) * NLB] = s;
                     const float e = fmaxf(s, hh);
                     brk = e >= R.sc;
                     const float env = reg_envelope(R, e);
@@ -598,7 +406,7 @@ __global__ void lattice_mask_kernel(const int32_t* entries, long long begin, lon
             return;
         }
         w[c >> 5] |= 1u << (c & 31);
-        const long long sidx = (long long)c * L.n_local + i, idx = i * N + k;
+        const long long sidx = slot_base(L, i) + (long long)c * NLB, idx = i * N + k;
         if (L.hist && src.hist)
             L.hist[sidx] = float(src.hist[idx]);
         if (L.btype)
@@ -614,8 +422,9 @@ __global__ void lattice_mask_kernel(const int32_t* entries, long long begin, lon
 // of the slot's offset is clear
 __global__ void lattice_materialize_kernel(const int32_t* entries0, const uint4* mask,
                                            long long begin, long long end, long long n, int N,
-                                           int nx, int ny, int32_t* out, const float* hist,
-                                           double* hist_out) {
+                                           LatticeArgs L, int32_t* out, double* hist_out) {
+    const int nx = L.nx, ny = L.ny;
+    const float* hist = L.hist;
     const long long i = blockIdx.x * 256LL + threadIdx.x;
     if (i >= n)
         return;
@@ -634,7 +443,7 @@ __global__ void lattice_materialize_kernel(const int32_t* entries0, const uint4*
             if (!((w[c >> 5] >> (c & 31)) & 1u))
                 v = -1;
             if (hist_out)  // broken bonds keep their last history (engine.cpp:88-92)
-                hist_out[i * N + k] = double(hist[(long long)c * n + i]);
+                hist_out[i * N + k] = double(hist[slot_base(L, i) + (long long)c * NLB]);
         }
         if (out)
             out[i * N + k] = v;
@@ -732,6 +541,11 @@ template <int MODE> void preload_mode() {
 
 } // namespace
 
+long long lattice_slot_count(const LatticeArgs& L) {
+    const long long nbx = (L.nx + 15) / 16, nby = (L.ny + 3) / 4, nbz = (L.nz_own + 3) / 4;
+    return nbx * nby * nbz * kBrickSlots;
+}
+
 bool lattice_detect(const double* coords, long long n, long long own_begin, long long own_end,
                     LatticeArgs& L) {
     if (n < 2)
@@ -756,6 +570,12 @@ bool lattice_detect(const double* coords, long long n, long long own_begin, long
     // (lattice_build_masks), together with the rows
     if (own_begin % plane != 0 || own_end % plane != 0)
         return false;  // owned range of a slab: whole planes
+    for (int c = 0; c < NPAT; ++c) {
+        L.pat[c][0] = (signed char)pat(c, 0);
+        L.pat[c][1] = (signed char)pat(c, 1);
+        L.pat[c][2] = (signed char)pat(c, 2);
+        L.pat[c][3] = (signed char)(pat(c, 0) * pat(c, 0) + pat(c, 1) * pat(c, 1) + pat(c, 2) * pat(c, 2));
+    }
     L.nx = int(nx);
     L.ny = int(ny);
     L.nz_local = int(nz);
@@ -835,10 +655,13 @@ cudaError_t launch_nl(const DevArgs& A, const LatticeArgs& L, cudaStream_t st) {
         return cudaSuccess;
     const dim3 grid{unsigned(nbx), unsigned(nby), unsigned(nbz)};
     const size_t smem = sizeof(float4) * nrec<4>();
-    if (L.multi)
+    if (L.multi || std::getenv("PD_LAT_NL_LOOP"))  // PD_LAT_NL_LOOP: the loop kernel
         lattice_nl_kernel<MODE, BC, true><<<grid, BX * BY * 4, smem, st>>>(A, L);
     else
-        lattice_nl_kernel<MODE, BC, false><<<grid, BX * BY * 4, smem, st>>>(A, L);
+        return MODE == 0   ? launch_nlu_m0(A, L, st)
+               : MODE == 1 ? launch_nlu_m1(A, L, st)
+               : MODE == 2 ? launch_nlu_m2(A, L, st)
+                           : launch_nlu_m3(A, L, st);
     return cudaGetLastError();
 }
 
@@ -869,7 +692,7 @@ cudaError_t launch_lattice_materialize(const int32_t* entries0, const uint4* mas
                                        int32_t* out, double* hist_out, cudaStream_t st) {
     if (n > 0)
         lattice_materialize_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(
-            entries0, mask, begin, end, n, N, L.nx, L.ny, out, L.hist, hist_out);
+            entries0, mask, begin, end, n, N, L, out, hist_out);
     return cudaGetLastError();
 }
 
@@ -892,16 +715,34 @@ void lattice_set_laws(const DevLaw* laws, int n, LatticeArgs& L, cudaStream_t st
     L.rl.sl0 = a.sl[0];
     L.rl.sl1 = a.nbp > 1 ? a.sl[1] : 0.f;
     L.rl.sl2 = a.nbp > 2 ? a.sl[2] : 0.f;
+    L.rl.nbp = a.nbp;
+    if (n >= 1 && laws[0].nbp >= 2) {  // a_k = f_{k-1} - bp_{k-1} sl_k in fp64
+        const DevLaw& d = laws[0];
+        const double sl0 = d.f[0] / d.bp[0];
+        const double sl1 = (d.f[1] - d.f[0]) / (d.bp[1] - d.bp[0]);
+        L.rl.a1 = float(d.f[0] - d.bp[0] * sl1);
+        L.rl.cvx1 = sl1 > sl0;
+        if (d.nbp >= 3) {
+            const double sl2 = (d.f[2] - d.f[1]) / (d.bp[2] - d.bp[1]);
+            L.rl.a2 = float(d.f[1] - d.bp[1] * sl2);
+            L.rl.cvx2 = sl2 > sl1;
+        } else {  // two breakpoints: the third segment repeats the second
+            L.rl.a2 = L.rl.a1;
+            L.rl.sl2 = L.rl.sl1;
+        }
+    }
 }
 
 template <int MODE> void preload_nl() {
     preload_fn(lattice_nl_kernel<MODE, true, true>);
     preload_fn(lattice_nl_kernel<MODE, false, true>);
-    preload_fn(lattice_nl_kernel<MODE, true, false>);
-    preload_fn(lattice_nl_kernel<MODE, false, false>);
 }
 
 void preload_lattice() {
+    preload_nlu_m0();
+    preload_nlu_m1();
+    preload_nlu_m2();
+    preload_nlu_m3();
     preload_nl<0>();
     preload_nl<1>();
     preload_nl<2>();

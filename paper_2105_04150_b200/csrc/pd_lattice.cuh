@@ -1,0 +1,230 @@
+// pd_lattice.cuh -- device helpers shared by the lattice kernels (pd_lattice.cu
+// and the per-integrator pd_lattice_nlu*.cu units): the 122-offset neighbour
+// pattern, the fp32 stretch arithmetic, the length-class slot order, the
+// brick-major per-bond layout and the halo staging.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <utility>
+
+#include "pd_device.cuh"
+#include "pd_fast.cuh"
+#include "pd_internal.h"
+
+namespace pdb {
+namespace {
+
+// brick = 16 x 4 x BZT nodes (one thread each); halo box HX x HY x (BZT + 6)
+constexpr int BX = 16, BY = 4;
+constexpr int HX = BX + 6, HY = BY + 6;
+constexpr int NPAT = 122;
+template <int BZT> constexpr int nrec() { return HX * HY * (BZT + 6); }
+
+// offset c of the pattern, components 0/1/2 = dx/dy/dz, in (dz, dy, dx)
+// lexicographic order = ascending reference index order of a row
+__host__ __device__ constexpr int pat(int c, int which) {
+    int k = 0;
+    for (int dz = -3; dz <= 3; ++dz)
+        for (int dy = -3; dy <= 3; ++dy)
+            for (int dx = -3; dx <= 3; ++dx) {
+                const int r2 = dx * dx + dy * dy + dz * dz;
+                if (r2 == 0 || r2 > 9)
+                    continue;
+                if (k == c)
+                    return which == 0 ? dx : (which == 1 ? dy : dz);
+                ++k;
+            }
+    return 0;
+}
+
+__host__ __device__ constexpr float root(int r2) {
+    return r2 == 1 ? 1.0f
+         : r2 == 2 ? 1.41421356237f
+         : r2 == 3 ? 1.73205080757f
+         : r2 == 4 ? 2.0f
+         : r2 == 5 ? 2.2360679775f
+         : r2 == 6 ? 2.44948974278f
+         : r2 == 8 ? 2.82842712475f
+         : 3.0f;
+}
+
+__device__ __forceinline__ float rsqrt_approx(float x) {
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+
+// The n-linear kernel's stretch (runtime offsets): s and 1/|xi + eta|.
+__device__ __forceinline__ void stretch(const float4& rj, const float4& ri, float dx, float dy,
+                                        float dz, float r2, float len, float rr, float& s,
+                                        float& rc, float& cx, float& cy, float& cz) {
+    const float2 hxy = __fadd2_rn(make_float2(rj.x, rj.y), make_float2(-ri.x, -ri.y));
+    const float hx = hxy.x, hy = hxy.y, hz = rj.z - ri.z;  // eta / spacing
+    cx = hx + dx;
+    cy = hy + dy;
+    cz = hz + dz;
+    // eta.(2 xi + eta), cancellation free
+    float num = hz * (hz + (dz + dz));
+    num = fmaf(hy, hy + (dy + dy), num);
+    num = fmaf(hx, hx + (dx + dx), num);
+    const float cur2 = num + r2;
+    rc = rsqrt_approx(cur2);
+    s = num * rr * rcp_approx(fmaf(cur2, rc, len));
+}
+
+// The PMB kernel's stretch.  With w = |xi + eta|^2 |xi|^2 (one FMA from num),
+//   a = rsqrt(w) = 1 / (|d| |c|),   s = num / (|d| (|c| + |d|)) = num * rcp(w a + |d|^2)
+// so the 1/|d| of s and of the force direction cost no multiply; the caller
+// scales each length class's sum by |d| once.  Zero components of d add
+// nothing (a compile-time fold the compiler may not do: h + 0.0f != h for
+// h = -0.0f).  The unrolled slots (compile-time d) and the break pass
+// (runtime d, zero components added as +0) give bit-identical s: they differ
+// at most in the sign of a zero term, which cannot change the sum unless
+// num = +-0, and then s = +-0 tests the same against s_c.
+template <int DX, int DY, int DZ>
+__device__ __forceinline__ void stretch_c(const float4& rj, const float4& ri, float& s, float& a,
+                                          float& cx, float& cy, float& cz) {
+    constexpr int R2 = DX * DX + DY * DY + DZ * DZ;
+    const float2 hxy = __fadd2_rn(make_float2(rj.x, rj.y), make_float2(-ri.x, -ri.y));
+    const float hx = hxy.x, hy = hxy.y, hz = rj.z - ri.z;  // eta / spacing
+    cx = DX ? hx + float(DX) : hx;
+    cy = DY ? hy + float(DY) : hy;
+    cz = DZ ? hz + float(DZ) : hz;
+    float num = hz * (DZ ? hz + float(2 * DZ) : hz);
+    num = fmaf(hy, DY ? hy + float(2 * DY) : hy, num);
+    num = fmaf(hx, DX ? hx + float(2 * DX) : hx, num);
+    const float w = fmaf(num, float(R2), float(R2 * R2));
+    a = rsqrt_approx(w);
+    s = num * rcp_approx(fmaf(w, a, float(R2)));
+}
+
+__device__ __forceinline__ float stretch_r(const float4& rj, const float4& ri, int dx, int dy,
+                                           int dz, float& a) {
+    const int r2 = dx * dx + dy * dy + dz * dz;
+    const float2 hxy = __fadd2_rn(make_float2(rj.x, rj.y), make_float2(-ri.x, -ri.y));
+    const float hx = hxy.x, hy = hxy.y, hz = rj.z - ri.z;
+    float num = hz * (hz + float(2 * dz));
+    num = fmaf(hy, hy + float(2 * dy), num);
+    num = fmaf(hx, hx + float(2 * dx), num);
+    const float w = fmaf(num, float(r2), float(r2 * r2));
+    a = rsqrt_approx(w);
+    return num * rcp_approx(fmaf(w, a, float(r2)));
+}
+
+// Slots are evaluated grouped by length class |d|^2 (1, 2, 3, 4, 5, 6, 8, 9),
+// pattern order within a class; K is the position in that order.
+struct ClassOrder {
+    int slot[NPAT];   // K -> pattern slot
+    bool last[NPAT];  // K closes its length class
+};
+constexpr ClassOrder make_class_order() {
+    ClassOrder o{};
+    int r2s[NPAT] = {};
+    int k = 0;
+    for (int dz = -3; dz <= 3; ++dz)
+        for (int dy = -3; dy <= 3; ++dy)
+            for (int dx = -3; dx <= 3; ++dx) {
+                const int r2 = dx * dx + dy * dy + dz * dz;
+                if (r2 != 0 && r2 <= 9)
+                    r2s[k++] = r2;
+            }
+    k = 0;
+    for (int r2 = 1; r2 <= 9; ++r2)
+        for (int c = 0; c < NPAT; ++c)
+            if (r2s[c] == r2)
+                o.slot[k++] = c;
+    for (int q = 0; q < NPAT; ++q)
+        o.last[q] = q == NPAT - 1 || r2s[o.slot[q]] != r2s[o.slot[q + 1]];
+    return o;
+}
+constexpr ClassOrder kOrder = make_class_order();
+
+// Per-bond (slot) arrays of the NL path are brick-major: the node at lane t
+// (= tx + 16 ty + 64 tz) of 16 x 4 x 4 brick b keeps slot c at
+// b * kBrickSlots + c * NLB + t.  A step thread reads slot c at a
+// compile-time offset from its own base, and a warp's access is one 128-byte
+// line.  Bricks tile the owned planes only (ghost rows carry no bond state).
+constexpr int NLB = 256;
+constexpr long long kBrickSlots = (long long)NPAT * NLB;
+__host__ __device__ inline long long slot_base(const LatticeArgs& L, long long i) {
+    const long long plane = (long long)L.nx * L.ny;
+    const int ix = int(i % L.nx), iy = int((i / L.nx) % L.ny), iz = int(i / plane) - L.z0;
+    const long long nbx = (L.nx + 15) / 16, nby = (L.ny + 3) / 4;
+    const long long b = ix / 16 + nbx * (iy / 4 + nby * (iz / 4));
+    return b * kBrickSlots + (ix % 16) + 16 * (iy % 4) + 64 * (iz % 4);
+}
+
+// Stage the halo box of the brick at (gx0, gy0, gz0) plane by plane
+// (HX x HY = 220 records; thread t owns record t % 220 of plane t / 220 of
+// each pass): fp32 (u - U_brick) / spacing, plus for NF the signed V_j / V_0.
+// Planes are loaded PL at a time so several L2/HBM round trips are in flight.
+template <int BZT, bool NF>
+__device__ __forceinline__ void stage_box(const DevArgs& A, const LatticeArgs& L, float4* rec,
+                                          int gx0, int gy0, int gz0, const double4& U0) {
+    constexpr int TT = BX * BY * BZT, HZ = BZT + 6;
+    const long long plane = (long long)L.nx * L.ny;
+    const float ih = float(L.inv_h);
+    {
+        constexpr int PREC = HX * HY;          // records per box plane
+        constexpr int PPASS = TT / PREC;       // planes per pass (1 or 2)
+#ifndef PD_LAT_PL
+#define PD_LAT_PL 2
+#endif
+        constexpr int PL = PD_LAT_PL;          // passes in flight
+        const int t = threadIdx.x;
+        const int q = t % PREC, pp = t / PREC;
+        const int px = q % HX, py = q / HX;
+        const int X = gx0 - 3 + px, Y = gy0 - 3 + py;
+        const bool xy_ok = pp < PPASS && X >= 0 && X < L.nx && Y >= 0 && Y < L.ny;
+        const double4* src = A.u_in + (X + (long long)L.nx * Y);
+        float4* dst = rec + q + PREC * pp;
+        for (int pz0 = 0; pz0 < HZ; pz0 += PPASS * PL) {
+            double ux[PL], uy[PL], uz[PL];
+            float wv[PL];
+            bool ok[PL];
+#pragma unroll
+            for (int k = 0; k < PL; ++k) {
+                const int pz = pz0 + pp + PPASS * k;
+                const int Z = gz0 - 3 + pz;
+                ok[k] = xy_ok && pz < HZ && Z >= 0 && Z < L.nz_local;
+                ux[k] = uy[k] = uz[k] = 0.0;
+                wv[k] = 0.f;
+                if (ok[k]) {
+                    const double4* pu = src + plane * Z;
+                    const double2 xy = *reinterpret_cast<const double2*>(pu);
+                    ux[k] = xy.x;
+                    uy[k] = xy.y;
+                    if (NF) {
+                        const double2 zw = reinterpret_cast<const double2*>(pu)[1];
+                        uz[k] = zw.x;
+                        // V_j / V_0 (1 with uniform volumes), negative for a no-failure node
+                        const float vf =
+                            L.vol_varies ? float(A.xv[(pu - A.u_in)].w * L.inv_v0) : 1.f;
+                        wv[k] = zw.y != 0.0 ? -vf : vf;
+                    } else {
+                        uz[k] = reinterpret_cast<const double*>(pu)[2];
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < PL; ++k) {
+                const int pz = pz0 + pp + PPASS * k;
+                if (pp < PPASS && pz < HZ)
+                    dst[PREC * (pz - pp)] =
+                        ok[k] ? make_float4(float(ux[k] - U0.x) * ih, float(uy[k] - U0.y) * ih,
+                                            float(uz[k] - U0.z) * ih, wv[k])
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
+    }
+}
+
+} // namespace
+} // namespace pdb

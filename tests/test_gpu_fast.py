@@ -14,8 +14,8 @@ import pytest
 
 import scenarios as S
 from paper_2105_04150_b200 import engine, geometry
-from paper_2105_04150_b200.types import (ForceField, IntegratorKind, KernelVariant,
-                                         SimulateOptions, make_state)
+from paper_2105_04150_b200.types import (BCKind, DamageLaw, ForceField, IntegratorKind,
+                                         KernelVariant, SimulateOptions, make_state)
 
 pytestmark = pytest.mark.gpu
 
@@ -318,3 +318,65 @@ def test_lattice_no_failure_and_volumes_match_oracle(oracle, integrator):
     diff = int((ref.connectivity.entries != fast.connectivity.entries).sum())
     assert diff <= max(4, 0.01 * broken), (diff, broken)
     assert max_rel_difference(ref.u, fast.u) <= FRACTURE_U_TOL
+
+
+NLU_LAWS = {
+    "bilinear": lambda: DamageLaw.bilinear(1.0, 1e-5, 4e-5),
+    "trilinear_convex_kink": lambda: DamageLaw.trilinear(1.0, 5e-6, 1.5e-5, 4e-5, 0.25),
+    "trilinear_concave": lambda: DamageLaw.trilinear(1.0, 1e-5, 2e-5, 3e-5, 0.9),
+    "pmb": lambda: DamageLaw.pmb(1.0, 4e-5),
+}
+
+
+@pytest.mark.parametrize("law", sorted(NLU_LAWS))
+@pytest.mark.parametrize("extras", ["plain", "beta_nofail_bc"])
+def test_lattice_unrolled_nl_kernel(oracle, monkeypatch, law, extras):
+    """The unrolled NL lattice kernel (one law: history through the register
+    ring, min/max envelope, recompute pass for breaking nodes) against the
+    fp64 oracle and against the NL loop kernel (PD_LAT_NL_LOOP), with beta,
+    no-failure nodes and a displacement BC in the second variant."""
+    b, h, g = S.bench_lattice_bundle((20, 16, 12))
+    b.model.laws = [NLU_LAWS[law]()]
+    n = b.particles.size()
+    fam = geometry.build_family(b.particles.coords, h, g)
+    if extras != "plain":
+        b.corrections.beta = np.random.default_rng(5).uniform(0.6, 1.0, fam.entries.size)
+        z = b.particles.coords[2::3]
+        b.bc.no_failure[z == 0] = 1
+        for i in np.flatnonzero(z == 11):
+            b.bc.kind[3 * i + 2] = BCKind.displacement
+            b.bc.magnitude[3 * i + 2] = 2e-4
+    hist = b.model.needs_history()
+    u0 = S.seed_displacements(b.particles.coords) * 3.0
+    steps = 120
+    outs = {}
+    for mode in ("unrolled", "loop"):
+        if mode == "loop":
+            monkeypatch.setenv("PD_LAT_NL_LOOP", "1")
+        else:
+            monkeypatch.delenv("PD_LAT_NL_LOOP", raising=False)
+        ctx = engine.Context(0)
+        st = make_state(fam, hist)
+        st.u = u0.copy()
+        ctx.upload(b, st, KernelVariant.fast)
+        assert ctx.layout() == "lattice"
+        ctx.run(steps, 0, IntegratorKind.velocity_verlet, 0, KernelVariant.fast)
+        ctx.download(st)
+        ctx.close()
+        outs[mode] = st
+    ref = make_state(fam, hist)
+    ref.u = u0.copy()
+    oracle.simulate(b, ref, SimulateOptions(steps, 0, 0, IntegratorKind.velocity_verlet))
+    broken = int(fam.n_neigh.sum() - ref.connectivity.n_neigh.sum())
+    assert broken > 0  # the laws above break bonds at this amplitude
+    s_c = b.model.laws[0].breakpoints[-1]
+    for mode, st in outs.items():
+        assert max_rel_difference(ref.u, st.u) <= FRACTURE_U_TOL, mode
+        diff = int((ref.connectivity.entries != st.connectivity.entries).sum())
+        assert diff <= max(4, 0.01 * broken), (mode, diff, broken)
+        assert np.array_equal(st.connectivity.n_neigh,
+                              (st.connectivity.entries.reshape(n, -1) >= 0).sum(1))
+        if hist:
+            live = (ref.connectivity.entries >= 0) & (st.connectivity.entries >= 0)
+            err = np.abs(ref.bond_history[live] - st.bond_history[live])
+            assert np.max(err) <= 1e-4 * max(s_c, np.max(np.abs(ref.bond_history))), mode

@@ -116,16 +116,47 @@ def measured_traffic(key):
         return None
 
 
+def rebar_bond_types(counts, fam):
+    """cfg5-style bond classes on the lattice (SURVEY 8(d) realisation of the RC
+    beam): two rebar lines along x at (y, z) = (ny/4, nz/5) and (3ny/4, nz/5);
+    type 1 = steel-steel (both ends on a rebar), 2 = interface (one end), 0 =
+    concrete.  Only rebar rows and rows that reach a rebar node carry types."""
+    nx, ny, nz = counts
+    n, N = fam.node_count(), int(fam.group_size)
+    ent = fam.entries.reshape(n, N)
+    on = np.zeros(n, bool)
+    for y in (ny // 4, (3 * ny) // 4):
+        z = nz // 5
+        on[np.arange(nx) + nx * (y + ny * z)] = True
+    bt = np.zeros((n, N), np.uint8)
+    rebar = np.flatnonzero(on)
+    rows = ent[rebar]
+    bt[rebar] = np.where(rows >= 0, np.where(on[np.maximum(rows, 0)], 1, 2), 0)
+    near = np.unique(rows[rows >= 0])
+    near = near[~on[near]]
+    nrows = ent[near]
+    bt[near] = np.where((nrows >= 0) & on[np.maximum(nrows, 0)], 2, 0)
+    return bt.reshape(-1)
+
+
 def build_workload(counts, law="pmb"):
     """The reference bench fixture; law "trilinear" is SURVEY 8(d)'s history
-    variant trilinear(1, 1e-3, 2e-3, 1e6) (n-linear path, nothing breaks)."""
+    variant trilinear(1, 1e-3, 2e-3, 1e6) (n-linear path, nothing breaks);
+    "multi" is the cfg5 law set on the same lattice: trilinear concrete, PMB
+    steel and bilinear interface selected per bond by type (rebar_bond_types)."""
     import scenarios as S
     from paper_2105_04150_b200 import geometry, make_state
     from paper_2105_04150_b200.types import DamageLaw
     bundle, h, g = S.bench_lattice_bundle(counts)
     if law == "trilinear":
         bundle.model.laws = [DamageLaw.trilinear(1.0, 1e-3, 2e-3, 1e6)]
+    elif law == "multi":
+        bundle.model.laws = [DamageLaw.trilinear(1.0, 1e-3, 2e-3, 1e6),
+                             DamageLaw.pmb(7.0, 1e6),
+                             DamageLaw.bilinear(3.0, 1e-3, 1e6)]
     fam = geometry.build_family(bundle.particles.coords, h, g)
+    if law == "multi":
+        fam.bond_type = rebar_bond_types(counts, fam)
     state = make_state(fam, bundle.model.needs_history())
     state.u = S.seed_displacements(bundle.particles.coords)
     return bundle, fam, state
@@ -202,8 +233,10 @@ def _summary(args, value, ms_step, world, n, N, live, bytes_step, achieved, e2e,
     law_key = "" if getattr(args, "law", "pmb") == "pmb" else f"_{args.law}"
     traffic = (measured_traffic(f"{layout}_{args.size}_{variant_name}{law_key}")
                if world == 1 and layout else None)
-    law = ("PMB c=1 s_c=1e6" if getattr(args, "law", "pmb") == "pmb"
-           else "trilinear(1, 1e-3, 2e-3, 1e6) with history")
+    law = {"pmb": "PMB c=1 s_c=1e6",
+           "trilinear": "trilinear(1, 1e-3, 2e-3, 1e6) with history",
+           "multi": "cfg5 laws by bond type: trilinear concrete, PMB steel, bilinear interface, "
+                    "two rebar lines, history"}[getattr(args, "law", "pmb")]
     cfg = {"workload": f"cfg4 lattice {args.size}^3 = {n} nodes, delta=3dx (N={N}), "
                        f"{law}, velocity-Verlet, dt=1e-3, seeded u"
                        + (f", {world} z-slabs" if world > 1 else ""),
@@ -262,8 +295,10 @@ def run_single(args, variant, local):
     ms_step = ms_total / args.steps
     value = live * args.steps / (ms_total / 1e3)
     bytes_step = algorithmic_bytes(n, N, live)
-    if args.law == "trilinear":  # + 2 h B history traffic (h = 4: fp32 history on the fast path)
+    if args.law in ("trilinear", "multi"):  # + 2 h B history (h = 4: fp32 on the fast path)
         bytes_step += 2 * (4 if args.variant == "fast" else 8) * live
+    if args.law == "multi":  # + B bond_type
+        bytes_step += live
     achieved = bytes_step / (ms_step / 1e3) / 1e9
     ctx.close()
     del ctx
@@ -418,7 +453,7 @@ def main():
     ap.add_argument("--size", type=int, default=216)
     ap.add_argument("--e2e-steps", type=int, default=1000)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--law", default="pmb", choices=["pmb", "trilinear"])
+    ap.add_argument("--law", default="pmb", choices=["pmb", "trilinear", "multi"])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

@@ -685,12 +685,22 @@ int try_lattice(pd_ctx* ctx, const pd_particles& p, const pd_state& st, const pd
     L.n_local = n;
     L.nl = nl ? 1 : 0;
     const size_t pslots = size_t(lattice_slot_count(L));
-    if (nl && ctx->history) {
+    // several laws (<= 8, <= 3 breakpoints each): the typed unrolled kernel,
+    // with the bond type in the history words (PD_LAT_NL_LOOP: the loop kernel)
+    bool small_laws = m.n_laws >= 2 && m.n_laws <= 8;
+    for (int k = 0; k < m.n_laws && small_laws; ++k)
+        small_laws = m.laws[k].n_breakpoints <= 3;
+    L.typed = (nl && small_laws && !std::getenv("PD_LAT_NL_LOOP")) ? 1 : 0;
+    if (L.typed) {
+        PD_CK(ctx->lhist.alloc(pslots));
+        PD_CK(cudaMemsetAsync(ctx->lhist.p, 0, sizeof(float) * pslots, s));
+        L.hist = ctx->lhist.p;
+    } else if (nl && ctx->history) {
         PD_CK(ctx->lhist.alloc(pslots));
         PD_CK(cudaMemsetAsync(ctx->lhist.p, 0, sizeof(float) * pslots, s));
         L.hist = ctx->lhist.p;
     }
-    if (nl && st.connectivity.bond_type_size != 0) {
+    if (nl && !L.typed && st.connectivity.bond_type_size != 0) {
         PD_CK(ctx->lbtype.alloc(pslots));
         PD_CK(cudaMemsetAsync(ctx->lbtype.p, 0, pslots, s));
         L.btype = ctx->lbtype.p;
@@ -729,6 +739,8 @@ int try_lattice(pd_ctx* ctx, const pd_particles& p, const pd_state& st, const pd
         }
         lattice_set_laws(laws.data(), m.n_laws, L, s);
         PD_CK(cudaGetLastError());
+        if (std::getenv("PD_LAT_NL_LOOP"))  // force the runtime-loop kernel (tests)
+            L.multi = 1;
     }
     L.sc = float(m.laws[0].breakpoints[0]);
     L.cv = nl ? float(p.volume[0]) : float(m.laws[0].stiffness * p.volume[0]);
@@ -1225,17 +1237,24 @@ int pd_abi_version(void) { return PD_ABI_VERSION; }
 const char* pd_last_error(void) { return g_err.c_str(); }
 
 int pd_device_count(void) {
-    int count = 0;
-    if (cudaGetDeviceCount(&count) != cudaSuccess) {
-        cudaGetLastError();
-        return 0;
-    }
-    int usable = 0;
-    for (int d = 0; d < count; ++d) {
-        cudaDeviceProp prop;
-        if (cudaGetDeviceProperties(&prop, d) == cudaSuccess && prop.major >= 10)
-            ++usable;
-    }
+    // the visible devices do not change within a process: count them once
+    // (cheap attribute queries, not cudaGetDeviceProperties)
+    static const int usable = [] {
+        int count = 0;
+        if (cudaGetDeviceCount(&count) != cudaSuccess) {
+            cudaGetLastError();
+            return 0;
+        }
+        int n = 0;
+        for (int d = 0; d < count; ++d) {
+            int major = 0;
+            if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, d) ==
+                    cudaSuccess &&
+                major >= 10)
+                ++n;
+        }
+        return n;
+    }();
     return usable;
 }
 
@@ -1260,13 +1279,17 @@ int pd_ctx_create(int device, pd_ctx** out) {
 void pd_ctx_destroy(pd_ctx* ctx) {
     if (!ctx)
         return;
+    PhaseTimer tm;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    tm.mark("destroy: sync");
     snapshot_stop(ctx);
     for (void* p : ctx->ipc_opened)
         cudaIpcCloseMemHandle(p);
     cudaStreamDestroy(ctx->stream);
+    tm.mark("destroy: stream");
     delete ctx;
+    tm.mark("destroy: buffers");
 }
 
 void* pd_ctx_stream(pd_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }

@@ -157,6 +157,11 @@ struct LatticeArgs {
     int multi = 1;   // per-bond laws from constant memory; else the register law rl
     NlRegLaw rl;
     signed char pat[128][4];  // the offset pattern (dx, dy, dz, |d|^2): the rare slow paths
+    // typed: several laws (<= 8, <= 3 breakpoints each) chosen by bond type on
+    // the unrolled kernel; the history words carry the type in their low 3
+    // bits and tl holds per type (c, sl_1, a_1, +-s_c), (sl_2, a_2, cvx_1, cvx_2)
+    int typed = 0;
+    float4 tl[16];
     int prefetch = 0;         // NL: bulk L2 prefetch of a brick's per-bond streams (PD_NLU_PF=1; measured slower than the per-slot prefetch)
 };
 bool lattice_detect(const double* coords, long long n, long long own_begin, long long own_end,

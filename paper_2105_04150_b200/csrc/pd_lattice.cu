@@ -407,8 +407,12 @@ __global__ void lattice_mask_kernel(const int32_t* entries, long long begin, lon
         }
         w[c >> 5] |= 1u << (c & 31);
         const long long sidx = slot_base(L, i) + (long long)c * NLB, idx = i * N + k;
-        if (L.hist && src.hist)
+        if (L.typed) {  // history word: fp32 history, bond type in the low 3 bits
+            const unsigned h = src.hist ? __float_as_uint(float(src.hist[idx])) & ~7u : 0u;
+            L.hist[sidx] = __uint_as_float(h | (src.btype ? unsigned(src.btype[idx]) & 7u : 0u));
+        } else if (L.hist && src.hist) {
             L.hist[sidx] = float(src.hist[idx]);
+        }
         if (L.btype)
             L.btype[sidx] = src.btype[idx];
         if (L.lam)  // lambda * beta in one stream (engine.cpp:103-107)
@@ -442,8 +446,12 @@ __global__ void lattice_materialize_kernel(const int32_t* entries0, const uint4*
             const int c = int(c_slot[(dz + 3) * 49 + (dy + 3) * 7 + (dx + 3)]);
             if (!((w[c >> 5] >> (c & 31)) & 1u))
                 v = -1;
-            if (hist_out)  // broken bonds keep their last history (engine.cpp:88-92)
-                hist_out[i * N + k] = double(hist[slot_base(L, i) + (long long)c * NLB]);
+            if (hist_out) {  // broken bonds keep their last history (engine.cpp:88-92)
+                float h = hist[slot_base(L, i) + (long long)c * NLB];
+                if (L.typed)
+                    h = __uint_as_float(__float_as_uint(h) & ~7u);
+                hist_out[i * N + k] = double(h);
+            }
         }
         if (out)
             out[i * N + k] = v;
@@ -655,7 +663,7 @@ cudaError_t launch_nl(const DevArgs& A, const LatticeArgs& L, cudaStream_t st) {
         return cudaSuccess;
     const dim3 grid{unsigned(nbx), unsigned(nby), unsigned(nbz)};
     const size_t smem = sizeof(float4) * nrec<4>();
-    if (L.multi || std::getenv("PD_LAT_NL_LOOP"))  // PD_LAT_NL_LOOP: the loop kernel
+    if (L.multi && !L.typed)  // the loop kernel (also forced by PD_LAT_NL_LOOP at setup)
         lattice_nl_kernel<MODE, BC, true><<<grid, BX * BY * 4, smem, st>>>(A, L);
     else
         return MODE == 0   ? launch_nlu_m0(A, L, st)
@@ -716,6 +724,32 @@ void lattice_set_laws(const DevLaw* laws, int n, LatticeArgs& L, cudaStream_t st
     L.rl.sl1 = a.nbp > 1 ? a.sl[1] : 0.f;
     L.rl.sl2 = a.nbp > 2 ? a.sl[2] : 0.f;
     L.rl.nbp = a.nbp;
+    if (L.typed) {  // per-type segment lines in fp64 -> fp32 (pd_lattice_nlu.cuh nl_law_typed)
+        for (int k = 0; k < 8; ++k) {
+            L.tl[2 * k] = make_float4(0.f, 0.f, 0.f, 1.f);
+            L.tl[2 * k + 1] = make_float4(0.f, 0.f, -1.f, -1.f);
+        }
+        for (int k = 0; k < n && k < 8; ++k) {
+            const DevLaw& d = laws[k];
+            const double c = d.c, sl0 = d.f[0] / d.bp[0];
+            double sl1 = sl0, a1 = 0.0, sl2 = sl0, a2 = 0.0;
+            if (d.nbp >= 2) {
+                sl1 = (d.f[1] - d.f[0]) / (d.bp[1] - d.bp[0]);
+                a1 = d.f[0] - d.bp[0] * sl1;
+                sl2 = sl1;
+                a2 = a1;
+            }
+            if (d.nbp >= 3) {
+                sl2 = (d.f[2] - d.f[1]) / (d.bp[2] - d.bp[1]);
+                a2 = d.f[1] - d.bp[1] * sl2;
+            }
+            const float sc = float(d.bp[d.nbp - 1]);
+            L.tl[2 * k] = make_float4(float(d.nbp == 1 ? c : sl0), float(sl1), float(a1),
+                                      d.nbp > 1 ? sc : -sc);
+            L.tl[2 * k + 1] = make_float4(float(sl2), float(a2), sl1 > sl0 ? 1.f : -1.f,
+                                          sl2 > sl1 ? 1.f : -1.f);
+        }
+    }
     if (n >= 1 && laws[0].nbp >= 2) {  // a_k = f_{k-1} - bp_{k-1} sl_k in fp64
         const DevLaw& d = laws[0];
         const double sl0 = d.f[0] / d.bp[0];

@@ -77,6 +77,29 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
     asm volatile("prefetch.global.L2 [%0];" :: "l"(p));
 }
 
+// typed (several laws): store the history word (s with the bond type in its
+// low 3 bits) when the slot is live, breakable, of a law with history
+// (hflag > 0) and s > hh
+template <bool NF>
+__device__ __forceinline__ void stg_typed_if(float* p, unsigned on, float w, float thr, float hflag,
+                                             float s, float hh, unsigned word) {
+    if (NF)
+        asm volatile("{\n\t.reg .pred q, r, t, u;\n\t"
+                     "setp.ne.u32 q, %1, 0;\n\t"
+                     "setp.ge.and.f32 r, %2, %3, q;\n\t"
+                     "setp.gt.and.f32 u, %4, 0f00000000, r;\n\t"
+                     "setp.gt.and.f32 t, %5, %6, u;\n\t"
+                     "@t st.global.b32 [%0], %7;\n\t}"
+                     :: "l"(p), "r"(on), "f"(w), "f"(thr), "f"(hflag), "f"(s), "f"(hh), "r"(word));
+    else
+        asm volatile("{\n\t.reg .pred q, t, u;\n\t"
+                     "setp.ne.u32 q, %1, 0;\n\t"
+                     "setp.gt.and.f32 u, %2, 0f00000000, q;\n\t"
+                     "setp.gt.and.f32 t, %3, %4, u;\n\t"
+                     "@t st.global.b32 [%0], %5;\n\t}"
+                     :: "l"(p), "r"(on), "f"(hflag), "f"(s), "f"(hh), "r"(word));
+}
+
 __device__ __forceinline__ void bulk_prefetch_l2(const void* p, unsigned bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(p), "r"(bytes) : "memory");
 }
@@ -90,6 +113,19 @@ constexpr int ND = 8;  // ring depth (slots of history / lambda loads in flight)
 
 // f for stretch s and history hh (hh ignored for NBP = 1); e is the stretch
 // the break test uses (max(s, h))
+// several laws (NBP = 0): the bond's law from the per-type table, three
+// segment lines (a law with fewer breakpoints repeats its last line);
+// p0 = (c, sl_1, a_1, +-s_c: + when the law keeps history), p1 = (sl_2, a_2,
+// +1 convex first kink / -1, +1 convex second kink / -1)
+__device__ __forceinline__ float nl_law_typed(const float4& p0, const float4& p1, float s, float hh,
+                                              float& e) {
+    e = fmaxf(fmaxf(s, hh), 1e-30f);
+    const float l0 = p0.x * e, l1 = fmaf(p0.y, e, p0.z), l2 = fmaf(p1.x, e, p1.y);
+    const float t = p1.w > 0.f ? fmaxf(l1, l2) : fminf(l1, l2);
+    const float env = p1.z > 0.f ? fmaxf(l0, t) : fminf(l0, t);
+    return env * (s * rcp_approx(e));
+}
+
 template <int NBP>
 __device__ __forceinline__ float nl_law(const NlRegLaw& R, float s, float hh, float& e) {
     if (NBP == 1) {
@@ -106,8 +142,8 @@ __device__ __forceinline__ float nl_law(const NlRegLaw& R, float s, float hh, fl
 template <int K, int NBP, bool LAM, bool NF>
 __device__ __forceinline__ void nl_slot(const float4* own, const float4& ri, const uint4& m,
                                         float* hb, const float* lb, float nfthr,
-                                        const NlRegLaw& R, float (&hr)[ND], float (&lr)[ND],
-                                        AccN& acc) {
+                                        const NlRegLaw& R, const float4* tab, float (&hr)[ND],
+                                        float (&lr)[ND], AccN& acc) {
     constexpr int C = kOrder.slot[K];
     constexpr int dx = pat(C, 0), dy = pat(C, 1), dz = pat(C, 2);
     constexpr int off = dx + HX * (dy + HY * dz);
@@ -116,20 +152,32 @@ __device__ __forceinline__ void nl_slot(const float4* own, const float4& ri, con
     const unsigned mw = word == 0 ? m.x : (word == 1 ? m.y : (word == 2 ? m.z : m.w));
     const bool live = (mw & bit) != 0u;
     // this slot's streamed values; refill the ring ND slots ahead
-    const float hh = NBP > 1 ? hr[K % ND] : 0.f;
+    float hh = NBP != 1 ? hr[K % ND] : 0.f;
     const float lam = LAM ? lr[K % ND] : 1.f;
+    // typed: the ring holds history words (bond type in the low 3 bits)
+    unsigned ty = 0u;
+    float4 p0, p1;
+    if (NBP == 0) {
+        const unsigned bits = __float_as_uint(hh);
+        ty = bits & 7u;
+        hh = __uint_as_float(bits & ~7u);
+        p0 = tab[2 * ty];
+        p1 = tab[2 * ty + 1];
+        if (!(p0.w > 0.f))
+            hh = 0.f;  // a law without history (PMB) never reads one (engine.cpp:84-87)
+    }
     if constexpr (K + ND < NPAT) {
         constexpr int CN = kOrder.slot[K + ND];
 #if PD_NLU_PRED
         constexpr unsigned nbit = 1u << (CN & 31);
         constexpr int nword = CN >> 5;
         const unsigned nmw = nword == 0 ? m.x : (nword == 1 ? m.y : (nword == 2 ? m.z : m.w));
-        if (NBP > 1)
+        if (NBP != 1)
             ldg_keep_if(hr[K % ND], hb + CN * NLB, nmw & nbit);
         if (LAM)
             ldg_keep_if(lr[K % ND], lb + CN * NLB, nmw & nbit);
 #else
-        if (NBP > 1)
+        if (NBP != 1)
             ldg_keep_if(hr[K % ND], hb + CN * NLB, 1u);
         if (LAM)
             ldg_keep_if(lr[K % ND], lb + CN * NLB, 1u);
@@ -140,7 +188,7 @@ __device__ __forceinline__ void nl_slot(const float4* own, const float4& ri, con
     // waits on L2, not HBM
     if constexpr (K + PD_NLU_PFD < NPAT) {
         constexpr int CP = kOrder.slot[K + PD_NLU_PFD];
-        if (NBP > 1)
+        if (NBP != 1)
             prefetch_l2(hb + CP * NLB);
         if (LAM)
             prefetch_l2(lb + CP * NLB);
@@ -153,13 +201,24 @@ __device__ __forceinline__ void nl_slot(const float4* own, const float4& ri, con
     // no-failure node; rj.w < 0 for a no-failure neighbour)
     const bool brk_ok = live && (!NF || rj.w >= nfthr);
     float e;
-    float f = nl_law<NBP>(R, s, hh, e);
-    if (NF && !brk_ok)
-        f = R.c * s;
-    if (NBP > 1)
-        stg_hist_if<NF>(hb + C * NLB, mw & bit, rj.w, nfthr, s, hh);
-    if (brk_ok)
-        acc.emax = fmaxf(acc.emax, e);
+    float f;
+    if (NBP == 0) {
+        f = nl_law_typed(p0, p1, s, hh, e);
+        if (NF && !brk_ok)
+            f = p0.x * s;
+        stg_typed_if<NF>(hb + C * NLB, mw & bit, rj.w, nfthr, p0.w, s, hh,
+                         (__float_as_uint(s) & ~7u) | ty);
+        if (brk_ok)  // e >= s_c of the bond's own law <=> e - |s_c| >= 0 (exact sign)
+            acc.emax = fmaxf(acc.emax, e - fabsf(p0.w));
+    } else {
+        f = nl_law<NBP>(R, s, hh, e);
+        if (NF && !brk_ok)
+            f = R.c * s;
+        if (NBP > 1)
+            stg_hist_if<NF>(hb + C * NLB, mw & bit, rj.w, nfthr, s, hh);
+        if (brk_ok)
+            acc.emax = fmaxf(acc.emax, e);
+    }
     float scale = f * a;
     if (NF)
         scale *= fabsf(rj.w);
@@ -183,7 +242,7 @@ template <int K, int NBP, bool LAM>
 __device__ __forceinline__ void nl_ring_one(const float* hb, const float* lb, float (&hr)[ND],
                                             float (&lr)[ND]) {
     constexpr int C = kOrder.slot[K];
-    hr[K] = NBP > 1 ? hb[C * NLB] : 0.f;
+    hr[K] = NBP != 1 ? hb[C * NLB] : 0.f;
     lr[K] = LAM ? __ldcs(lb + C * NLB) : 1.f;
 }
 
@@ -197,8 +256,9 @@ template <int NBP, bool LAM, bool NF, int... K>
 __device__ __forceinline__ void nl_all_slots(std::integer_sequence<int, K...>, const float4* own,
                                              const float4& ri, const uint4& m, float* hb,
                                              const float* lb, float nfthr, const NlRegLaw& R,
-                                             float (&hr)[ND], float (&lr)[ND], AccN& acc) {
-    (nl_slot<K, NBP, LAM, NF>(own, ri, m, hb, lb, nfthr, R, hr, lr, acc), ...);
+                                             const float4* tab, float (&hr)[ND], float (&lr)[ND],
+                                             AccN& acc) {
+    (nl_slot<K, NBP, LAM, NF>(own, ri, m, hb, lb, nfthr, R, tab, hr, lr, acc), ...);
 }
 
 // the rare pass for a node that loses bonds: the history is already updated,
@@ -207,7 +267,7 @@ template <int NBP, bool LAM, bool NF>
 __device__ __forceinline__ uint4 nl_slow_node(const LatticeArgs& L, const float4* own,
                                               const float4 ri, const uint4 m, const float* hb,
                                               const float* lb, float nfthr, const NlRegLaw& R,
-                                              float sc, float3& fo) {
+                                              const float4* tab, float sc, float3& fo) {
     unsigned dead[4] = {0u, 0u, 0u, 0u};
     const unsigned w[4] = {m.x, m.y, m.z, m.w};
     float fx = 0.f, fy = 0.f, fz = 0.f;
@@ -220,14 +280,23 @@ __device__ __forceinline__ uint4 nl_slow_node(const LatticeArgs& L, const float4
         float a;
         const float s = stretch_r(rj, ri, dx, dy, dz, a);
         const bool brk_ok = !NF || rj.w >= nfthr;
-        float e;
-        float f = nl_law<NBP>(R, s, NBP > 1 ? hb[c * NLB] : 0.f, e);
-        if (brk_ok && e >= sc) {
+        float e, f, c_lin = R.c, s_c = sc;
+        if (NBP == 0) {
+            const unsigned bits = __float_as_uint(hb[c * NLB]);
+            const float4 p0 = tab[2 * (bits & 7u)], p1 = tab[2 * (bits & 7u) + 1];
+            const float hh = p0.w > 0.f ? __uint_as_float(bits & ~7u) : 0.f;
+            f = nl_law_typed(p0, p1, s, hh, e);
+            c_lin = p0.x;
+            s_c = fabsf(p0.w);
+        } else {
+            f = nl_law<NBP>(R, s, NBP > 1 ? hb[c * NLB] : 0.f, e);
+        }
+        if (brk_ok && e >= s_c) {
             dead[c >> 5] |= 1u << (c & 31);
             continue;
         }
         if (!brk_ok)
-            f = R.c * s;
+            f = c_lin * s;
         float scale = f * a * sqrtf(float(L.pat[c][3]));  // |d| (= root(r2), correctly rounded)
         if (NF)
             scale *= fabsf(rj.w);
@@ -256,14 +325,17 @@ __global__ void __launch_bounds__(BX * BY * 4, 4) lattice_nlu_kernel(DevArgs A, 
     const uint4 m = active ? __ldcs(L.mask + i) : make_uint4(0, 0, 0, 0);
     const long long sb = (blockIdx.x + (long long)gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)) *
                              kBrickSlots + threadIdx.x;  // == slot_base(L, i)
-    float* hb = NBP > 1 ? L.hist + sb : nullptr;
+    float* hb = NBP != 1 ? L.hist + sb : nullptr;
+    __shared__ float4 tab[2 * 8];  // typed: per-type law lines (LatticeArgs::tl)
+    if (NBP == 0 && threadIdx.x < 2 * 8)
+        tab[threadIdx.x] = L.tl[threadIdx.x];
     const float* lb = LAM ? L.lam + sb : nullptr;
-    // The brick's per-bond streams are contiguous (kBrickSlots values): one
-    // thread asks L2 for all of them up front (bulk prefetch, no registers),
-    // so the ring loads below mostly hit L2 instead of waiting on HBM.
+    // Opt-in (PD_NLU_PF=1): the brick's per-bond streams are contiguous
+    // (kBrickSlots values), so one thread can ask L2 for all of them up front.
+    // Measured slower than the per-slot prefetch below.
     if (L.prefetch && threadIdx.x == 0) {
         const long long base = sb - threadIdx.x;
-        if (NBP > 1)
+        if (NBP != 1)
             bulk_prefetch_l2(L.hist + base, unsigned(kBrickSlots * sizeof(float)));
         if (LAM)
             bulk_prefetch_l2(L.lam + base, unsigned(kBrickSlots * sizeof(float)));
@@ -284,11 +356,11 @@ __global__ void __launch_bounds__(BX * BY * 4, 4) lattice_nlu_kernel(DevArgs A, 
     const NlRegLaw& R = L.rl;
     AccN acc{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, -inf};
     nl_all_slots<NBP, LAM, NF>(std::make_integer_sequence<int, NPAT>{}, own, ri, m, hb, lb,
-                               nfthr, R, hr, lr, acc);
-    if (acc.emax >= R.sc) {  // some live bond breaks this step
+                               nfthr, R, tab, hr, lr, acc);
+    if (acc.emax >= (NBP == 0 ? 0.f : R.sc)) {  // some live bond breaks this step
         asm volatile("" ::: "memory");  // after this node's history stores
         float3 f;
-        const uint4 d = nl_slow_node<NBP, LAM, NF>(L, own, ri, m, hb, lb, nfthr, R, R.sc, f);
+        const uint4 d = nl_slow_node<NBP, LAM, NF>(L, own, ri, m, hb, lb, nfthr, R, tab, R.sc, f);
         L.mask[i] = make_uint4(m.x & ~d.x, m.y & ~d.y, m.z & ~d.z, m.w & ~d.w);
         A.n_neigh[i] -= __popc(d.x) + __popc(d.y) + __popc(d.z) + __popc(d.w);
         acc.fx = f.x;
@@ -327,13 +399,16 @@ cudaError_t launch_nlu3(const DevArgs& A, const LatticeArgs& L, cudaStream_t st)
 
 // one register law: NBP = 1 (no history) or 3 (two breakpoints: the third
 // segment repeats the second)
+// ... or several laws by bond type (NBP = 0, L.typed)
 template <int MODE> cudaError_t launch_nlu_impl(const DevArgs& A, const LatticeArgs& L,
                                                 cudaStream_t st) {
     if (A.bc_kind)
-        return L.rl.nbp == 1 ? launch_nlu3<MODE, true, 1>(A, L, st)
-                             : launch_nlu3<MODE, true, 3>(A, L, st);
-    return L.rl.nbp == 1 ? launch_nlu3<MODE, false, 1>(A, L, st)
-                         : launch_nlu3<MODE, false, 3>(A, L, st);
+        return L.typed         ? launch_nlu3<MODE, true, 0>(A, L, st)
+               : L.rl.nbp == 1 ? launch_nlu3<MODE, true, 1>(A, L, st)
+                               : launch_nlu3<MODE, true, 3>(A, L, st);
+    return L.typed         ? launch_nlu3<MODE, false, 0>(A, L, st)
+           : L.rl.nbp == 1 ? launch_nlu3<MODE, false, 1>(A, L, st)
+                           : launch_nlu3<MODE, false, 3>(A, L, st);
 }
 
 template <class K> void nlu_preload_fn(K k) {
@@ -349,6 +424,8 @@ template <int MODE, bool BC, int NBP> void preload_nlu3() {
 }
 
 template <int MODE> void preload_nlu_impl() {
+    preload_nlu3<MODE, true, 0>();
+    preload_nlu3<MODE, false, 0>();
     preload_nlu3<MODE, true, 1>();
     preload_nlu3<MODE, true, 3>();
     preload_nlu3<MODE, false, 1>();

@@ -253,28 +253,30 @@ def test_lattice_layout_selection():
 
 
 def test_lattice_nl_kernel_matches_tiles_and_oracle(oracle, monkeypatch):
-    """The NL lattice kernel (trilinear multi-material with bond types, beta and
-    history) against the tile kernel and the fp64 oracle."""
+    """Several laws by bond type on the lattice (trilinear concrete, PMB steel,
+    bilinear interface, beta, history): the typed unrolled kernel and the loop
+    kernel against the tile kernel and the fp64 oracle."""
     b, h, g = S.multimaterial_bundle((16, 8, 10))
     fam = geometry.build_family(b.particles.coords, h, g)
     fam.bond_type = S.classify_bonds(b.particles.coords, fam)
     b.corrections.beta = np.random.default_rng(2).uniform(0.7, 1.0, fam.entries.size)
-    opts = SimulateOptions(150, 0, 0, IntegratorKind.velocity_verlet, KernelVariant.fast)
     outs = {}
-    for forced in (None, "general"):
-        if forced:
-            monkeypatch.setenv("PD_FAST_LAYOUT", forced)
-        else:
-            monkeypatch.delenv("PD_FAST_LAYOUT", raising=False)
+    # the typed unrolled lattice kernel, the lattice loop kernel, the tile kernel
+    for name, env in (("typed", {}), ("loop", {"PD_LAT_NL_LOOP": "1"}),
+                      ("tiles", {"PD_FAST_LAYOUT": "general"})):
+        for k in ("PD_LAT_NL_LOOP", "PD_FAST_LAYOUT"):
+            if k in env:
+                monkeypatch.setenv(k, env[k])
+            else:
+                monkeypatch.delenv(k, raising=False)
         ctx = engine.Context(0)
         st = make_state(fam, True)
         ctx.upload(b, st, KernelVariant.fast)
-        lay = ctx.layout()
+        assert ctx.layout() == ("tiles" if name == "tiles" else "lattice")
         ctx.run(150, 0, IntegratorKind.velocity_verlet, 0, KernelVariant.fast)
         ctx.download(st)
         ctx.close()
-        outs[lay] = st
-    assert set(outs) == {"lattice", "tiles"}
+        outs[name] = st
     ref = make_state(fam, True)
     oracle.simulate(b, ref, SimulateOptions(150, 0, 0, IntegratorKind.velocity_verlet))
     s = stretches(b.particles, fam, ref.u)

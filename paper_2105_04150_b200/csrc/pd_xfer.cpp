@@ -9,6 +9,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <condition_variable>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -61,27 +64,98 @@ struct Bounce {
 
 thread_local Bounce t_bounce;
 
-// memcpy split over a few host threads (one memcpy stream tops out near
-// 10 GB/s; the chunk is large enough to amortise the thread start)
-void par_memcpy(void* dst, const void* src, size_t bytes) {
-    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    const size_t parts = std::min<size_t>({size_t(8), size_t(hw), bytes / (size_t(4) << 20) + 1});
-    if (parts <= 1) {
-        std::memcpy(dst, src, bytes);
-        return;
+// memcpy split over a persistent pool of host threads (one memcpy stream tops
+// out near 10 GB/s).  A pool, not threads per call: a 5 GB row array is 160
+// chunks, and spawning the workers for each chunk cost ~10 % of the copy.
+// PD_XFER_THREADS overrides the worker count (default min(16, cores)).
+class CopyPool {
+  public:
+    static CopyPool& get() {
+        static CopyPool* p = new CopyPool;  // never destroyed: workers outlive static teardown
+        return *p;
     }
-    std::vector<std::thread> th;
-    const size_t step = (bytes + parts - 1) / parts;
-    for (size_t p = 0; p < parts; ++p) {
-        const size_t b = p * step, e = std::min(bytes, b + step);
+    void copy(void* dst, const void* src, size_t bytes) {
+        const size_t parts = std::min<size_t>(size_t(workers_) + 1, bytes / (size_t(2) << 20) + 1);
+        if (parts <= 1) {
+            std::memcpy(dst, src, bytes);
+            return;
+        }
+        std::lock_guard<std::mutex> job(job_mu_);  // one job at a time
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            dst_ = static_cast<char*>(dst);
+            src_ = static_cast<const char*>(src);
+            bytes_ = bytes;
+            step_ = (bytes + parts - 1) / parts;
+            next_ = 1;  // part 0 is the caller's
+            parts_ = parts;
+            pending_ = parts - 1;
+            ++gen_;
+        }
+        cv_.notify_all();
+        run_part(0);
+        for (;;) {  // help with the remaining parts, then wait for the workers
+            const size_t k = claim();
+            if (k >= parts)
+                break;
+            run_part(k);
+            finish();
+        }
+        std::unique_lock<std::mutex> lk(mu_);
+        done_cv_.wait(lk, [&] { return pending_ == 0; });
+    }
+
+  private:
+    CopyPool() {
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        int n = int(std::min(16u, hw)) - 1;
+        if (const char* e = std::getenv("PD_XFER_THREADS"))
+            n = std::max(0, std::atoi(e) - 1);
+        workers_ = n;
+        for (int t = 0; t < n; ++t)
+            std::thread([this] { loop(); }).detach();
+    }
+    size_t claim() {
+        std::lock_guard<std::mutex> lk(mu_);
+        return next_ < parts_ ? next_++ : parts_;
+    }
+    void finish() {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (--pending_ == 0)
+            done_cv_.notify_all();
+    }
+    void run_part(size_t k) {
+        const size_t b = k * step_, e = std::min(bytes_, b + step_);
         if (b < e)
-            th.emplace_back([=] {
-                std::memcpy(static_cast<char*>(dst) + b, static_cast<const char*>(src) + b, e - b);
-            });
+            std::memcpy(dst_ + b, src_ + b, e - b);
     }
-    for (auto& t : th)
-        t.join();
-}
+    void loop() {
+        unsigned long long seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return gen_ != seen && next_ < parts_; });
+                seen = gen_;
+            }
+            for (;;) {
+                const size_t k = claim();
+                if (k >= parts_)
+                    break;
+                run_part(k);
+                finish();
+            }
+        }
+    }
+    int workers_ = 0;
+    std::mutex job_mu_, mu_;
+    std::condition_variable cv_, done_cv_;
+    char* dst_ = nullptr;
+    const char* src_ = nullptr;
+    size_t bytes_ = 0, step_ = 0, next_ = 0, parts_ = 0, pending_ = 0;
+    unsigned long long gen_ = 0;
+};
+
+void par_memcpy(void* dst, const void* src, size_t bytes) { CopyPool::get().copy(dst, src, bytes); }
 
 } // namespace
 
@@ -162,8 +236,10 @@ BlockCache& cache() {
     return *c;
 }
 
-// blocks below 1 MB are not worth caching
-constexpr size_t kMinCached = size_t(1) << 20;
+// every block is cached, small ones included: a cudaFree synchronises the
+// device and was measured at up to 200 ms for a 24-byte block at the end of a
+// 10M-node simulate() (PD_TIMING reports slow frees)
+constexpr size_t kMinCached = 1;
 
 } // namespace
 
@@ -191,9 +267,28 @@ cudaError_t dev_alloc(void** p, size_t bytes) {
     return e;
 }
 
+namespace {
+// PD_TIMING: report device frees that take longer than 5 ms
+struct SlowFree {
+    bool on = std::getenv("PD_TIMING") != nullptr;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    size_t bytes;
+    const char* how = "cache";
+    explicit SlowFree(size_t b) : bytes(b) {}
+    ~SlowFree() {
+        const double ms = std::chrono::duration<double, std::milli>(
+                              std::chrono::steady_clock::now() - t0).count();
+        if (on && ms > 5.0)
+            std::fprintf(stderr, "[pd timing] dev_free %zu bytes (%s) %.3f ms\n", bytes, how, ms);
+    }
+};
+} // namespace
+
 void dev_free(void* p, size_t bytes) {
     BlockCache& c = cache();
+    SlowFree sf(bytes);
     if (!c.enabled || bytes < kMinCached) {
+        sf.how = "cudaFree";
         cudaFree(p);
         return;
     }
@@ -208,6 +303,7 @@ void dev_free(void* p, size_t bytes) {
         c.limit = tot / 2;  // keep at most half the device mapped for reuse
     }
     if (c.cached + bytes > c.limit) {
+        sf.how = "cudaFree over limit";
         cudaFree(p);
         return;
     }

@@ -70,14 +70,15 @@ struct Contribution {
 
 // One slot of bond_contribution (engine.cpp:53-109).  Returns the slot's
 // contribution; clears `alive` on a break.
-__device__ __forceinline__ Contribution slot_contribution(const DevArgs& A, long long idx,
+// j is loaded (and its records prefetched into L1) by the caller before any
+// slot is evaluated.
+__device__ __forceinline__ Contribution slot_contribution(const DevArgs& A, long long idx, int j,
                                                           const double4& xi, const double4& ui,
                                                           bool i_no_fail, bool& alive,
                                                           int& broke) {
     Contribution c{0.0, 0.0, 0.0};
     if (!alive)
         return c;
-    const int j = __ldg(A.entries + idx);
     const double4 xj = A.xv[j];
     const double4 uj = A.u_in[j];
     const double rx = __dsub_rn(xj.x, xi.x), ry = __dsub_rn(xj.y, xi.y), rz = __dsub_rn(xj.z, xi.z);
@@ -126,10 +127,16 @@ __device__ __forceinline__ Contribution slot_contribution(const DevArgs& A, long
     return c;
 }
 
+// 4 CTAs of 256 per SM (64 registers, small spill): 16.6 ms/step at 10M against 18.6 ms at
+// the compiler's 80 registers (3 CTAs) -- the kernel is gather-latency bound
+// (PD_EXACT_MINB for experiments)
+#ifndef PD_EXACT_MINB
+#define PD_EXACT_MINB 4
+#endif
 // MODE: 0 = force pass only (compute_forces), 1 = velocity-Verlet step,
 //       2 = Euler step, 3 = Euler-Cromer step.
 template <int MODE, int M, bool NODE_SUM>
-__global__ void __launch_bounds__(256) exact_step_kernel(DevArgs A) {
+__global__ void __launch_bounds__(256, PD_EXACT_MINB) exact_step_kernel(DevArgs A) {
     if (MODE != 0 && *(volatile long long*)A.err_step != kNoError)
         return; // a previous step saw non-finite u: the reference threw there
     const int G = (M > 1) ? 32 : (A.N < 32 ? A.N : 32);
@@ -152,12 +159,27 @@ __global__ void __launch_bounds__(256) exact_step_kernel(DevArgs A) {
     uint32_t old_words[M];
     bool alive[M];
     int broke = 0;
+    // every live slot's neighbour index first, and its x and u records
+    // prefetched into L1 (no registers held), before the first slot's long
+    // fp64 evaluation chain: otherwise each slot's gather waits on L2 in turn
+    int jm[M];
 #pragma unroll
     for (int m = 0; m < M; ++m) {
         const int k = gl + G * m;
         old_words[m] = valid ? A.alive[i * A.W + (k >> 5)] : 0u;
         alive[m] = valid && ((old_words[m] >> (k & 31)) & 1u);
-        c[m] = slot_contribution(A, i * N + k, xi, ui, i_no_fail, alive[m], broke);
+        jm[m] = alive[m] ? __ldg(A.entries + i * N + k) : 0;
+    }
+#pragma unroll
+    for (int m = 1; m < M; ++m)
+        if (alive[m]) {
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(A.xv + jm[m]));
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(A.u_in + jm[m]));
+        }
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+        const int k = gl + G * m;
+        c[m] = slot_contribution(A, i * N + k, jm[m], xi, ui, i_no_fail, alive[m], broke);
     }
 
     // fused break bookkeeping: alive words and n_neigh (engine.cpp:93-96)

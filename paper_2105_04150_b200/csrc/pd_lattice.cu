@@ -42,9 +42,11 @@ namespace pdb {
 
 namespace {
 struct Acc {
-    float gx, gy, gz;  // sum over the current length class of c * s / (|c| |d|)
-    float fx, fy, fz;  // sum over finished classes (times |d|): the node's force / (c V)
-    float smax;        // largest stretch over the live breakable slots
+    float2 gxy;  // sum over the current length class of c * s / (|c| |d|), x and y lanes
+    float gz;
+    float2 fxy;  // sum over finished classes (times |d|): the node's force / (c V)
+    float fz;
+    float smax;  // largest stretch over the live breakable slots
 };
 
 // NF (no-failure nodes and/or per-node volumes present): a record's w holds
@@ -62,41 +64,28 @@ __device__ __forceinline__ void slot(const float4* own, const float4& ri, const 
     // branch free: a dead slot's record may be anything finite (an
     // out-of-domain box record is 0); its contribution is predicated away
     const float4 rj = own[off];
-    float s, a, cx, cy, cz;
-    stretch_c<dx, dy, dz>(rj, ri, s, a, cx, cy, cz);
+    float s, a, cz;
+    float2 cxy;
+    stretch_c<dx, dy, dz>(rj, ri, s, a, cxy, cz);
     // Every live slot adds its force and raises smax; a live slot that
     // breaks (s >= s_c, bond_contribution's PMB test, engine.cpp:90-98) makes
     // smax >= s_c, and the node is then recomputed without its broken bonds
     // (slow_node) -- so the common no-break slot has no break test at all.
-    if (NF) {
-        // a no-failure neighbour's bond never breaks (rj.w < 0): no smax
-        const float scale = s * a * fabsf(rj.w);
-        asm("{\n\t.reg .pred pl, pb;\n\t"
-            "setp.ne.u32 pl, %4, 0;\n\t"
-            "setp.ge.and.f32 pb, %10, 0f00000000, pl;\n\t"
-            "@pb max.f32 %0, %0, %5;\n\t"
-            "@pl fma.rn.f32 %1, %6, %9, %1;\n\t"
-            "@pl fma.rn.f32 %2, %7, %9, %2;\n\t"
-            "@pl fma.rn.f32 %3, %8, %9, %3;\n\t}"
-            : "+f"(acc.smax), "+f"(acc.gx), "+f"(acc.gy), "+f"(acc.gz)
-            : "r"(mw & bit), "f"(s), "f"(cx), "f"(cy), "f"(cz), "f"(scale), "f"(rj.w));
-    } else {
-        const float scale = s * a;
-        asm("{\n\t.reg .pred pl;\n\t"
-            "setp.ne.u32 pl, %4, 0;\n\t"
-            "@pl max.f32 %0, %0, %5;\n\t"
-            "@pl fma.rn.f32 %1, %6, %9, %1;\n\t"
-            "@pl fma.rn.f32 %2, %7, %9, %2;\n\t"
-            "@pl fma.rn.f32 %3, %8, %9, %3;\n\t}"
-            : "+f"(acc.smax), "+f"(acc.gx), "+f"(acc.gy), "+f"(acc.gz)
-            : "r"(mw & bit), "f"(s), "f"(cx), "f"(cy), "f"(cz), "f"(scale));
+    // A no-failure neighbour's bond (NF: rj.w < 0) never breaks: no smax.
+    const bool live = (mw & bit) != 0u;
+    const float scale = NF ? s * a * fabsf(rj.w) : s * a;
+    if (live) {
+        acc.gxy = __ffma2_rn(cxy, make_float2(scale, scale), acc.gxy);
+        acc.gz = fmaf(cz, scale, acc.gz);
+        if (!NF || rj.w >= 0.f)
+            acc.smax = fmaxf(acc.smax, s);
     }
     if constexpr (kOrder.last[K]) {  // close the class: times |d|
         constexpr float len = root(dx * dx + dy * dy + dz * dz);
-        acc.fx = fmaf(acc.gx, len, acc.fx);
-        acc.fy = fmaf(acc.gy, len, acc.fy);
+        acc.fxy = __ffma2_rn(acc.gxy, make_float2(len, len), acc.fxy);
         acc.fz = fmaf(acc.gz, len, acc.fz);
-        acc.gx = acc.gy = acc.gz = 0.f;
+        acc.gxy = make_float2(0.f, 0.f);
+        acc.gz = 0.f;
     }
 }
 
@@ -173,18 +162,17 @@ __global__ void __launch_bounds__(BX * BY * BZT, MINB) lattice_step_kernel(DevAr
     const float4 ri = *own;
     // a no-failure node's own bonds never break
     const float sc = (NF && ri.w < 0.f) ? __int_as_float(0x7f800000) : L.sc;
-    Acc a{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, -__int_as_float(0x7f800000)};
+    Acc a{make_float2(0.f, 0.f), 0.f, make_float2(0.f, 0.f), 0.f, -__int_as_float(0x7f800000)};
     all_slots<NF>(std::make_integer_sequence<int, NPAT>{}, own, ri, m, a);
     if (a.smax >= sc) {  // some live bond breaks this step
         float3 f;
         const uint4 d = slow_node<NF>(own, ri, m, sc, f);
         L.mask[i] = make_uint4(m.x & ~d.x, m.y & ~d.y, m.z & ~d.z, m.w & ~d.w);
         A.n_neigh[i] -= __popc(d.x) + __popc(d.y) + __popc(d.z) + __popc(d.w);
-        a.fx = f.x;
-        a.fy = f.y;
+        a.fxy = make_float2(f.x, f.y);
         a.fz = f.z;
     }
-    const double fx = double(a.fx * L.cv), fy = double(a.fy * L.cv), fz = double(a.fz * L.cv);
+    const double fx = double(a.fxy.x * L.cv), fy = double(a.fxy.y * L.cv), fz = double(a.fz * L.cv);
 
     // 3. fp64 epilogue
     if (MODE == 0) {

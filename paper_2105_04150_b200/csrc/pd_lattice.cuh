@@ -90,32 +90,46 @@ __device__ __forceinline__ void stretch(const float4& rj, const float4& ri, floa
 // num = +-0, and then s = +-0 tests the same against s_c.
 template <int DX, int DY, int DZ>
 __device__ __forceinline__ void stretch_c(const float4& rj, const float4& ri, float& s, float& a,
-                                          float& cx, float& cy, float& cz) {
+                                          float2& cxy, float& cz) {
     constexpr int R2 = DX * DX + DY * DY + DZ * DZ;
+    // x and y lanes packed (FADD2 / FMUL2; the offset pair comes from a
+    // uniform register): eta, xi + eta and xi + eta + d
     const float2 hxy = __fadd2_rn(make_float2(rj.x, rj.y), make_float2(-ri.x, -ri.y));
-    const float hx = hxy.x, hy = hxy.y, hz = rj.z - ri.z;  // eta / spacing
-    cx = DX ? hx + float(DX) : hx;
-    cy = DY ? hy + float(DY) : hy;
+    const float hz = rj.z - ri.z;  // eta / spacing
+    float2 txy;
+    if (DX != 0 || DY != 0) {
+        const float2 d = make_float2(float(DX), float(DY));
+        cxy = __fadd2_rn(hxy, d);
+        txy = __fadd2_rn(cxy, d);
+    } else {
+        cxy = txy = hxy;
+    }
     cz = DZ ? hz + float(DZ) : hz;
-    float num = hz * (DZ ? hz + float(2 * DZ) : hz);
-    num = fmaf(hy, DY ? hy + float(2 * DY) : hy, num);
-    num = fmaf(hx, DX ? hx + float(2 * DX) : hx, num);
+    const float tz = DZ ? cz + float(DZ) : hz;
+    // eta.(2 xi + eta), cancellation free
+    const float2 pxy = __fmul2_rn(hxy, txy);
+    float num = __fadd_rn(pxy.x, pxy.y);
+    num = fmaf(hz, tz, num);
     const float w = fmaf(num, float(R2), float(R2 * R2));
     a = rsqrt_approx(w);
     s = num * rcp_approx(fmaf(w, a, float(R2)));
 }
 
+// the same arithmetic with a runtime offset (the rare recompute passes): no
+// contraction, lane by lane as the packed instructions round
 __device__ __forceinline__ float stretch_r(const float4& rj, const float4& ri, int dx, int dy,
                                            int dz, float& a) {
     const int r2 = dx * dx + dy * dy + dz * dz;
     const float2 hxy = __fadd2_rn(make_float2(rj.x, rj.y), make_float2(-ri.x, -ri.y));
-    const float hx = hxy.x, hy = hxy.y, hz = rj.z - ri.z;
-    float num = hz * (hz + float(2 * dz));
-    num = fmaf(hy, hy + float(2 * dy), num);
-    num = fmaf(hx, hx + float(2 * dx), num);
+    const float hx = hxy.x, hy = hxy.y, hz = __fsub_rn(rj.z, ri.z);
+    const float tx = __fadd_rn(__fadd_rn(hx, float(dx)), float(dx));
+    const float ty = __fadd_rn(__fadd_rn(hy, float(dy)), float(dy));
+    const float tz = __fadd_rn(__fadd_rn(hz, float(dz)), float(dz));
+    float num = __fadd_rn(__fmul_rn(hx, tx), __fmul_rn(hy, ty));
+    num = fmaf(hz, tz, num);
     const float w = fmaf(num, float(r2), float(r2 * r2));
     a = rsqrt_approx(w);
-    return num * rcp_approx(fmaf(w, a, float(r2)));
+    return __fmul_rn(num, rcp_approx(fmaf(w, a, float(r2))));
 }
 
 // Slots are evaluated grouped by length class |d|^2 (1, 2, 3, 4, 5, 6, 8, 9),

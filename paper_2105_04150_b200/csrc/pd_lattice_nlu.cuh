@@ -105,7 +105,10 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* p, unsigned bytes) 
 }
 
 struct AccN {
-    float gx, gy, gz, fx, fy, fz;
+    float2 gxy;
+    float gz;
+    float2 fxy;
+    float fz;
     float emax;  // largest e over live breakable slots
 };
 
@@ -195,8 +198,9 @@ __device__ __forceinline__ void nl_slot(const float4* own, const float4& ri, con
     }
 #endif
     const float4 rj = own[off];
-    float s, a, cx, cy, cz;
-    stretch_c<dx, dy, dz>(rj, ri, s, a, cx, cy, cz);
+    float s, a, cz;
+    float2 cxy;
+    stretch_c<dx, dy, dz>(rj, ri, s, a, cxy, cz);
     // breakable: live and neither end no-failure (nfthr = +inf for a
     // no-failure node; rj.w < 0 for a no-failure neighbour)
     const bool brk_ok = live && (!NF || rj.w >= nfthr);
@@ -225,16 +229,15 @@ __device__ __forceinline__ void nl_slot(const float4* own, const float4& ri, con
     if (LAM)
         scale *= lam;
     if (live) {
-        acc.gx = fmaf(cx, scale, acc.gx);
-        acc.gy = fmaf(cy, scale, acc.gy);
+        acc.gxy = __ffma2_rn(cxy, make_float2(scale, scale), acc.gxy);
         acc.gz = fmaf(cz, scale, acc.gz);
     }
     if constexpr (kOrder.last[K]) {
         constexpr float len = root(dx * dx + dy * dy + dz * dz);
-        acc.fx = fmaf(acc.gx, len, acc.fx);
-        acc.fy = fmaf(acc.gy, len, acc.fy);
+        acc.fxy = __ffma2_rn(acc.gxy, make_float2(len, len), acc.fxy);
         acc.fz = fmaf(acc.gz, len, acc.fz);
-        acc.gx = acc.gy = acc.gz = 0.f;
+        acc.gxy = make_float2(0.f, 0.f);
+        acc.gz = 0.f;
     }
 }
 
@@ -354,7 +357,7 @@ __global__ void __launch_bounds__(BX * BY * 4, 4) lattice_nlu_kernel(DevArgs A, 
     const float inf = __int_as_float(0x7f800000);
     const float nfthr = (NF && ri.w < 0.f) ? inf : 0.f;
     const NlRegLaw& R = L.rl;
-    AccN acc{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, -inf};
+    AccN acc{make_float2(0.f, 0.f), 0.f, make_float2(0.f, 0.f), 0.f, -inf};
     nl_all_slots<NBP, LAM, NF>(std::make_integer_sequence<int, NPAT>{}, own, ri, m, hb, lb,
                                nfthr, R, tab, hr, lr, acc);
     if (acc.emax >= (NBP == 0 ? 0.f : R.sc)) {  // some live bond breaks this step
@@ -363,11 +366,11 @@ __global__ void __launch_bounds__(BX * BY * 4, 4) lattice_nlu_kernel(DevArgs A, 
         const uint4 d = nl_slow_node<NBP, LAM, NF>(L, own, ri, m, hb, lb, nfthr, R, tab, R.sc, f);
         L.mask[i] = make_uint4(m.x & ~d.x, m.y & ~d.y, m.z & ~d.z, m.w & ~d.w);
         A.n_neigh[i] -= __popc(d.x) + __popc(d.y) + __popc(d.z) + __popc(d.w);
-        acc.fx = f.x;
-        acc.fy = f.y;
+        acc.fxy = make_float2(f.x, f.y);
         acc.fz = f.z;
     }
-    const double Fx = double(acc.fx * L.cv), Fy = double(acc.fy * L.cv), Fz = double(acc.fz * L.cv);
+    const double Fx = double(acc.fxy.x * L.cv), Fy = double(acc.fxy.y * L.cv),
+                 Fz = double(acc.fz * L.cv);
     if (MODE == 0) {
         A.body_force[3 * i] = Fx;
         A.body_force[3 * i + 1] = Fy;

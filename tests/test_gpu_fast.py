@@ -327,6 +327,10 @@ NLU_LAWS = {
     "trilinear_convex_kink": lambda: DamageLaw.trilinear(1.0, 5e-6, 1.5e-5, 4e-5, 0.25),
     "trilinear_concave": lambda: DamageLaw.trilinear(1.0, 1e-5, 2e-5, 3e-5, 0.9),
     "pmb": lambda: DamageLaw.pmb(1.0, 4e-5),
+    # several laws by bond type (the typed kernel): bond types from a rebar line
+    "typed": lambda: [DamageLaw.trilinear(1.0, 5e-6, 1.5e-5, 4e-5, 0.25),
+                      DamageLaw.pmb(3.0, 6e-5),
+                      DamageLaw.bilinear(2.0, 1e-5, 3e-5)],
 }
 
 
@@ -338,9 +342,12 @@ def test_lattice_unrolled_nl_kernel(oracle, monkeypatch, law, extras):
     fp64 oracle and against the NL loop kernel (PD_LAT_NL_LOOP), with beta,
     no-failure nodes and a displacement BC in the second variant."""
     b, h, g = S.bench_lattice_bundle((20, 16, 12))
-    b.model.laws = [NLU_LAWS[law]()]
+    laws = NLU_LAWS[law]()
+    b.model.laws = laws if isinstance(laws, list) else [laws]
     n = b.particles.size()
     fam = geometry.build_family(b.particles.coords, h, g)
+    if law == "typed":
+        fam.bond_type = S.classify_bonds(b.particles.coords, fam, rebar_y=8.0, rebar_z=6.0)
     if extras != "plain":
         b.corrections.beta = np.random.default_rng(5).uniform(0.6, 1.0, fam.entries.size)
         z = b.particles.coords[2::3]
@@ -371,7 +378,7 @@ def test_lattice_unrolled_nl_kernel(oracle, monkeypatch, law, extras):
     oracle.simulate(b, ref, SimulateOptions(steps, 0, 0, IntegratorKind.velocity_verlet))
     broken = int(fam.n_neigh.sum() - ref.connectivity.n_neigh.sum())
     assert broken > 0  # the laws above break bonds at this amplitude
-    s_c = b.model.laws[0].breakpoints[-1]
+    s_c = max(lw.breakpoints[-1] for lw in b.model.laws)
     for mode, st in outs.items():
         assert max_rel_difference(ref.u, st.u) <= FRACTURE_U_TOL, mode
         diff = int((ref.connectivity.entries != st.connectivity.entries).sum())

@@ -188,7 +188,9 @@ __global__ void __launch_bounds__(TT, MINB) fast_step_kernel(DevArgs A, FastDev 
             const float s = num * rr * rcp_approx(cur2 * rc + ref2 * rr);
             float scale;
             if (KIND != 2) {
-                const bool brk = KIND == 0 ? (s >= sc_pmb) : (s >= sc_pmb && offB < nf_start);
+                // !(s < s_c): an fp32 stretch that overflowed is NaN and breaks, as the
+                // reference's +inf stretch does (engine.cpp:90-98)
+                const bool brk = KIND == 0 ? !(s < sc_pmb) : (!(s < sc_pmb) && offB < nf_start);
                 if (brk) {
                     bmask |= 1u << q;  // stored after the 8 slots, off the hot path
                     continue;
@@ -206,7 +208,7 @@ __global__ void __launch_bounds__(TT, MINB) fast_step_kernel(DevArgs A, FastDev 
                 if (no_fail) {
                     f = law.c * s;
                 } else if (law.nbp == 1) {
-                    if (s >= law.bp[0]) {
+                    if (!(s < law.bp[0])) {
                         lrow[q] = 0;
                         ++broke;
                         continue;
@@ -217,7 +219,7 @@ __global__ void __launch_bounds__(TT, MINB) fast_step_kernel(DevArgs A, FastDev 
                     const float hh = F.hist[sidx];
                     if (s > hh)
                         F.hist[sidx] = s;
-                    if (hh >= s_c || s >= s_c) {
+                    if (hh >= s_c || !(s < s_c)) {
                         lrow[q] = 0;
                         ++broke;
                         continue;

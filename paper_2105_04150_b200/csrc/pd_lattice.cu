@@ -78,7 +78,7 @@ __device__ __forceinline__ void slot(const float4* own, const float4& ri, const 
         acc.gxy = __ffma2_rn(cxy, make_float2(scale, scale), acc.gxy);
         acc.gz = fmaf(cz, scale, acc.gz);
         if (!NF || rj.w >= 0.f)
-            acc.smax = fmaxf(acc.smax, s);
+            acc.smax = fmax_nan(acc.smax, s);
     }
     if constexpr (kOrder.last[K]) {  // close the class: times |d|
         constexpr float len = root(dx * dx + dy * dy + dz * dz);
@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(BX * BY * BZT, MINB) lattice_step_kernel(DevAr
     const float sc = (NF && ri.w < 0.f) ? __int_as_float(0x7f800000) : L.sc;
     Acc a{make_float2(0.f, 0.f), 0.f, make_float2(0.f, 0.f), 0.f, -__int_as_float(0x7f800000)};
     all_slots<NF>(std::make_integer_sequence<int, NPAT>{}, own, ri, m, a);
-    if (a.smax >= sc) {  // some live bond breaks this step
+    if (!(a.smax < sc)) {  // some live bond breaks this step (or its stretch overflowed)
         float3 f;
         const uint4 d = slow_node<NF>(own, ri, m, sc, f);
         L.mask[i] = make_uint4(m.x & ~d.x, m.y & ~d.y, m.z & ~d.z, m.w & ~d.w);
@@ -289,13 +289,13 @@ __global__ void __launch_bounds__(BX * BY * 4, 4) lattice_nl_kernel(DevArgs A, L
                 if (nfi || rj.w < 0.f) {
                     f = law.c * s;  // a no-failure end: never breaks, no history
                 } else if (law.nbp == 1) {
-                    brk = s >= law.bp[0];
+                    brk = !(s < law.bp[0]);
                     f = law.c * s;
                 } else {
                     const float s_c = law.bp[law.nbp - 1];
                     if (s > hh)
                         hp[(c0 + q) * NLB] = s;  // history before the break test (engine.cpp:88-92)
-                    brk = hh >= s_c || s >= s_c;
+                    brk = hh >= s_c || !(s < s_c);
                     f = (s >= hh) ? fast_envelope(law, s)
                                   : (hh < law.bp[0] ? law.sl[0] : fast_envelope(law, hh) * rcp_approx(hh)) * s;
                 }
@@ -303,13 +303,13 @@ __global__ void __launch_bounds__(BX * BY * 4, 4) lattice_nl_kernel(DevArgs A, L
                 if (nfi || rj.w < 0.f) {
                     f = R.c * s;
                 } else if (!R.hist) {
-                    brk = s >= R.sc;
+                    brk = !(s < R.sc);
                     f = R.c * s;
                 } else {
                     if (s > hh)
                         hp[(c0 + q) * NLB] = s;
                     const float e = fmaxf(s, hh);
-                    brk = e >= R.sc;
+                    brk = !(e < R.sc) || !(s < R.sc);
                     const float env = reg_envelope(R, e);
                     f = (s >= hh) ? env : (hh < R.bp0 ? R.sl0 : env * rcp_approx(hh)) * s;
                 }

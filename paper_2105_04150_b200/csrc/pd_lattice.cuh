@@ -132,6 +132,21 @@ __device__ __forceinline__ float stretch_r(const float4& rj, const float4& ri, i
     return __fmul_rn(num, rcp_approx(fmaf(w, a, float(r2))));
 }
 
+// max that propagates NaN (max.NaN.f32, one FMNMX): an fp32 stretch that
+// overflowed (|xi + eta|^2 beyond fp32 range gives inf * 0 in the cancellation-
+// free form) is NaN, and a NaN stretch breaks its bond as the reference's
+// +inf stretch does (engine.cpp:90-98); breaks are tested as !(s < s_c)
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+    float r;
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ float fmax_nan3(float a, float b, float c) {  // one FMNMX3
+    float r;
+    asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+
 // Slots are evaluated grouped by length class |d|^2 (1, 2, 3, 4, 5, 6, 8, 9),
 // pattern order within a class; K is the position in that order.
 struct ClassOrder {

@@ -122,7 +122,7 @@ constexpr int ND = 8;  // ring depth (slots of history / lambda loads in flight)
 // +1 convex first kink / -1, +1 convex second kink / -1)
 __device__ __forceinline__ float nl_law_typed(const float4& p0, const float4& p1, float s, float hh,
                                               float& e) {
-    e = fmaxf(fmaxf(s, hh), 1e-30f);
+    e = fmax_nan3(s, hh, 1e-30f);
     const float l0 = p0.x * e, l1 = fmaf(p0.y, e, p0.z), l2 = fmaf(p1.x, e, p1.y);
     const float t = p1.w > 0.f ? fmaxf(l1, l2) : fminf(l1, l2);
     const float env = p1.z > 0.f ? fmaxf(l0, t) : fminf(l0, t);
@@ -135,7 +135,7 @@ __device__ __forceinline__ float nl_law(const NlRegLaw& R, float s, float hh, fl
         e = s;
         return R.c * s;
     }
-    e = fmaxf(fmaxf(s, hh), 1e-30f);
+    e = fmax_nan3(s, hh, 1e-30f);
     const float l0 = R.sl0 * e, l1 = fmaf(R.sl1, e, R.a1), l2 = fmaf(R.sl2, e, R.a2);
     const float t = R.cvx2 ? fmaxf(l1, l2) : fminf(l1, l2);
     const float env = R.cvx1 ? fmaxf(l0, t) : fminf(l0, t);
@@ -213,7 +213,7 @@ __device__ __forceinline__ void nl_slot(const float4* own, const float4& ri, con
         stg_typed_if<NF>(hb + C * NLB, mw & bit, rj.w, nfthr, p0.w, s, hh,
                          (__float_as_uint(s) & ~7u) | ty);
         if (brk_ok)  // e >= s_c of the bond's own law <=> e - |s_c| >= 0 (exact sign)
-            acc.emax = fmaxf(acc.emax, e - fabsf(p0.w));
+            acc.emax = fmax_nan(acc.emax, e - fabsf(p0.w));
     } else {
         f = nl_law<NBP>(R, s, hh, e);
         if (NF && !brk_ok)
@@ -221,7 +221,7 @@ __device__ __forceinline__ void nl_slot(const float4* own, const float4& ri, con
         if (NBP > 1)
             stg_hist_if<NF>(hb + C * NLB, mw & bit, rj.w, nfthr, s, hh);
         if (brk_ok)
-            acc.emax = fmaxf(acc.emax, e);
+            acc.emax = fmax_nan(acc.emax, e);
     }
     float scale = f * a;
     if (NF)
@@ -294,7 +294,7 @@ __device__ __forceinline__ uint4 nl_slow_node(const LatticeArgs& L, const float4
         } else {
             f = nl_law<NBP>(R, s, NBP > 1 ? hb[c * NLB] : 0.f, e);
         }
-        if (brk_ok && e >= s_c) {
+        if (brk_ok && !(e < s_c)) {
             dead[c >> 5] |= 1u << (c & 31);
             continue;
         }
@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(BX * BY * 4, 4) lattice_nlu_kernel(DevArgs A, 
     AccN acc{make_float2(0.f, 0.f), 0.f, make_float2(0.f, 0.f), 0.f, -inf};
     nl_all_slots<NBP, LAM, NF>(std::make_integer_sequence<int, NPAT>{}, own, ri, m, hb, lb,
                                nfthr, R, tab, hr, lr, acc);
-    if (acc.emax >= (NBP == 0 ? 0.f : R.sc)) {  // some live bond breaks this step
+    if (!(acc.emax < (NBP == 0 ? 0.f : R.sc))) {  // a live bond breaks (or overflowed)
         asm volatile("" ::: "memory");  // after this node's history stores
         float3 f;
         const uint4 d = nl_slow_node<NBP, LAM, NF>(L, own, ri, m, hb, lb, nfthr, R, tab, R.sc, f);

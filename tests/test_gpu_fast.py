@@ -389,3 +389,52 @@ def test_lattice_unrolled_nl_kernel(oracle, monkeypatch, law, extras):
             live = (ref.connectivity.entries >= 0) & (st.connectivity.entries >= 0)
             err = np.abs(ref.bond_history[live] - st.bond_history[live])
             assert np.max(err) <= 1e-4 * max(s_c, np.max(np.abs(ref.bond_history))), mode
+
+
+@pytest.mark.parametrize("layout", [None, "general"])
+@pytest.mark.parametrize("law", ["pmb", "trilinear"])
+def test_fast_nonfinite_raises_like_the_reference(oracle, monkeypatch, layout, law):
+    """A non-finite displacement stops the fast variant with the reference's
+    error (check_state_finite, engine.cpp:23-28): same exception, same step,
+    on the lattice kernels and on the tile kernel."""
+    from paper_2105_04150_b200 import abi
+    if layout:
+        monkeypatch.setenv("PD_FAST_LAYOUT", layout)
+    else:
+        monkeypatch.delenv("PD_FAST_LAYOUT", raising=False)
+    b, h, g = S.bench_lattice_bundle((16, 12, 10))
+    if law == "trilinear":
+        b.model.laws = [DamageLaw.trilinear(1.0, 1e-3, 2e-3, 1e6)]
+    fam = geometry.build_family(b.particles.coords, h, g)
+    msgs = []
+    for be, variant in ((oracle, KernelVariant.bond_parallel), (engine.backend(), KernelVariant.fast)):
+        st = make_state(fam, b.model.needs_history())
+        st.u = S.seed_displacements(b.particles.coords)
+        st.u[3 * 77 + 1] = np.nan
+        with pytest.raises(abi.PeridynRuntimeError) as ei:
+            be.simulate(b, st, SimulateOptions(20, 0, 5, IntegratorKind.velocity_verlet, variant))
+        msgs.append(str(ei.value))
+    assert msgs[0] == msgs[1]
+
+
+@pytest.mark.parametrize("layout", [None, "general"])
+def test_fast_nonfinite_midrun_raises_like_the_reference(oracle, monkeypatch, layout):
+    """A blow-up mid-run (an enormous force BC, as test_gpu_parity's exact-path
+    case) stops the fast variant at the reference's step with its message."""
+    from paper_2105_04150_b200 import abi
+    if layout:
+        monkeypatch.setenv("PD_FAST_LAYOUT", layout)
+    else:
+        monkeypatch.delenv("PD_FAST_LAYOUT", raising=False)
+    b, h, g = S.bench_lattice_bundle((16, 12, 10), s_c=1e9)
+    b.dt = 0.05  # the reference overflows u at step 25
+    b.bc.kind[3 * 300] = BCKind.force
+    b.bc.magnitude[3 * 300] = 1.5e308
+    fam = geometry.build_family(b.particles.coords, h, g)
+    msgs = []
+    for be, variant in ((oracle, KernelVariant.bond_parallel), (engine.backend(), KernelVariant.fast)):
+        st = make_state(fam, False)
+        with pytest.raises(abi.PeridynRuntimeError) as ei:
+            be.simulate(b, st, SimulateOptions(200, 0, 0, IntegratorKind.velocity_verlet, variant))
+        msgs.append(str(ei.value))
+    assert msgs[0] == msgs[1]

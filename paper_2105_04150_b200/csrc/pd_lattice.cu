@@ -491,8 +491,26 @@ cudaError_t launch_cfg(const DevArgs& A, const LatticeArgs& L, cudaStream_t st) 
 // is lighter and 6 CTAs/SM (40 registers) fit.  PD_LAT_CFG selects
 // alternatives for the bench configuration: 1 = 16x4x8 x3, 2 = 16x4x4 x4,
 // 3 = 16x4x8 x2, 4 = 16x4x4 x5.
+int sm_count() {
+    static const int n = [] {
+        int dev = 0, v = 0;
+        cudaGetDevice(&dev);
+        return cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0
+                   ? v
+                   : 148;
+    }();
+    return n;
+}
+
 template <int MODE, bool BC, bool NF>
 cudaError_t launch_bc(const DevArgs& A, const LatticeArgs& L, cudaStream_t st) {
+    // Small models (fewer 16x4x4 bricks than two per SM, e.g. cfg1's beam):
+    // the step is one latency chain per thread, so use 16x4x1 bricks (more
+    // CTAs over the SMs) and the full register file (the compiler can overlap
+    // several slots).  PD_LAT_CFG = 5 forces it, 6 forbids it.
+    const long long bricks4 = (long long)((L.nx + 15) / 16) * ((L.ny + 3) / 4) * ((L.nz_own + 3) / 4);
+    if (L.cfg == 5 || (L.cfg != 6 && bricks4 < 2LL * sm_count()))
+        return launch_cfg<MODE, 1, 1, BC, NF>(A, L, st);
     if constexpr (!NF && !BC) {
         switch (L.cfg) {
         case 1: return launch_cfg<MODE, 8, 3, BC, NF>(A, L, st);
@@ -516,6 +534,8 @@ template <int MODE> cudaError_t launch_mode(const DevArgs& A, const LatticeArgs&
 template <int MODE, bool BC, bool NF> void preload_bc() {
     preload_fn(lattice_step_kernel<MODE, 4, BC ? 5 : 6, BC, NF>);
     configure_one<MODE, 4, BC ? 5 : 6, BC, NF>();
+    preload_fn(lattice_step_kernel<MODE, 1, 1, BC, NF>);
+    configure_one<MODE, 1, 1, BC, NF>();
     if constexpr (!NF && !BC) {
         preload_fn(lattice_step_kernel<MODE, 8, 2, BC, NF>);
         preload_fn(lattice_step_kernel<MODE, 8, 3, BC, NF>);

@@ -200,6 +200,43 @@ __device__ __forceinline__ void stage_box(const DevArgs& A, const LatticeArgs& L
     constexpr int TT = BX * BY * BZT, HZ = BZT + 6;
     const long long plane = (long long)L.nx * L.ny;
     const float ih = float(L.inv_h);
+    if constexpr (TT < HX * HY) {
+        // small bricks (fewer threads than a box plane has records): record r
+        // of the box at r = t, t + TT, ..., four in flight per thread
+        constexpr int NR = HX * HY * HZ, PL = 4;
+        for (int r0 = threadIdx.x; r0 < NR; r0 += TT * PL) {
+            double4 u[PL];
+            bool ok[PL];
+            float wv[PL];
+#pragma unroll
+            for (int k = 0; k < PL; ++k) {
+                const int r = r0 + k * TT;
+                const int pz = r / (HX * HY), q = r % (HX * HY);
+                const int X = gx0 - 3 + q % HX, Y = gy0 - 3 + q / HX, Z = gz0 - 3 + pz;
+                ok[k] = r < NR && X >= 0 && X < L.nx && Y >= 0 && Y < L.ny && Z >= 0 &&
+                        Z < L.nz_local;
+                u[k] = make_double4(0.0, 0.0, 0.0, 0.0);
+                wv[k] = 0.f;
+                if (ok[k]) {
+                    const long long j = X + (long long)L.nx * Y + plane * Z;
+                    u[k] = A.u_in[j];
+                    if (NF) {
+                        const float vf = L.vol_varies ? float(A.xv[j].w * L.inv_v0) : 1.f;
+                        wv[k] = u[k].w != 0.0 ? -vf : vf;
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < PL; ++k) {
+                const int r = r0 + k * TT;
+                if (r < NR)
+                    rec[r] = ok[k] ? make_float4(float(u[k].x - U0.x) * ih, float(u[k].y - U0.y) * ih,
+                                                 float(u[k].z - U0.z) * ih, wv[k])
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
+        return;
+    }
     {
         constexpr int PREC = HX * HY;          // records per box plane
         constexpr int PPASS = TT / PREC;       // planes per pass (1 or 2)

@@ -193,10 +193,13 @@ def test_fast_million_node_lattice(oracle):
     assert max_rel_difference(outs[1].a, outs[0].a) <= FORCE_TOL
 
 
-def test_lattice_layout_selected_and_matches_tiles(oracle, monkeypatch):
+@pytest.mark.parametrize("lat_cfg", ["0", "5", "6"])
+def test_lattice_layout_selected_and_matches_tiles(oracle, monkeypatch, lat_cfg):
     """PD_FAST on the bench lattice runs the implicit-connectivity kernel
-    (pd_lattice.cu); forced onto the general tile layout the same run must
+    (pd_lattice.cu) -- by size (0), the small-brick latency variant (5) or the
+    16x4x4 bricks (6); forced onto the general tile layout the same run must
     agree with it within the fast-path tolerance, and both with the oracle."""
+    monkeypatch.setenv("PD_LAT_CFG", lat_cfg)
     b, h, g = S.bench_lattice_bundle((20, 18, 26), s_c=1.5e-5)
     fam = geometry.build_family(b.particles.coords, h, g)
     layouts, states = [], []
@@ -291,11 +294,13 @@ def test_lattice_nl_kernel_matches_tiles_and_oracle(oracle, monkeypatch):
     assert fam.n_neigh.sum() > ref.connectivity.n_neigh.sum()  # it fractured
 
 
+@pytest.mark.parametrize("lat_cfg", ["5", "6"])
 @pytest.mark.parametrize("integrator", [IntegratorKind.euler, IntegratorKind.velocity_verlet])
-def test_lattice_no_failure_and_volumes_match_oracle(oracle, integrator):
+def test_lattice_no_failure_and_volumes_match_oracle(oracle, integrator, monkeypatch, lat_cfg):
     """cfg1-style run on the lattice layout: the 3-point-bend beam (no-failure
     supports and load patch, PMB, quintic ramp) with per-node volumes, against
-    the fp64 oracle."""
+    the fp64 oracle, on the small-brick (5) and 16x4x4-brick (6) kernels."""
+    monkeypatch.setenv("PD_LAT_CFG", lat_cfg)
     b, h, g = S.beam_bundle(30, 10, 10)
     rng = np.random.default_rng(11)
     b.particles.volume = b.particles.volume * rng.uniform(0.8, 1.2, b.particles.volume.size)

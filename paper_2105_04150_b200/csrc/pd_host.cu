@@ -131,12 +131,43 @@ bool needs_history(const pd_damage_model& m) {
     return false;
 }
 
+// true when pred(k) holds for some k in [0, n): chunks on several host threads
+// (the validation scans are O(n) over 10M-node arrays); the callers rescan
+// serially only on failure, to report the first failing index
+template <class Pred> bool par_any(int64_t n, Pred pred) {
+    const int64_t parts = std::min<int64_t>(std::max(1u, std::thread::hardware_concurrency()),
+                                            n / (int64_t(1) << 20) + 1);
+    if (parts <= 1) {
+        for (int64_t k = 0; k < n; ++k)
+            if (pred(k))
+                return true;
+        return false;
+    }
+    std::atomic<bool> hit{false};
+    std::vector<std::thread> th;
+    const int64_t step = (n + parts - 1) / parts;
+    for (int64_t p = 0; p < parts; ++p)
+        th.emplace_back([&, p] {
+            const int64_t b = p * step, e = std::min(n, b + step);
+            for (int64_t k = b; k < e && !hit.load(std::memory_order_relaxed); ++k)
+                if (pred(k)) {
+                    hit = true;
+                    return;
+                }
+        });
+    for (auto& t : th)
+        t.join();
+    return hit;
+}
+
 int particles_validate(const pd_particles& p) {
     const int64_t n = p.n;
     if (n < 1)
         return fail(PD_E_INVALID_ARGUMENT, "ParticleSet: empty");
     if (p.coords_size != 3 * n || p.density_size != n)
         return fail(PD_E_INVALID_ARGUMENT, "ParticleSet: field lengths differ");
+    if (!par_any(n, [&](int64_t i) { return !(p.volume[i] > 0) || !(p.density[i] > 0); }))
+        return PD_OK;
     for (int64_t i = 0; i < n; ++i) {
         if (!(p.volume[i] > 0))
             return fail(PD_E_INVALID_ARGUMENT, "ParticleSet: non-positive volume at node %lld",
@@ -155,9 +186,8 @@ int bc_validate(const pd_boundary& bc, int64_t n) {
                     "BoundaryConditions: field lengths do not match node count");
     if (bc.n_ramps < 1)
         return fail(PD_E_INVALID_ARGUMENT, "BoundaryConditions: no ramp profiles");
-    for (int64_t k = 0; k < 3 * n; ++k)
-        if (bc.ramp_id[k] >= bc.n_ramps)
-            return fail(PD_E_INVALID_ARGUMENT, "BoundaryConditions: ramp id out of range");
+    if (par_any(3 * n, [&](int64_t k) { return bc.ramp_id[k] >= bc.n_ramps; }))
+        return fail(PD_E_INVALID_ARGUMENT, "BoundaryConditions: ramp id out of range");
     for (int32_t s = 0; s < bc.n_tip_sets; ++s)
         for (int64_t t = bc.tip_offsets[s]; t < bc.tip_offsets[s + 1]; ++t)
             if (bc.tip_nodes[t] < 0 || bc.tip_nodes[t] >= n)
@@ -494,9 +524,7 @@ int upload_common(pd_ctx* ctx, const pd_particles& p, const pd_state& st,
 int upload_bc(pd_ctx* ctx, const pd_boundary& bc) {
     cudaStream_t s = ctx->stream;
     const int64_t n = ctx->n;
-    bool any = false;
-    for (int64_t k = 0; k < 3 * n && !any; ++k)
-        any = bc.kind[k] != PD_BC_FREE;
+    const bool any = par_any(3 * n, [&](int64_t k) { return bc.kind[k] != PD_BC_FREE; });
     ctx->has_bc = any;
     if (any) {
         PD_CK(ctx->bc_kind.upload(bc.kind, size_t(3 * n), s));

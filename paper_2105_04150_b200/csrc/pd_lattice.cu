@@ -380,12 +380,40 @@ __global__ void lattice_mask_kernel(const int32_t* entries, long long begin, lon
         return;
     const long long plane = (long long)nx * ny;
     const int ix = int(i % nx), iy = int((i / nx) % ny), iz = int(i / plane);
+    // decode d = j - i = dx + nx dy + plane dz by rounding with fp32
+    // reciprocals (no integer division per entry): exact whenever |dx|, |dy|
+    // <= 3 and nx, ny >= 8 (|dx + nx dy| < plane / 2, |dx| < nx / 2); the
+    // decoded offset is then checked against the pattern box and the lattice
+    // bounds, so a wrong decode can only flag a row as off-pattern
+    const float inv_plane = 1.0f / float(plane), inv_nx = 1.0f / float(nx);
+    const bool fast_decode = nx >= 8 && ny >= 8 && plane < (1LL << 22);
     unsigned w[4] = {0u, 0u, 0u, 0u};
     for (int k = 0; k < N; ++k) {
         const int32_t j = entries[i * N + k];
         if (j < 0)
             continue;
-        const int dx = int(j % nx) - ix, dy = int((j / nx) % ny) - iy, dz = int(j / plane) - iz;
+        int dx, dy, dz;
+        if (fast_decode) {
+            const long long dl = (long long)j - i;
+            if (dl < -4 * plane || dl > 4 * plane) {
+                atomicExch(bad, 1);
+                return;
+            }
+            const int d = int(dl);
+            dz = __float2int_rn(float(d) * inv_plane);
+            const int r = d - dz * int(plane);
+            dy = __float2int_rn(float(r) * inv_nx);
+            dx = r - dy * nx;
+            if (ix + dx < 0 || ix + dx >= nx || iy + dy < 0 || iy + dy >= ny || iz + dz < 0 ||
+                iz + dz >= L.nz_local) {
+                atomicExch(bad, 1);
+                return;
+            }
+        } else {
+            dx = int(j % nx) - ix;
+            dy = int((j / nx) % ny) - iy;
+            dz = int(j / plane) - iz;
+        }
         const int c = (dx < -3 || dx > 3 || dy < -3 || dy > 3 || dz < -3 || dz > 3)
                           ? -1
                           : int(c_slot[(dz + 3) * 49 + (dy + 3) * 7 + (dx + 3)]);

@@ -27,13 +27,14 @@ namespace {
 
 constexpr size_t kChunk = size_t(32) << 20;
 constexpr size_t kDirect = size_t(8) << 20;
+constexpr int kBuf = 3;  // bounce buffers: host fill, DMA and one spare in flight
 
 struct Bounce {
-    void* buf[2] = {nullptr, nullptr};
-    cudaEvent_t done[2] = {nullptr, nullptr};
+    void* buf[kBuf] = {};
+    cudaEvent_t done[kBuf] = {};
     int device = -1;
     ~Bounce() {
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < kBuf; ++k) {
             if (buf[k])
                 cudaFreeHost(buf[k]);
             if (done[k])
@@ -45,7 +46,7 @@ struct Bounce {
         cudaGetDevice(&dev);
         if (buf[0] && device == dev)
             return cudaSuccess;
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < kBuf; ++k) {
             if (!buf[k]) {
                 cudaError_t e = cudaHostAlloc(&buf[k], kChunk, cudaHostAllocPortable);
                 if (e != cudaSuccess)
@@ -166,9 +167,9 @@ cudaError_t h2d_large(void* dev, const void* host, size_t bytes, cudaStream_t s)
     cudaError_t e = B.ensure();
     if (e != cudaSuccess)
         return e;
-    bool used[2] = {false, false};
+    bool used[kBuf] = {};
     for (size_t off = 0, k = 0; off < bytes; off += kChunk, ++k) {
-        const int b = int(k & 1);
+        const int b = int(k % kBuf);
         const size_t n = std::min(kChunk, bytes - off);
         if (used[b] && (e = cudaEventSynchronize(B.done[b])) != cudaSuccess)
             return e;
@@ -195,18 +196,20 @@ cudaError_t d2h_large(void* host, const void* dev, size_t bytes, cudaStream_t s)
     const size_t chunks = (bytes + kChunk - 1) / kChunk;
     auto issue = [&](size_t k) -> cudaError_t {
         const size_t off = k * kChunk, n = std::min(kChunk, bytes - off);
-        const int b = int(k & 1);
+        const int b = int(k % kBuf);
         cudaError_t r = cudaMemcpyAsync(B.buf[b], static_cast<const char*>(dev) + off, n,
                                         cudaMemcpyDeviceToHost, s);
         return r != cudaSuccess ? r : cudaEventRecord(B.done[b], s);
     };
-    if ((e = issue(0)) != cudaSuccess)
-        return e;
+    for (size_t k = 0; k + 1 < size_t(kBuf) && k < chunks; ++k)
+        if ((e = issue(k)) != cudaSuccess)
+            return e;
     for (size_t k = 0; k < chunks; ++k) {
-        const int b = int(k & 1);
+        const int b = int(k % kBuf);
         if ((e = cudaEventSynchronize(B.done[b])) != cudaSuccess)
             return e;
-        if (k + 1 < chunks && (e = issue(k + 1)) != cudaSuccess)
+        // the buffer drained last iteration is free again: keep kBuf - 1 DMAs queued
+        if (k + kBuf - 1 < chunks && (e = issue(k + kBuf - 1)) != cudaSuccess)
             return e;
         const size_t off = k * kChunk, n = std::min(kChunk, bytes - off);
         par_memcpy(static_cast<char*>(host) + off, B.buf[b], n);

@@ -372,11 +372,15 @@ struct SlotSrc {  // reference-layout per-slot arrays (n x N) to scatter into [c
     const double* beta;
 };
 
+// One warp per row: lane l reads slots l, l + 32, ... (coalesced), decodes each
+// live entry to its pattern slot, scatters the per-bond values to the
+// brick-major arrays, and the row's mask is the warp's OR.
 __global__ void lattice_mask_kernel(const int32_t* entries, long long begin, long long end, int N,
                                     int nx, int ny, uint4* mask, int* bad, SlotSrc src,
                                     LatticeArgs L) {
-    const long long i = begin + blockIdx.x * 256LL + threadIdx.x;
-    if (i >= end)
+    const long long i = begin + (blockIdx.x * 256LL + threadIdx.x) / 32;
+    const int lane = threadIdx.x & 31;
+    if (i >= end)  // warp-uniform
         return;
     const long long plane = (long long)nx * ny;
     const int ix = int(i % nx), iy = int((i / nx) % ny), iz = int(i / plane);
@@ -387,27 +391,25 @@ __global__ void lattice_mask_kernel(const int32_t* entries, long long begin, lon
     // bounds, so a wrong decode can only flag a row as off-pattern
     const float inv_plane = 1.0f / float(plane), inv_nx = 1.0f / float(nx);
     const bool fast_decode = nx >= 8 && ny >= 8 && plane < (1LL << 22);
+    const long long sb = slot_base(L, i);
     unsigned w[4] = {0u, 0u, 0u, 0u};
-    for (int k = 0; k < N; ++k) {
+    bool off = false;
+    for (int k = lane; k < N; k += 32) {
         const int32_t j = entries[i * N + k];
         if (j < 0)
             continue;
         int dx, dy, dz;
         if (fast_decode) {
             const long long dl = (long long)j - i;
-            if (dl < -4 * plane || dl > 4 * plane) {
-                atomicExch(bad, 1);
-                return;
-            }
-            const int d = int(dl);
+            const int d = int(max(min(dl, 4 * plane), -4 * plane));
             dz = __float2int_rn(float(d) * inv_plane);
             const int r = d - dz * int(plane);
             dy = __float2int_rn(float(r) * inv_nx);
             dx = r - dy * nx;
-            if (ix + dx < 0 || ix + dx >= nx || iy + dy < 0 || iy + dy >= ny || iz + dz < 0 ||
-                iz + dz >= L.nz_local) {
-                atomicExch(bad, 1);
-                return;
+            if (dl != d || ix + dx < 0 || ix + dx >= nx || iy + dy < 0 || iy + dy >= ny ||
+                iz + dz < 0 || iz + dz >= L.nz_local) {
+                off = true;
+                continue;
             }
         } else {
             dx = int(j % nx) - ix;
@@ -418,11 +420,11 @@ __global__ void lattice_mask_kernel(const int32_t* entries, long long begin, lon
                           ? -1
                           : int(c_slot[(dz + 3) * 49 + (dy + 3) * 7 + (dx + 3)]);
         if (c < 0) {
-            atomicExch(bad, 1);
-            return;
+            off = true;
+            continue;
         }
         w[c >> 5] |= 1u << (c & 31);
-        const long long sidx = slot_base(L, i) + (long long)c * NLB, idx = i * N + k;
+        const long long sidx = sb + (long long)c * NLB, idx = i * N + k;
         if (L.typed) {  // history word: fp32 history, bond type in the low 3 bits
             const unsigned h = src.hist ? __float_as_uint(float(src.hist[idx])) & ~7u : 0u;
             L.hist[sidx] = __uint_as_float(h | (src.btype ? unsigned(src.btype[idx]) & 7u : 0u));
@@ -435,7 +437,12 @@ __global__ void lattice_mask_kernel(const int32_t* entries, long long begin, lon
             L.lam[sidx] = float((src.lambda ? src.lambda[idx] : 1.0) *
                                 (src.beta ? src.beta[idx] : 1.0));
     }
-    mask[i] = make_uint4(w[0], w[1], w[2], w[3]);
+    if (off)
+        atomicExch(bad, 1);
+    const uint4 m = make_uint4(__reduce_or_sync(0xffffffffu, w[0]), __reduce_or_sync(0xffffffffu, w[1]),
+                               __reduce_or_sync(0xffffffffu, w[2]), __reduce_or_sync(0xffffffffu, w[3]));
+    if (lane == 0)
+        mask[i] = m;
 }
 
 // entries in the reference layout: the uploaded row with -1 where the mask bit
@@ -687,7 +694,7 @@ cudaError_t lattice_build_masks(const double4* xv, long long n, const int32_t* e
     }
     SlotSrc src{hist, btype, lambda, beta};
     if (end > begin)
-        lattice_mask_kernel<<<unsigned((end - begin + 255) / 256), 256, 0, st>>>(
+        lattice_mask_kernel<<<unsigned((end - begin + 7) / 8), 256, 0, st>>>(
             entries, begin, end, N, L.nx, L.ny, mask, bad, src, L);
     return cudaGetLastError();
 }

@@ -552,8 +552,22 @@ cudaError_t launch_bc(const DevArgs& A, const LatticeArgs& L, cudaStream_t st) {
         case 2: return launch_cfg<MODE, 4, 4, BC, NF>(A, L, st);
         case 3: return launch_cfg<MODE, 8, 2, BC, NF>(A, L, st);
         case 4: return launch_cfg<MODE, 4, 5, BC, NF>(A, L, st);
+        case 7: return launch_cfg<MODE, 6, 4, BC, NF>(A, L, st);
+        case 8: return launch_cfg<MODE, 12, 2, BC, NF>(A, L, st);
         default: break;
         }
+    }
+    // Without BC code, 16x4x8 bricks at 3 CTAs/SM (40 registers) stage 6.0
+    // halo records per node against 8.6 for 16x4x4 and measured 5 % faster
+    // at 10M (profiles/) -- unless the owned planes
+    // leave a much emptier last z-brick (e.g. 27-plane slabs of 216 over 8
+    // GPUs), where 16x4x4 bricks waste less.
+    if constexpr (!BC) {
+        const int nz = L.nz_own;
+        const double waste8 = double((nz + 7) / 8 * 8 - nz) / nz;
+        const double waste4 = double((nz + 3) / 4 * 4 - nz) / nz;
+        if (L.cfg == 0 && waste8 - waste4 < 0.04)
+            return launch_cfg<MODE, 8, 3, BC, NF>(A, L, st);
     }
     return launch_cfg<MODE, 4, BC ? 5 : 6, BC, NF>(A, L, st);
 }
@@ -569,6 +583,10 @@ template <int MODE> cudaError_t launch_mode(const DevArgs& A, const LatticeArgs&
 template <int MODE, bool BC, bool NF> void preload_bc() {
     preload_fn(lattice_step_kernel<MODE, 4, BC ? 5 : 6, BC, NF>);
     configure_one<MODE, 4, BC ? 5 : 6, BC, NF>();
+    if constexpr (!BC) {
+        preload_fn(lattice_step_kernel<MODE, 8, 3, BC, NF>);
+        configure_one<MODE, 8, 3, BC, NF>();
+    }
     preload_fn(lattice_step_kernel<MODE, 1, 1, BC, NF>);
     configure_one<MODE, 1, 1, BC, NF>();
     if constexpr (!NF && !BC) {
@@ -576,6 +594,10 @@ template <int MODE, bool BC, bool NF> void preload_bc() {
         preload_fn(lattice_step_kernel<MODE, 8, 3, BC, NF>);
         preload_fn(lattice_step_kernel<MODE, 4, 4, BC, NF>);
         preload_fn(lattice_step_kernel<MODE, 4, 5, BC, NF>);
+        preload_fn(lattice_step_kernel<MODE, 6, 4, BC, NF>);
+        preload_fn(lattice_step_kernel<MODE, 12, 2, BC, NF>);
+        configure_one<MODE, 6, 4, BC, NF>();
+        configure_one<MODE, 12, 2, BC, NF>();
         configure_one<MODE, 8, 2, BC, NF>();
         configure_one<MODE, 8, 3, BC, NF>();
         configure_one<MODE, 4, 4, BC, NF>();

@@ -200,7 +200,10 @@ __device__ __forceinline__ void stage_box(const DevArgs& A, const LatticeArgs& L
     constexpr int TT = BX * BY * BZT, HZ = BZT + 6;
     const long long plane = (long long)L.nx * L.ny;
     const float ih = float(L.inv_h);
-    if constexpr (TT < HX * HY) {
+#ifndef PD_STAGE_FLAT
+#define PD_STAGE_FLAT 0
+#endif
+    if constexpr (TT < HX * HY || PD_STAGE_FLAT) {
         // small bricks (fewer threads than a box plane has records): record r
         // of the box at r = t, t + TT, ..., four in flight per thread
         constexpr int NR = HX * HY * HZ, PL = 4;

@@ -193,11 +193,12 @@ def test_fast_million_node_lattice(oracle):
     assert max_rel_difference(outs[1].a, outs[0].a) <= FORCE_TOL
 
 
-@pytest.mark.parametrize("lat_cfg", ["0", "5", "6"])
+@pytest.mark.parametrize("lat_cfg", ["0", "4", "5", "6"])
 def test_lattice_layout_selected_and_matches_tiles(oracle, monkeypatch, lat_cfg):
     """PD_FAST on the bench lattice runs the implicit-connectivity kernel
-    (pd_lattice.cu) -- by size (0), the small-brick latency variant (5) or the
-    16x4x4 bricks (6); forced onto the general tile layout the same run must
+    (pd_lattice.cu) -- chosen by size (0), 16x4x4 bricks at 5 CTAs/SM (4), the
+    small-brick latency variant (5) or the large-model choice (6: 16x4x8 bricks
+    without BC code); forced onto the general tile layout the same run must
     agree with it within the fast-path tolerance, and both with the oracle."""
     monkeypatch.setenv("PD_LAT_CFG", lat_cfg)
     b, h, g = S.bench_lattice_bundle((20, 18, 26), s_c=1.5e-5)

@@ -13,3 +13,6 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:latt
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:lattice_nlu -s 3 -c 1 -o gpurun_out/prof_nlu216 python bench.py --law trilinear --steps 2 --warmup 3 --no-cpu --e2e-steps 1 > gpurun_out/ncu_nlu.log 2>&1
 tail -3 gpurun_out/pytest_gpu.log; tail -2 gpurun_out/smoke.log
 for f in bench216 bench100 tri216 multi216 exact216; do tail -1 gpurun_out/$f.log | python3 -c "import json,sys; d=json.loads(sys.stdin.read()); print('$f', round(d['ms_per_step'],4), round(d['roofline']['frac'],4), '%.3e' % d['value'], 'e2e %.3e' % d['e2e']['value'])"; done
+timeout 600 env K=16 python scripts/bench_batch.py 2>&1 | tail -1 > gpurun_out/batch_cfg1.json
+timeout 300 python scripts/cfg1_one.py 1000 > gpurun_out/cfg1_one.log 2>&1
+cut -c1-300 gpurun_out/batch_cfg1.json; tail -1 gpurun_out/cfg1_one.log

@@ -214,8 +214,9 @@ __device__ __forceinline__ float reg_envelope(const NlRegLaw& R, float e) {
 // bond type, if any, can only name it).  MULTI = true: per-bond law from
 // constant memory, any number of breakpoints.
 template <int MODE, bool BC, bool MULTI>
-__global__ void __launch_bounds__(BX * BY * 4, 4) lattice_nl_kernel(DevArgs A, LatticeArgs L) {
-    constexpr int BZT = 4;
+__global__ void __launch_bounds__(BX * BY * NLBZ, 16 / NLBZ) lattice_nl_kernel(DevArgs A,
+                                                                              LatticeArgs L) {
+    constexpr int BZT = NLBZ;
     if (MODE != 0 && *(volatile long long*)A.err_step != kNoError)
         return;
     extern __shared__ float4 rec[];
@@ -615,7 +616,8 @@ template <int MODE> void preload_mode() {
 } // namespace
 
 long long lattice_slot_count(const LatticeArgs& L) {
-    const long long nbx = (L.nx + 15) / 16, nby = (L.ny + 3) / 4, nbz = (L.nz_own + 3) / 4;
+    const long long nbx = (L.nx + 15) / 16, nby = (L.ny + 3) / 4,
+                    nbz = (L.nz_own + NLBZ - 1) / NLBZ;
     return nbx * nby * nbz * kBrickSlots;
 }
 
@@ -723,13 +725,19 @@ cudaError_t lattice_build_masks(const double4* xv, long long n, const int32_t* e
 
 template <int MODE, bool BC>
 cudaError_t launch_nl(const DevArgs& A, const LatticeArgs& L, cudaStream_t st) {
-    const int nbx = (L.nx + BX - 1) / BX, nby = (L.ny + BY - 1) / BY, nbz = (L.nz_own + 3) / 4;
+    const int nbx = (L.nx + BX - 1) / BX, nby = (L.ny + BY - 1) / BY,
+              nbz = (L.nz_own + NLBZ - 1) / NLBZ;
     if (nbx * nby * nbz == 0)
         return cudaSuccess;
     const dim3 grid{unsigned(nbx), unsigned(nby), unsigned(nbz)};
-    const size_t smem = sizeof(float4) * nrec<4>();
+    const size_t smem = sizeof(float4) * nrec<NLBZ>();
     if (L.multi && !L.typed)  // the loop kernel (also forced by PD_LAT_NL_LOOP at setup)
-        lattice_nl_kernel<MODE, BC, true><<<grid, BX * BY * 4, smem, st>>>(A, L);
+    {
+        const cudaError_t e = smem_optin<lattice_nl_kernel<MODE, BC, true>>(int(smem));
+        if (e != cudaSuccess)
+            return e;
+        lattice_nl_kernel<MODE, BC, true><<<grid, BX * BY * NLBZ, smem, st>>>(A, L);
+    }
     else
         return MODE == 0   ? launch_nlu_m0(A, L, st)
                : MODE == 1 ? launch_nlu_m1(A, L, st)
@@ -835,6 +843,8 @@ void lattice_set_laws(const DevLaw* laws, int n, LatticeArgs& L, cudaStream_t st
 template <int MODE> void preload_nl() {
     preload_fn(lattice_nl_kernel<MODE, true, true>);
     preload_fn(lattice_nl_kernel<MODE, false, true>);
+    smem_optin<lattice_nl_kernel<MODE, true, true>>(int(sizeof(float4)) * nrec<NLBZ>());
+    smem_optin<lattice_nl_kernel<MODE, false, true>>(int(sizeof(float4)) * nrec<NLBZ>());
 }
 
 void preload_lattice() {

@@ -5,6 +5,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <utility>
 
 #include "pd_device.cuh"
@@ -175,19 +176,38 @@ constexpr ClassOrder make_class_order() {
 }
 constexpr ClassOrder kOrder = make_class_order();
 
+// The dynamic shared-memory opt-in above 48 KB, once per kernel and device
+// (a process may drive several GPUs: slab ranks as threads).
+template <auto Kernel> cudaError_t smem_optin(int bytes) {
+    static std::atomic<unsigned long long> done{0};  // bit d: set on device d
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess)
+        return e;
+    const unsigned long long bit = dev < 64 ? (1ull << dev) : 0ull;
+    if (done.load(std::memory_order_acquire) & bit)
+        return cudaSuccess;
+    e = cudaFuncSetAttribute(reinterpret_cast<const void*>(Kernel),
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess)
+        done.fetch_or(bit, std::memory_order_acq_rel);
+    return e;
+}
+
 // Per-bond (slot) arrays of the NL path are brick-major: the node at lane t
-// (= tx + 16 ty + 64 tz) of 16 x 4 x 4 brick b keeps slot c at
+// (= tx + 16 ty + 64 tz) of 16 x 4 x NLBZ brick b keeps slot c at
 // b * kBrickSlots + c * NLB + t.  A step thread reads slot c at a
 // compile-time offset from its own base, and a warp's access is one 128-byte
 // line.  Bricks tile the owned planes only (ghost rows carry no bond state).
-constexpr int NLB = 256;
+constexpr int NLBZ = 8;             // z planes of an NL brick (16 x 4 x NLBZ nodes)
+constexpr int NLB = BX * BY * NLBZ;  // nodes of an NL brick
 constexpr long long kBrickSlots = (long long)NPAT * NLB;
 __host__ __device__ inline long long slot_base(const LatticeArgs& L, long long i) {
     const long long plane = (long long)L.nx * L.ny;
     const int ix = int(i % L.nx), iy = int((i / L.nx) % L.ny), iz = int(i / plane) - L.z0;
     const long long nbx = (L.nx + 15) / 16, nby = (L.ny + 3) / 4;
-    const long long b = ix / 16 + nbx * (iy / 4 + nby * (iz / 4));
-    return b * kBrickSlots + (ix % 16) + 16 * (iy % 4) + 64 * (iz % 4);
+    const long long b = ix / 16 + nbx * (iy / 4 + nby * (iz / NLBZ));
+    return b * kBrickSlots + (ix % 16) + 16 * (iy % 4) + 64 * (iz % NLBZ);
 }
 
 // Stage the halo box of the brick at (gx0, gy0, gz0) plane by plane

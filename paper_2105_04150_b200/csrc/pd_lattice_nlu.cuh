@@ -314,8 +314,9 @@ __device__ __forceinline__ uint4 nl_slow_node(const LatticeArgs& L, const float4
 }
 
 template <int MODE, bool BC, int NBP, bool LAM, bool NF>
-__global__ void __launch_bounds__(BX * BY * 4, 4) lattice_nlu_kernel(DevArgs A, LatticeArgs L) {
-    constexpr int BZT = 4;
+__global__ void __launch_bounds__(BX * BY * NLBZ, 16 / NLBZ) lattice_nlu_kernel(DevArgs A,
+                                                                                LatticeArgs L) {
+    constexpr int BZT = NLBZ;
     if (MODE != 0 && *(volatile long long*)A.err_step != kNoError)
         return;
     extern __shared__ float4 rec[];
@@ -382,12 +383,16 @@ __global__ void __launch_bounds__(BX * BY * 4, 4) lattice_nlu_kernel(DevArgs A, 
 
 template <int MODE, bool BC, int NBP, bool LAM, bool NF>
 cudaError_t launch_nlu5(const DevArgs& A, const LatticeArgs& L, cudaStream_t st) {
-    const int nbx = (L.nx + BX - 1) / BX, nby = (L.ny + BY - 1) / BY, nbz = (L.nz_own + 3) / 4;
+    const int nbx = (L.nx + BX - 1) / BX, nby = (L.ny + BY - 1) / BY,
+              nbz = (L.nz_own + NLBZ - 1) / NLBZ;
     if (nbx * nby * nbz == 0)
         return cudaSuccess;
+    const int smem = int(sizeof(float4)) * nrec<NLBZ>();
+    const cudaError_t e = smem_optin<lattice_nlu_kernel<MODE, BC, NBP, LAM, NF>>(smem);
+    if (e != cudaSuccess)
+        return e;
     lattice_nlu_kernel<MODE, BC, NBP, LAM, NF>
-        <<<dim3(unsigned(nbx), unsigned(nby), unsigned(nbz)), BX * BY * 4,
-           sizeof(float4) * nrec<4>(), st>>>(A, L);
+        <<<dim3(unsigned(nbx), unsigned(nby), unsigned(nbz)), BX * BY * NLBZ, smem, st>>>(A, L);
     return cudaGetLastError();
 }
 
@@ -414,16 +419,17 @@ template <int MODE> cudaError_t launch_nlu_impl(const DevArgs& A, const LatticeA
                            : launch_nlu3<MODE, false, 3>(A, L, st);
 }
 
-template <class K> void nlu_preload_fn(K k) {
+template <auto Kernel> void nlu_preload_fn() {
     cudaFuncAttributes a;
-    cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(k));
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(Kernel));
+    smem_optin<Kernel>(int(sizeof(float4)) * nrec<NLBZ>());
 }
 
 template <int MODE, bool BC, int NBP> void preload_nlu3() {
-    nlu_preload_fn(lattice_nlu_kernel<MODE, BC, NBP, true, true>);
-    nlu_preload_fn(lattice_nlu_kernel<MODE, BC, NBP, true, false>);
-    nlu_preload_fn(lattice_nlu_kernel<MODE, BC, NBP, false, true>);
-    nlu_preload_fn(lattice_nlu_kernel<MODE, BC, NBP, false, false>);
+    nlu_preload_fn<lattice_nlu_kernel<MODE, BC, NBP, true, true>>();
+    nlu_preload_fn<lattice_nlu_kernel<MODE, BC, NBP, true, false>>();
+    nlu_preload_fn<lattice_nlu_kernel<MODE, BC, NBP, false, true>>();
+    nlu_preload_fn<lattice_nlu_kernel<MODE, BC, NBP, false, false>>();
 }
 
 template <int MODE> void preload_nlu_impl() {

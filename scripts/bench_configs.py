@@ -10,7 +10,8 @@ cfg4 is bench.py's default line.  cfg5's law set (several laws chosen by bond ty
 
 GPU: the fast and exact variants of one simulate() call (host buffers in, state out), after
 one untimed call.  Reference: the unmodified reference (oracle/_ref) on all host cores.
-Writes one JSON object (stdout, and profiles/r01_configs.json when --save is given).
+Writes one JSON object (stdout, and gpurun_out/r01_configs.json when --save is given;
+profiles/r01_configs.json is a copy).
 """
 import json
 import os
@@ -83,7 +84,8 @@ def main():
         print(name, json.dumps(row), file=sys.stderr)
     print(json.dumps(out))
     if "--save" in sys.argv:
-        with open(os.path.join(ROOT, "profiles", "r01_configs.json"), "w") as f:
+        os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)  # merged back by gpurun
+        with open(os.path.join(ROOT, "gpurun_out", "r01_configs.json"), "w") as f:
             json.dump(out, f, indent=1)
 
 

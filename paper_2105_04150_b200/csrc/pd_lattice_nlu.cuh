@@ -112,7 +112,10 @@ struct AccN {
     float emax;  // largest e over live breakable slots
 };
 
-constexpr int ND = 8;  // ring depth (slots of history / lambda loads in flight)
+#ifndef PD_NLU_ND
+#define PD_NLU_ND 8
+#endif
+constexpr int ND = PD_NLU_ND;  // ring depth (slots of history / lambda loads in flight)
 
 // f for stretch s and history hh (hh ignored for NBP = 1); e is the stretch
 // the break test uses (max(s, h))

@@ -266,7 +266,7 @@ struct pd_ctx {
     bool lattice = false;
     LatticeArgs lat;
     DevBuf<uint4> lmask;
-    DevBuf<float> lhist, llam;  // NL: slot-major [c][node] (llam = lambda * beta)
+    DevBuf<float> lhist, llam;  // NL: brick-major per-bond arrays (llam = lambda * beta)
     DevBuf<uint8_t> lbtype;
     bool permuted() const { return fast && !lattice; }
     // async snapshots (pd_ctx_snapshot_every)
@@ -687,7 +687,7 @@ int download(pd_ctx* ctx, pd_state* st, pd_force_field* forces, int32_t fields) 
 // PD_FAST on a lattice: implicit connectivity (pd_lattice.cu).  One PMB law
 // runs the unrolled kernel (no-failure nodes and per-node volumes ride in the
 // staged records); n-linear laws, bond types and lambda / beta run the NL
-// kernel with slot-major per-bond arrays.  Returns false (and
+// kernels with brick-major per-bond arrays.  Returns false (and
 // leaves the context untouched) when the model does not qualify;
 // PD_FAST_LAYOUT=general forces the general tile layout.
 int try_lattice(pd_ctx* ctx, const pd_particles& p, const pd_state& st, const pd_damage_model& m,
@@ -698,8 +698,8 @@ int try_lattice(pd_ctx* ctx, const pd_particles& p, const pd_state& st, const pd
         if (std::strcmp(e, "general") == 0)
             return PD_OK;
     const int64_t n = ctx->n;
-    // n-linear laws, several laws, bond types or lambda / beta: the NL kernel
-    // with slot-major per-bond arrays
+    // n-linear laws, several laws, bond types or lambda / beta: the NL kernels
+    // with brick-major per-bond arrays
     const bool nl = m.n_laws != 1 || m.laws[0].n_breakpoints != 1 || ctx->history ||
                     st.connectivity.bond_type_size != 0 || corr.lambda_size != 0 ||
                     corr.beta_size != 0;

@@ -186,12 +186,12 @@ __global__ void __launch_bounds__(BX * BY * BZT, MINB) lattice_step_kernel(DevAr
 
 // ---- n-linear laws, bond types, lambda / beta on the lattice (NL) -------------
 //
-// Per pattern slot c the per-bond data live in slot-major arrays [c][node]
-// (coalesced across a warp): fp32 stretch history, u8 bond type, fp32 lambda
-// and beta.  The slot loop is a runtime loop (the law evaluation would blow
-// the unrolled code out of the instruction cache); this path is bound by the
-// history stream, not by issue.  Semantics are bond_contribution's
-// (engine.cpp:53-109), in fp32 like the tile kernel.
+// The general NL kernel (more than 8 laws or more than 3 breakpoints; the
+// unrolled kernels of pd_lattice_nlu.cuh take every other n-linear model).
+// The per-bond data live in the brick-major arrays (pd_lattice.cuh
+// slot_base): fp32 stretch history, u8 bond type, fp32 lambda * beta.  The
+// slot loop is a runtime loop with the laws in constant memory.  Semantics are
+// bond_contribution's (engine.cpp:53-109), in fp32 like the tile kernel.
 
 __constant__ FastLaw c_llaws[PD_MAX_LAWS];
 // per slot (padded to 128; slots 122..127 never have a mask bit):

@@ -713,6 +713,16 @@ int try_lattice(pd_ctx* ctx, const pd_particles& p, const pd_state& st, const pd
     PD_CK(ctx->lmask.alloc(size_t(n)));
     L.n_local = n;
     L.nl = nl ? 1 : 0;
+    // NL brick depth: 8 planes unless the owned planes leave a much emptier last
+    // brick than 4 would (thin plates, 27-plane slabs); PD_NL_BZ=4|8 forces it
+    {
+        const int nz = L.nz_own > 0 ? L.nz_own : 1;
+        const double waste8 = double((nz + 7) / 8 * 8 - nz) / nz;
+        const double waste4 = double((nz + 3) / 4 * 4 - nz) / nz;
+        L.nlbz = waste8 - waste4 < 0.04 ? 8 : 4;
+        if (const char* e = std::getenv("PD_NL_BZ"))
+            L.nlbz = std::atoi(e) == 4 ? 4 : 8;
+    }
     const size_t pslots = size_t(lattice_slot_count(L));
     // several laws (<= 8, <= 3 breakpoints each): the typed unrolled kernel,
     // with the bond type in the history words (PD_LAT_NL_LOOP: the loop kernel)

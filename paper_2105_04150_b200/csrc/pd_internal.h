@@ -161,6 +161,7 @@ struct LatticeArgs {
     // the unrolled kernel; the history words carry the type in their low 3
     // bits and tl holds per type (c, sl_1, a_1, +-s_c), (sl_2, a_2, cvx_1, cvx_2)
     int typed = 0;
+    int nlbz = 8;  // z planes of the NL bricks: the per-bond layout (pd_lattice.cuh slot_base)
     float4 tl[16];
     int prefetch = 0;         // NL: bulk L2 prefetch of a brick's per-bond streams (PD_NLU_PF=1; measured slower than the per-slot prefetch)
 };

@@ -213,10 +213,11 @@ __device__ __forceinline__ float reg_envelope(const NlRegLaw& R, float e) {
 // MULTI = false: one law of at most three breakpoints, held in registers (the
 // bond type, if any, can only name it).  MULTI = true: per-bond law from
 // constant memory, any number of breakpoints.
-template <int MODE, bool BC, bool MULTI>
-__global__ void __launch_bounds__(BX * BY * NLBZ, 16 / NLBZ) lattice_nl_kernel(DevArgs A,
-                                                                              LatticeArgs L) {
-    constexpr int BZT = NLBZ;
+template <int MODE, bool BC, bool MULTI, int BZT>
+__global__ void __launch_bounds__(BX * BY * BZT, 16 / BZT) lattice_nl_kernel(DevArgs A,
+                                                                            LatticeArgs L) {
+    constexpr int NLB = BX * BY * BZT;
+    constexpr long long kBrickSlots = (long long)NPAT * NLB;
     if (MODE != 0 && *(volatile long long*)A.err_step != kNoError)
         return;
     extern __shared__ float4 rec[];
@@ -425,7 +426,7 @@ __global__ void lattice_mask_kernel(const int32_t* entries, long long begin, lon
             continue;
         }
         w[c >> 5] |= 1u << (c & 31);
-        const long long sidx = sb + (long long)c * NLB, idx = i * N + k;
+        const long long sidx = sb + (long long)c * (64 * L.nlbz), idx = i * N + k;
         if (L.typed) {  // history word: fp32 history, bond type in the low 3 bits
             const unsigned h = src.hist ? __float_as_uint(float(src.hist[idx])) & ~7u : 0u;
             L.hist[sidx] = __uint_as_float(h | (src.btype ? unsigned(src.btype[idx]) & 7u : 0u));
@@ -471,7 +472,7 @@ __global__ void lattice_materialize_kernel(const int32_t* entries0, const uint4*
             if (!((w[c >> 5] >> (c & 31)) & 1u))
                 v = -1;
             if (hist_out) {  // broken bonds keep their last history (engine.cpp:88-92)
-                float h = hist[slot_base(L, i) + (long long)c * NLB];
+                float h = hist[slot_base(L, i) + (long long)c * (64 * L.nlbz)];
                 if (L.typed)
                     h = __uint_as_float(__float_as_uint(h) & ~7u);
                 hist_out[i * N + k] = double(h);
@@ -617,8 +618,8 @@ template <int MODE> void preload_mode() {
 
 long long lattice_slot_count(const LatticeArgs& L) {
     const long long nbx = (L.nx + 15) / 16, nby = (L.ny + 3) / 4,
-                    nbz = (L.nz_own + NLBZ - 1) / NLBZ;
-    return nbx * nby * nbz * kBrickSlots;
+                    nbz = (L.nz_own + L.nlbz - 1) / L.nlbz;
+    return nbx * nby * nbz * (long long)NPAT * (64 * L.nlbz);
 }
 
 bool lattice_detect(const double* coords, long long n, long long own_begin, long long own_end,
@@ -723,27 +724,30 @@ cudaError_t lattice_build_masks(const double4* xv, long long n, const int32_t* e
     return cudaGetLastError();
 }
 
-template <int MODE, bool BC>
-cudaError_t launch_nl(const DevArgs& A, const LatticeArgs& L, cudaStream_t st) {
+template <int MODE, bool BC, int BZT>
+cudaError_t launch_nl_loop(const DevArgs& A, const LatticeArgs& L, cudaStream_t st) {
     const int nbx = (L.nx + BX - 1) / BX, nby = (L.ny + BY - 1) / BY,
-              nbz = (L.nz_own + NLBZ - 1) / NLBZ;
+              nbz = (L.nz_own + BZT - 1) / BZT;
     if (nbx * nby * nbz == 0)
         return cudaSuccess;
     const dim3 grid{unsigned(nbx), unsigned(nby), unsigned(nbz)};
-    const size_t smem = sizeof(float4) * nrec<NLBZ>();
-    if (L.multi && !L.typed)  // the loop kernel (also forced by PD_LAT_NL_LOOP at setup)
-    {
-        const cudaError_t e = smem_optin<lattice_nl_kernel<MODE, BC, true>>(int(smem));
-        if (e != cudaSuccess)
-            return e;
-        lattice_nl_kernel<MODE, BC, true><<<grid, BX * BY * NLBZ, smem, st>>>(A, L);
-    }
-    else
-        return MODE == 0   ? launch_nlu_m0(A, L, st)
-               : MODE == 1 ? launch_nlu_m1(A, L, st)
-               : MODE == 2 ? launch_nlu_m2(A, L, st)
-                           : launch_nlu_m3(A, L, st);
+    const size_t smem = sizeof(float4) * nrec<BZT>();
+    const cudaError_t e = smem_optin<lattice_nl_kernel<MODE, BC, true, BZT>>(int(smem));
+    if (e != cudaSuccess)
+        return e;
+    lattice_nl_kernel<MODE, BC, true, BZT><<<grid, BX * BY * BZT, smem, st>>>(A, L);
     return cudaGetLastError();
+}
+
+template <int MODE, bool BC>
+cudaError_t launch_nl(const DevArgs& A, const LatticeArgs& L, cudaStream_t st) {
+    if (L.multi && !L.typed)  // the loop kernel (also forced by PD_LAT_NL_LOOP at setup)
+        return L.nlbz == 4 ? launch_nl_loop<MODE, BC, 4>(A, L, st)
+                           : launch_nl_loop<MODE, BC, 8>(A, L, st);
+    return MODE == 0   ? launch_nlu_m0(A, L, st)
+           : MODE == 1 ? launch_nlu_m1(A, L, st)
+           : MODE == 2 ? launch_nlu_m2(A, L, st)
+                       : launch_nlu_m3(A, L, st);
 }
 
 template <int MODE> cudaError_t launch_nl_mode(const DevArgs& A, const LatticeArgs& L,
@@ -841,10 +845,12 @@ void lattice_set_laws(const DevLaw* laws, int n, LatticeArgs& L, cudaStream_t st
 }
 
 template <int MODE> void preload_nl() {
-    preload_fn(lattice_nl_kernel<MODE, true, true>);
-    preload_fn(lattice_nl_kernel<MODE, false, true>);
-    smem_optin<lattice_nl_kernel<MODE, true, true>>(int(sizeof(float4)) * nrec<NLBZ>());
-    smem_optin<lattice_nl_kernel<MODE, false, true>>(int(sizeof(float4)) * nrec<NLBZ>());
+    preload_fn(lattice_nl_kernel<MODE, true, true, 4>);
+    preload_fn(lattice_nl_kernel<MODE, false, true, 4>);
+    preload_fn(lattice_nl_kernel<MODE, true, true, 8>);
+    preload_fn(lattice_nl_kernel<MODE, false, true, 8>);
+    smem_optin<lattice_nl_kernel<MODE, true, true, 8>>(int(sizeof(float4)) * nrec<8>());
+    smem_optin<lattice_nl_kernel<MODE, false, true, 8>>(int(sizeof(float4)) * nrec<8>());
 }
 
 void preload_lattice() {

@@ -195,19 +195,19 @@ template <auto Kernel> cudaError_t smem_optin(int bytes) {
 }
 
 // Per-bond (slot) arrays of the NL path are brick-major: the node at lane t
-// (= tx + 16 ty + 64 tz) of 16 x 4 x NLBZ brick b keeps slot c at
-// b * kBrickSlots + c * NLB + t.  A step thread reads slot c at a
-// compile-time offset from its own base, and a warp's access is one 128-byte
-// line.  Bricks tile the owned planes only (ghost rows carry no bond state).
-constexpr int NLBZ = 8;             // z planes of an NL brick (16 x 4 x NLBZ nodes)
-constexpr int NLB = BX * BY * NLBZ;  // nodes of an NL brick
-constexpr long long kBrickSlots = (long long)NPAT * NLB;
+// (= tx + 16 ty + 64 tz) of 16 x 4 x L.nlbz brick b keeps slot c at
+// b * 122 * NB + c * NB + t, NB = 64 L.nlbz the brick's node count.  A step
+// thread reads slot c at a compile-time offset from its own base, and a
+// warp's access is one 128-byte line.  Bricks tile the owned planes only
+// (ghost rows carry no bond state).  The depth (4 or 8 planes) is chosen at
+// upload: 8 stages fewer halo records per node, 4 wastes less on thin models.
 __host__ __device__ inline long long slot_base(const LatticeArgs& L, long long i) {
     const long long plane = (long long)L.nx * L.ny;
     const int ix = int(i % L.nx), iy = int((i / L.nx) % L.ny), iz = int(i / plane) - L.z0;
     const long long nbx = (L.nx + 15) / 16, nby = (L.ny + 3) / 4;
-    const long long b = ix / 16 + nbx * (iy / 4 + nby * (iz / NLBZ));
-    return b * kBrickSlots + (ix % 16) + 16 * (iy % 4) + 64 * (iz % NLBZ);
+    const int bz = L.nlbz;
+    const long long b = ix / 16 + nbx * (iy / 4 + nby * (iz / bz));
+    return b * (long long)NPAT * (64 * bz) + (ix % 16) + 16 * (iy % 4) + 64 * (iz % bz);
 }
 
 // Stage the halo box of the brick at (gx0, gy0, gz0) plane by plane

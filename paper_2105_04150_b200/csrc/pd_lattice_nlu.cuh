@@ -145,7 +145,7 @@ __device__ __forceinline__ float nl_law(const NlRegLaw& R, float s, float hh, fl
     return env * (s * rcp_approx(e));
 }
 
-template <int K, int NBP, bool LAM, bool NF>
+template <int K, int NBP, bool LAM, bool NF, int NB>
 __device__ __forceinline__ void nl_slot(const float4* own, const float4& ri, const uint4& m,
                                         float* hb, const float* lb, float nfthr,
                                         const NlRegLaw& R, const float4* tab, float (&hr)[ND],
@@ -179,14 +179,14 @@ __device__ __forceinline__ void nl_slot(const float4* own, const float4& ri, con
         constexpr int nword = CN >> 5;
         const unsigned nmw = nword == 0 ? m.x : (nword == 1 ? m.y : (nword == 2 ? m.z : m.w));
         if (NBP != 1)
-            ldg_keep_if(hr[K % ND], hb + CN * NLB, nmw & nbit);
+            ldg_keep_if(hr[K % ND], hb + CN * NB, nmw & nbit);
         if (LAM)
-            ldg_keep_if(lr[K % ND], lb + CN * NLB, nmw & nbit);
+            ldg_keep_if(lr[K % ND], lb + CN * NB, nmw & nbit);
 #else
         if (NBP != 1)
-            ldg_keep_if(hr[K % ND], hb + CN * NLB, 1u);
+            ldg_keep_if(hr[K % ND], hb + CN * NB, 1u);
         if (LAM)
-            ldg_keep_if(lr[K % ND], lb + CN * NLB, 1u);
+            ldg_keep_if(lr[K % ND], lb + CN * NB, 1u);
 #endif
     }
 #if PD_NLU_PFD > 0
@@ -195,9 +195,9 @@ __device__ __forceinline__ void nl_slot(const float4* own, const float4& ri, con
     if constexpr (K + PD_NLU_PFD < NPAT) {
         constexpr int CP = kOrder.slot[K + PD_NLU_PFD];
         if (NBP != 1)
-            prefetch_l2(hb + CP * NLB);
+            prefetch_l2(hb + CP * NB);
         if (LAM)
-            prefetch_l2(lb + CP * NLB);
+            prefetch_l2(lb + CP * NB);
     }
 #endif
     const float4 rj = own[off];
@@ -213,7 +213,7 @@ __device__ __forceinline__ void nl_slot(const float4* own, const float4& ri, con
         f = nl_law_typed(p0, p1, s, hh, e);
         if (NF && !brk_ok)
             f = p0.x * s;
-        stg_typed_if<NF>(hb + C * NLB, mw & bit, rj.w, nfthr, p0.w, s, hh,
+        stg_typed_if<NF>(hb + C * NB, mw & bit, rj.w, nfthr, p0.w, s, hh,
                          (__float_as_uint(s) & ~7u) | ty);
         if (brk_ok)  // e >= s_c of the bond's own law <=> e - |s_c| >= 0 (exact sign)
             acc.emax = fmax_nan(acc.emax, e - fabsf(p0.w));
@@ -222,7 +222,7 @@ __device__ __forceinline__ void nl_slot(const float4* own, const float4& ri, con
         if (NF && !brk_ok)
             f = R.c * s;
         if (NBP > 1)
-            stg_hist_if<NF>(hb + C * NLB, mw & bit, rj.w, nfthr, s, hh);
+            stg_hist_if<NF>(hb + C * NB, mw & bit, rj.w, nfthr, s, hh);
         if (brk_ok)
             acc.emax = fmax_nan(acc.emax, e);
     }
@@ -244,32 +244,32 @@ __device__ __forceinline__ void nl_slot(const float4* own, const float4& ri, con
     }
 }
 
-template <int K, int NBP, bool LAM>
+template <int K, int NBP, bool LAM, int NB>
 __device__ __forceinline__ void nl_ring_one(const float* hb, const float* lb, float (&hr)[ND],
                                             float (&lr)[ND]) {
     constexpr int C = kOrder.slot[K];
-    hr[K] = NBP != 1 ? hb[C * NLB] : 0.f;
-    lr[K] = LAM ? __ldcs(lb + C * NLB) : 1.f;
+    hr[K] = NBP != 1 ? hb[C * NB] : 0.f;
+    lr[K] = LAM ? __ldcs(lb + C * NB) : 1.f;
 }
 
-template <int NBP, bool LAM, int... K>
+template <int NBP, bool LAM, int NB, int... K>
 __device__ __forceinline__ void nl_ring_init(std::integer_sequence<int, K...>, const float* hb,
                                              const float* lb, float (&hr)[ND], float (&lr)[ND]) {
-    (nl_ring_one<K, NBP, LAM>(hb, lb, hr, lr), ...);
+    (nl_ring_one<K, NBP, LAM, NB>(hb, lb, hr, lr), ...);
 }
 
-template <int NBP, bool LAM, bool NF, int... K>
+template <int NBP, bool LAM, bool NF, int NB, int... K>
 __device__ __forceinline__ void nl_all_slots(std::integer_sequence<int, K...>, const float4* own,
                                              const float4& ri, const uint4& m, float* hb,
                                              const float* lb, float nfthr, const NlRegLaw& R,
                                              const float4* tab, float (&hr)[ND], float (&lr)[ND],
                                              AccN& acc) {
-    (nl_slot<K, NBP, LAM, NF>(own, ri, m, hb, lb, nfthr, R, tab, hr, lr, acc), ...);
+    (nl_slot<K, NBP, LAM, NF, NB>(own, ri, m, hb, lb, nfthr, R, tab, hr, lr, acc), ...);
 }
 
 // the rare pass for a node that loses bonds: the history is already updated,
 // which leaves e and f of every slot unchanged (e = max(s, h_old) = max(s, h_new))
-template <int NBP, bool LAM, bool NF>
+template <int NBP, bool LAM, bool NF, int NB>
 __device__ __forceinline__ uint4 nl_slow_node(const LatticeArgs& L, const float4* own,
                                               const float4 ri, const uint4 m, const float* hb,
                                               const float* lb, float nfthr, const NlRegLaw& R,
@@ -288,14 +288,14 @@ __device__ __forceinline__ uint4 nl_slow_node(const LatticeArgs& L, const float4
         const bool brk_ok = !NF || rj.w >= nfthr;
         float e, f, c_lin = R.c, s_c = sc;
         if (NBP == 0) {
-            const unsigned bits = __float_as_uint(hb[c * NLB]);
+            const unsigned bits = __float_as_uint(hb[c * NB]);
             const float4 p0 = tab[2 * (bits & 7u)], p1 = tab[2 * (bits & 7u) + 1];
             const float hh = p0.w > 0.f ? __uint_as_float(bits & ~7u) : 0.f;
             f = nl_law_typed(p0, p1, s, hh, e);
             c_lin = p0.x;
             s_c = fabsf(p0.w);
         } else {
-            f = nl_law<NBP>(R, s, NBP > 1 ? hb[c * NLB] : 0.f, e);
+            f = nl_law<NBP>(R, s, NBP > 1 ? hb[c * NB] : 0.f, e);
         }
         if (brk_ok && !(e < s_c)) {
             dead[c >> 5] |= 1u << (c & 31);
@@ -307,7 +307,7 @@ __device__ __forceinline__ uint4 nl_slow_node(const LatticeArgs& L, const float4
         if (NF)
             scale *= fabsf(rj.w);
         if (LAM)
-            scale *= lb[c * NLB];
+            scale *= lb[c * NB];
         fx = fmaf(rj.x - ri.x + float(dx), scale, fx);
         fy = fmaf(rj.y - ri.y + float(dy), scale, fy);
         fz = fmaf(rj.z - ri.z + float(dz), scale, fz);
@@ -316,10 +316,11 @@ __device__ __forceinline__ uint4 nl_slow_node(const LatticeArgs& L, const float4
     return make_uint4(dead[0], dead[1], dead[2], dead[3]);
 }
 
-template <int MODE, bool BC, int NBP, bool LAM, bool NF>
-__global__ void __launch_bounds__(BX * BY * NLBZ, 16 / NLBZ) lattice_nlu_kernel(DevArgs A,
-                                                                                LatticeArgs L) {
-    constexpr int BZT = NLBZ;
+template <int MODE, bool BC, int NBP, bool LAM, bool NF, int BZT>
+__global__ void __launch_bounds__(BX * BY * BZT, 16 / BZT) lattice_nlu_kernel(DevArgs A,
+                                                                              LatticeArgs L) {
+    constexpr int NB = BX * BY * BZT;  // nodes of the brick: the per-bond slot stride
+    constexpr long long kBrickSlots = (long long)NPAT * NB;
     if (MODE != 0 && *(volatile long long*)A.err_step != kNoError)
         return;
     extern __shared__ float4 rec[];
@@ -349,7 +350,7 @@ __global__ void __launch_bounds__(BX * BY * NLBZ, 16 / NLBZ) lattice_nlu_kernel(
     }
     // the first ring of streamed values is in flight while the halo is staged
     float hr[ND], lr[ND];
-    nl_ring_init<NBP, LAM>(std::make_integer_sequence<int, ND>{}, hb, lb, hr, lr);
+    nl_ring_init<NBP, LAM, NB>(std::make_integer_sequence<int, ND>{}, hb, lb, hr, lr);
     const double4 U0 = A.u_in[gx0 + (long long)L.nx * gy0 + plane * gz0];
     stage_box<BZT, NF>(A, L, rec, gx0, gy0, gz0, U0);
     __syncthreads();
@@ -362,12 +363,12 @@ __global__ void __launch_bounds__(BX * BY * NLBZ, 16 / NLBZ) lattice_nlu_kernel(
     const float nfthr = (NF && ri.w < 0.f) ? inf : 0.f;
     const NlRegLaw& R = L.rl;
     AccN acc{make_float2(0.f, 0.f), 0.f, make_float2(0.f, 0.f), 0.f, -inf};
-    nl_all_slots<NBP, LAM, NF>(std::make_integer_sequence<int, NPAT>{}, own, ri, m, hb, lb,
+    nl_all_slots<NBP, LAM, NF, NB>(std::make_integer_sequence<int, NPAT>{}, own, ri, m, hb, lb,
                                nfthr, R, tab, hr, lr, acc);
     if (!(acc.emax < (NBP == 0 ? 0.f : R.sc))) {  // a live bond breaks (or overflowed)
         asm volatile("" ::: "memory");  // after this node's history stores
         float3 f;
-        const uint4 d = nl_slow_node<NBP, LAM, NF>(L, own, ri, m, hb, lb, nfthr, R, tab, R.sc, f);
+        const uint4 d = nl_slow_node<NBP, LAM, NF, NB>(L, own, ri, m, hb, lb, nfthr, R, tab, R.sc, f);
         L.mask[i] = make_uint4(m.x & ~d.x, m.y & ~d.y, m.z & ~d.z, m.w & ~d.w);
         A.n_neigh[i] -= __popc(d.x) + __popc(d.y) + __popc(d.z) + __popc(d.w);
         acc.fxy = make_float2(f.x, f.y);
@@ -384,19 +385,26 @@ __global__ void __launch_bounds__(BX * BY * NLBZ, 16 / NLBZ) lattice_nlu_kernel(
     node_epilogue<MODE, BC>(A, i, A.u_in[i], Fx, Fy, Fz);
 }
 
-template <int MODE, bool BC, int NBP, bool LAM, bool NF>
-cudaError_t launch_nlu5(const DevArgs& A, const LatticeArgs& L, cudaStream_t st) {
+template <int MODE, bool BC, int NBP, bool LAM, bool NF, int BZT>
+cudaError_t launch_nlu6(const DevArgs& A, const LatticeArgs& L, cudaStream_t st) {
     const int nbx = (L.nx + BX - 1) / BX, nby = (L.ny + BY - 1) / BY,
-              nbz = (L.nz_own + NLBZ - 1) / NLBZ;
+              nbz = (L.nz_own + BZT - 1) / BZT;
     if (nbx * nby * nbz == 0)
         return cudaSuccess;
-    const int smem = int(sizeof(float4)) * nrec<NLBZ>();
-    const cudaError_t e = smem_optin<lattice_nlu_kernel<MODE, BC, NBP, LAM, NF>>(smem);
+    const int smem = int(sizeof(float4)) * nrec<BZT>();
+    const cudaError_t e = smem_optin<lattice_nlu_kernel<MODE, BC, NBP, LAM, NF, BZT>>(smem);
     if (e != cudaSuccess)
         return e;
-    lattice_nlu_kernel<MODE, BC, NBP, LAM, NF>
-        <<<dim3(unsigned(nbx), unsigned(nby), unsigned(nbz)), BX * BY * NLBZ, smem, st>>>(A, L);
+    lattice_nlu_kernel<MODE, BC, NBP, LAM, NF, BZT>
+        <<<dim3(unsigned(nbx), unsigned(nby), unsigned(nbz)), BX * BY * BZT, smem, st>>>(A, L);
     return cudaGetLastError();
+}
+
+// the brick depth of the per-bond layout (L.nlbz, fixed at upload)
+template <int MODE, bool BC, int NBP, bool LAM, bool NF>
+cudaError_t launch_nlu5(const DevArgs& A, const LatticeArgs& L, cudaStream_t st) {
+    return L.nlbz == 4 ? launch_nlu6<MODE, BC, NBP, LAM, NF, 4>(A, L, st)
+                       : launch_nlu6<MODE, BC, NBP, LAM, NF, 8>(A, L, st);
 }
 
 template <int MODE, bool BC, int NBP>
@@ -422,17 +430,21 @@ template <int MODE> cudaError_t launch_nlu_impl(const DevArgs& A, const LatticeA
                            : launch_nlu3<MODE, false, 3>(A, L, st);
 }
 
-template <auto Kernel> void nlu_preload_fn() {
+template <auto Kernel, int BZT> void nlu_preload_fn() {
     cudaFuncAttributes a;
     cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(Kernel));
-    smem_optin<Kernel>(int(sizeof(float4)) * nrec<NLBZ>());
+    smem_optin<Kernel>(int(sizeof(float4)) * nrec<BZT>());
 }
 
 template <int MODE, bool BC, int NBP> void preload_nlu3() {
-    nlu_preload_fn<lattice_nlu_kernel<MODE, BC, NBP, true, true>>();
-    nlu_preload_fn<lattice_nlu_kernel<MODE, BC, NBP, true, false>>();
-    nlu_preload_fn<lattice_nlu_kernel<MODE, BC, NBP, false, true>>();
-    nlu_preload_fn<lattice_nlu_kernel<MODE, BC, NBP, false, false>>();
+    nlu_preload_fn<lattice_nlu_kernel<MODE, BC, NBP, true, true, 4>, 4>();
+    nlu_preload_fn<lattice_nlu_kernel<MODE, BC, NBP, true, true, 8>, 8>();
+    nlu_preload_fn<lattice_nlu_kernel<MODE, BC, NBP, true, false, 4>, 4>();
+    nlu_preload_fn<lattice_nlu_kernel<MODE, BC, NBP, true, false, 8>, 8>();
+    nlu_preload_fn<lattice_nlu_kernel<MODE, BC, NBP, false, true, 4>, 4>();
+    nlu_preload_fn<lattice_nlu_kernel<MODE, BC, NBP, false, true, 8>, 8>();
+    nlu_preload_fn<lattice_nlu_kernel<MODE, BC, NBP, false, false, 4>, 4>();
+    nlu_preload_fn<lattice_nlu_kernel<MODE, BC, NBP, false, false, 8>, 8>();
 }
 
 template <int MODE> void preload_nlu_impl() {

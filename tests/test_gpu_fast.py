@@ -444,3 +444,36 @@ def test_fast_nonfinite_midrun_raises_like_the_reference(oracle, monkeypatch, la
             be.simulate(b, st, SimulateOptions(200, 0, 0, IntegratorKind.velocity_verlet, variant))
         msgs.append(str(ei.value))
     assert msgs[0] == msgs[1]
+
+
+@pytest.mark.parametrize("nl_bz", ["4", "8"])
+@pytest.mark.parametrize("law", ["trilinear_convex_kink", "typed"])
+def test_lattice_nl_brick_depths_match_oracle(oracle, monkeypatch, nl_bz, law):
+    """The n-linear lattice kernels on either per-bond layout depth (16x4x4 or
+    16x4x8 bricks, PD_NL_BZ) against the fp64 oracle, with beta."""
+    monkeypatch.setenv("PD_NL_BZ", nl_bz)
+    b, h, g = S.bench_lattice_bundle((20, 16, 12))
+    laws = NLU_LAWS[law]()
+    b.model.laws = laws if isinstance(laws, list) else [laws]
+    fam = geometry.build_family(b.particles.coords, h, g)
+    if law == "typed":
+        fam.bond_type = S.classify_bonds(b.particles.coords, fam, rebar_y=8.0, rebar_z=6.0)
+    b.corrections.beta = np.random.default_rng(9).uniform(0.6, 1.0, fam.entries.size)
+    u0 = S.seed_displacements(b.particles.coords) * 3.0
+    outs = []
+    for be, variant in ((engine.backend(), KernelVariant.fast),
+                        (oracle, KernelVariant.bond_parallel)):
+        st = make_state(fam, True)
+        st.u = u0.copy()
+        be.simulate(b, st, SimulateOptions(120, 0, 0, IntegratorKind.velocity_verlet, variant))
+        outs.append(st)
+    fast, ref = outs
+    broken = int(fam.n_neigh.sum() - ref.connectivity.n_neigh.sum())
+    assert broken > 0
+    diff = int((ref.connectivity.entries != fast.connectivity.entries).sum())
+    assert diff <= max(4, 0.01 * broken), (diff, broken)
+    assert max_rel_difference(ref.u, fast.u) <= FRACTURE_U_TOL
+    live = (ref.connectivity.entries >= 0) & (fast.connectivity.entries >= 0)
+    s_c = max(lw.breakpoints[-1] for lw in b.model.laws)
+    err = np.abs(ref.bond_history[live] - fast.bond_history[live])
+    assert np.max(err) <= 1e-4 * max(s_c, np.max(np.abs(ref.bond_history)))

@@ -52,68 +52,167 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled DURING the timed
+    region: NVML every ~2 ms on a thread (a 20-step region lasts ~22 ms), or
+    nvidia-smi -lms 50 when NVML is unavailable."""
 
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4}
     QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
         self.index = index
+        self.samples = []  # (sm_mhz, max_mhz, reasons)
+        self.stop = threading.Event()
         self.proc = None
-        self.lines = []
+        self.source = None
+
+    def _nvml_handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        try:
+            import torch
+            p = torch.cuda.get_device_properties(self.index)
+            bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
+
+    def _nvml_loop(self, nv, h):
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self.stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            except Exception:
+                break
+            self.samples.append((float(sm), float(mx),
+                                 {k for k, b in self.REASONS.items() if bits & b}))
+            time.sleep(0.002)
 
     def __enter__(self):
+        try:
+            nv, h = self._nvml_handle()
+            self.t = threading.Thread(target=self._nvml_loop, args=(nv, h), daemon=True)
+            self.source = "nvml"
+            self.t.start()
+            return self
+        except Exception:
+            pass
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}",
                  "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            self.source = "nvidia-smi"
+            self.t = threading.Thread(target=self._smi_read, daemon=True)
             self.t.start()
         except OSError:
             self.proc = None
         return self
 
-    def _read(self):
+    def _smi_read(self):
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                self.samples.append((float(f[1]), float(f[2]),
+                                     {n for n, fl in zip(names, f[5:9]) if fl.lower() == "active"}))
+            except ValueError:
+                continue
 
     def __exit__(self, *exc):
+        self.stop.set()
         if self.proc:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
+        if getattr(self, "t", None):
+            self.t.join(timeout=5)
 
     def summary(self):
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.lines:
-            f = [x.strip() for x in line.split(",")]
-            if len(f) < 9:
-                continue
-            try:
-                sm.append(float(f[1]))
-                mx = max(mx, float(f[2]))
-            except ValueError:
-                continue
-            for name, flag in zip(names, f[5:9]):
-                if flag.lower() == "active":
-                    reasons.add(name)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        sm = [x[0] for x in self.samples]
+        reasons = set().union(*[x[2] for x in self.samples]) if self.samples else set()
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(x[1] for x in self.samples) if self.samples else None,
+                "reasons": sorted(reasons), "samples": len(sm), "source": self.source}
 
 
-def measured_traffic(key):
-    """DRAM bytes per launch of the step kernel from the committed ncu capture
-    (profiles/traffic.json, written from `ncu --set full`), or None."""
-    p = os.path.join(ROOT, "profiles", "traffic.json")
+def cpu_model() -> str:
     try:
-        return json.load(open(p))[key]["traffic_bytes_per_launch"]
-    except (OSError, KeyError, ValueError):
-        return None
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+NCU_METRICS = ("dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,"
+               "sm__inst_executed.sum,smsp__issue_active.avg.pct_of_peak_sustained_active,"
+               "sm__warps_active.avg.pct_of_peak_sustained_active")
+
+
+def ncu_probe(args, kernel: str):
+    """Measured DRAM traffic of the step kernel in THIS run's configuration:
+    `ncu` profiles one warm launch of `kernel` in a child `bench.py --probe-run`
+    (same workload, law and variant), reading dram__bytes_read/write.sum, the
+    issue-slot utilisation and the warp instructions.  Profiler numbers are
+    never the bench value; only the per-launch byte count and ratios are used.
+    Returns a dict, or {"error": ...} when ncu is unavailable."""
+    import csv
+    import shutil
+    import tempfile
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(ncu):
+        return {"error": "ncu not found"}
+    base = kernel.split("<", 1)[0]
+    with tempfile.TemporaryDirectory() as td:
+        log = os.path.join(td, "probe.csv")
+        cmd = [ncu, "--metrics", NCU_METRICS, "--clock-control", "none", "-k", f"regex:^{base}$",
+               "-s", "2", "-c", "1", "--csv", "--page", "raw", "--log-file", log,
+               sys.executable, os.path.abspath(__file__), "--probe-run", "--size", str(args.size),
+               "--law", args.law, "--variant", args.variant]
+        try:
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+        except (OSError, subprocess.TimeoutExpired) as exc:
+            return {"error": f"ncu probe failed: {exc}"}
+        if not os.path.exists(log):
+            return {"error": f"ncu probe rc={r.returncode}: {r.stderr[-300:]}"}
+        rows = list(csv.reader(open(log)))
+    hdr = next((i for i, row in enumerate(rows) if "dram__bytes_read.sum" in row), None)
+    if hdr is None or len(rows) < hdr + 3:
+        return {"error": "ncu probe: no kernel row"}
+    head, units, vals = rows[hdr], rows[hdr + 1], rows[hdr + 2]
+
+    def val(name, scale_units=True):
+        v = float(vals[head.index(name)].replace(",", ""))
+        u = units[head.index(name)].strip().lower()
+        if scale_units:
+            v *= {"byte": 1, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9, "nsecond": 1e-9,
+                  "usecond": 1e-6, "msecond": 1e-3, "second": 1.0}.get(u, 1.0)
+        return v
+    name = vals[head.index("Kernel Name")] if "Kernel Name" in head else base
+    return {"kernel": name[:120],
+            "dram_bytes": val("dram__bytes_read.sum") + val("dram__bytes_write.sum"),
+            "dram_read_bytes": val("dram__bytes_read.sum"),
+            "ncu_time_s": val("gpu__time_duration.sum"),
+            "warp_instructions": val("sm__inst_executed.sum", False),
+            "issue_active_pct": val("smsp__issue_active.avg.pct_of_peak_sustained_active", False),
+            "warps_active_pct": val("sm__warps_active.avg.pct_of_peak_sustained_active", False)}
 
 
 def rebar_bond_types(counts, fam):
@@ -139,15 +238,27 @@ def rebar_bond_types(counts, fam):
     return bt.reshape(-1)
 
 
+LAWS = {
+    "pmb": "PMB c=1 s_c=1e6 (no breaking)",
+    "fracture": "PMB c=1 s_c=1e-5 (SURVEY 8(d) fracturing variant: ~12 % of the bonds break "
+                "at step 1, breaks continue)",
+    "trilinear": "trilinear(1, 1e-3, 2e-3, 1e6) with history",
+    "multi": "cfg5 laws by bond type: trilinear concrete, PMB steel, bilinear interface, "
+             "two rebar lines, history",
+}
+S_C = {"pmb": 1e6, "fracture": 1e-5, "trilinear": 1e6, "multi": 1e6}
+
+
 def build_workload(counts, law="pmb"):
-    """The reference bench fixture; law "trilinear" is SURVEY 8(d)'s history
-    variant trilinear(1, 1e-3, 2e-3, 1e6) (n-linear path, nothing breaks);
-    "multi" is the cfg5 law set on the same lattice: trilinear concrete, PMB
-    steel and bilinear interface selected per bond by type (rebar_bond_types)."""
+    """The reference bench fixture (bench.cpp:76-104); law "fracture" is SURVEY
+    8(d)'s fracturing variant (PMB s_c = 1e-5), "trilinear" its history variant
+    trilinear(1, 1e-3, 2e-3, 1e6) (n-linear path, nothing breaks); "multi" is
+    the cfg5 law set on the same lattice: trilinear concrete, PMB steel and
+    bilinear interface selected per bond by type (rebar_bond_types)."""
     import scenarios as S
     from paper_2105_04150_b200 import geometry, make_state
     from paper_2105_04150_b200.types import DamageLaw
-    bundle, h, g = S.bench_lattice_bundle(counts)
+    bundle, h, g = S.bench_lattice_bundle(counts, s_c=S_C[law])
     if law == "trilinear":
         bundle.model.laws = [DamageLaw.trilinear(1.0, 1e-3, 2e-3, 1e6)]
     elif law == "multi":
@@ -162,104 +273,154 @@ def build_workload(counts, law="pmb"):
     return bundle, fam, state
 
 
-def cpu_baseline(counts_full, steps=2):
-    """The reference CPU path (oracle/_ref, built from /root/reference/proj/src)
-    on a bounded sample of the workload: a z-slab of the full lattice."""
-    sample = (counts_full[0], counts_full[1], min(counts_full[2], 24))
-    threads = os.cpu_count() or 1
+def reference_runs(counts, law, run_steps, threads):
+    """The UNMODIFIED reference (oracle/_ref, compiled from
+    /root/reference/proj/src) on the SAME workload: simulate(bond_parallel,
+    velocity-Verlet) of the full lattice, one call per run continuing the
+    state (bench.cpp:106-117).  Returns (seconds per run, live bonds, family
+    build seconds), or None when the reference is not built or the law has no
+    reference fixture here ("multi" needs the bond classes)."""
+    if law == "multi":
+        return None
     try:
         from oracle.pyoracle import Reference
-        ref = Reference(threads=threads)
-        secs, live, build_s = ref.bench_lattice(sample, HORIZON, 1e6, steps, threads)
-        kind = "reference"
+        ref = Reference(threads=0)
     except OSError:
-        import scenarios as S
-        from oracle.pyoracle import COracle
-        from paper_2105_04150_b200 import SimulateOptions, make_state
-        orc = COracle(threads=threads)
-        bundle, h, g = S.bench_lattice_bundle(sample)
-        fam = orc.build_family(bundle.particles.coords, h, g.hint())
-        st = make_state(fam, False)
-        st.u = S.seed_displacements(bundle.particles.coords)
-        t0 = time.perf_counter()
-        orc.simulate(bundle, st, SimulateOptions(steps))
-        secs = time.perf_counter() - t0
-        live = int(fam.n_neigh.sum())
-        kind = "port"
-    n = sample[0] * sample[1] * sample[2]
-    return {"value": live * steps / secs, "unit": UNIT, "cores": threads, "kind": kind,
-            "ms_per_step": 1e3 * secs / steps,
-            "sample": f"{sample[0]}x{sample[1]}x{sample[2]} = {n} nodes z-slab of the same "
-                      f"lattice, {steps} velocity-Verlet steps of simulate(bond_parallel), "
-                      f"{live} live bonds"}
+        return None
+    return ref.bench_lattice_runs(counts, HORIZON, S_C[law], run_steps, threads,
+                                  law=1 if law == "trilinear" else 0)
+
+
+def split_runs(k: int):
+    """K timed steps as runs of >= 3 steps (>= 3 runs when K >= 9)."""
+    if k >= 9:
+        return [k // 3, k // 3, k - 2 * (k // 3)]
+    return [k]
+
+
+def cpu_baseline(counts, law):
+    """The reference CPU path on this box's host cores, on the same workload as
+    the GPU line: one warm-up step, then the median of 3 runs of 3 steps on
+    all cores (median of >= 3 runs of >= 3 steps)."""
+    cores = host_cores()
+    got = reference_runs(counts, law, [1, 3, 3, 3], [cores] * 4)
+    if got is None:
+        return None
+    secs, live, build_s = got
+    per = [t / 3 for t in secs[1:]]
+    ms = 1e3 * statistics.median(per)
+    n = counts[0] * counts[1] * counts[2]
+    return {"value": live * 1e3 / ms, "unit": UNIT, "cores": cores, "kind": "reference",
+            "ms_per_step": ms, "cpu": cpu_model(), "same_config": True,
+            "runs_ms_per_step": [1e3 * x for x in per], "family_build_s": build_s,
+            "sample": f"the full workload ({counts[0]}x{counts[1]}x{counts[2]} = {n} nodes, "
+                      f"{live} live bonds at the start): simulate(bond_parallel, velocity-Verlet) "
+                      f"of the unmodified reference, 1 warm-up step then the median of 3 runs x "
+                      f"3 steps on {cores} threads"}
 
 
 def run_reference_arm(args):
+    """--impl reference: the reference's own CPU implementation (oracle/_ref)
+    on the SAME configuration as our arm, all host cores, W warm-up steps
+    then exactly K timed steps in runs of >= 3 steps; plus one 1-core run."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     counts = (args.size, args.size, args.size)
-    steps_each = 2
-    vals = []
-    cb = None
-    for _ in range(args.warmup + args.steps):
-        cb = cpu_baseline(counts, steps_each)
-        vals.append(cb["value"])
-    timed = vals[args.warmup:]
-    value = statistics.median(timed)
+    cores = host_cores()
+    timed = split_runs(args.steps)
+    one = [args.ref_one_core_steps] if args.ref_one_core_steps > 0 else []
+    got = reference_runs(counts, args.law, [args.warmup] + timed + one,
+                         [cores] * (1 + len(timed)) + [1] * len(one))
     n = counts[0] * counts[1] * counts[2]
-    # the full workload's live bonds (interior rows of a 216^3 lattice), to
-    # express the sample throughput as ms/step of the whole workload
-    live_full = 1209979144 if counts == (216, 216, 216) else None
-    print(json.dumps({
+    if got is None:
+        print(json.dumps({"impl": "reference", "unavailable":
+                          f"no reference fixture for law {args.law} (oracle/_ref not built or "
+                          "the law needs bond classes)"}))
+        return 0
+    secs, live, build_s = got
+    runs = secs[1:1 + len(timed)]
+    per_run = [t / k for t, k in zip(runs, timed)]
+    ms = 1e3 * statistics.median(per_run)
+    value = live * 1e3 / ms
+    out = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": (1e3 * live_full / value) if live_full else None,
-        "ms_per_step_note": "extrapolated from the sample's bond throughput to the full lattice",
-        "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "n_gpus": args.gpus, "steps": sum(timed), "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
         "config": {"workload": f"cfg4 lattice {args.size}^3 = {n} nodes, delta=3dx (N=128), "
-                               "PMB, velocity-Verlet (reference CPU, bounded z-slab sample)",
-                   "nodes": n},
-        "cpu_baseline": cb,
+                               f"{LAWS[args.law]}, velocity-Verlet, dt=1e-3, seeded u",
+                   "nodes": n, "live_bonds": live, "law": args.law, "same_config": True},
+        "runs": [{"steps": k, "seconds": t, "ms_per_step": 1e3 * t / k}
+                 for k, t in zip(timed, runs)],
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "cpu": cpu_model(), "family_build_s": build_s,
+                         "sample": f"the full workload, {len(timed)} runs of {timed} steps, "
+                                   "median ms/step"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }))
+    }
+    if one:
+        t1 = secs[-1] / one[0]
+        out["one_core"] = {"steps": one[0], "ms_per_step": 1e3 * t1, "value": live / t1,
+                           "unit": UNIT}
+    print(json.dumps(out))
     return 0
 
 
 def _summary(args, value, ms_step, world, n, N, live, bytes_step, achieved, e2e, launches,
-             clocks, cpu, variant_name, extra_config=None, layout=None):
+             clocks, cpu, variant_name, probe=None, extra_config=None):
     peak, peak_kind = measured_peaks()
-    law_key = "" if getattr(args, "law", "pmb") == "pmb" else f"_{args.law}"
-    traffic = (measured_traffic(f"{layout}_{args.size}_{variant_name}{law_key}")
-               if world == 1 and layout else None)
-    law = {"pmb": "PMB c=1 s_c=1e6",
-           "trilinear": "trilinear(1, 1e-3, 2e-3, 1e6) with history",
-           "multi": "cfg5 laws by bond type: trilinear concrete, PMB steel, bilinear interface, "
-                    "two rebar lines, history"}[getattr(args, "law", "pmb")]
     cfg = {"workload": f"cfg4 lattice {args.size}^3 = {n} nodes, delta=3dx (N={N}), "
-                       f"{law}, velocity-Verlet, dt=1e-3, seeded u"
+                       f"{LAWS[args.law]}, velocity-Verlet, dt=1e-3, seeded u"
                        + (f", {world} z-slabs" if world > 1 else ""),
            "nodes": n, "group_size": N, "live_bonds": live, "variant": variant_name,
+           "law": args.law,
            "l2": f"inputs larger than L2 ({bytes_step / 1e9:.2f} GB/step algorithmic)",
            "parallelism": f"z-slab x{world}" if world > 1 else "single GPU"}
     cfg.update(extra_config or {})
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
+            "bytes_per_step": bytes_step,
+            "note": "achieved = SURVEY 8(d) algorithmic bytes per step / device time per step"}
+    if probe and "dram_bytes" in probe:
+        dram_gbs = probe["dram_bytes"] / (ms_step / 1e3) / 1e9
+        issue = probe["issue_active_pct"] / 100.0
+        roof.update({
+            "traffic": probe["dram_bytes"] / 1e9,
+            "traffic_unit": "GB per launch, measured by ncu in this run "
+                            "(dram__bytes_read.sum + dram__bytes_write.sum)",
+            "dram_gbs": dram_gbs, "dram_frac": dram_gbs / peak, "issue_frac": issue,
+            "occupancy": probe["warps_active_pct"] / 100.0,
+            "thread_instructions_per_bond": 32.0 * probe["warp_instructions"] / max(live, 1),
+        })
+        # what actually limits the kernel: HBM when the measured DRAM rate is
+        # near peak, the issue slots otherwise
+        if roof["dram_frac"] < 0.6 and issue > 0.6:
+            roof["bound"] = "issue"
+            roof["note"] += ("; the kernel moves fewer DRAM bytes than the formula counts "
+                             "(implicit / compact connectivity), so it is issue-bound: see "
+                             "dram_frac and issue_frac")
+    elif probe:
+        roof["probe_error"] = probe.get("error")
     return {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None,
         "dtype": "f64" if variant_name == "exact" else "f32 bond math / f64 state",
-        "data": "synthetic", "config": cfg,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak,
-                     "traffic": None if traffic is None else traffic / 1e9,
-                     "traffic_unit": "GB per launch (ncu dram__bytes_read+write)",
-                     "peak_source": peak_kind, "bytes_per_step": bytes_step,
-                     "note": "achieved = SURVEY 8(d) algorithmic bytes / device time; the "
-                             "lattice kernel keeps connectivity implicit, so DRAM traffic is "
-                             "below the algorithmic bytes and the kernel is issue-bound"},
+        "data": "synthetic", "config": cfg, "roofline": roof,
         "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "cpu_baseline": cpu,
     }
+
+
+def probe_run(args, variant):
+    """--probe-run: the workload's upload and a few steps (ncu_probe's child)."""
+    from paper_2105_04150_b200 import IntegratorKind, engine
+    bundle, fam, state0 = build_workload((args.size,) * 3, args.law)
+    ctx = engine.Context(0)
+    ctx.upload(bundle, state0, variant)
+    ctx.run(4, 0, IntegratorKind.velocity_verlet, 0, variant)
+    ctx.close()
+    return 0
 
 
 def run_single(args, variant, local):
@@ -270,7 +431,6 @@ def run_single(args, variant, local):
     bundle, fam, state0 = build_workload(counts, args.law)
     n = bundle.particles.size()
     N = int(fam.group_size)
-    live = int(fam.n_neigh.sum())
     setup_s = time.perf_counter() - t_setup
 
     ctx = engine.Context(local)
@@ -281,7 +441,9 @@ def run_single(args, variant, local):
     ctx.run(args.warmup, step, IntegratorKind.velocity_verlet, 0, variant)
     step += args.warmup
     torch.cuda.synchronize()
+    kernel = ctx.kernel()
     launches0 = ctx.launch_count()
+    live0 = ctx.live_bonds()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -290,9 +452,14 @@ def run_single(args, variant, local):
         ctx.run(args.steps, step, IntegratorKind.velocity_verlet, 0, variant)
         ev1.record(stream)
         torch.cuda.synchronize()
+    step += args.steps
     launches = ctx.launch_count() - launches0
+    live1 = ctx.live_bonds()
     ms_total = ev0.elapsed_time(ev1)
     ms_step = ms_total / args.steps
+    # live bonds fall while the fracturing variant breaks: count the mean of
+    # the live bonds before and after the timed steps
+    live = (live0 + live1) // 2
     value = live * args.steps / (ms_total / 1e3)
     bytes_step = algorithmic_bytes(n, N, live)
     if args.law in ("trilinear", "multi"):  # + 2 h B history (h = 4: fp32 on the fast path)
@@ -300,6 +467,21 @@ def run_single(args, variant, local):
     if args.law == "multi":  # + B bond_type
         bytes_step += live
     achieved = bytes_step / (ms_step / 1e3) / 1e9
+    # the same kernel over a longer stretch, so the clock sampler sees it under
+    # sustained load (reported beside the timed value, not instead of it)
+    sustain = None
+    if args.sustain_steps > 0:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local) as clk2:
+            torch.cuda.synchronize()
+            e0.record(stream)
+            ctx.run(args.sustain_steps, step, IntegratorKind.velocity_verlet, 0, variant)
+            e1.record(stream)
+            torch.cuda.synchronize()
+        sustain = {"steps": args.sustain_steps,
+                   "ms_per_step": e0.elapsed_time(e1) / args.sustain_steps,
+                   "clocks": clk2.summary()}
     ctx.close()
     del ctx
 
@@ -307,10 +489,12 @@ def run_single(args, variant, local):
     st = make_state(fam, bundle.model.needs_history())
     st.u = state0.u.copy()
     e2e_steps = args.e2e_steps
-    # bytes that cross PCIe: coords, u, v, a, V, rho, rows, counts in; u, v, a,
-    # n_neigh and only the rows that changed (none without breaks) out
-    h2d = (3 * n * 8 * 4 + 2 * n * 8 + n * N * 4 + 2 * n * 4)
-    d2h = (3 * n * 8 * 3 + n * 4)
+    hist_b = 8 * n * N if bundle.model.needs_history() else 0
+    # bytes that cross PCIe: coords, u, v, a, V, rho, rows, counts (+ bond
+    # types, history) in; u, v, a, n_neigh (+ history) and only the rows that
+    # changed out
+    h2d = (3 * n * 8 * 4 + 2 * n * 8 + n * N * 4 + 2 * n * 4 + hist_b
+           + (n * N if fam.bond_type is not None else 0))
     # one untimed call first (driver/pinned-buffer first-use costs), then the timed one
     warm = make_state(fam, bundle.model.needs_history())
     warm.u = state0.u.copy()
@@ -321,15 +505,25 @@ def run_single(args, variant, local):
     engine.simulate(bundle, st, SimulateOptions(e2e_steps, 0, 0, IntegratorKind.velocity_verlet,
                                                 variant))
     e2e_s = time.perf_counter() - t0
-    e2e = {"value": live * e2e_steps / e2e_s, "unit": UNIT,
+    changed = int(np.count_nonzero(st.connectivity.n_neigh != fam.n_neigh))
+    d2h = 3 * n * 8 * 3 + n * 4 + changed * N * 4 + hist_b
+    live_e2e = (int(fam.n_neigh.sum()) + int(st.connectivity.n_neigh.sum())) // 2
+    e2e = {"value": live_e2e * e2e_steps / e2e_s, "unit": UNIT,
            "h2d_bytes_per_step": h2d // e2e_steps, "d2h_bytes_per_step": d2h // e2e_steps,
-           "seconds": e2e_s,
+           "seconds": e2e_s, "rows_changed": changed,
            "how": f"one simulate() call via the C ABI, {e2e_steps} steps, host buffers "
                   "(upload + layout + run + download inside the timed region)"}
-    cpu = None if args.no_cpu else cpu_baseline(counts)
+    del st, fam, state0, bundle
+    probe = None if args.no_probe else ncu_probe(args, kernel)
+    cpu = None if args.no_cpu else cpu_baseline(counts, args.law)
+    extra = {"setup_s": round(setup_s, 2), "layout": layout, "kernel": kernel,
+             "live_bonds_timed": [live0, live1]}
+    if sustain:
+        extra["sustained"] = sustain
     out = _summary(args, value, ms_step, 1, n, N, live, bytes_step, achieved, e2e, launches,
-                   clk.summary(), cpu, args.variant,
-                   {"setup_s": round(setup_s, 2), "layout": layout}, layout)
+                   clk.summary(), cpu, args.variant, probe, extra)
+    if probe and "dram_bytes" in probe:
+        out["ncu_probe"] = probe
     print(json.dumps(out))
     return 0
 
@@ -436,7 +630,7 @@ def run_slabs(args, variant, rank, world, local):
     clocks = comm.allgather(clk.summary())
     if rank == 0:
         out = _summary(args, value, ms_step, world, n, N, live, bytes_step, achieved, e2e,
-                       launches, clocks[0], None, args.variant,
+                       launches, clocks[0], None, args.variant, None,
                        {"setup_s": round(setup_s, 2), "halo_bytes_per_step_nvlink": halo_bytes,
                         "clocks_all_ranks": clocks})
         print(json.dumps(out))
@@ -453,11 +647,21 @@ def main():
     ap.add_argument("--size", type=int, default=216)
     ap.add_argument("--e2e-steps", type=int, default=1000)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--law", default="pmb", choices=["pmb", "trilinear", "multi"])
+    ap.add_argument("--law", default="pmb", choices=sorted(LAWS))
+    ap.add_argument("--no-probe", action="store_true", help="skip the ncu DRAM-traffic probe")
+    ap.add_argument("--sustain-steps", type=int, default=200,
+                    help="extra untimed-for-value steps under the clock sampler")
+    ap.add_argument("--ref-one-core-steps", type=int, default=3,
+                    help="reference arm: steps of the extra 1-core run (0 = none)")
+    ap.add_argument("--probe-run", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.probe_run:
+        from paper_2105_04150_b200 import KernelVariant
+        return probe_run(args, KernelVariant.fast if args.variant == "fast"
+                         else KernelVariant.bond_parallel)
 
     import torch
     from paper_2105_04150_b200 import KernelVariant

@@ -292,6 +292,10 @@ enum {
     PD_LAYOUT_LATTICE = 2  /* PD_FAST on a lattice: implicit 122-offset pattern + live mask */
 };
 int pd_ctx_layout(pd_ctx* ctx);
+/* The step kernel instantiation the last step launched, e.g.
+ * "lattice_step_kernel<1,8,3,0,0>" (MODE, brick depth, CTAs/SM, BC, NF);
+ * "" before the first step.  The string is static. */
+const char* pd_ctx_kernel(pd_ctx* ctx);
 
 /* ---- binary containers (io.cpp:297-564), byte-compatible with the reference
  * PDST = restart state (save_state/load_state), PDNL = family cache

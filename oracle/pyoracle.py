@@ -212,6 +212,28 @@ class Reference(Backend):
         finally:
             self.lib.ref_random_free(h)
 
+    def bench_lattice_runs(self, dims, horizon: float, s_c: float, run_steps, threads,
+                           law: int = 0):
+        """ref_bench_lattice_runs: the bench fixture built once, then one
+        simulate() call per entry of run_steps on threads[r] workers (0 = all),
+        continuing the same state.  Returns (seconds per run, live bonds at
+        the start, family build seconds)."""
+        k = len(run_steps)
+        d = (C.c_int64 * 3)(*[int(x) for x in dims])
+        rs = (C.c_int64 * k)(*[int(x) for x in run_steps])
+        th = (C.c_int * k)(*[int(x) for x in threads])
+        secs = (C.c_double * k)()
+        live = C.c_int64()
+        build = C.c_double()
+        self.lib.ref_bench_lattice_runs.argtypes = [
+            C.POINTER(C.c_int64), C.c_double, C.c_double, C.c_int, C.POINTER(C.c_int64),
+            C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int64),
+            C.POINTER(C.c_double)]
+        self._check(self.lib.ref_bench_lattice_runs(d, float(horizon), float(s_c), int(law), rs,
+                                                    th, k,
+                                                    secs, C.byref(live), C.byref(build)))
+        return list(secs), live.value, build.value
+
     def bench_lattice(self, dims, horizon: float, s_c: float, steps: int, threads: int):
         d = (C.c_int64 * 3)(*[int(x) for x in dims])
         secs = C.c_double()

@@ -498,4 +498,62 @@ int ref_bench_lattice(const int64_t dims[3], double horizon, double s_c, int64_t
     });
 }
 
+// The bench fixture (bench.cpp:76-104) built once, then `n_runs` consecutive
+// simulate(bond_parallel, velocity-Verlet) calls continuing the same state:
+// run r takes run_steps[r] steps on threads[r] workers (set_worker_cap; 0 =
+// all) and its wall time goes to seconds_out[r] (bench.cpp:106-117 time_run,
+// family build excluded).
+int ref_bench_lattice_runs(const int64_t dims[3], double horizon, double s_c, int law,
+                           const int64_t* run_steps, const int* threads, int n_runs,
+                           double* seconds_out, int64_t* live_bonds_out,
+                           double* build_seconds_out) {
+    return map_exceptions([&] {
+        set_worker_cap(0);
+        GridDesc grid;
+        grid.spacing = 1;
+        grid.counts = {dims[0], dims[1], dims[2]};
+        ModelBundle bundle;
+        bundle.particles.coords = grid_coordinates(grid);
+        const Index n = grid.node_count();
+        bundle.particles.volume.assign(std::size_t(n), 1);
+        bundle.particles.density.assign(std::size_t(n), 1);
+        bundle.particles.material_tag.assign(std::size_t(n), 0);
+        bundle.model.laws.push_back(law == 1 ? DamageLaw::trilinear(1, Real(1e-3), Real(2e-3), s_c)
+                                             : DamageLaw::pmb(1, s_c));
+        bundle.bc = BoundaryConditions::none(n);
+        bundle.dt = Real(1e-3);
+        const auto b0 = std::chrono::steady_clock::now();
+        NeighborList family = build_family(bundle.particles.coords, horizon, &grid);
+        const auto b1 = std::chrono::steady_clock::now();
+        *build_seconds_out = std::chrono::duration<double>(b1 - b0).count();
+        SimulationState state = make_state_for(bundle, family);
+        family = NeighborList{};  // the state holds its own copy
+        for (Index i = 0; i < n; ++i) {
+            const Vec3 x = load_vec3(bundle.particles.coords, i);
+            store_vec3(state.u, i,
+                       {Real(1e-4) * std::sin(Real(0.1) * x.x + Real(0.2) * x.y),
+                        Real(1e-4) * std::cos(Real(0.15) * x.y + Real(0.1) * x.z),
+                        Real(1e-4) * std::sin(Real(0.12) * x.z + Real(0.17) * x.x)});
+        }
+        int64_t live = 0;
+        for (auto c : state.connectivity.n_neigh)
+            live += c;
+        *live_bonds_out = live;
+        int64_t step = 0;
+        for (int r = 0; r < n_runs; ++r) {
+            set_worker_cap(unsigned(threads[r]));
+            SimulateOptions opts;
+            opts.steps = run_steps[r];
+            opts.first_step = step;
+            opts.variant = KernelVariant::bond_parallel;
+            const auto t0 = std::chrono::steady_clock::now();
+            simulate(bundle, state, opts);
+            const auto t1 = std::chrono::steady_clock::now();
+            seconds_out[r] = std::chrono::duration<double>(t1 - t0).count();
+            step += run_steps[r];
+        }
+        set_worker_cap(0);
+    });
+}
+
 } // extern "C"

@@ -248,15 +248,19 @@ template <int MODE, bool NODE_SUM>
 cudaError_t launch_m(const DevArgs& A, int M, dim3 grid, cudaStream_t st) {
     switch (M) {
     case 1:
+        t_last_kernel = kernel_name<0, MODE, 1, NODE_SUM>("exact_step_kernel");
         exact_step_kernel<MODE, 1, NODE_SUM><<<grid, 256, 0, st>>>(A);
         break;
     case 2:
+        t_last_kernel = kernel_name<0, MODE, 2, NODE_SUM>("exact_step_kernel");
         exact_step_kernel<MODE, 2, NODE_SUM><<<grid, 256, 0, st>>>(A);
         break;
     case 4:
+        t_last_kernel = kernel_name<0, MODE, 4, NODE_SUM>("exact_step_kernel");
         exact_step_kernel<MODE, 4, NODE_SUM><<<grid, 256, 0, st>>>(A);
         break;
     case 8:
+        t_last_kernel = kernel_name<0, MODE, 8, NODE_SUM>("exact_step_kernel");
         exact_step_kernel<MODE, 8, NODE_SUM><<<grid, 256, 0, st>>>(A);
         break;
     default:

@@ -162,30 +162,43 @@ __global__ void __launch_bounds__(TT, MINB) fast_step_kernel(DevArgs A, FastDev 
     float fz = 0.f;
     int broke = 0;
     // one group of 8 slots (one 16-byte index load)
+    // one slot's geometry: xi + eta (cxy, cz), |xi + eta|^2, 1 / |xi + eta| and
+    // s = (|cur| - |xi|) / |xi| = eta.(xi + cur) / (|xi| (|cur| + |xi|))
+    auto geom = [&](unsigned offB, float2& cxy, float& cz, float& cur2, float& rc) -> float {
+        const float4 ar = *reinterpret_cast<const float4*>(cA + 2 * offB);
+        const float2 br = *reinterpret_cast<const float2*>(cB + offB);
+        const float2 exy = __fadd2_rn(make_float2(ar.x, ar.y), nxi);
+        const float2 hxy = __fadd2_rn(make_float2(ar.z, ar.w), nui);
+        const float2 ezh = __fadd2_rn(br, nzi);  // (xi_z, eta_z)
+        cxy = __fadd2_rn(exy, hxy);
+        const float2 sxy = __fadd2_rn(exy, cxy);
+        const float ez = ezh.x, hz = ezh.y;
+        cz = ez + hz;
+        const float2 e2 = __fmul2_rn(exy, exy);
+        const float2 n2 = __fmul2_rn(hxy, sxy);
+        const float ref2 = fmaf(ez, ez, e2.x + e2.y);
+        const float num = fmaf(hz, ez + cz, n2.x + n2.y);  // eta.(2 xi + eta)
+        cur2 = ref2 + num;                                  // |xi + eta|^2
+        const float rr = rsqrt_approx(ref2);
+        rc = rsqrt_approx(cur2);
+        return num * rr * rcp_approx(cur2 * rc + ref2 * rr);
+    };
+    // A collapsed bond (|xi + eta|^2 = 0 or below fp32's normal range, which
+    // the approximate rsqrt flushes: rc = +inf, s = NaN) keeps its bond and
+    // adds nothing -- the reference's stretch is -1 < s_c there and its
+    // contribution 0 (engine.cpp:61-65, 100-101).  In KIND 0/1 its NaN stretch
+    // takes the rare break branch, which re-checks it; a NaN force (a
+    // collapsed bond to a no-failure neighbour) is recomputed after the row.
+    constexpr float kMinNormal = 1.17549435e-38f;
     auto group = [&](const uint4 w, unsigned short* lrow) {
         const unsigned words[4] = {w.x, w.y, w.z, w.w};
         unsigned bmask = 0;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
             const unsigned offB = (q & 1) ? (words[q >> 1] >> 16) : (words[q >> 1] & 0xFFFFu);
-            const float4 ar = *reinterpret_cast<const float4*>(cA + 2 * offB);
-            const float2 br = *reinterpret_cast<const float2*>(cB + offB);
-            const float2 exy = __fadd2_rn(make_float2(ar.x, ar.y), nxi);
-            const float2 hxy = __fadd2_rn(make_float2(ar.z, ar.w), nui);
-            const float2 ezh = __fadd2_rn(br, nzi);  // (xi_z, eta_z)
-            const float2 cxy = __fadd2_rn(exy, hxy);
-            const float2 sxy = __fadd2_rn(exy, cxy);
-            const float ez = ezh.x, hz = ezh.y;
-            const float cz = ez + hz;
-            const float2 e2 = __fmul2_rn(exy, exy);
-            const float2 n2 = __fmul2_rn(hxy, sxy);
-            const float ref2 = fmaf(ez, ez, e2.x + e2.y);
-            const float num = fmaf(hz, ez + cz, n2.x + n2.y);  // eta.(2 xi + eta)
-            const float cur2 = ref2 + num;                     // |xi + eta|^2
-            const float rr = rsqrt_approx(ref2);
-            const float rc = rsqrt_approx(cur2);
-            // s = (|cur| - |xi|) / |xi| = eta.(xi + cur) / (|xi| (|cur| + |xi|))
-            const float s = num * rr * rcp_approx(cur2 * rc + ref2 * rr);
+            float2 cxy;
+            float cz, cur2, rc;
+            const float s = geom(offB, cxy, cz, cur2, rc);
             float scale;
             if (KIND != 2) {
                 // !(s < s_c): an fp32 stretch that overflowed is NaN and breaks, as the
@@ -199,8 +212,8 @@ __global__ void __launch_bounds__(TT, MINB) fast_step_kernel(DevArgs A, FastDev 
                 scale = KIND == 0 ? s * rc
                                   : s * *reinterpret_cast<const float*>(cV + (offB >> 1)) * rc;
             } else {
-                if (offB == 0)
-                    continue;  // broken/padding: its history must not re-trigger the break
+                if (offB == 0 || cur2 < kMinNormal)
+                    continue;  // broken/padding (its history must not re-trigger the break), collapsed
                 const bool no_fail = nfi || offB >= nf_start;
                 const long long sidx = (lrow - F.lidx) + q;
                 const FastLaw& law = c_flaws[F.btype ? int(F.btype[sidx]) : 0];
@@ -239,9 +252,16 @@ __global__ void __launch_bounds__(TT, MINB) fast_step_kernel(DevArgs A, FastDev 
         }
         if (KIND != 2 && bmask) {
             for (int q = 0; q < 8; ++q)
-                if (bmask >> q & 1u)
+                if (bmask >> q & 1u) {
+                    const unsigned offB = (q & 1) ? (words[q >> 1] >> 16) : (words[q >> 1] & 0xFFFFu);
+                    float2 cxy;
+                    float cz, cur2, rc;
+                    geom(offB, cxy, cz, cur2, rc);
+                    if (cur2 < kMinNormal)
+                        continue;  // collapsed: kept, adds nothing
                     lrow[q] = 0;
-            broke += __popc(bmask);
+                    ++broke;
+                }
         }
     };
     int kb = 0;
@@ -259,6 +279,25 @@ __global__ void __launch_bounds__(TT, MINB) fast_step_kernel(DevArgs A, FastDev 
     }
     if (kb < nkb)
         group(wnext, lrow);
+    if (KIND == 1 && isnan(fxy.x + fxy.y + fz)) {
+        // rare: walk the row again (breaks are applied: offset 0 adds 0),
+        // skipping collapsed bonds; a genuinely non-finite state stays NaN
+        fxy = make_float2(0.f, 0.f);
+        fz = 0.f;
+        const unsigned short* r = F.lidx + F.slot_off[tile] + (long long)t * 8;
+        for (int g = 0; g < nkb; ++g, r += kstride)
+            for (int q = 0; q < 8; ++q) {
+                const unsigned offB = r[q];
+                float2 cxy;
+                float cz, cur2, rc;
+                const float s = geom(offB, cxy, cz, cur2, rc);
+                if (cur2 < kMinNormal)
+                    continue;
+                const float scale = s * *reinterpret_cast<const float*>(cV + (offB >> 1)) * rc;
+                fxy = __ffma2_rn(cxy, make_float2(scale, scale), fxy);
+                fz = fmaf(cz, scale, fz);
+            }
+    }
     if (broke)
         A.n_neigh[i] -= broke;
     if (KIND == 0) {
@@ -311,6 +350,7 @@ cudaError_t launch_cfg(const DevArgs& A, const FastDev& F, int tiles, cudaStream
     const cudaError_t e = KernelCfg<MODE, KIND, TT, MINB, PRE, R>::ensure();
     if (e != cudaSuccess)
         return e;
+    t_last_kernel = kernel_name<4, MODE, KIND, TT, MINB, PRE, R>("fast_step_kernel");
     fast_step_kernel<MODE, KIND, TT, MINB, PRE, R><<<tiles, TT, smem_bytes(KIND, F.cap), st>>>(A, F);
     return cudaGetLastError();
 }

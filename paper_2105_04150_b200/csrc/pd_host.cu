@@ -214,6 +214,7 @@ struct pd_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     int64_t launches = 0;
+    const char* kernel = "";  // the step kernel instantiation last launched
 
     int64_t n = 0;
     int N = 0, W = 0, log2N = 0;
@@ -726,7 +727,14 @@ int try_lattice(pd_ctx* ctx, const pd_particles& p, const pd_state& st, const pd
     const size_t pslots = size_t(lattice_slot_count(L));
     // several laws (<= 8, <= 3 breakpoints each): the typed unrolled kernel,
     // with the bond type in the history words (PD_LAT_NL_LOOP: the loop kernel)
-    bool small_laws = m.n_laws >= 2 && m.n_laws <= 8;
+    // The unrolled kernels evaluate each law's envelope as min/max of its
+    // segment lines; laws where that composition is not the envelope
+    // (e.g. hardening then softening) take the loop kernel's segment selection
+    bool minmax_ok = true;
+    for (int k = 0; k < m.n_laws && minmax_ok; ++k)
+        minmax_ok = lattice_minmax_ok(m.laws[k].breakpoints, m.laws[k].forces,
+                                      m.laws[k].n_breakpoints);
+    bool small_laws = m.n_laws >= 2 && m.n_laws <= 8 && minmax_ok;
     for (int k = 0; k < m.n_laws && small_laws; ++k)
         small_laws = m.laws[k].n_breakpoints <= 3;
     L.typed = (nl && small_laws && !std::getenv("PD_LAT_NL_LOOP")) ? 1 : 0;
@@ -778,7 +786,7 @@ int try_lattice(pd_ctx* ctx, const pd_particles& p, const pd_state& st, const pd
         }
         lattice_set_laws(laws.data(), m.n_laws, L, s);
         PD_CK(cudaGetLastError());
-        if (std::getenv("PD_LAT_NL_LOOP"))  // force the runtime-loop kernel (tests)
+        if (std::getenv("PD_LAT_NL_LOOP") || !minmax_ok)  // the runtime-loop kernel
             L.multi = 1;
     }
     L.sc = float(m.laws[0].breakpoints[0]);
@@ -911,17 +919,13 @@ int setup_fast(pd_ctx* ctx, const pd_particles& p, const pd_state& st,
 }
 
 int launch_step(pd_ctx* ctx, DevArgs& A, int mode) {
-    if (ctx->lattice) {
+    if (ctx->lattice)
         PD_CK(launch_lattice(A, ctx->lat, mode, ctx->stream));
-        ++ctx->launches;
-        return PD_OK;
-    }
-    if (ctx->fast) {
+    else if (ctx->fast)
         PD_CK(launch_fast(A, ctx->fast_args(), mode, ctx->kind, ctx->lay.n_tiles, ctx->stream));
-        ++ctx->launches;
-        return PD_OK;
-    }
-    PD_CK(launch_exact(A, mode, ctx->variant == PD_NODE_PARALLEL, ctx->stream));
+    else
+        PD_CK(launch_exact(A, mode, ctx->variant == PD_NODE_PARALLEL, ctx->stream));
+    ctx->kernel = t_last_kernel;
     ++ctx->launches;
     return PD_OK;
 }
@@ -1434,6 +1438,8 @@ int pd_ctx_snapshot_every(pd_ctx* ctx, int64_t every, const char* pattern) {
     ctx->snap_pattern = pattern ? pattern : "";
     return ok();
 }
+
+const char* pd_ctx_kernel(pd_ctx* ctx) { return ctx ? ctx->kernel : ""; }
 
 int pd_ctx_layout(pd_ctx* ctx) {
     if (!ctx || !ctx->fast)

@@ -13,6 +13,21 @@
 
 namespace pdb {
 
+// The step kernel the last launch on this host thread ran, as
+// "<family><template values>" (pd_ctx_kernel; the parity tests assert which
+// instantiation they exercised).
+inline thread_local const char* t_last_kernel = "";
+template <int Family, int... V> const char* kernel_name(const char* base) {
+    static const std::string s = [base] {
+        std::string r = base;
+        r += '<';
+        ((r += std::to_string(V) + ","), ...);
+        r.back() = '>';
+        return r;
+    }();
+    return s.c_str();
+}
+
 // pd_xfer.cpp: large host <-> device copies through pinned bounce buffers
 // (synchronous with respect to the host on return)
 cudaError_t h2d_large(void* dev, const void* host, size_t bytes, cudaStream_t s);
@@ -173,6 +188,11 @@ cudaError_t lattice_build_masks(const double4* xv, long long n, const int32_t* e
                                 const double* lambda, const double* beta, cudaStream_t st);
 void lattice_set_laws(const DevLaw* laws, int n, LatticeArgs& L, cudaStream_t st);
 long long lattice_slot_count(const LatticeArgs& L);  // length of the brick-major slot arrays
+// true when the unrolled lattice kernels' branch-free envelope
+// op1(l_0, op2(l_1, l_2)) (pd_lattice_nlu.cuh nl_law) reproduces
+// envelope_force (formulas.hpp:77-89) of this law on [0, s_c]; false for
+// more than 3 breakpoints and for shapes such as hardening-then-softening
+bool lattice_minmax_ok(const double* bp, const double* f, int nbp);
 cudaError_t launch_lattice(const DevArgs& A, const LatticeArgs& L, int mode, cudaStream_t st);
 cudaError_t launch_lattice_materialize(const int32_t* entries0, const uint4* mask, long long begin,
                                        long long end, long long n, int N, const LatticeArgs& L,

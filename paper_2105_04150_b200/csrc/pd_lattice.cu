@@ -32,6 +32,8 @@
 #include <cstring>
 #include <limits>
 #include <utility>
+#include <vector>
+#include <algorithm>
 
 #include "pd_device.cuh"
 #include "pd_fast.cuh"
@@ -113,6 +115,12 @@ __device__ __forceinline__ uint4 slow_node(const float4* own, const float4 ri, c
         const float4 rj = own[dx + HX * (dy + HY * dz)];
         float a;
         const float s = stretch_r(rj, ri, dx, dy, dz, a);
+        // a collapsed bond (|xi + eta| = 0, or below fp32's normal range: the
+        // approximate rsqrt flushes it and a = +inf) keeps its bit and adds
+        // nothing: the reference's stretch is -1 < s_c there and its
+        // contribution 0 (engine.cpp:61-65, 100-101)
+        if (a == __int_as_float(0x7f800000))
+            continue;
         if (!(s < sc) && !(rj.w < 0.f)) {  // a no-failure neighbour keeps the bond
             dead[c >> 5] |= 1u << (c & 31);
             continue;
@@ -164,7 +172,10 @@ __global__ void __launch_bounds__(BX * BY * BZT, MINB) lattice_step_kernel(DevAr
     const float sc = (NF && ri.w < 0.f) ? __int_as_float(0x7f800000) : L.sc;
     Acc a{make_float2(0.f, 0.f), 0.f, make_float2(0.f, 0.f), 0.f, -__int_as_float(0x7f800000)};
     all_slots<NF>(std::make_integer_sequence<int, NPAT>{}, own, ri, m, a);
-    if (!(a.smax < sc)) {  // some live bond breaks this step (or its stretch overflowed)
+    // some live bond breaks this step (or its stretch overflowed), or a
+    // collapsed bond (|xi + eta| = 0: NaN stretch) made the force NaN -- rare
+    // cases, recomputed slot by slot with the reference's semantics
+    if (!(a.smax < sc) || isnan(a.fxy.x + a.fxy.y + a.fz)) {
         float3 f;
         const uint4 d = slow_node<NF>(own, ri, m, sc, f);
         L.mask[i] = make_uint4(m.x & ~d.x, m.y & ~d.y, m.z & ~d.z, m.w & ~d.w);
@@ -283,6 +294,8 @@ __global__ void __launch_bounds__(BX * BY * BZT, 16 / BZT) lattice_nl_kernel(Dev
             const float4 rj = own[c_goff[c0 + q]];
             float s, rc, cx, cy, cz;
             stretch(rj, ri, g1.x, g1.y, g1.z, g1.w, g2.x, g2.y, s, rc, cx, cy, cz);
+            if (rc == __int_as_float(0x7f800000))
+                continue;  // collapsed (|xi + eta| = 0): s = -1 in the reference, no break, 0
             const float hh = hcur[q];
             float f;
             bool brk = false;
@@ -515,6 +528,7 @@ cudaError_t launch_cfg(const DevArgs& A, const LatticeArgs& L, cudaStream_t st) 
     const cudaError_t e = configure_one<MODE, BZT, MINB, BC, NF>();
     if (e != cudaSuccess)
         return e;
+    t_last_kernel = kernel_name<1, MODE, BZT, MINB, BC, NF>("lattice_step_kernel");
     lattice_step_kernel<MODE, BZT, MINB, BC, NF>
         <<<dim3(unsigned(nbx), unsigned(nby), unsigned(nbz)), BX * BY * BZT,
            sizeof(float4) * nrec<BZT>(), st>>>(A, L);
@@ -544,9 +558,11 @@ cudaError_t launch_bc(const DevArgs& A, const LatticeArgs& L, cudaStream_t st) {
     // Small models (fewer 16x4x4 bricks than two per SM, e.g. cfg1's beam):
     // the step is one latency chain per thread, so use 16x4x1 bricks (more
     // CTAs over the SMs) and the full register file (the compiler can overlap
-    // several slots).  PD_LAT_CFG = 5 forces it, 6 forbids it.
+    // several slots).  PD_LAT_CFG = 5 forces it; any other
+    // nonzero value forbids it (6: the large-model rule below without its
+    // brick-depth waste test, i.e. 16x4x4 bricks; 1-4, 7, 8: fixed shapes).
     const long long bricks4 = (long long)((L.nx + 15) / 16) * ((L.ny + 3) / 4) * ((L.nz_own + 3) / 4);
-    if (L.cfg == 5 || (L.cfg != 6 && bricks4 < 2LL * sm_count()))
+    if (L.cfg == 5 || (L.cfg == 0 && bricks4 < 2LL * sm_count()))
         return launch_cfg<MODE, 1, 1, BC, NF>(A, L, st);
     if constexpr (!NF && !BC) {
         switch (L.cfg) {
@@ -735,6 +751,7 @@ cudaError_t launch_nl_loop(const DevArgs& A, const LatticeArgs& L, cudaStream_t 
     const cudaError_t e = smem_optin<lattice_nl_kernel<MODE, BC, true, BZT>>(int(smem));
     if (e != cudaSuccess)
         return e;
+    t_last_kernel = kernel_name<2, MODE, BC, 1, BZT>("lattice_nl_kernel");
     lattice_nl_kernel<MODE, BC, true, BZT><<<grid, BX * BY * BZT, smem, st>>>(A, L);
     return cudaGetLastError();
 }
@@ -779,6 +796,47 @@ cudaError_t launch_lattice_materialize(const int32_t* entries0, const uint4* mas
         lattice_materialize_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(
             entries0, mask, begin, end, n, N, L, out, hist_out);
     return cudaGetLastError();
+}
+
+bool lattice_minmax_ok(const double* bp, const double* f, int nbp) {
+    if (nbp <= 2)
+        return nbp >= 1;  // one line, or two lines meeting at bp_0: always max/min of them
+    if (nbp > 3)
+        return false;
+    // the kernels' lines in fp64 (lattice_set_laws): l_0 = sl_0 e, l_k = a_k + sl_k e
+    const double sl0 = f[0] / bp[0];
+    const double sl1 = (f[1] - f[0]) / (bp[1] - bp[0]), a1 = f[0] - bp[0] * sl1;
+    const double sl2 = (f[2] - f[1]) / (bp[2] - bp[1]), a2 = f[1] - bp[1] * sl2;
+    const bool cvx1 = sl1 > sl0, cvx2 = sl2 > sl1;
+    const double sl[3] = {sl0, sl1, sl2}, a[3] = {0.0, a1, a2};
+    auto comp = [&](double e) {
+        const double l0 = sl0 * e, l1 = a1 + sl1 * e, l2 = a2 + sl2 * e;
+        const double t = cvx2 ? std::max(l1, l2) : std::min(l1, l2);
+        return cvx1 ? std::max(l0, t) : std::min(l0, t);
+    };
+    auto env = [&](double e) {  // envelope_force: the segment whose end exceeds e
+        const int k = e < bp[0] ? 0 : (e < bp[1] ? 1 : 2);
+        return a[k] + sl[k] * e;
+    };
+    // both sides are piecewise linear with kinks only at the breakpoints and
+    // where two lines cross: equal at every such point (and at 0) => equal on
+    // [0, s_c]
+    std::vector<double> pts = {0.0, bp[0], bp[1], bp[2]};
+    for (int p = 0; p < 3; ++p)
+        for (int q = p + 1; q < 3; ++q)
+            if (sl[p] != sl[q]) {
+                const double e = (a[q] - a[p]) / (sl[p] - sl[q]);
+                if (e > 0.0 && e < bp[2])
+                    pts.push_back(e);
+            }
+    double scale = 0.0;
+    for (int k = 0; k < 3; ++k)
+        scale = std::max(scale, std::fabs(f[k]));
+    scale = std::max(scale, std::fabs(sl0 * bp[0]));
+    for (double e : pts)
+        if (std::fabs(comp(e) - env(e)) > 1e-9 * scale)
+            return false;
+    return true;
 }
 
 void lattice_set_laws(const DevLaw* laws, int n, LatticeArgs& L, cudaStream_t st) {

@@ -285,6 +285,12 @@ __device__ __forceinline__ uint4 nl_slow_node(const LatticeArgs& L, const float4
         const float4 rj = own[dx + HX * (dy + HY * dz)];
         float a;
         const float s = stretch_r(rj, ri, dx, dy, dz, a);
+        // collapsed (|xi + eta| = 0 or below fp32's normal range, a = +inf):
+        // the reference's s = -1 updates no history, never breaks and adds 0
+        // (engine.cpp:61-65, 88-101); the unrolled pass stored no history for
+        // it either (NaN > h is false)
+        if (a == __int_as_float(0x7f800000))
+            continue;
         const bool brk_ok = !NF || rj.w >= nfthr;
         float e, f, c_lin = R.c, s_c = sc;
         if (NBP == 0) {
@@ -365,7 +371,8 @@ __global__ void __launch_bounds__(BX * BY * BZT, 16 / BZT) lattice_nlu_kernel(De
     AccN acc{make_float2(0.f, 0.f), 0.f, make_float2(0.f, 0.f), 0.f, -inf};
     nl_all_slots<NBP, LAM, NF, NB>(std::make_integer_sequence<int, NPAT>{}, own, ri, m, hb, lb,
                                nfthr, R, tab, hr, lr, acc);
-    if (!(acc.emax < (NBP == 0 ? 0.f : R.sc))) {  // a live bond breaks (or overflowed)
+    // a live bond breaks (or overflowed), or a collapsed bond made the force NaN
+    if (!(acc.emax < (NBP == 0 ? 0.f : R.sc)) || isnan(acc.fxy.x + acc.fxy.y + acc.fz)) {
         asm volatile("" ::: "memory");  // after this node's history stores
         float3 f;
         const uint4 d = nl_slow_node<NBP, LAM, NF, NB>(L, own, ri, m, hb, lb, nfthr, R, tab, R.sc, f);
@@ -395,6 +402,7 @@ cudaError_t launch_nlu6(const DevArgs& A, const LatticeArgs& L, cudaStream_t st)
     const cudaError_t e = smem_optin<lattice_nlu_kernel<MODE, BC, NBP, LAM, NF, BZT>>(smem);
     if (e != cudaSuccess)
         return e;
+    t_last_kernel = kernel_name<3, MODE, BC, NBP, LAM, NF, BZT>("lattice_nlu_kernel");
     lattice_nlu_kernel<MODE, BC, NBP, LAM, NF, BZT>
         <<<dim3(unsigned(nbx), unsigned(nby), unsigned(nbz)), BX * BY * BZT, smem, st>>>(A, L);
     return cudaGetLastError();

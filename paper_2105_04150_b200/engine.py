@@ -159,6 +159,8 @@ def library() -> C.CDLL:
         lib.pd_ctx_launch_count.argtypes = [C.c_void_p]
         lib.pd_ctx_launch_count.restype = C.c_int64
         lib.pd_ctx_layout.argtypes = [C.c_void_p]
+        lib.pd_ctx_kernel.argtypes = [C.c_void_p]
+        lib.pd_ctx_kernel.restype = C.c_char_p
         lib.pd_ctx_live_bonds.argtypes = [C.c_void_p]
         lib.pd_ctx_live_bonds.restype = C.c_int64
         lib.pd_damage.argtypes = [C.POINTER(abi.pd_neighbor_list), C.POINTER(C.c_double)]
@@ -509,6 +511,11 @@ class Context:
     def layout(self) -> str:
         """"exact", "tiles" or "lattice" (pd_ctx_layout)."""
         return ("exact", "tiles", "lattice")[self.lib.pd_ctx_layout(self.h)]
+
+    def kernel(self) -> str:
+        """The step kernel instantiation the last step launched (pd_ctx_kernel),
+        e.g. "lattice_step_kernel<1,8,3,0,0>"."""
+        return self.lib.pd_ctx_kernel(self.h).decode()
 
     def launch_count(self) -> int:
         return int(self.lib.pd_ctx_launch_count(self.h))

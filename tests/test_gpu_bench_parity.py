@@ -1,0 +1,251 @@
+"""Parity of the kernels BENCH numbers come from, at the bench size, and of the
+fast variant's break path along fracturing trajectories.
+
+The yardstick is the exact GPU path (KernelVariant.bond_parallel): it is
+bitwise equal to the reference and the C oracle (test_gpu_parity.py, up to
+1M nodes), and unlike the CPU oracle it finishes a 10M-node step in
+milliseconds.  Contract, one pass from
+identical states:
+
+  forces   max_rel_difference (oracles.hpp:215-228) <= FORCE_TOL over the nodes
+           whose broken sets agree
+  breaks   the broken sets are identical except bonds whose fp64 stretch lies
+           within EPS_S * s_c of the critical stretch (engine.cpp:90-98)
+
+Fracturing K-step runs are compared the same way at EVERY step, re-synced on
+the exact trajectory: step k's exact state is uploaded to the fast variant,
+which takes one step, and is compared with the exact state k+1.
+"""
+import numpy as np
+import pytest
+
+import scenarios as S
+from paper_2105_04150_b200 import engine, geometry
+from paper_2105_04150_b200.types import (DamageLaw, IntegratorKind, KernelVariant,
+                                         SimulationState, make_state)
+
+pytestmark = pytest.mark.gpu
+
+FORCE_TOL = 2e-5
+EPS_S = 1e-5
+HIST_TOL = 1e-5  # fp32 history, relative to s_c
+
+
+def max_rel_difference(a, b):
+    """oracles::max_rel_difference (tests/oracles.hpp:215-228)."""
+    scale = max(np.max(np.abs(a)), 1e-300)
+    denom = np.maximum(np.maximum(np.abs(a), np.abs(b)), scale)
+    return float(np.max(np.abs(a - b) / denom))
+
+
+def slot_stretch(coords, u, N, idx, entries):
+    """fp64 stretch (engine.cpp:61-65) of the slots `idx` of padded rows."""
+    i = idx // N
+    j = entries[idx].astype(np.int64)
+    x = coords.reshape(-1, 3)
+    uu = u.reshape(-1, 3)
+    ref = x[j] - x[i]
+    cur = ref + (uu[j] - uu[i])
+    rl = np.sqrt((ref ** 2).sum(1))
+    return (np.sqrt((cur ** 2).sum(1)) - rl) / rl
+
+
+def step_once(bundle, state, variant, integrator, env=None, monkeypatch=None):
+    """One simulate() step of `state` on a fresh context; returns the new
+    state and the step kernel that ran."""
+    if env is not None:
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+    ctx = engine.Context(0)
+    hist = bundle.model.needs_history()
+    st = SimulationState(state.u.copy(), state.v.copy(), state.a.copy(), state.step,
+                         state.connectivity.copy(),
+                         state.bond_history.copy() if hist else np.zeros(0))
+    ctx.upload(bundle, st, variant)
+    ctx.run(1, state.step, integrator, 0, variant)
+    ctx.download(st)
+    kernel = ctx.kernel()
+    ctx.close()
+    return st, kernel
+
+
+def compare_pass(coords, ref, fast, u_force, s_c, N, hist_ref=None):
+    """The one-pass contract above; returns (differing slots, force error)."""
+    e_r, e_f = ref.connectivity.entries, fast.connectivity.entries
+    diff = np.flatnonzero(e_r != e_f)
+    if diff.size:
+        orig = np.where(e_r[diff] >= 0, e_r[diff], e_f[diff])
+        ent = np.zeros_like(e_r)
+        ent[diff] = orig
+        s = slot_stretch(coords, u_force, N, diff, ent)
+        if hist_ref is not None:  # n-linear: the break test is on max(s, h)
+            s = np.maximum(s, hist_ref[diff])
+        far = np.abs(s - s_c) > EPS_S * s_c
+        assert not far.any(), (f"{int(far.sum())} of {diff.size} broken-set differences lie "
+                               f"farther than {EPS_S} s_c from s_c")
+    n = ref.connectivity.n_neigh.size
+    ok = np.ones(n, bool)
+    ok[np.unique(diff // N)] = False
+    a_r = ref.a.reshape(n, 3)[ok]
+    a_f = fast.a.reshape(n, 3)[ok]
+    err = max_rel_difference(a_r, a_f)
+    assert err <= FORCE_TOL, err
+    assert np.array_equal(fast.connectivity.n_neigh,
+                          (fast.connectivity.entries.reshape(n, N) >= 0).sum(1))
+    return int(diff.size), err
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("s_c", [1e6, 1e-5])
+def test_bench_kernel_216_one_pass_matches_exact(monkeypatch, s_c):
+    """cfg4 (216^3, 1.21e9 live bonds): the BENCH instantiation
+    lattice_step_kernel<1,8,3,0,0> (velocity-Verlet, 16x4x8 bricks, 3
+    CTAs/SM) for one step from the seeded state, against the bitwise exact
+    path.  s_c = 1e-5 is SURVEY 8(d)'s fracturing variant: ~12 % of the bonds
+    break in this pass, through the recompute (break) path."""
+    monkeypatch.setenv("PD_LAT_CFG", "1")
+    b, h, g = S.bench_lattice_bundle((216, 216, 216), s_c=s_c)
+    fam = geometry.build_family(b.particles.coords, h, g)
+    N = int(fam.group_size)
+    st0 = make_state(fam, False)
+    st0.u = S.seed_displacements(b.particles.coords)
+    vv = IntegratorKind.velocity_verlet
+    fast, kernel = step_once(b, st0, KernelVariant.fast, vv)
+    assert kernel == "lattice_step_kernel<1,8,3,0,0>", kernel
+    ref, kernel_ref = step_once(b, st0, KernelVariant.bond_parallel, vv)
+    assert kernel_ref.startswith("exact_step_kernel<1,"), kernel_ref
+    del st0
+    broken = int(fam.n_neigh.sum() - ref.connectivity.n_neigh.sum())
+    if s_c < 1:
+        assert broken > 0.1 * fam.n_neigh.sum(), broken
+    else:
+        assert broken == 0
+    # velocity-Verlet from v = a = 0: the force pass sees u_0 (the drift adds 0)
+    ndiff, err = compare_pass(b.particles.coords, ref, fast, ref.u, s_c, N)
+    print(f"216^3 s_c={s_c}: {broken} broken, {ndiff} slots within eps of s_c differ, "
+          f"force max_rel_difference {err:.2e}")
+
+
+def _resynced(bundle, fam, st0, integrator, steps, env, monkeypatch, layout):
+    """Per-step comparison along the exact trajectory (module docstring)."""
+    monkeypatch.delenv("PD_FAST_LAYOUT", raising=False)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    N = int(fam.group_size)
+    hist = bundle.model.needs_history()
+    s_c = max(lw.breakpoints[-1] for lw in bundle.model.laws)
+    ex = engine.Context(0)
+    cur = SimulationState(st0.u.copy(), st0.v.copy(), st0.a.copy(), st0.step,
+                          st0.connectivity.copy(), st0.bond_history.copy() if hist else np.zeros(0))
+    ex.upload(bundle, cur, KernelVariant.bond_parallel)
+    total_diff, worst, broken_total = 0, 0.0, 0
+    for k in range(steps):
+        fast, kernel = step_once(bundle, cur, KernelVariant.fast, integrator)
+        ex.run(1, cur.step, integrator, 0, KernelVariant.bond_parallel)
+        nxt = make_state(fam, hist)
+        ex.download(nxt)
+        # the force of step k+1 is evaluated at the drifted u (velocity-Verlet)
+        # or at u_k (Euler / Euler-Cromer update u after the force)
+        u_force = nxt.u if integrator == IntegratorKind.velocity_verlet else cur.u
+        ndiff, err = compare_pass(bundle.particles.coords, nxt, fast, u_force, s_c, N,
+                                  cur.bond_history if hist else None)
+        if hist:
+            live = (nxt.connectivity.entries >= 0) & (fast.connectivity.entries >= 0)
+            herr = np.max(np.abs(nxt.bond_history[live] - fast.bond_history[live]), initial=0.0)
+            assert herr <= HIST_TOL * s_c, (k, herr)
+        total_diff += ndiff
+        worst = max(worst, err)
+        broken_total = int(fam.n_neigh.sum() - nxt.connectivity.n_neigh.sum())
+        cur = nxt
+    ex.close()
+    assert layout in kernel, kernel
+    assert broken_total > 0  # the trajectory fractures
+    return total_diff, worst, broken_total
+
+
+@pytest.mark.parametrize("layout", ["lattice_step", "fast_step"])
+def test_resynced_fracture_lattice(monkeypatch, layout):
+    """SURVEY 8(d)'s fracturing lattice (PMB s_c = 1.5e-5, 48^3, the
+    large-model brick shape; forced tiles as the second case): 20
+    velocity-Verlet steps, every step from the exact state."""
+    b, h, g = S.bench_lattice_bundle((48, 48, 48), s_c=1.5e-5)
+    fam = geometry.build_family(b.particles.coords, h, g)
+    st0 = make_state(fam, False)
+    st0.u = S.seed_displacements(b.particles.coords) * 3.0
+    env = {"PD_LAT_CFG": "1"} if layout == "lattice_step" else {"PD_FAST_LAYOUT": "general"}
+    nd, err, broken = _resynced(b, fam, st0, IntegratorKind.velocity_verlet, 20, env,
+                                monkeypatch, layout)
+    print(f"{layout}: {broken} broken over 20 steps, {nd} slot differences within eps, "
+          f"worst force error {err:.2e}")
+
+
+@pytest.mark.parametrize("layout", ["lattice_nlu", "fast_step"])
+@pytest.mark.parametrize("integrator", [IntegratorKind.euler_cromer,
+                                        IntegratorKind.velocity_verlet])
+def test_resynced_fracture_plate(oracle, monkeypatch, layout, integrator):
+    """cfg2 (downscaled notched bilinear plate with BCs and no-failure edges,
+    history): 40 steps of a propagating crack, every step from the exact state."""
+    b, h, g, notch = S.notched_plate_bundle(32, 32, 4, 40, pull=1.5)
+    fam = oracle.build_family(b.particles.coords, h, g.hint())
+    oracle.break_notch(fam, b.particles.coords, notch["axis"], notch["position"],
+                       notch["sweep_axis"], notch["depth"])
+    st0 = make_state(fam, True)
+    env = {} if layout == "lattice_nlu" else {"PD_FAST_LAYOUT": "general"}
+    nd, err, broken = _resynced(b, fam, st0, integrator, 40, env, monkeypatch, layout)
+    print(f"{layout}: {broken} broken over 40 steps, {nd} slot differences within eps, "
+          f"worst force error {err:.2e}")
+
+
+def test_hardening_softening_trilinear_takes_segment_kernel(oracle, monkeypatch):
+    """A trilinear law whose second kink is concave after a convex first one
+    (kink_beta > s1/s0 hardens, then softens -- DamageLaw::validate accepts
+    it) is not a min/max composition of its segment lines; the lattice path
+    must run the segment-selecting loop kernel and match the oracle."""
+    b, h, g = S.bench_lattice_bundle((20, 16, 12))
+    law = DamageLaw.trilinear(1.0, 1e-5, 2e-5, 4e-5, 3.0)
+    b.model.laws = [law]
+    fam = geometry.build_family(b.particles.coords, h, g)
+    st0 = make_state(fam, True)
+    st0.u = S.seed_displacements(b.particles.coords) * 3.0
+    fast, kernel = step_once(b, st0, KernelVariant.fast, IntegratorKind.velocity_verlet)
+    assert kernel.startswith("lattice_nl_kernel<"), kernel
+    ref, _ = step_once(b, st0, KernelVariant.bond_parallel, IntegratorKind.velocity_verlet)
+    compare_pass(b.particles.coords, ref, fast, ref.u, 4e-5, int(fam.group_size),
+                 st0.bond_history)
+    # the unrolled kernel still serves the well-shaped laws
+    b.model.laws = [DamageLaw.trilinear(1.0, 1e-5, 2e-5, 4e-5, 0.25)]
+    _, kernel = step_once(b, st0, KernelVariant.fast, IntegratorKind.velocity_verlet)
+    assert kernel.startswith("lattice_nlu_kernel<"), kernel
+
+
+@pytest.mark.parametrize("layout", [None, "general"])
+@pytest.mark.parametrize("law", ["pmb", "trilinear"])
+def test_collapsed_bond_kept_with_zero_force(monkeypatch, layout, law):
+    """|xi + eta| = 0: the reference's stretch is -1 (no break, no history)
+    and the contribution 0 (engine.cpp:61-65, 100-101).  The fast kernels
+    must keep the bond and stay finite."""
+    if layout:
+        monkeypatch.setenv("PD_FAST_LAYOUT", layout)
+    b, h, g = S.bench_lattice_bundle((18, 12, 10), s_c=1e-3)
+    if law == "trilinear":
+        b.model.laws = [DamageLaw.trilinear(1.0, 2e-4, 5e-4, 1e-3)]
+    fam = geometry.build_family(b.particles.coords, h, g)
+    st0 = make_state(fam, b.model.needs_history())
+    x = b.particles.coords.reshape(-1, 3)
+    i = 5 + 18 * (6 + 12 * 5)  # an interior node; its +x neighbour moves onto it
+    j = i + 1
+    assert np.allclose(x[j] - x[i], [1, 0, 0])
+    st0.u[3 * j] = -1.0
+    out = {}
+    for variant in (KernelVariant.bond_parallel, KernelVariant.fast):
+        st, _ = step_once(b, st0, variant, IntegratorKind.velocity_verlet)
+        out[variant] = st
+    ref, fast = out[KernelVariant.bond_parallel], out[KernelVariant.fast]
+    assert np.all(np.isfinite(fast.a)) and np.all(np.isfinite(fast.u))
+    N = int(fam.group_size)
+    row_i = fam.entries[i * N:(i + 1) * N]
+    k = int(np.flatnonzero(row_i == j)[0])
+    assert ref.connectivity.entries[i * N + k] == j  # the reference keeps it
+    assert fast.connectivity.entries[i * N + k] == j
+    assert np.array_equal(ref.connectivity.entries, fast.connectivity.entries)
+    assert max_rel_difference(ref.a, fast.a) <= FORCE_TOL

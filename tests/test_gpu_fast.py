@@ -193,13 +193,22 @@ def test_fast_million_node_lattice(oracle):
     assert max_rel_difference(outs[1].a, outs[0].a) <= FORCE_TOL
 
 
-@pytest.mark.parametrize("lat_cfg", ["0", "4", "5", "6"])
+LAT_KERNELS = {  # PD_LAT_CFG -> the instantiation it selects on a 20x18x26 lattice
+    "0": "lattice_step_kernel<1,1,1,0,0>",  # by size: below two 16x4x4 bricks per SM
+    "1": "lattice_step_kernel<1,8,3,0,0>",  # the BENCH instantiation (16x4x8, 3 CTAs/SM)
+    "4": "lattice_step_kernel<1,4,5,0,0>",  # 16x4x4 bricks at 5 CTAs/SM
+    "5": "lattice_step_kernel<1,1,1,0,0>",  # the small-brick latency variant, forced
+    "6": "lattice_step_kernel<1,4,6,0,0>",  # large-model rule without the waste test
+}
+
+
+@pytest.mark.parametrize("lat_cfg", sorted(LAT_KERNELS))
 def test_lattice_layout_selected_and_matches_tiles(oracle, monkeypatch, lat_cfg):
     """PD_FAST on the bench lattice runs the implicit-connectivity kernel
-    (pd_lattice.cu) -- chosen by size (0), 16x4x4 bricks at 5 CTAs/SM (4), the
-    small-brick latency variant (5) or the large-model choice (6: 16x4x8 bricks
-    without BC code); forced onto the general tile layout the same run must
-    agree with it within the fast-path tolerance, and both with the oracle."""
+    (pd_lattice.cu) on the brick shape PD_LAT_CFG selects (LAT_KERNELS, checked
+    through pd_ctx_kernel); forced onto the general tile layout the same run
+    must agree with it within the fast-path tolerance, and both with the
+    oracle."""
     monkeypatch.setenv("PD_LAT_CFG", lat_cfg)
     b, h, g = S.bench_lattice_bundle((20, 18, 26), s_c=1.5e-5)
     fam = geometry.build_family(b.particles.coords, h, g)
@@ -215,6 +224,8 @@ def test_lattice_layout_selected_and_matches_tiles(oracle, monkeypatch, lat_cfg)
         ctx.upload(b, st, KernelVariant.fast)
         layouts.append(ctx.layout())
         ctx.run(20, 0, IntegratorKind.velocity_verlet, 0, KernelVariant.fast)
+        if not forced:
+            assert ctx.kernel() == LAT_KERNELS[lat_cfg], ctx.kernel()
         ctx.download(st)
         ctx.close()
         states.append(st)
@@ -300,7 +311,8 @@ def test_lattice_nl_kernel_matches_tiles_and_oracle(oracle, monkeypatch):
 def test_lattice_no_failure_and_volumes_match_oracle(oracle, integrator, monkeypatch, lat_cfg):
     """cfg1-style run on the lattice layout: the 3-point-bend beam (no-failure
     supports and load patch, PMB, quintic ramp) with per-node volumes, against
-    the fp64 oracle, on the small-brick (5) and 16x4x4-brick (6) kernels."""
+    the fp64 oracle, on the small-brick (5) and 16x4x4-brick (6) kernels
+    (with no-failure nodes and BCs: 16x4x4 bricks at 5 CTAs/SM)."""
     monkeypatch.setenv("PD_LAT_CFG", lat_cfg)
     b, h, g = S.beam_bundle(30, 10, 10)
     rng = np.random.default_rng(11)

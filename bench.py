@@ -185,7 +185,7 @@ def ncu_probe(args, kernel: str):
         cmd = [ncu, "--metrics", NCU_METRICS, "--clock-control", "none", "-k", f"regex:^{base}$",
                "-s", "2", "-c", "1", "--csv", "--page", "raw", "--log-file", log,
                sys.executable, os.path.abspath(__file__), "--probe-run", "--size", str(args.size),
-               "--law", args.law, "--variant", args.variant]
+               "--law", args.law, "--variant", args.variant, "--mesh", args.mesh]
         try:
             r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
         except (OSError, subprocess.TimeoutExpired) as exc:
@@ -249,7 +249,19 @@ LAWS = {
 S_C = {"pmb": 1e6, "fracture": 1e-5, "trilinear": 1e6, "multi": 1e6}
 
 
-def build_workload(counts, law="pmb"):
+MESHES = {
+    "lattice": "cubic lattice (the reference bench fixture)",
+    "jitter": "irregular mesh: the same lattice with every coordinate jittered by a seeded "
+              "uniform +-0.2 spacing (rows of 90-150 neighbours; the general tile kernel)",
+}
+
+
+def jitter_coords(coords, amp=0.2, seed=2105):
+    rng = np.random.default_rng(seed)
+    return coords + rng.uniform(-amp, amp, coords.shape)
+
+
+def build_workload(counts, law="pmb", mesh="lattice"):
     """The reference bench fixture (bench.cpp:76-104); law "fracture" is SURVEY
     8(d)'s fracturing variant (PMB s_c = 1e-5), "trilinear" its history variant
     trilinear(1, 1e-3, 2e-3, 1e6) (n-linear path, nothing breaks); "multi" is
@@ -259,6 +271,9 @@ def build_workload(counts, law="pmb"):
     from paper_2105_04150_b200 import geometry, make_state
     from paper_2105_04150_b200.types import DamageLaw
     bundle, h, g = S.bench_lattice_bundle(counts, s_c=S_C[law])
+    if mesh == "jitter":
+        bundle.particles.coords = jitter_coords(bundle.particles.coords)
+        g = None
     if law == "trilinear":
         bundle.model.laws = [DamageLaw.trilinear(1.0, 1e-3, 2e-3, 1e6)]
     elif law == "multi":
@@ -370,11 +385,12 @@ def run_reference_arm(args):
 def _summary(args, value, ms_step, world, n, N, live, bytes_step, achieved, e2e, launches,
              clocks, cpu, variant_name, probe=None, extra_config=None):
     peak, peak_kind = measured_peaks()
-    cfg = {"workload": f"cfg4 lattice {args.size}^3 = {n} nodes, delta=3dx (N={N}), "
+    mesh = "lattice" if args.mesh == "lattice" else "jittered lattice (irregular mesh)"
+    cfg = {"workload": f"cfg4 {mesh} {args.size}^3 = {n} nodes, delta=3dx (N={N}), "
                        f"{LAWS[args.law]}, velocity-Verlet, dt=1e-3, seeded u"
                        + (f", {world} z-slabs" if world > 1 else ""),
            "nodes": n, "group_size": N, "live_bonds": live, "variant": variant_name,
-           "law": args.law,
+           "law": args.law, "mesh": args.mesh,
            "l2": f"inputs larger than L2 ({bytes_step / 1e9:.2f} GB/step algorithmic)",
            "parallelism": f"z-slab x{world}" if world > 1 else "single GPU"}
     cfg.update(extra_config or {})
@@ -415,7 +431,7 @@ def _summary(args, value, ms_step, world, n, N, live, bytes_step, achieved, e2e,
 def probe_run(args, variant):
     """--probe-run: the workload's upload and a few steps (ncu_probe's child)."""
     from paper_2105_04150_b200 import IntegratorKind, engine
-    bundle, fam, state0 = build_workload((args.size,) * 3, args.law)
+    bundle, fam, state0 = build_workload((args.size,) * 3, args.law, args.mesh)
     ctx = engine.Context(0)
     ctx.upload(bundle, state0, variant)
     ctx.run(4, 0, IntegratorKind.velocity_verlet, 0, variant)
@@ -428,7 +444,7 @@ def run_single(args, variant, local):
     from paper_2105_04150_b200 import IntegratorKind, SimulateOptions, engine, make_state
     counts = (args.size, args.size, args.size)
     t_setup = time.perf_counter()
-    bundle, fam, state0 = build_workload(counts, args.law)
+    bundle, fam, state0 = build_workload(counts, args.law, args.mesh)
     n = bundle.particles.size()
     N = int(fam.group_size)
     setup_s = time.perf_counter() - t_setup
@@ -515,7 +531,8 @@ def run_single(args, variant, local):
                   "(upload + layout + run + download inside the timed region)"}
     del st, fam, state0, bundle
     probe = None if args.no_probe else ncu_probe(args, kernel)
-    cpu = None if args.no_cpu else cpu_baseline(counts, args.law)
+    # the reference fixture is the lattice: no CPU line for the jittered mesh
+    cpu = None if args.no_cpu or args.mesh != "lattice" else cpu_baseline(counts, args.law)
     extra = {"setup_s": round(setup_s, 2), "layout": layout, "kernel": kernel,
              "live_bonds_timed": [live0, live1]}
     if sustain:
@@ -648,6 +665,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=1000)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--law", default="pmb", choices=sorted(LAWS))
+    ap.add_argument("--mesh", default="lattice", choices=sorted(MESHES))
     ap.add_argument("--no-probe", action="store_true", help="skip the ncu DRAM-traffic probe")
     ap.add_argument("--sustain-steps", type=int, default=200,
                     help="extra untimed-for-value steps under the clock sampler")

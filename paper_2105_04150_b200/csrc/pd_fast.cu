@@ -56,8 +56,16 @@ __device__ __forceinline__ float rcp_approx(float x) {
     return y;
 }
 
+// max over three that propagates NaN (one FMNMX3): a NaN stretch (overflow,
+// collapsed bond, non-finite state) must reach the break re-check
+__device__ __forceinline__ float max3_nan(float a, float b, float c) {
+    float r;
+    asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
 
-// Shared-memory records (F.cap reserved per array; position 0 is a dummy that
+
+// Shared-memory records (F.cap reserved per array; record 0 is a dummy that
 // dead/padding slots point at -- 1e18 away with zero volume, so its
 // contribution is 0 (or ~1e-18 relative with a uniform volume) and its stretch
 // never reaches s_c; the slot loop needs no branch):
@@ -65,8 +73,8 @@ __device__ __forceinline__ float rcp_approx(float x) {
 //   sB[p] = {z, uz} - (O_t, U_t)         LDS.64
 //   sV[p] = c * V_j (PMB) or V_j         LDS.32, only when volumes differ
 // = 24 B per bond with uniform volumes, 28 B otherwise.  A slot stores the
-// byte offset 8*p of its neighbour's sB record (sA is at 16*p); no-failure
-// neighbours are staged last, so "offset >= nf_start" flags them.
+// record index p; no-failure neighbours are staged last, so "p >= nf_start"
+// flags them.
 //
 // KIND 0: single PMB law, uniform volume, no no-failure node (c*V constant,
 //         applied once per node after the slot loop)
@@ -75,6 +83,12 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // TT:     threads (= owned nodes) per tile; MINB: CTAs per SM the register
 //         budget is sized for; PRE: load the node's integrator inputs before
 //         the slot loop so their latency hides behind the bond work.
+//
+// KIND 0/1 have no per-slot break test: every slot adds its force and raises a
+// running NaN-propagating max of its stretch (no-failure neighbours excluded);
+// a node whose max reaches s_c (or whose force is NaN: a collapsed bond) walks
+// its row again with the per-slot test, clears the broken slots and sums the
+// bonds that stay (the reference's order of effects, engine.cpp:90-101).
 template <int MODE, int KIND, int TT, int MINB, bool PRE, int R>
 __global__ void __launch_bounds__(TT, MINB) fast_step_kernel(DevArgs A, FastDev F) {
     if (MODE != 0 && *(volatile long long*)A.err_step != kNoError)
@@ -84,9 +98,6 @@ __global__ void __launch_bounds__(TT, MINB) fast_step_kernel(DevArgs A, FastDev 
     float4* sA = smem;
     float2* sB = reinterpret_cast<float2*>(smem + cap);
     float* sV = reinterpret_cast<float*>(sB + cap);
-    const char* cA = reinterpret_cast<const char*>(sA);
-    const char* cB = reinterpret_cast<const char*>(sB);
-    const char* cV = reinterpret_cast<const char*>(sV);
     const int tile = F.tile0 + int(blockIdx.x);
     const int ts = F.tile_start[tile];
     const int te = F.tile_start[tile + 1];
@@ -99,11 +110,8 @@ __global__ void __launch_bounds__(TT, MINB) fast_step_kernel(DevArgs A, FastDev 
     const long long i = ts + t;
     const bool active = i < te;
     unsigned short* lrow = F.lidx + F.slot_off[tile] + (long long)t * 8;
-    const int nkb = active ? (F.kmax8[tile] >> 3) : 0;
+    const int nkb = active ? F.wgroups[(long long)tile * (TT / 32) + t / 32] : 0;
     const long long kstride = (long long)TT * 8;
-    uint4 wnext = nkb > 0 ? __ldcs(reinterpret_cast<const uint4*>(lrow)) : make_uint4(0, 0, 0, 0);
-    uint4 wnext2 =
-        nkb > 1 ? __ldcs(reinterpret_cast<const uint4*>(lrow + kstride)) : make_uint4(0, 0, 0, 0);
     const unsigned own_raw = active ? unsigned(F.own_slot[i]) : 0u;
     const unsigned nf_start = KIND == 0 ? 0u : unsigned(F.nf_start[tile]);
 
@@ -117,13 +125,18 @@ __global__ void __launch_bounds__(TT, MINB) fast_step_kernel(DevArgs A, FastDev 
         if (KIND != 0)
             sV[0] = 0.f;
     }
+    // the halo ids of the next pass load while this pass's records are in flight
+    int idn[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int hh = threadIdx.x + r * TT;
+        idn[r] = hh < H ? F.halo[h0 + hh] : -1;
+    }
     for (int h = threadIdx.x; h < H; h += R * TT) {
         int id[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const int hh = h + r * TT;
-            id[r] = hh < H ? F.halo[h0 + hh] : -1;
-        }
+        for (int r = 0; r < R; ++r)
+            id[r] = idn[r];
         double4 x[R], u[R];
 #pragma unroll
         for (int r = 0; r < R; ++r)
@@ -131,6 +144,11 @@ __global__ void __launch_bounds__(TT, MINB) fast_step_kernel(DevArgs A, FastDev 
                 x[r] = A.xv[id[r]];
                 u[r] = A.u_in[id[r]];
             }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int hh = h + (R + r) * TT;
+            idn[r] = hh < H ? F.halo[h0 + hh] : -1;
+        }
 #pragma unroll
         for (int r = 0; r < R; ++r)
             if (id[r] >= 0) {
@@ -147,6 +165,9 @@ __global__ void __launch_bounds__(TT, MINB) fast_step_kernel(DevArgs A, FastDev 
     __syncthreads();
     if (!active)
         return;
+    uint4 wnext = nkb > 0 ? __ldcs(reinterpret_cast<const uint4*>(lrow)) : make_uint4(0, 0, 0, 0);
+    uint4 wnext2 =
+        nkb > 1 ? __ldcs(reinterpret_cast<const uint4*>(lrow + kstride)) : make_uint4(0, 0, 0, 0);
 
     // 2. the node's bonds
     const unsigned own = own_raw & 0x1FFFu;
@@ -161,107 +182,106 @@ __global__ void __launch_bounds__(TT, MINB) fast_step_kernel(DevArgs A, FastDev 
     float2 fxy = make_float2(0.f, 0.f);
     float fz = 0.f;
     int broke = 0;
-    // one group of 8 slots (one 16-byte index load)
     // one slot's geometry: xi + eta (cxy, cz), |xi + eta|^2, 1 / |xi + eta| and
     // s = (|cur| - |xi|) / |xi| = eta.(xi + cur) / (|xi| (|cur| + |xi|))
-    auto geom = [&](unsigned offB, float2& cxy, float& cz, float& cur2, float& rc) -> float {
-        const float4 ar = *reinterpret_cast<const float4*>(cA + 2 * offB);
-        const float2 br = *reinterpret_cast<const float2*>(cB + offB);
+    auto geom = [&](unsigned p, float2& cxy, float& cz, float& cur2, float& rc) -> float {
+        const float4 ar = sA[p];
+        const float2 br = sB[p];
         const float2 exy = __fadd2_rn(make_float2(ar.x, ar.y), nxi);
         const float2 hxy = __fadd2_rn(make_float2(ar.z, ar.w), nui);
         const float2 ezh = __fadd2_rn(br, nzi);  // (xi_z, eta_z)
         cxy = __fadd2_rn(exy, hxy);
         const float2 sxy = __fadd2_rn(exy, cxy);
         const float ez = ezh.x, hz = ezh.y;
-        cz = ez + hz;
+        cz = __fadd_rn(ez, hz);
         const float2 e2 = __fmul2_rn(exy, exy);
         const float2 n2 = __fmul2_rn(hxy, sxy);
-        const float ref2 = fmaf(ez, ez, e2.x + e2.y);
-        const float num = fmaf(hz, ez + cz, n2.x + n2.y);  // eta.(2 xi + eta)
-        cur2 = ref2 + num;                                  // |xi + eta|^2
+        const float ref2 = fmaf(ez, ez, __fadd_rn(e2.x, e2.y));
+        const float num = fmaf(hz, __fadd_rn(ez, cz), __fadd_rn(n2.x, n2.y));  // eta.(2 xi + eta)
+        cur2 = __fadd_rn(ref2, num);                                           // |xi + eta|^2
         const float rr = rsqrt_approx(ref2);
         rc = rsqrt_approx(cur2);
-        return num * rr * rcp_approx(cur2 * rc + ref2 * rr);
+        return __fmul_rn(__fmul_rn(num, rr), rcp_approx(fmaf(cur2, rc, __fmul_rn(ref2, rr))));
     };
     // A collapsed bond (|xi + eta|^2 = 0 or below fp32's normal range, which
     // the approximate rsqrt flushes: rc = +inf, s = NaN) keeps its bond and
     // adds nothing -- the reference's stretch is -1 < s_c there and its
     // contribution 0 (engine.cpp:61-65, 100-101).  In KIND 0/1 its NaN stretch
-    // takes the rare break branch, which re-checks it; a NaN force (a
-    // collapsed bond to a no-failure neighbour) is recomputed after the row.
+    // sends the node to the re-check, which skips it.
     constexpr float kMinNormal = 1.17549435e-38f;
+    const float kNegInf = __int_as_float(0xff800000);
+    float smax = kNegInf;
+    // KIND 0/1: one group of 8 slots (one 16-byte index load), no break test
+    auto fslot = [&](unsigned p) -> float {
+        float2 cxy;
+        float cz, cur2, rc;
+        const float s = geom(p, cxy, cz, cur2, rc);
+        float scale;
+        if (KIND == 0) {
+            scale = __fmul_rn(s, rc);  // c*V is applied once per node after the loop
+        } else {
+            scale = __fmul_rn(__fmul_rn(s, sV[p]), rc);
+        }
+        fxy = __ffma2_rn(cxy, make_float2(scale, scale), fxy);
+        fz = fmaf(cz, scale, fz);
+        if (KIND == 0)
+            return s;
+        return p >= nf_start ? kNegInf : s;  // a no-failure neighbour never breaks
+    };
+    auto fgroup = [&](const uint4 w) {
+        const unsigned words[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float s0 = fslot(words[q] & 0xFFFFu);
+            const float s1 = fslot(words[q] >> 16);
+            smax = max3_nan(smax, s0, s1);
+        }
+    };
+    // KIND 2: per-slot laws, history, corrections
     auto group = [&](const uint4 w, unsigned short* lrow) {
         const unsigned words[4] = {w.x, w.y, w.z, w.w};
-        unsigned bmask = 0;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            const unsigned offB = (q & 1) ? (words[q >> 1] >> 16) : (words[q >> 1] & 0xFFFFu);
+            const unsigned p = (q & 1) ? (words[q >> 1] >> 16) : (words[q >> 1] & 0xFFFFu);
             float2 cxy;
             float cz, cur2, rc;
-            const float s = geom(offB, cxy, cz, cur2, rc);
-            float scale;
-            if (KIND != 2) {
-                // !(s < s_c): an fp32 stretch that overflowed is NaN and breaks, as the
-                // reference's +inf stretch does (engine.cpp:90-98)
-                const bool brk = KIND == 0 ? !(s < sc_pmb) : (!(s < sc_pmb) && offB < nf_start);
-                if (brk) {
-                    bmask |= 1u << q;  // stored after the 8 slots, off the hot path
-                    continue;
-                }
-                // KIND 0: c*V is applied once per node after the loop
-                scale = KIND == 0 ? s * rc
-                                  : s * *reinterpret_cast<const float*>(cV + (offB >> 1)) * rc;
-            } else {
-                if (offB == 0 || cur2 < kMinNormal)
-                    continue;  // broken/padding (its history must not re-trigger the break), collapsed
-                const bool no_fail = nfi || offB >= nf_start;
-                const long long sidx = (lrow - F.lidx) + q;
-                const FastLaw& law = c_flaws[F.btype ? int(F.btype[sidx]) : 0];
-                float f;
-                if (no_fail) {
-                    f = law.c * s;
-                } else if (law.nbp == 1) {
-                    if (!(s < law.bp[0])) {
-                        lrow[q] = 0;
-                        ++broke;
-                        continue;
-                    }
-                    f = law.c * s;
-                } else {
-                    const float s_c = law.bp[law.nbp - 1];
-                    const float hh = F.hist[sidx];
-                    if (s > hh)
-                        F.hist[sidx] = s;
-                    if (hh >= s_c || !(s < s_c)) {
-                        lrow[q] = 0;
-                        ++broke;
-                        continue;
-                    }
-                    f = (s >= hh) ? fast_envelope(law, s)
-                                  : (hh < law.bp[0] ? law.sl[0] : fast_envelope(law, hh) * rcp_approx(hh)) * s;
-                }
-                if (F.lambda)
-                    f *= F.lambda[sidx];
-                if (F.beta)
-                    f *= F.beta[sidx];
-                f *= *reinterpret_cast<const float*>(cV + (offB >> 1));
-                scale = f * rc;
-            }
-            fxy = __ffma2_rn(cxy, make_float2(scale, scale), fxy);
-            fz = fmaf(cz, scale, fz);
-        }
-        if (KIND != 2 && bmask) {
-            for (int q = 0; q < 8; ++q)
-                if (bmask >> q & 1u) {
-                    const unsigned offB = (q & 1) ? (words[q >> 1] >> 16) : (words[q >> 1] & 0xFFFFu);
-                    float2 cxy;
-                    float cz, cur2, rc;
-                    geom(offB, cxy, cz, cur2, rc);
-                    if (cur2 < kMinNormal)
-                        continue;  // collapsed: kept, adds nothing
+            const float s = geom(p, cxy, cz, cur2, rc);
+            if (p == 0 || cur2 < kMinNormal)
+                continue;  // broken/padding (its history must not re-trigger the break), collapsed
+            const bool no_fail = nfi || p >= nf_start;
+            const long long sidx = (lrow - F.lidx) + q;
+            const FastLaw& law = c_flaws[F.btype ? int(F.btype[sidx]) : 0];
+            float f;
+            if (no_fail) {
+                f = law.c * s;
+            } else if (law.nbp == 1) {
+                if (!(s < law.bp[0])) {
                     lrow[q] = 0;
                     ++broke;
+                    continue;
                 }
+                f = law.c * s;
+            } else {
+                const float s_c = law.bp[law.nbp - 1];
+                const float hh = F.hist[sidx];
+                if (s > hh)
+                    F.hist[sidx] = s;
+                if (hh >= s_c || !(s < s_c)) {
+                    lrow[q] = 0;
+                    ++broke;
+                    continue;
+                }
+                f = (s >= hh) ? fast_envelope(law, s)
+                              : (hh < law.bp[0] ? law.sl[0] : fast_envelope(law, hh) * rcp_approx(hh)) * s;
+            }
+            if (F.lambda)
+                f *= F.lambda[sidx];
+            if (F.beta)
+                f *= F.beta[sidx];
+            f *= sV[p];
+            const float scale = f * rc;
+            fxy = __ffma2_rn(cxy, make_float2(scale, scale), fxy);
+            fz = fmaf(cz, scale, fz);
         }
     };
     int kb = 0;
@@ -270,30 +290,49 @@ __global__ void __launch_bounds__(TT, MINB) fast_step_kernel(DevArgs A, FastDev 
         wnext = wnext2;
         if (kb + 2 < nkb)
             wnext2 = __ldcs(reinterpret_cast<const uint4*>(lrow + 2 * kstride));
-        group(w, lrow);
+        if (KIND == 2)
+            group(w, lrow);
+        else
+            fgroup(w);
     }
     // PRE: the integrator inputs load while the last group computes
     if (PRE && MODE != 0) {
         pre = load_node_in(A, i);
         ui_pre = A.u_in[i];
     }
-    if (kb < nkb)
-        group(wnext, lrow);
-    if (KIND == 1 && isnan(fxy.x + fxy.y + fz)) {
-        // rare: walk the row again (breaks are applied: offset 0 adds 0),
-        // skipping collapsed bonds; a genuinely non-finite state stays NaN
+    if (kb < nkb) {
+        if (KIND == 2)
+            group(wnext, lrow);
+        else
+            fgroup(wnext);
+    }
+    if (KIND != 2 && (!(smax < sc_pmb) || isnan(fxy.x + fxy.y + fz))) {
+        // rare: a bond reached s_c (or a stretch / the force is NaN) -- walk
+        // the row again with the per-slot test: clear the broken slots (the
+        // reference writes -1, engine.cpp:93-96), skip collapsed bonds, sum
+        // the bonds that stay; a genuinely non-finite state stays NaN
         fxy = make_float2(0.f, 0.f);
         fz = 0.f;
-        const unsigned short* r = F.lidx + F.slot_off[tile] + (long long)t * 8;
+        unsigned short* r = F.lidx + F.slot_off[tile] + (long long)t * 8;
         for (int g = 0; g < nkb; ++g, r += kstride)
             for (int q = 0; q < 8; ++q) {
-                const unsigned offB = r[q];
+                const unsigned p = r[q];
+                if (p == 0)
+                    continue;
                 float2 cxy;
                 float cz, cur2, rc;
-                const float s = geom(offB, cxy, cz, cur2, rc);
+                const float s = geom(p, cxy, cz, cur2, rc);
                 if (cur2 < kMinNormal)
+                    continue;  // collapsed: kept, adds nothing
+                // !(s < s_c): an fp32 stretch that overflowed is NaN and breaks,
+                // as the reference's +inf stretch does (engine.cpp:90-98)
+                if (!(s < sc_pmb) && (KIND == 0 || p < nf_start)) {
+                    r[q] = 0;
+                    ++broke;
                     continue;
-                const float scale = s * *reinterpret_cast<const float*>(cV + (offB >> 1)) * rc;
+                }
+                const float scale = KIND == 0 ? __fmul_rn(s, rc)
+                                              : __fmul_rn(__fmul_rn(s, sV[p]), rc);
                 fxy = __ffma2_rn(cxy, make_float2(scale, scale), fxy);
                 fz = fmaf(cz, scale, fz);
             }
@@ -359,7 +398,7 @@ cudaError_t launch_cfg(const DevArgs& A, const FastDev& F, int tiles, cudaStream
 // 2 = 256 x 3 with prefetched node inputs; 3 = 512 x 2 with prefetch
 template <int MODE, int KIND>
 cudaError_t launch_one(const DevArgs& A, const FastDev& F, int tiles, cudaStream_t st) {
-    if (MODE == 1 && KIND == 0) {
+    if constexpr (MODE == 1 && KIND == 0) {
         switch (F.cfg) {
         case 1: return launch_cfg<MODE, KIND, 256, 4, false>(A, F, tiles, st);
         case 2: return launch_cfg<MODE, KIND, 256, 3, true>(A, F, tiles, st);
@@ -452,7 +491,7 @@ template <int MODE, int KIND, int TT, int MINB, bool PRE, int R = 2> static void
 template <int MODE, int KIND> static void preload_mk() {
     preload_one<MODE, KIND, 256, 4, false>();
     preload_one<MODE, KIND, 512, 2, false>();
-    if (MODE == 1 && KIND == 0) {
+    if constexpr (MODE == 1 && KIND == 0) {
         preload_one<MODE, KIND, 256, 3, true>();
         preload_one<MODE, KIND, 512, 2, true>();
         preload_one<MODE, KIND, 512, 2, false, 3>();

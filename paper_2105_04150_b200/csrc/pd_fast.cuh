@@ -7,11 +7,14 @@
 //                                       reference (owned nodes included), staged
 //                                       into shared memory once per step as
 //                                       fp32 {x - O_t, V} and {u - U_t, no_fail}
-//   lidx   uint16 per live slot          bits 0-14: shared-memory index of the
-//                                       neighbour (halo position + 1); 0 = broken
-//                                       or padding (a dummy record that adds 0);
-//                                       bit 15: the neighbour is a no-fail node.  Slot c of
-//                                       tile-thread t lives at
+//   lidx   uint16 per live slot          index p of the neighbour's shared-memory
+//                                       record (halo position + 1; the records
+//                                       are sA[p] float4, sB[p] float2, sV[p]);
+//                                       0 = broken or padding (record 0 is a
+//                                       dummy that adds 0).  No-failure
+//                                       neighbours are staged last in the halo,
+//                                       so p >= nf_start[tile] flags them.  Slot
+//                                       c of tile-thread t lives at
 //                                       slot_off[t] + (c/8)*T*8 + t*8 + c%8, so
 //                                       one 16-byte load fetches 8 slots and a
 //                                       warp's loads are contiguous.
@@ -37,9 +40,10 @@ struct FastDev {
     const int* halo;           // internal ids
     const long long* slot_off; // n_tiles
     const int* kmax8;          // per tile, multiple of 8
+    const int* wgroups;        // per (tile, warp): 8-slot groups of the warp's longest row
     const unsigned short* own_slot; // shared-memory position of each (internal) node in its tile,
                                     // bit 15 = the node is a no-failure node
-    const int* nf_start;       // per tile: first slot offset that names a no-failure node
+    const int* nf_start;       // per tile: first record index that is a no-failure node
     unsigned short* lidx;
     float* hist;               // compact fp32 history (n-linear laws)
     const uint8_t* btype;      // compact bond types or NULL

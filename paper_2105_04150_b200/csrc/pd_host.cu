@@ -228,7 +228,7 @@ struct pd_ctx {
     int cur = 0;
 
     DevBuf<double4> xv, u[2];
-    DevBuf<double> v, a, rho, inv_rho, hist, lambda, beta, body, ext;
+    DevBuf<double> v, a, rho, inv_rho, hist, hist_keep, lambda, beta, body, ext;
     DevBuf<int32_t> entries, n_neigh, initial, scratch_i32;
     DevBuf<uint32_t> alive;
     DevBuf<uint8_t> btype, bc_kind, bc_ramp, nofail;
@@ -306,6 +306,7 @@ struct pd_ctx {
         F.halo = lay.halo.p;
         F.slot_off = lay.slot_off.p;
         F.kmax8 = lay.kmax8.p;
+        F.wgroups = lay.wgroups.p;
         F.own_slot = lay.own_slot.p;
         F.nf_start = lay.nf_start.p;
         F.lidx = lay.lidx.p;
@@ -496,8 +497,16 @@ int upload_common(pd_ctx* ctx, const pd_particles& p, const pd_state& st,
             PD_CK(ctx->hist.alloc(size_t(slots)));
             PD_CK(cudaMemsetAsync(ctx->hist.p, 0, sizeof(double) * slots, s));
         }
+        ctx->hist_keep.release();
     } else {
         ctx->hist.release();
+        // a state that carries bond_history under a model without n-linear
+        // laws: the reference keeps it untouched and save_state still writes
+        // it (io.cpp section 10), so it is kept on the device unchanged
+        if (st.bond_history && st.bond_history_size == slots)
+            PD_CK(ctx->hist_keep.upload(st.bond_history, size_t(slots), s));
+        else
+            ctx->hist_keep.release();
     }
     if (corr.lambda_size != 0)
         PD_CK(ctx->lambda.upload(corr.lambda, size_t(slots), s));
@@ -595,7 +604,8 @@ int download(pd_ctx* ctx, pd_state* st, pd_force_field* forces, int32_t fields) 
         PD_TRY(vec3_out(ctx->v.p, st->v));
     if ((fields & PD_FIELD_A) && st && st->a)
         PD_TRY(vec3_out(ctx->a.p, st->a));
-    const bool want_hist = (fields & PD_FIELD_HISTORY) && st && st->bond_history && ctx->history;
+    const bool want_hist = (fields & PD_FIELD_HISTORY) && st && st->bond_history &&
+                           (ctx->history || ctx->hist_keep.p);
     if (want_hist && st->bond_history_size != slots)
         return fail(PD_E_INVALID_ARGUMENT, "download: bond_history must be sized n x N");
     if ((fields & PD_FIELD_CONNECTIVITY) && st) {
@@ -658,18 +668,19 @@ int download(pd_ctx* ctx, pd_state* st, pd_force_field* forces, int32_t fields) 
         PD_CK(cudaStreamSynchronize(s));
     }
     if (want_hist) {
-        if (ctx->lattice) {
+        if (ctx->history && ctx->lattice) {
             PD_CK(launch_lattice_materialize(ctx->entries.p, ctx->lmask.p, ctx->own_begin,
                                              ctx->own_end, n, ctx->N, ctx->lat, nullptr,
                                              ctx->hist.p, s));
             ++ctx->launches;
-        } else if (ctx->permuted()) {
+        } else if (ctx->history && ctx->permuted()) {
             launch_fast_materialize(ctx->entries.p, ctx->lay.inv.p, ctx->lay.tile_of.p, ctx->lay.tile_start.p,
                                     ctx->lay.slot_off.p, ctx->fast_T, ctx->lay.lidx.p, ctx->lay.hist32.p, n,
                                     ctx->N, nullptr, ctx->hist.p, s);
             ++ctx->launches;
         }
-        PD_CK(d2h_large(st->bond_history, ctx->hist.p, sizeof(double) * slots, s));
+        PD_CK(d2h_large(st->bond_history, ctx->history ? ctx->hist.p : ctx->hist_keep.p,
+                        sizeof(double) * slots, s));
     }
     if ((fields & PD_FIELD_FORCES) && forces) {
         if (forces->body_force)
@@ -983,12 +994,15 @@ void snapshot_worker(pd_ctx* ctx) {
             ctx->snap_jobs.pop_front();
         }
         const int64_t n = ctx->n;
-        h.resize(size_t(10 * n));
+        h.resize(size_t(10 * n + 1));
         std::string err;
         if (cudaStreamWaitEvent(ctx->snap_stream, ctx->snap_ready[job.slot], 0) != cudaSuccess ||
             d2h_large(h.data(), ctx->snap_dev[job.slot].p, sizeof(double) * h.size(),
                       ctx->snap_stream) != cudaSuccess) {
             err = "snapshot download failed";
+        } else if (long long e; std::memcpy(&e, h.data() + 10 * n, sizeof e), e < job.step) {
+            // the run failed at step e before this write step: the reference
+            // throws inside step e's force pass and never writes this file
         } else {
             char path[4096];
             std::snprintf(path, sizeof path, ctx->snap_pattern.c_str(), (long long)job.step);
@@ -1023,8 +1037,12 @@ int snapshot_async(pd_ctx* ctx, int64_t step) {
         slot = ctx->snap_busy[0] ? 1 : 0;
         ctx->snap_busy[slot] = true;
     }
-    PD_CK(ctx->snap_dev[slot].alloc(size_t(10 * ctx->n)));
+    PD_CK(ctx->snap_dev[slot].alloc(size_t(10 * ctx->n + 1)));
     PD_TRY(snapshot_fields(ctx, ctx->snap_dev[slot].p, ctx->stream));
+    // the first failed step rides along, so the writer can drop snapshots
+    // queued past a non-finite error (the later step kernels returned early)
+    PD_CK(cudaMemcpyAsync(ctx->snap_dev[slot].p + 10 * ctx->n, ctx->err.p, sizeof(long long),
+                          cudaMemcpyDeviceToDevice, ctx->stream));
     PD_CK(cudaEventRecord(ctx->snap_ready[slot], ctx->stream));
     {
         std::lock_guard<std::mutex> lk(ctx->snap_mu);
@@ -1407,6 +1425,8 @@ int pd_ctx_save_state(pd_ctx* ctx, const char* path) {
                                     ctx->lay.lidx.p, ctx->lay.hist32.p, n, ctx->N, nullptr,
                                     ctx->hist.p, s);
         PD_TRY(w.section_device(10, ctx->hist.p, 8 * uint64_t(slots), s));
+    } else if (ctx->hist_keep.p) {
+        PD_TRY(w.section_device(10, ctx->hist_keep.p, 8 * uint64_t(slots), s));
     }
     ctx->launches += 8;
     PD_TRY(w.close());

@@ -103,7 +103,7 @@ int set_error(int code, const char* msg);
 struct FastLayoutDev {
     int T = 0, n_tiles = 0, max_halo = 0;
     long long total_slots = 0;
-    DevBuf<int> perm, inv, tile_of, tile_start, kmax8, halo, nf_start;
+    DevBuf<int> perm, inv, tile_of, tile_start, kmax8, wgroups, halo, nf_start;
     DevBuf<unsigned short> own_slot, lidx;
     DevBuf<long long> halo_off, slot_off;
     DevBuf<float> hist32, lambda32, beta32;

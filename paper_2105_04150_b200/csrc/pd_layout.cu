@@ -1,18 +1,23 @@
 // pd_layout.cu -- the fast path's tile layout (pd_fast.cuh), built on the device.
 //
 // Same result as the layout a host would build from the rows: nodes renumbered
-// into spatial bricks, tiles of <= T consecutive internal nodes of one brick,
-// per tile a halo of every node its rows touch (ascending reference order,
-// no-failure nodes last), and per live slot the byte offset of the
-// neighbour's shared-memory record.  All passes are sorts, scans and
+// into spatial bricks (lattices) or along a Morton curve (other meshes), tiles
+// of <= T consecutive internal nodes, per tile a halo of every node its rows
+// touch (no-failure nodes last; ascending reference order on bricks, internal
+// order on Morton tiles), and per live slot the index of the neighbour's
+// shared-memory record.  All passes are sorts, scans and
 // per-node kernels over data already resident for the step, so setting up a
 // 10M-node model costs milliseconds instead of seconds of host work:
 //
 //   1. per axis: sort the coordinates, count distinct values (<= 4096: a
-//      lattice axis, bricks of 16 x 4 x T/64 grid planes; else bins of about
-//      8 mean spacings); brick key per owned node; stable radix sort of the
-//      owned nodes by brick -> perm / inv; run lengths -> tiles (host, one
-//      value per brick);
+//      lattice axis on all three: bricks of 16 x 4 x T/64 grid planes; else
+//      a Morton curve of mean-spacing cells); brick / Morton key per owned
+//      node; stable radix sort of the owned nodes by key -> perm; run lengths
+//      -> balanced tiles of <= T nodes (host, one value per brick; the Morton
+//      curve is one run) -> perm / inv.  A warp's nodes stay spatial
+//      neighbours, so its shared-memory reads of one slot hit nearby records
+//      (ordering a tile's nodes by row length instead scattered them over the
+//      banks: 20 % slower on a jittered lattice);
 //   2. live count per row -> kmax8 per tile -> slot offsets (host scan of one
 //      value per tile);
 //   3. one 64-bit key (tile, no-failure flag, node) per live slot and per
@@ -80,7 +85,19 @@ struct BrickGrid {
     long long kbrick[3];
     double lo[3], len[3];
     long long nb[3];
+    int morton;      // not a lattice on every axis: Morton order of h-cells
+    double inv_h;
 };
+
+__device__ __forceinline__ unsigned long long spread3(unsigned long long v) {  // 21 bits -> 63
+    v &= 0x1fffffull;
+    v = (v | v << 32) & 0x1f00000000ffffull;
+    v = (v | v << 16) & 0x1f0000ff0000ffull;
+    v = (v | v << 8) & 0x100f00f00f00f00full;
+    v = (v | v << 4) & 0x10c30c30c30c30c3ull;
+    v = (v | v << 2) & 0x1249249249249249ull;
+    return v;
+}
 
 __device__ __forceinline__ long long lower_bound_d(const double* a, int n, double v) {
     int lo = 0, hi = n;
@@ -102,6 +119,19 @@ __global__ void brick_key_kernel(const double4* xv, long long begin, long long c
     const long long i = begin + k;
     const double4 x = xv[i];
     const double c3[3] = {x.x, x.y, x.z};
+    if (g.morton) {
+        unsigned long long key = 0;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            const double q = floor((c3[d] - g.lo[d]) * g.inv_h);
+            const unsigned long long c = q < 0 ? 0ull : (q > 2097151.0 ? 2097151ull
+                                                                        : (unsigned long long)q);
+            key |= spread3(c) << d;
+        }
+        keys[k] = key;
+        vals[k] = int(i);
+        return;
+    }
     long long b[3];
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
@@ -152,12 +182,20 @@ __global__ void live_kernel(const int32_t* entries, const int* perm, const int* 
     atomicMax(kmax + tile_of[ii], c);
 }
 
-__device__ __forceinline__ unsigned long long pair_key(int tile, const uint8_t* nofail, int j) {
+// halo key of node j (reference id) in tile `tile`: a tile's halo is sorted by
+// (no-failure flag, order id) so that the records a warp's neighbours read at
+// one slot sit close together, as the warp's own nodes do (few bank
+// conflicts): the reference id on lattice bricks (x-fastest runs), the
+// internal (Morton) id on irregular meshes (inv != NULL)
+__device__ __forceinline__ unsigned long long pair_key(int tile, const uint8_t* nofail,
+                                                       const int* inv, int j) {
     const unsigned long long nf = (nofail && nofail[j]) ? 1ull : 0ull;
-    return ((unsigned long long)tile << 33) | (nf << 32) | (unsigned long long)(unsigned)j;
+    const unsigned o = unsigned(inv ? inv[j] : j);
+    return ((unsigned long long)tile << 33) | (nf << 32) | (unsigned long long)o;
 }
 
-__global__ void pair_keys_kernel(const int32_t* entries, const int* perm, const int* tile_of,
+__global__ void pair_keys_kernel(const int32_t* entries, const int* perm, const int* inv,
+                                 const int* tile_of,
                                  const uint8_t* nofail, const long long* off, long long n_own,
                                  int N, unsigned long long* keys) {
     const long long ii = blockIdx.x * (long long)TPB + threadIdx.x;
@@ -166,11 +204,11 @@ __global__ void pair_keys_kernel(const int32_t* entries, const int* perm, const 
     const long long i = perm[ii];
     const int t = tile_of[ii];
     long long o = off[ii];
-    keys[o++] = pair_key(t, nofail, int(i));
+    keys[o++] = pair_key(t, nofail, inv, int(i));
     for (int k = 0; k < N; ++k) {
         const int32_t j = entries[i * N + k];
         if (j >= 0)
-            keys[o++] = pair_key(t, nofail, j);
+            keys[o++] = pair_key(t, nofail, inv, j);
     }
 }
 
@@ -184,10 +222,12 @@ __global__ void halo_kernel(const unsigned long long* hk, long long H, const int
     const int t = int(key >> 33);
     if (k == 0 || int(hk[k - 1] >> 33) != t)
         halo_off[t] = k;
-    halo[k] = inv[unsigned(key & 0xffffffffull)];
+    const int o = int(unsigned(key & 0xffffffffull));
+    halo[k] = inv ? inv[o] : o;
 }
 
-// nf_start[t] = 8 * (position of the first no-failure key + 1), found per key
+// nf_start[t] = position of the first no-failure key + 1 (its shared-memory
+// record index), found per key
 __global__ void nf_start_kernel(const unsigned long long* hk, long long H, const long long* halo_off,
                                 int* nf_start) {
     const long long k = blockIdx.x * (long long)TPB + threadIdx.x;
@@ -199,7 +239,7 @@ __global__ void nf_start_kernel(const unsigned long long* hk, long long H, const
     const int t = int(key >> 33);
     const bool first = k == halo_off[t] || !((hk[k - 1] >> 32) & 1ull);
     if (first)
-        nf_start[t] = int(8 * (k - halo_off[t] + 1));
+        nf_start[t] = int(k - halo_off[t] + 1);
 }
 
 __device__ __forceinline__ long long lower_bound_u64(const unsigned long long* a, long long lo,
@@ -217,6 +257,7 @@ __device__ __forceinline__ long long lower_bound_u64(const unsigned long long* a
 struct SlotArgs {
     const int32_t* entries;
     const int* perm;
+    const int* inv;
     const int* tile_of;
     const int* tile_start;
     const long long* slot_off;
@@ -231,6 +272,7 @@ struct SlotArgs {
     int N, T;
     unsigned short* lidx;
     unsigned short* own_slot;
+    int* wgroups;
     float* hist32;
     uint8_t* btype_c;
     float* lambda32;
@@ -245,7 +287,7 @@ __global__ void slot_kernel(SlotArgs S) {
     const int t = S.tile_of[ii];
     const long long h0 = S.halo_off[t], h1 = S.halo_off[t + 1];
     const long long base = S.slot_off[t] + (long long)(ii - S.tile_start[t]) * 8;
-    const long long own = lower_bound_u64(S.hk, h0, h1, pair_key(t, S.nofail, int(i))) - h0;
+    const long long own = lower_bound_u64(S.hk, h0, h1, pair_key(t, S.nofail, S.inv, int(i))) - h0;
     const bool nfi = S.nofail && S.nofail[i];
     S.own_slot[ii] = (unsigned short)((own + 1) | (nfi ? 0x8000 : 0));
     int c = 0;
@@ -254,9 +296,9 @@ __global__ void slot_kernel(SlotArgs S) {
         const int32_t j = S.entries[idx];
         if (j < 0)
             continue;
-        const long long pos = lower_bound_u64(S.hk, h0, h1, pair_key(t, S.nofail, j)) - h0;
+        const long long pos = lower_bound_u64(S.hk, h0, h1, pair_key(t, S.nofail, S.inv, j)) - h0;
         const long long s = base + (long long)(c >> 3) * S.T * 8 + (c & 7);
-        S.lidx[s] = (unsigned short)(8 * (pos + 1));
+        S.lidx[s] = (unsigned short)(pos + 1);
         if (S.hist32)
             S.hist32[s] = S.hist ? float(S.hist[idx]) : 0.f;
         if (S.btype_c)
@@ -267,6 +309,9 @@ __global__ void slot_kernel(SlotArgs S) {
             S.beta32[s] = float(S.beta[idx]);
         ++c;
     }
+    // per warp of tile threads: the 8-slot groups its longest row needs
+    if (c > 0)
+        atomicMax(S.wgroups + (long long)t * (S.T / 32) + (ii - S.tile_start[t]) / 32, (c + 7) / 8);
 }
 
 template <class T> __global__ void fill_kernel(T* p, long long n, T v) {
@@ -367,10 +412,14 @@ cudaError_t gpu_build_layout(FastLayoutDev& L, const FastLayoutIn& in, int* erro
             g.nb[d] = (g.n_uniq[d] + kBrick[d] - 1) / kBrick[d];
             g.len[d] = 1.0;
         } else {
-            g.nb[d] = ext[d] > 0 ? std::max(1LL, (long long)std::llround(ext[d] / (8.0 * h))) : 1;
+            g.nb[d] = 1;
             g.len[d] = ext[d] > 0 ? ext[d] / double(g.nb[d]) : 1.0;
         }
     }
+    // irregular meshes: tiles are runs of T nodes along a Morton curve of
+    // mean-spacing cells (compact, nearly cubic, all but the last full)
+    g.morton = !(g.lattice[0] && g.lattice[1] && g.lattice[2]);
+    g.inv_h = 1.0 / h;
     const unsigned long long nbricks = (unsigned long long)(g.nb[0] * g.nb[1] * g.nb[2]);
     LY_CK(L.perm.alloc(size_t(n)));
     LY_CK(L.inv.alloc(size_t(n)));
@@ -383,7 +432,7 @@ cudaError_t gpu_build_layout(FastLayoutDev& L, const FastLayoutIn& in, int* erro
         LY_CK(tmp.get(&vals, size_t(n_own)));
         brick_key_kernel<<<blocks_for(n_own), TPB, 0, s>>>(in.xv, ob, n_own, g, keys, vals);
         LY_CK(cudaGetLastError());
-        const int kb = bits_for(nbricks);
+        const int kb = g.morton ? 63 : bits_for(nbricks);
         size_t need = 0;
         LY_CK(cub::DeviceRadixSort::SortPairs(nullptr, need, keys, keys_sorted, vals, L.perm.p,
                                               int(n_own), 0, kb, s));
@@ -406,17 +455,19 @@ cudaError_t gpu_build_layout(FastLayoutDev& L, const FastLayoutIn& in, int* erro
         LY_CK(cudaMemcpyAsync(counts.data(), rle_counts, sizeof(int) * size_t(runs),
                               cudaMemcpyDeviceToHost, s));
         LY_CK(cudaStreamSynchronize(s));
+        if (g.morton)  // one run: the whole curve is cut into T-node pieces
+            counts.assign(1, int(n_own));
+        // a brick of c nodes becomes ceil(c / T) tiles of balanced size (a
+        // 530-node bin is two 265-node tiles, not 512 + 18)
         long long at = 0;
         for (int c : counts) {
-            for (long long q = 0; q < c; q += T)
-                tile_start.push_back(int(at + q));
+            const long long nt = (c + T - 1) / T;
+            for (long long q = 0; q < nt; ++q)
+                tile_start.push_back(int(at + q * c / nt));
             at += c;
         }
     }
     tile_start.push_back(int(n_own));
-    if (n > n_own)
-        perm_tail_kernel<<<blocks_for(n - n_own), TPB, 0, s>>>(L.perm.p, n, ob, oe);
-    inv_kernel<<<blocks_for(n), TPB, 0, s>>>(L.perm.p, n, L.inv.p);
     const int tiles = int(tile_start.size()) - 1;
     L.T = T;
     L.n_tiles = tiles;
@@ -425,7 +476,14 @@ cudaError_t gpu_build_layout(FastLayoutDev& L, const FastLayoutIn& in, int* erro
     LY_CK(cudaMemsetAsync(L.tile_of.p, 0xff, sizeof(int) * size_t(n), s));
     if (tiles > 0)
         tile_of_kernel<<<unsigned(tiles), TPB, 0, s>>>(L.tile_start.p, tiles, L.tile_of.p);
+    if (n > n_own)
+        perm_tail_kernel<<<blocks_for(n - n_own), TPB, 0, s>>>(L.perm.p, n, ob, oe);
+    inv_kernel<<<blocks_for(n), TPB, 0, s>>>(L.perm.p, n, L.inv.p);
     LY_CK(cudaGetLastError());
+
+    // halo order: reference ids on bricks, internal ids on Morton tiles
+    const int* halo_key_inv = g.morton ? L.inv.p : nullptr;  // key -> order id map
+    const int* halo_by_ref = g.morton ? nullptr : L.inv.p;     // order id -> internal id
 
     // ---- 2. slot offsets -------------------------------------------------
     int *live, *kmax;
@@ -475,7 +533,7 @@ cudaError_t gpu_build_layout(FastLayoutDev& L, const FastLayoutIn& in, int* erro
     LY_CK(tmp.get(&pk_sorted, size_t(n_pairs)));
     LY_CK(tmp.get(&n_uniq_d, 1));
     if (n_own > 0)
-        pair_keys_kernel<<<blocks_for(n_own), TPB, 0, s>>>(in.entries, L.perm.p, L.tile_of.p,
+        pair_keys_kernel<<<blocks_for(n_own), TPB, 0, s>>>(in.entries, L.perm.p, halo_key_inv, L.tile_of.p,
                                                            in.nofail, pair_off, n_own, N, pk);
     LY_CK(cudaGetLastError());
     const int key_bits = 33 + bits_for((unsigned long long)std::max(tiles, 1));
@@ -503,7 +561,7 @@ cudaError_t gpu_build_layout(FastLayoutDev& L, const FastLayoutIn& in, int* erro
     LY_CK(fill<int>(L.nf_start.p, tiles, 0x7fffffff, s));
     LY_CK(cudaMemcpyAsync(L.halo_off.p + tiles, &H, sizeof(long long), cudaMemcpyHostToDevice, s));
     if (H > 0) {
-        halo_kernel<<<blocks_for(H), TPB, 0, s>>>(hk, H, L.inv.p, L.halo_off.p, L.halo.p);
+        halo_kernel<<<blocks_for(H), TPB, 0, s>>>(hk, H, halo_by_ref, L.halo_off.p, L.halo.p);
         nf_start_kernel<<<blocks_for(H), TPB, 0, s>>>(hk, H, L.halo_off.p, L.nf_start.p);
     }
     LY_CK(cudaGetLastError());
@@ -555,6 +613,7 @@ cudaError_t gpu_build_layout(FastLayoutDev& L, const FastLayoutIn& in, int* erro
     }
     S.entries = in.entries;
     S.perm = L.perm.p;
+    S.inv = halo_key_inv;
     S.tile_of = L.tile_of.p;
     S.tile_start = L.tile_start.p;
     S.slot_off = L.slot_off.p;
@@ -570,6 +629,9 @@ cudaError_t gpu_build_layout(FastLayoutDev& L, const FastLayoutIn& in, int* erro
     S.T = T;
     S.lidx = L.lidx.p;
     S.own_slot = L.own_slot.p;
+    LY_CK(L.wgroups.alloc(size_t(std::max(tiles, 1)) * size_t(T / 32)));
+    LY_CK(cudaMemsetAsync(L.wgroups.p, 0, sizeof(int) * size_t(std::max(tiles, 1)) * size_t(T / 32), s));
+    S.wgroups = L.wgroups.p;
     if (n_own > 0)
         slot_kernel<<<blocks_for(n_own), TPB, 0, s>>>(S);
     LY_CK(cudaGetLastError());

@@ -1,6 +1,10 @@
-set -x
+# ncu capture of one step kernel + the launch list of the same bench command (logs under gpurun_out/)
+# usage: KERNEL=lattice_step NAME=lattice216 BENCH_ARGS="--law pmb" bash scripts/gpu_prof.sh
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_exact.csv python bench.py --size 100 --steps 5 --warmup 3 --no-cpu --e2e-steps 2 > gpurun_out/ncu_launch.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:exact_step -s 4 -c 1 -o gpurun_out/prof_exact python bench.py --size 100 --steps 3 --warmup 3 --no-cpu --e2e-steps 1 > gpurun_out/ncu_full.log 2>&1
-tail -5 gpurun_out/pytest_gpu.log; tail -3 gpurun_out/ncu_full.log
+K=${KERNEL:-lattice_step}; N=${NAME:-prof}
+ARGS="--steps 2 --warmup 3 --no-cpu --no-probe --sustain-steps 0 --e2e-steps 2 ${BENCH_ARGS:-}"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s 3 -c 1 \
+  -o gpurun_out/$N python bench.py $ARGS > gpurun_out/ncu_$N.log 2>&1; echo "ncu full rc=$?"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file gpurun_out/launches_$N.csv python bench.py $ARGS > gpurun_out/ncu_launch_$N.log 2>&1
+echo "launch list rc=$?"

@@ -236,6 +236,59 @@ int pd_family_download(pd_family* family, int32_t* entries, int32_t* n_neigh,
                        int32_t* initial_n_neigh);
 void pd_family_free(pd_family* family);
 
+/* ---- setup-time family operations on the device (geometry.cpp) -------- */
+
+/* A rule-table BondClassifier (geometry.hpp:45-54, applied in pack_rows,
+ * geometry.cpp:131-161): each node's class is the class of the LAST region
+ * rule containing it (default_class when none does); the bond type of slot
+ * (i, j) is type_table[class_i * n_classes + class_j] (symmetric, as the
+ * reference requires of a classifier).  Padding slots keep type 0. */
+enum { PD_REGION_BOX = 0, PD_REGION_CYLINDER = 1 };
+typedef struct pd_region {
+    int32_t kind;   /* PD_REGION_BOX: lo <= x <= hi on every axis (inclusive) */
+    int32_t axis;   /* PD_REGION_CYLINDER: axis 0/1/2, lo[axis] <= x[axis] <= hi[axis] and */
+    int32_t cls;    /* (x[b0] - c[0])^2 + (x[b1] - c[1])^2 <= radius^2, b0 < b1 the other axes */
+    int32_t pad;
+    double lo[3];
+    double hi[3];
+    double c[2];
+    double radius;
+} pd_region;
+typedef struct pd_classifier {
+    int32_t n_classes;           /* 1..256 */
+    int32_t default_class;
+    int32_t n_regions;
+    int32_t pad;
+    const pd_region* regions;
+    const uint8_t* type_table;   /* n_classes x n_classes */
+} pd_classifier;
+
+/* bond_type (n x N) of a family under a rule-table classifier. */
+int pd_classify_bonds(const double* coords, const pd_neighbor_list* family,
+                      const pd_classifier* classifier, uint8_t* bond_type_out);
+/* neighborhood_volumes (geometry.cpp:238-252): per node the in-order sum of
+ * its live members' volumes. */
+int pd_neighborhood_volumes(const double* volumes, const pd_neighbor_list* family, double* out);
+/* surface_correction_factors (geometry.cpp:263-283): lambda_ij = 2 V0 /
+ * (V_i + V_j) per live slot, 1 on padding; domain errors as the reference. */
+int pd_surface_correction_factors(const double* volumes, const pd_neighbor_list* family,
+                                  double v0, double* lambda_out);
+
+/* break_initial_bonds (geometry.cpp:285-306) with plane_crossing_predicate
+ * (:300-305) or notch_predicate (:308-319): matching slots become -1 and
+ * n_neigh drops; initial_n_neigh is untouched. */
+enum { PD_PREDICATE_PLANE = 0, PD_PREDICATE_NOTCH = 1 };
+typedef struct pd_bond_predicate {
+    int32_t kind;
+    int32_t axis;
+    int32_t sweep_axis;  /* notch only */
+    int32_t pad;
+    double position;
+    double depth;        /* notch only: crossing point along sweep_axis <= depth */
+} pd_bond_predicate;
+int pd_break_initial_bonds(pd_neighbor_list* family, const double* coords,
+                           const pd_bond_predicate* predicate);
+
 /* ---- device-resident context ------------------------------------------ */
 
 typedef struct pd_ctx pd_ctx;

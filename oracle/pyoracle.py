@@ -153,6 +153,70 @@ class Reference(Backend):
     def build_family(self, coords, horizon, hint=None) -> NeighborList:
         return _family_from(self.lib, "ref_", coords, horizon, hint)
 
+    def build_family_classified(self, coords, horizon, hint, classifier):
+        """build_family(coords, horizon, hint, classify) of the reference with a
+        BondClassifier lambda applying `classifier`'s region rules
+        (geometry.py RuleClassifier): (entries, bond_type, group_size)."""
+        fn = self.lib.ref_build_family_classified
+        fn.argtypes = [C.POINTER(C.c_double), C.c_int64, C.c_double, C.POINTER(C.c_double),
+                       C.POINTER(abi.pd_classifier), C.POINTER(C.POINTER(C.c_int32)),
+                       C.POINTER(C.POINTER(C.c_uint8)), C.POINTER(C.c_int64)]
+        self.lib.ref_free.argtypes = [C.c_void_p]
+        coords = abi.as_f64(coords)
+        n = coords.size // 3
+        keep: list = []
+        cls = classifier.descriptor(keep)
+        e, t = C.POINTER(C.c_int32)(), C.POINTER(C.c_uint8)()
+        g = C.c_int64()
+        hint_arr = None if hint is None else np.asarray(hint, dtype=np.float64)
+        self._check(fn(abi.ptr(coords, C.c_double), n, float(horizon),
+                       abi.ptr(hint_arr, C.c_double) if hint_arr is not None else None,
+                       C.byref(cls), C.byref(e), C.byref(t), C.byref(g)))
+        try:
+            N = int(g.value)
+            entries = np.ctypeslib.as_array(e, shape=(n * N,)).copy()
+            types = np.ctypeslib.as_array(t, shape=(n * N,)).copy()
+        finally:
+            self.lib.ref_free(e)
+            self.lib.ref_free(t)
+        return entries, types, N
+
+    def neighborhood_volumes(self, volumes, family) -> np.ndarray:
+        self.lib.ref_neighborhood_volumes.argtypes = [C.POINTER(C.c_double),
+                                                      C.POINTER(abi.pd_neighbor_list),
+                                                      C.POINTER(C.c_double)]
+        m = abi.Marshal()
+        f = m.family(family)
+        v = abi.as_f64(volumes)
+        out = np.empty(family.node_count())
+        self._check(self.lib.ref_neighborhood_volumes(abi.ptr(v, C.c_double), C.byref(f),
+                                                      abi.ptr(out, C.c_double)))
+        return out
+
+    def surface_correction_factors(self, volumes, family, v0) -> np.ndarray:
+        self.lib.ref_surface_correction_factors.argtypes = [
+            C.POINTER(C.c_double), C.POINTER(abi.pd_neighbor_list), C.c_double,
+            C.POINTER(C.c_double)]
+        m = abi.Marshal()
+        f = m.family(family)
+        v = abi.as_f64(volumes)
+        out = np.empty(family.entries.size)
+        self._check(self.lib.ref_surface_correction_factors(abi.ptr(v, C.c_double), C.byref(f),
+                                                            float(v0), abi.ptr(out, C.c_double)))
+        return out
+
+    def break_bonds(self, family, coords, kind, axis, position, sweep_axis=0, depth=0.0):
+        """break_initial_bonds with plane_crossing_predicate (kind 0) or
+        notch_predicate (kind 1) of the reference, in place."""
+        self.lib.ref_break_bonds.argtypes = [C.POINTER(abi.pd_neighbor_list),
+                                             C.POINTER(C.c_double), C.c_int, C.c_int,
+                                             C.c_double, C.c_int, C.c_double]
+        m = abi.Marshal()
+        f = m.family(family)
+        c = abi.as_f64(coords)
+        self.lib.ref_break_bonds(C.byref(f), abi.ptr(c, C.c_double), int(kind), int(axis),
+                                 float(position), int(sweep_axis), float(depth))
+
     def save_state(self, state, path: str) -> None:
         """io::save_state of the reference."""
         self.lib.ref_save_state.argtypes = [C.POINTER(abi.pd_state), C.c_char_p]

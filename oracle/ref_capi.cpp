@@ -346,6 +346,65 @@ int ref_build_family(const double* coords, int64_t n, double horizon, const doub
 
 void ref_free(void* p) { std::free(p); }
 
+// build_family with a BondClassifier (geometry.hpp:45-54) that applies the
+// same region rules as pd_classifier: class = last matching region (else the
+// default), type = table[class_a][class_b].  The reference calls it per slot
+// from pack_rows; the bond types come back n x N.
+int ref_build_family_classified(const double* coords, int64_t n, double horizon,
+                                const double* grid_hint, const pd_classifier* cls,
+                                int32_t** entries_out, uint8_t** types_out,
+                                int64_t* group_size_out) {
+    return map_exceptions([&] {
+        GridDesc g;
+        const GridDesc* hint = nullptr;
+        if (grid_hint) {
+            g.origin = {grid_hint[0], grid_hint[1], grid_hint[2]};
+            g.spacing = grid_hint[3];
+            g.counts = {Index(grid_hint[4]), Index(grid_hint[5]), Index(grid_hint[6])};
+            hint = &g;
+        }
+        auto in_region = [](const pd_region& r, const Vec3& x) {
+            const Real p[3] = {x.x, x.y, x.z};
+            if (r.kind == PD_REGION_BOX) {
+                for (int d = 0; d < 3; ++d)
+                    if (!(p[d] >= r.lo[d] && p[d] <= r.hi[d]))
+                        return false;
+                return true;
+            }
+            const int a = r.axis, b0 = a == 0 ? 1 : 0, b1 = a == 2 ? 1 : 2;
+            if (!(p[a] >= r.lo[a] && p[a] <= r.hi[a]))
+                return false;
+            const Real d0 = p[b0] - r.c[0], d1 = p[b1] - r.c[1];
+            return d0 * d0 + d1 * d1 <= r.radius * r.radius;
+        };
+        auto class_of = [&](const Vec3& x) {
+            int c = cls->default_class;
+            for (int k = 0; k < cls->n_regions; ++k)
+                if (in_region(cls->regions[k], x))
+                    c = cls->regions[k].cls;
+            return c;
+        };
+        const BondClassifier classify = [&](const Vec3& a, const Vec3& b) {
+            return std::uint8_t(cls->type_table[class_of(a) * cls->n_classes + class_of(b)]);
+        };
+        const NeighborList f = build_family(std::span<const Real>(coords, std::size_t(3 * n)),
+                                            horizon, hint, classify);
+        *group_size_out = f.group_size;
+        *entries_out = static_cast<int32_t*>(std::malloc(f.entries.size() * sizeof(int32_t)));
+        *types_out = static_cast<uint8_t*>(std::malloc(f.bond_type.size()));
+        std::memcpy(*entries_out, f.entries.data(), f.entries.size() * sizeof(int32_t));
+        std::memcpy(*types_out, f.bond_type.data(), f.bond_type.size());
+    });
+}
+
+int ref_neighborhood_volumes(const double* volumes, const pd_neighbor_list* family, double* out) {
+    return map_exceptions([&] {
+        const auto v = neighborhood_volumes(std::span<const Real>(volumes, std::size_t(family->n)),
+                                            to_family(*family));
+        std::memcpy(out, v.data(), v.size() * sizeof(double));
+    });
+}
+
 void ref_break_bonds(pd_neighbor_list* family, const double* coords, int kind, int axis,
                      double position, int sweep_axis, double depth) {
     NeighborList f = to_family(*family);

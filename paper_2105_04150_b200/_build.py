@@ -28,6 +28,7 @@ UNITS = {
     "pd_host.cu": ["-fmad=false"],
     "pd_fast.cu": ["-fmad=true", "-diag-suppress=186"],
     "pd_family.cu": ["-fmad=false"],
+    "pd_family_ops.cu": ["-fmad=false"],
     "pd_layout.cu": ["-fmad=false"],
     "pd_lattice.cu": ["-fmad=true", "-diag-suppress=177"],
     "pd_lattice_nlu0.cu": ["-fmad=true", "-diag-suppress=177"],

@@ -116,6 +116,26 @@ class pd_peer_handle(C.Structure):
                 ("u0", C.c_uint64), ("u1", C.c_uint64), ("sync", C.c_uint64)]
 
 
+PD_REGION_BOX, PD_REGION_CYLINDER = 0, 1
+PD_PREDICATE_PLANE, PD_PREDICATE_NOTCH = 0, 1
+
+
+class pd_region(C.Structure):
+    _fields_ = [("kind", i32), ("axis", i32), ("cls", i32), ("pad", i32),
+                ("lo", C.c_double * 3), ("hi", C.c_double * 3), ("c", C.c_double * 2),
+                ("radius", C.c_double)]
+
+
+class pd_classifier(C.Structure):
+    _fields_ = [("n_classes", i32), ("default_class", i32), ("n_regions", i32), ("pad", i32),
+                ("regions", C.POINTER(pd_region)), ("type_table", u8p)]
+
+
+class pd_bond_predicate(C.Structure):
+    _fields_ = [("kind", i32), ("axis", i32), ("sweep_axis", i32), ("pad", i32),
+                ("position", C.c_double), ("depth", C.c_double)]
+
+
 class InvalidArgument(ValueError):
     """std::invalid_argument"""
 

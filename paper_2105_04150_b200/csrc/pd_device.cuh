@@ -89,7 +89,9 @@ constexpr long long kPeerTimeout = -2;  // err_step value: a peer rank never arr
 
 // Store an owned node's new displacement into the ghost rows of the
 // neighbouring ranks (peer memory) and make it visible system-wide before the
-// step's sync kernel publishes the step.
+// step's sync kernel publishes the step.  One system fence per warp, not per
+// node: the converged lanes meet at __syncwarp (which orders their stores
+// before the leader's) and the leader's fence.sc.sys is cumulative over them.
 __device__ __forceinline__ void push_ghost(const DevArgs& A, long long i, const double4& un) {
     if (!A.xfer)
         return;
@@ -98,8 +100,13 @@ __device__ __forceinline__ void push_ghost(const DevArgs& A, long long i, const 
         A.peer_lo[t.x] = un;
     if (t.y >= 0)
         A.peer_hi[t.y] = un;
-    if (t.x >= 0 || t.y >= 0)
-        __threadfence_system();
+    const unsigned act = __activemask();
+    const unsigned pushed = __ballot_sync(act, t.x >= 0 || t.y >= 0);
+    if (pushed) {
+        __syncwarp(act);
+        if ((threadIdx.x & 31) == unsigned(__ffs(act) - 1))
+            __threadfence_system();
+    }
 }
 
 // RampProfile::scale/rate/accel (types.cpp:119-169); same operation order, so

@@ -1532,9 +1532,13 @@ int pd_ctx_connect(pd_ctx* ctx, int32_t rank, int32_t world, const pd_peer_handl
     // every kernel a run may launch is loaded now: under CUDA lazy loading a
     // first launch can wait for the whole device, which would deadlock
     // against a peer rank's spinning sync kernel (callers barrier after
-    // connect, so no rank spins before every rank has loaded)
-    static std::once_flag loaded;
-    std::call_once(loaded, [] {
+    // connect, so no rank spins before every rank has loaded).  Modules load
+    // per device, so each device is preloaded once (thread ranks on several
+    // GPUs of one process each load their own device)
+    static std::once_flag loaded[64];
+    if (ctx->device < 0 || ctx->device >= 64)
+        return fail(PD_E_INVALID_ARGUMENT, "connect: device ordinal %d out of range", ctx->device);
+    std::call_once(loaded[ctx->device], [] {
         preload_aux();
         preload_exact();
         preload_fast();

@@ -37,9 +37,8 @@ def cfg1():
 def cfg2():
     b, h, g, notch = S.notched_plate_bundle(100, 100, 10, 1000)
     fam = geometry.build_family(b.particles.coords, h, g)
-    COracle(threads=os.cpu_count() or 1).break_notch(
-        fam, b.particles.coords, notch["axis"], notch["position"], notch["sweep_axis"],
-        notch["depth"])
+    geometry.break_notch(fam, b.particles.coords, notch["axis"], notch["position"],
+                         notch["sweep_axis"], notch["depth"])
     return ("cfg2 notched plate 100x100x10, bilinear, Euler-Cromer", b, fam,
             IntegratorKind.euler_cromer, 1000, 1000)
 

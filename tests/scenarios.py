@@ -59,11 +59,16 @@ def trilinear_bar_bundle():
     return ModelBundle(p, model, Corrections(), bc, 0.05), 1.8, None
 
 
-def notched_plate_bundle(nx=40, ny=40, nz=4, integrator_steps=200, pull=0.6):
+def notched_plate_bundle(nx=40, ny=40, nz=4, integrator_steps=200, pull=None):
     """cfg2 (downscaled): pre-cracked plate, Mode I, bilinear law, Euler-Cromer.
     Edge notch at y = ny/2 - 0.5 from x = 0 to x = nx/4; opposite y faces pulled
     apart on a linear ramp; a force patch and a no-failure strip exercise the
-    remaining BC kinds.  Notch applied by the caller (break_initial_bonds)."""
+    remaining BC kinds.  Notch applied by the caller (break_initial_bonds).
+    The pull scales with the plate (0.015 ny per face: a 3 % far-field strain
+    at the end of the ramp, above s0 = 2.3 %), so the notch propagates at any
+    size (0.6 at ny = 40)."""
+    if pull is None:
+        pull = 0.015 * ny
     g, p = lattice_particles((nx, ny, nz))
     n = p.size()
     delta = math.pi

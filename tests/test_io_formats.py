@@ -177,3 +177,61 @@ def test_device_snapshots_sync_and_async(tmp_path, oracle):
     for step in written:
         assert _bytes(tmp_path / f"async_{step:06d}.pdsnap") == \
             _bytes(tmp_path / f"ref_{step:06d}.pdsnap"), step
+
+
+@pytest.mark.gpu
+def test_device_save_state_keeps_history_under_pmb(tmp_path, oracle):
+    """A PMB model run from a state that carries bond_history: the reference
+    leaves the history untouched and save_state still writes its section
+    (io.cpp section 10); the resident run saves the same bytes."""
+    from paper_2105_04150_b200 import geometry
+    b, h, g = S.bench_lattice_bundle((9, 8, 7), s_c=1e6)
+    fam = geometry.build_family(b.particles.coords, h, g)
+    rng = np.random.default_rng(7)
+    hist = np.where(fam.entries >= 0, rng.uniform(0, 1e-3, fam.entries.size), 0.0)
+    files = []
+    for be in ("oracle", "device"):
+        st = make_state(fam, False)
+        st.u = S.seed_displacements(b.particles.coords)
+        st.bond_history = hist.copy()
+        p = tmp_path / f"{be}.pdst"
+        if be == "oracle":
+            oracle.simulate(b, st, SimulateOptions(6, 0, 0, IntegratorKind.velocity_verlet))
+            engine.save_state(st, str(p))
+        else:
+            ctx = engine.Context(0)
+            ctx.upload(b, st, KernelVariant.bond_parallel)
+            ctx.run(6, 0, IntegratorKind.velocity_verlet, 0, KernelVariant.bond_parallel)
+            ctx.save_state(str(p))
+            ctx.close()
+        files.append(_bytes(p))
+    assert files[0] == files[1]
+    assert engine.load_state(str(tmp_path / "device.pdst")).bond_history is not None
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", [KernelVariant.bond_parallel, KernelVariant.fast])
+def test_async_snapshots_stop_at_the_failed_step(tmp_path, oracle, variant):
+    """A run that turns non-finite at step e: the reference throws inside step
+    e's force pass, so no snapshot after e is written; the queued asynchronous
+    snapshots past e are dropped."""
+    b, h, _ = S.small_fracture_bundle()
+    fam = oracle.build_family(b.particles.coords, h)
+    b.model.laws[0] = type(b.model.laws[0]).pmb(0.05, 1e9)
+    b.bc.kind[:] = 0
+    b.bc.kind[3 * 7] = 2  # force axis with an enormous load
+    b.bc.magnitude[3 * 7] = 1.5e308
+    ref = make_state(fam, False)
+    with pytest.raises(abi.PeridynRuntimeError) as ei:
+        oracle.simulate(b, ref, SimulateOptions(120, 0, 0, IntegratorKind.euler))
+    failed = int(str(ei.value).rsplit("step", 1)[1].split()[0])
+    st = make_state(fam, False)
+    ctx = engine.Context(0)
+    ctx.upload(b, st, variant)
+    ctx.snapshot_every(1, str(tmp_path / "s_%06lld.pdsnap"))
+    with pytest.raises(abi.PeridynRuntimeError):
+        ctx.run(120, 0, IntegratorKind.euler, 0, variant)
+    ctx.close()
+    steps = sorted(int(f[2:8]) for f in os.listdir(tmp_path) if f.endswith(".pdsnap"))
+    assert steps and max(steps) <= failed, (failed, steps[-3:])
+    assert steps == list(range(1, max(steps) + 1))

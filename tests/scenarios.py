@@ -252,3 +252,68 @@ def finish_random_config(p, model, family, draws, rng):
                     state.connectivity.n_neigh[j] -= 1
     state.u = (rng.uniform(0, 1, 3 * n) - 0.5) * 0.02
     return corr, state
+
+
+def rc_beam_setup(dx_mm=1.6, length_mm=2100.0, height_mm=320.0, width_mm=190.0):
+    """cfg5: the reinforced-concrete beam of PAPER.md:580-597 (Stuttgart shear
+    test beam 5): 320 x 190 mm section, 1950 mm span between supports (75 mm
+    overhang each end), two 26 mm bars at 270 mm effective depth, four-point
+    loading with a shear span of 810 mm.  dx = 1.6 mm gives 1313 x 200 x 119
+    = 31.2M nodes (the paper's dx = 5 mm mesh scaled by (5/1.6)^3).
+    Materials: concrete E_c = 30.5 GPa, rho 2346,
+    trilinear s0/s1/s_c = 1.05e-4 / 6.9e-4 / 5.56e-3 (the Yang 2018 column);
+    steel E_s = 208 GPa, rho 7850, linear (never breaks); a bilinear
+    steel-concrete interface.  delta = pi dx; c = 18 K / (pi delta^4) with
+    K = E / 1.5 (nu = 1/4).  Supports: clamped (left) and roller (right)
+    no-failure patches under the bottom face; loads: quintic-ramped downward
+    displacement patches on the top face.  Returns (bundle, grid, horizon,
+    classifier); the caller builds the family, classifies the bonds and
+    computes the surface correction (geometry.build_family / classify /
+    surface_correction_factors)."""
+    from paper_2105_04150_b200.geometry import Region, RuleClassifier
+    dx = dx_mm * 1e-3
+    counts = (int(round(length_mm / dx_mm)) + 1, int(round(height_mm / dx_mm)),
+              int(round(width_mm / dx_mm)))
+    g = GridDesc((0.0, 0.0, 0.0), dx, counts)
+    coords = grid_coordinates(g)
+    n = g.node_count()
+    x, y, z = coords[0::3], coords[1::3], coords[2::3]
+    delta = math.pi * dx
+    E_c, E_s = 30.5e9, 208.0e9
+    c_c = 18.0 * (E_c / 1.5) / (math.pi * delta ** 4)
+    c_s = 18.0 * (E_s / 1.5) / (math.pi * delta ** 4)
+    c_i = 0.5 * (c_c + c_s)
+    laws = [DamageLaw.trilinear(c_c, 1.05e-4, 6.9e-4, 5.56e-3),   # concrete-concrete
+            DamageLaw.pmb(c_s, 1.0),                              # steel-steel (linear)
+            DamageLaw.bilinear(c_i, 2.0e-4, 1.75e-3)]             # steel-concrete interface
+    model = DamageModel(laws, damping=0.0)
+    # two bars, 26 mm diameter, centres 50 mm above the bottom face (effective
+    # depth 270 mm) and 45 mm in from each side
+    yb = (height_mm - 270.0) * 1e-3
+    bars = [Region(cls=1, kind="cylinder", axis=0, center=(yb, zc), radius=13e-3)
+            for zc in (45e-3, (width_mm - 45.0) * 1e-3)]
+    classifier = RuleClassifier(np.array([[0, 2], [2, 1]], dtype=np.uint8), bars)
+    on_bar = classifier.node_classes(coords) == 1
+    density = np.where(on_bar, 7850.0, 2346.0)
+    particles = ParticleSet(coords, np.full(n, dx ** 3), density, np.zeros(n, np.uint16))
+    bc = BoundaryConditions.none(n)
+    bc.ramps.append(RampProfile(RampKind.quintic_smooth, 200000, 1.0))
+    top, bottom = y >= y.max() - 0.5 * dx, y <= 0.5 * dx
+    span0, span1 = 75e-3, 75e-3 + 1950e-3
+    near = lambda x0: np.abs(x - x0) <= 10e-3  # noqa: E731  (20 mm wide patches)
+    left, right = bottom & near(span0), bottom & near(span1)
+    load = top & (near(span0 + 810e-3) | near(span1 - 810e-3))
+    for ax in range(3):
+        bc.kind[3 * np.flatnonzero(left) + ax] = BCKind.displacement      # clamped
+    for ax in (1, 2):
+        bc.kind[3 * np.flatnonzero(right) + ax] = BCKind.displacement     # roller
+    li = 3 * np.flatnonzero(load) + 1
+    bc.kind[li] = BCKind.displacement
+    bc.magnitude[li] = -2e-3
+    bc.ramp_id[li] = 1
+    bc.no_failure[left | right | load] = 1
+    mid = top & (np.abs(x - 0.5 * (span0 + span1)) <= 0.6 * dx)
+    bc.tip_sets["midspan"] = [int(i) for i in np.flatnonzero(mid)]
+    bc.tip_sets["load"] = [int(i) for i in np.flatnonzero(load)]
+    dt = 2.0e-8
+    return ModelBundle(particles, model, Corrections(), bc, dt), g, delta, classifier

@@ -236,6 +236,38 @@ int pd_family_download(pd_family* family, int32_t* entries, int32_t* n_neigh,
                        int32_t* initial_n_neigh);
 void pd_family_free(pd_family* family);
 
+/* ---- the reference's stand-alone integrators and boundary passes -------
+ * (engine.hpp:38-78, engine.cpp:187-305) on the device, over host buffers:
+ * each call reads and writes the same arrays as the reference function, in
+ * its expression order, so hand-composed steps (test_engine.cpp:196-357)
+ * give the reference's bits.  Errors: dt <= 0 -> PD_E_DOMAIN "<fn>: dt must
+ * be positive"; density size -> PD_E_INVALID_ARGUMENT, density <= 0 ->
+ * PD_E_DOMAIN (check_density, engine.cpp:177-183). */
+int pd_verlet_drift(pd_state* state, double dt);
+int pd_verlet_kick(pd_state* state, const pd_force_field* forces, double dt, double damping,
+                   const double* density, int64_t density_size);
+int pd_step_euler(pd_state* state, const pd_force_field* forces, double dt,
+                  const double* density, int64_t density_size);
+int pd_step_euler_cromer(pd_state* state, const pd_force_field* forces, double dt,
+                         const double* density, int64_t density_size);
+/* ForceEval (engine.hpp:56): fill forces->body_force for the state's u;
+ * nonzero = failure (the step fails with PD_E_RUNTIME). */
+typedef int (*pd_force_eval)(void* user, pd_state* state, pd_force_field* forces);
+/* step_velocity_verlet (engine.cpp:254-260): drift, forces(state, scratch),
+ * kick, ++step. */
+int pd_step_velocity_verlet(pd_state* state, pd_force_eval forces, void* user,
+                            pd_force_field* scratch, double dt, double damping,
+                            const double* density, int64_t density_size);
+int pd_apply_displacement_positions(pd_state* state, const pd_boundary* bc, int64_t step);
+int pd_apply_displacement_kinematics(pd_state* state, const pd_boundary* bc, int64_t step,
+                                     double dt);
+/* adds force-BC densities into out->external_force (n nodes); no clearing */
+int pd_accumulate_external_force(const pd_boundary* bc, int64_t step, pd_force_field* out,
+                                 int64_t n);
+/* apply_boundary: bc.validate, positions, kinematics, external force */
+int pd_apply_boundary(pd_state* state, const pd_boundary* bc, int64_t step, double dt,
+                      pd_force_field* out);
+
 /* ---- setup-time family operations on the device (geometry.cpp) -------- */
 
 /* A rule-table BondClassifier (geometry.hpp:45-54, applied in pack_rows,

@@ -8,6 +8,11 @@
 //       == peridyn::compute_forces (engine.hpp:35-36): same arguments, same
 //          in-place mutation of state.connectivity / bond_history, same
 //          exception types and messages; bitwise-equal results.
+//   peridyn::b200::step_euler / step_euler_cromer / verlet_drift / verlet_kick /
+//   step_velocity_verlet / apply_displacement_positions / _kinematics /
+//   accumulate_external_force / apply_boundary
+//       == the reference's stand-alone integrators and boundary passes
+//          (engine.hpp:38-78), same signatures, bitwise-equal results.
 //   peridyn::b200::simulate(bundle, state, options, on_write[, fast])
 //       == peridyn::simulate (engine.hpp:128-129), the whole loop device-resident;
 //          the write hook sees the caller's SimulationState exactly as the
@@ -19,6 +24,7 @@
 
 #include <cstring>
 #include <map>
+#include <span>
 #include <stdexcept>
 #include <string>
 #include <type_traits>
@@ -265,6 +271,88 @@ inline SimulateResult simulate(const ModelBundle& bundle, SimulationState& state
         result.tips[bc.names[std::size_t(r) % sets]].push_back(rec);
     }
     return result;
+}
+
+// ---- stand-alone integrators and boundary passes (engine.hpp:38-78) -------
+
+namespace detail {
+inline void check_sizes(const SimulationState& s, const char* who) {
+    const Index n = s.size();
+    if (Index(s.u.size()) != 3 * n || Index(s.v.size()) != 3 * n || Index(s.a.size()) != 3 * n)
+        throw std::invalid_argument(std::string(who) + ": state fields do not match node count");
+}
+inline pd_force_field forces(const ForceField& f) {
+    return pd_force_field{const_cast<double*>(f.body_force.data()),
+                          const_cast<double*>(f.external_force.data())};
+}
+} // namespace detail
+
+inline void step_euler(SimulationState& state, const ForceField& forces, Real dt,
+                       std::span<const Real> density) {
+    detail::check_sizes(state, "step_euler");
+    pd_state st = detail::state(state);
+    pd_force_field ff = detail::forces(forces);
+    detail::raise(pd_step_euler(&st, &ff, dt, density.data(), Index(density.size())));
+}
+
+inline void step_euler_cromer(SimulationState& state, const ForceField& forces, Real dt,
+                              std::span<const Real> density) {
+    detail::check_sizes(state, "step_euler_cromer");
+    pd_state st = detail::state(state);
+    pd_force_field ff = detail::forces(forces);
+    detail::raise(pd_step_euler_cromer(&st, &ff, dt, density.data(), Index(density.size())));
+}
+
+inline void verlet_drift(SimulationState& state, Real dt) {
+    detail::check_sizes(state, "verlet_drift");
+    pd_state st = detail::state(state);
+    detail::raise(pd_verlet_drift(&st, dt));
+}
+
+inline void verlet_kick(SimulationState& state, const ForceField& forces, Real dt, Real damping,
+                        std::span<const Real> density) {
+    detail::check_sizes(state, "verlet_kick");
+    pd_state st = detail::state(state);
+    pd_force_field ff = detail::forces(forces);
+    detail::raise(pd_verlet_kick(&st, &ff, dt, damping, density.data(), Index(density.size())));
+}
+
+inline void step_velocity_verlet(SimulationState& state, const ForceEval& forces,
+                                 ForceField& scratch, Real dt, Real damping,
+                                 std::span<const Real> density) {
+    b200::verlet_drift(state, dt);  // qualified: ADL also finds peridyn::verlet_drift
+    forces(state, scratch);
+    b200::verlet_kick(state, scratch, dt, damping, density);
+    state.step += 1;
+}
+
+inline void apply_displacement_positions(SimulationState& state, const BoundaryConditions& bc,
+                                         Index step) {
+    detail::Boundary b(bc);
+    pd_state st = detail::state(state);
+    detail::raise(pd_apply_displacement_positions(&st, &b.bc, step));
+}
+
+inline void apply_displacement_kinematics(SimulationState& state, const BoundaryConditions& bc,
+                                          Index step, Real dt) {
+    detail::Boundary b(bc);
+    pd_state st = detail::state(state);
+    detail::raise(pd_apply_displacement_kinematics(&st, &b.bc, step, dt));
+}
+
+inline void accumulate_external_force(const BoundaryConditions& bc, Index step, ForceField& out) {
+    detail::Boundary b(bc);
+    pd_force_field ff{out.body_force.data(), out.external_force.data()};
+    detail::raise(pd_accumulate_external_force(&b.bc, step, &ff,
+                                               Index(out.external_force.size()) / 3));
+}
+
+inline void apply_boundary(SimulationState& state, const BoundaryConditions& bc, Index step,
+                           Real dt, ForceField& out) {
+    detail::Boundary b(bc);
+    pd_state st = detail::state(state);
+    pd_force_field ff{out.body_force.data(), out.external_force.data()};
+    detail::raise(pd_apply_boundary(&st, &b.bc, step, dt, &ff));
 }
 
 } // namespace peridyn::b200

@@ -9,6 +9,7 @@
 // and requires byte-identical results.  Prints one line per case and exits
 // with the number of failures.
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -214,12 +215,85 @@ void error_mapping() {
     report("lambda size mismatch -> invalid_argument '" + gpu_msg + "'", ok);
 }
 
+// Hand-composed steps (test_engine.cpp:196-357): the reference's stand-alone
+// integrators and boundary passes against peridyn::b200's, on random configs
+// with a ForceEval that calls each side's compute_forces.
+void hand_composed_steps() {
+    for (unsigned seed : {1003u, 1011u, 1027u}) {
+        RandomConfig cfg = make_random_config(seed);
+        const Index n = cfg.state.size();
+        SimulationState a = cfg.state, b = cfg.state;
+        ForceField fa, fb;
+        fa.resize(n);
+        fb.resize(n);
+        BoundaryConditions bc = BoundaryConditions::none(n);
+        bc.ramps.push_back(RampProfile{RampProfile::Kind::quintic_smooth, 30, 1});
+        for (Index i = 0; i < n; i += 7) {
+            bc.kind[std::size_t(3 * i)] = BCKind::displacement;
+            bc.magnitude[std::size_t(3 * i)] = Real(1e-3);
+            bc.ramp_id[std::size_t(3 * i)] = 1;
+            bc.kind[std::size_t(3 * i + 1)] = BCKind::force;
+            bc.magnitude[std::size_t(3 * i + 1)] = Real(0.25);
+        }
+        const Real dt = Real(1e-3);
+        const ForceEval ea = [&](SimulationState& s, ForceField& out) {
+            peridyn::compute_forces(KernelVariant::bond_parallel, s, cfg.particles, cfg.model,
+                                    cfg.corrections, out);
+        };
+        const ForceEval eb = [&](SimulationState& s, ForceField& out) {
+            peridyn::b200::compute_forces(KernelVariant::bond_parallel, s, cfg.particles,
+                                          cfg.model, cfg.corrections, out);
+        };
+        bool ok = true;
+        for (Index k = 0; k < 12 && ok; ++k) {
+            std::fill(fa.external_force.begin(), fa.external_force.end(), 0);
+            std::fill(fb.external_force.begin(), fb.external_force.end(), 0);
+            peridyn::apply_boundary(a, bc, k, dt, fa);
+            peridyn::b200::apply_boundary(b, bc, k, dt, fb);
+            if (k % 3 == 0) {
+                peridyn::step_velocity_verlet(a, ea, fa, dt, Real(0.1), cfg.particles.density);
+                peridyn::b200::step_velocity_verlet(b, eb, fb, dt, Real(0.1),
+                                                    cfg.particles.density);
+            } else {
+                ea(a, fa);
+                eb(b, fb);
+                if (k % 3 == 1) {
+                    peridyn::step_euler(a, fa, dt, cfg.particles.density);
+                    peridyn::b200::step_euler(b, fb, dt, cfg.particles.density);
+                } else {
+                    peridyn::step_euler_cromer(a, fa, dt, cfg.particles.density);
+                    peridyn::b200::step_euler_cromer(b, fb, dt, cfg.particles.density);
+                }
+            }
+            ok = same_state(a, b) && same(fa.external_force, fb.external_force);
+        }
+        report("hand-composed steps (apply_boundary, step_velocity_verlet, step_euler, "
+               "step_euler_cromer) seed " + std::to_string(seed), ok);
+    }
+    // errors: dt <= 0 and a density of the wrong size
+    std::string ref_msg, gpu_msg;
+    RandomConfig cfg = make_random_config(1001);
+    try {
+        peridyn::verlet_drift(cfg.state, 0);
+    } catch (const std::domain_error& e) {
+        ref_msg = e.what();
+    }
+    try {
+        peridyn::b200::verlet_drift(cfg.state, 0);
+    } catch (const std::domain_error& e) {
+        gpu_msg = e.what();
+    }
+    report("verlet_drift dt <= 0 -> domain_error '" + gpu_msg + "'",
+           !ref_msg.empty() && ref_msg == gpu_msg);
+}
+
 } // namespace
 
 int main() {
     random_configs();
     simulate_runs();
     error_mapping();
+    hand_composed_steps();
     std::printf("failures %d\n", failures);
     return failures;
 }

@@ -283,6 +283,69 @@ __global__ void gather_list_rows_kernel(const int32_t* cur, const int* list, lon
         out[r * N + k] = cur[i * N + k];
 }
 
+// The reference's stand-alone integrators over flat n x 3 host-layout arrays
+// (engine.cpp:187-252), in its expression order (-fmad=false):
+//   op 0 verlet_drift:   u = u + v dt + a (dt dt / 2)
+//   op 1 verlet_kick:    v_half = v + a (dt/2); a = (F - v_half eta) (1/rho);
+//                        v = v_half + a (dt/2)
+//   op 2 step_euler:     a = F (1/rho); v = v_old + a dt; u = u + v_old dt
+//   op 3 step_euler_cromer: a = F (1/rho); v = v + a dt; u = u + v_new dt
+// with F = body_force + external_force (engine.cpp:173-175).
+__global__ void integrate_kernel(IntegrateArgs I) {
+    const long long i = blockIdx.x * (long long)TPB + threadIdx.x;
+    if (i >= I.n)
+        return;
+    const double dt = I.dt;
+    const double inv = I.op == 0 ? 0.0 : __ddiv_rn(1.0, I.density[i]);
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+        const long long k = 3 * i + ax;
+        if (I.op == 0) {
+            I.u[k] = __dadd_rn(__dadd_rn(I.u[k], __dmul_rn(I.v[k], dt)),
+                               __dmul_rn(I.a[k], __ddiv_rn(__dmul_rn(dt, dt), 2.0)));
+            continue;
+        }
+        const double F = __dadd_rn(I.body[k], I.ext[k]);
+        if (I.op == 1) {
+            const double half = __ddiv_rn(dt, 2.0);
+            const double vh = __dadd_rn(I.v[k], __dmul_rn(I.a[k], half));
+            const double an = __dmul_rn(__dsub_rn(F, __dmul_rn(vh, I.damping)), inv);
+            I.a[k] = an;
+            I.v[k] = __dadd_rn(vh, __dmul_rn(an, half));
+        } else {
+            const double acc = __dmul_rn(F, inv);
+            const double v_old = I.v[k];
+            const double v_new = __dadd_rn(v_old, __dmul_rn(acc, dt));
+            I.a[k] = acc;
+            I.v[k] = v_new;
+            I.u[k] = __dadd_rn(I.u[k], __dmul_rn(I.op == 2 ? v_old : v_new, dt));
+        }
+    }
+}
+
+// apply_displacement_positions / _kinematics and accumulate_external_force
+// (engine.cpp:262-297) over the node-axes, selected by the bits of B.ops
+__global__ void boundary_kernel(BoundaryArgs B) {
+    const long long k = blockIdx.x * (long long)TPB + threadIdx.x;
+    if (k >= 3 * B.n)
+        return;
+    const int kind = B.kind[k];
+    if (kind == PD_BC_FREE)
+        return;
+    const DevRamp r = B.ramps[B.ramp_id[k]];
+    const double mag = B.mag[k];
+    if (kind == PD_BC_DISPLACEMENT) {
+        if (B.ops & 1)
+            B.u[k] = __dmul_rn(mag, ramp_scale(r, B.step));
+        if (B.ops & 2) {
+            B.v[k] = __ddiv_rn(__dmul_rn(mag, ramp_rate(r, B.step)), B.dt);
+            B.a[k] = __ddiv_rn(__dmul_rn(mag, ramp_accel(r, B.step)), __dmul_rn(B.dt, B.dt));
+        }
+    } else if (kind == PD_BC_FORCE && (B.ops & 4)) {
+        B.ext[k] = __dadd_rn(B.ext[k], __dmul_rn(mag, ramp_scale(r, B.step)));
+    }
+}
+
 } // namespace
 
 void launch_changed_rows(const int32_t* cur, const int32_t* orig, long long n, int N, int* list,
@@ -407,6 +470,16 @@ void launch_tips(const double4* u, const double* v, const double* a, const doubl
     if (n_sets > 0)
         tips_kernel<<<(n_sets + 63) / 64, 64, 0, st>>>(u, v, a, xv, body, ext, n_sets, offsets,
                                                        nodes, step, out);
+}
+
+void launch_integrate(const IntegrateArgs& I, cudaStream_t st) {
+    if (I.n > 0)
+        integrate_kernel<<<grid_for(I.n), TPB, 0, st>>>(I);
+}
+
+void launch_boundary(const BoundaryArgs& B, cudaStream_t st) {
+    if (B.n > 0)
+        boundary_kernel<<<grid_for(3 * B.n), TPB, 0, st>>>(B);
 }
 
 } // namespace pdb

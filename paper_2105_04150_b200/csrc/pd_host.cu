@@ -1910,4 +1910,159 @@ int pd_damage(const pd_neighbor_list* family, double* phi) {
     return pd_ctx_damage(ctx, phi);
 }
 
+
+// ---- the reference's stand-alone integrators and boundary passes ----------
+// (engine.hpp:38-78, engine.cpp:187-305) on the device over host buffers:
+// each call uploads the arrays it reads, runs one kernel with the reference's
+// expression order (pd_aux.cu, -fmad=false) and writes back the arrays the
+// reference writes, so hand-composed steps (test_engine.cpp:196-357) give the
+// reference's bits.
+
+static int integrate_host(const char* who, int op, pd_state* st, const pd_force_field* f,
+                          double dt, double damping, const double* density, int64_t density_size) {
+    if (!(dt > 0))
+        return fail(PD_E_DOMAIN, "%s: dt must be positive", who);
+    const int64_t n = st->connectivity.n;
+    if (op != 0) {  // check_density (engine.cpp:177-183)
+        if (density_size != n)
+            return fail(PD_E_INVALID_ARGUMENT,
+                        "integrator: density array does not match node count");
+        if (par_any(n, [&](int64_t i) { return !(density[i] > 0); }))
+            return fail(PD_E_DOMAIN, "integrator: density must be positive");
+    }
+    if (n == 0)
+        return ok();
+    pd_ctx* ctx = nullptr;
+    PD_TRY(pd_ctx_create(0, &ctx));
+    struct Guard {
+        pd_ctx* c;
+        ~Guard() { pd_ctx_destroy(c); }
+    } guard{ctx};
+    cudaStream_t s = ctx->stream;
+    const size_t n3 = size_t(3 * n);
+    DevBuf<double> u, v, a, body, ext, rho;
+    PD_CK(v.upload(st->v, n3, s));
+    PD_CK(a.upload(st->a, n3, s));
+    if (op != 1)
+        PD_CK(u.upload(st->u, n3, s));
+    if (op != 0) {
+        PD_CK(body.upload(f->body_force, n3, s));
+        PD_CK(ext.upload(f->external_force, n3, s));
+        PD_CK(rho.upload(density, size_t(n), s));
+    }
+    IntegrateArgs I{u.p, v.p, a.p, body.p, ext.p, rho.p, (long long)n, dt, damping, op};
+    launch_integrate(I, s);
+    PD_CK(cudaGetLastError());
+    if (op != 1)
+        PD_CK(cudaMemcpyAsync(st->u, u.p, sizeof(double) * n3, cudaMemcpyDeviceToHost, s));
+    if (op != 0) {
+        PD_CK(cudaMemcpyAsync(st->v, v.p, sizeof(double) * n3, cudaMemcpyDeviceToHost, s));
+        PD_CK(cudaMemcpyAsync(st->a, a.p, sizeof(double) * n3, cudaMemcpyDeviceToHost, s));
+    }
+    PD_CK(cudaStreamSynchronize(s));
+    return ok();
+}
+
+static int boundary_host(int ops, pd_state* st, const pd_boundary* bc, int64_t step, double dt,
+                         pd_force_field* out, int64_t n) {
+    if (n == 0)
+        return ok();
+    pd_ctx* ctx = nullptr;
+    PD_TRY(pd_ctx_create(0, &ctx));
+    struct Guard {
+        pd_ctx* c;
+        ~Guard() { pd_ctx_destroy(c); }
+    } guard{ctx};
+    cudaStream_t s = ctx->stream;
+    const size_t n3 = size_t(3 * n);
+    std::vector<DevRamp> ramps(size_t(bc->n_ramps));
+    for (int k = 0; k < bc->n_ramps; ++k)
+        ramps[size_t(k)] = DevRamp{bc->ramps[k].kind, 0, bc->ramps[k].rise_steps,
+                                   bc->ramps[k].target_scale};
+    DevBuf<double> u, v, a, ext, mag;
+    DevBuf<uint8_t> kind, rid;
+    DevBuf<DevRamp> dr;
+    PD_CK(kind.upload(bc->kind, n3, s));
+    PD_CK(mag.upload(bc->magnitude, n3, s));
+    PD_CK(rid.upload(bc->ramp_id, n3, s));
+    PD_CK(dr.upload(ramps.data(), ramps.size(), s));
+    if (ops & 1)
+        PD_CK(u.upload(st->u, n3, s));
+    if (ops & 2) {
+        PD_CK(v.upload(st->v, n3, s));
+        PD_CK(a.upload(st->a, n3, s));
+    }
+    if (ops & 4)
+        PD_CK(ext.upload(out->external_force, n3, s));
+    BoundaryArgs B{u.p, v.p, a.p, ext.p, kind.p, mag.p, rid.p, dr.p, (long long)n,
+                   (long long)step, dt, ops};
+    launch_boundary(B, s);
+    PD_CK(cudaGetLastError());
+    if (ops & 1)
+        PD_CK(cudaMemcpyAsync(st->u, u.p, sizeof(double) * n3, cudaMemcpyDeviceToHost, s));
+    if (ops & 2) {
+        PD_CK(cudaMemcpyAsync(st->v, v.p, sizeof(double) * n3, cudaMemcpyDeviceToHost, s));
+        PD_CK(cudaMemcpyAsync(st->a, a.p, sizeof(double) * n3, cudaMemcpyDeviceToHost, s));
+    }
+    if (ops & 4)
+        PD_CK(cudaMemcpyAsync(out->external_force, ext.p, sizeof(double) * n3,
+                              cudaMemcpyDeviceToHost, s));
+    PD_CK(cudaStreamSynchronize(s));
+    return ok();
+}
+
+int pd_verlet_drift(pd_state* state, double dt) {
+    return integrate_host("verlet_drift", 0, state, nullptr, dt, 0.0, nullptr, 0);
+}
+
+int pd_verlet_kick(pd_state* state, const pd_force_field* forces, double dt, double damping,
+                   const double* density, int64_t density_size) {
+    return integrate_host("verlet_kick", 1, state, forces, dt, damping, density, density_size);
+}
+
+int pd_step_euler(pd_state* state, const pd_force_field* forces, double dt, const double* density,
+                  int64_t density_size) {
+    return integrate_host("step_euler", 2, state, forces, dt, 0.0, density, density_size);
+}
+
+int pd_step_euler_cromer(pd_state* state, const pd_force_field* forces, double dt,
+                         const double* density, int64_t density_size) {
+    return integrate_host("step_euler_cromer", 3, state, forces, dt, 0.0, density, density_size);
+}
+
+int pd_step_velocity_verlet(pd_state* state, pd_force_eval forces, void* user,
+                            pd_force_field* scratch, double dt, double damping,
+                            const double* density, int64_t density_size) {
+    // step_velocity_verlet (engine.cpp:254-260): drift, forces at the advanced
+    // positions (the caller's ForceEval, e.g. pd_compute_forces), kick
+    PD_TRY(pd_verlet_drift(state, dt));
+    if (forces && forces(user, state, scratch) != 0)
+        return fail(PD_E_RUNTIME, "step_velocity_verlet: force evaluation failed");
+    PD_TRY(pd_verlet_kick(state, scratch, dt, damping, density, density_size));
+    state->step += 1;
+    return ok();
+}
+
+int pd_apply_displacement_positions(pd_state* state, const pd_boundary* bc, int64_t step) {
+    return boundary_host(1, state, bc, step, 1.0, nullptr, state->connectivity.n);
+}
+
+int pd_apply_displacement_kinematics(pd_state* state, const pd_boundary* bc, int64_t step,
+                                     double dt) {
+    return boundary_host(2, state, bc, step, dt, nullptr, state->connectivity.n);
+}
+
+int pd_accumulate_external_force(const pd_boundary* bc, int64_t step, pd_force_field* out,
+                                 int64_t n) {
+    return boundary_host(4, nullptr, bc, step, 1.0, out, n);
+}
+
+int pd_apply_boundary(pd_state* state, const pd_boundary* bc, int64_t step, double dt,
+                      pd_force_field* out) {
+    // apply_boundary (engine.cpp:299-305): validate, positions, kinematics, forces
+    PD_TRY(bc_validate(*bc, state->connectivity.n));
+    return boundary_host(7, state, bc, step, dt, out, state->connectivity.n);
+}
+
 } // extern "C"
+

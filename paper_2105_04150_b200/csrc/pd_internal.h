@@ -222,6 +222,34 @@ struct SyncArgs {
     long long timeout_ns;
 };
 void launch_slab_sync(const SyncArgs& S, cudaStream_t st);
+
+// stand-alone integrators and boundary passes (pd_aux.cu; C ABI in pd_host.cu)
+struct IntegrateArgs {
+    double* u;
+    double* v;
+    double* a;
+    const double* body;
+    const double* ext;
+    const double* density;
+    long long n;
+    double dt, damping;
+    int op;  // 0 verlet_drift, 1 verlet_kick, 2 step_euler, 3 step_euler_cromer
+};
+struct BoundaryArgs {
+    double* u;
+    double* v;
+    double* a;
+    double* ext;
+    const uint8_t* kind;
+    const double* mag;
+    const uint8_t* ramp_id;
+    const DevRamp* ramps;
+    long long n, step;
+    double dt;
+    int ops;  // bit 0 positions, bit 1 kinematics, bit 2 external force
+};
+void launch_integrate(const IntegrateArgs& I, cudaStream_t st);
+void launch_boundary(const BoundaryArgs& B, cudaStream_t st);
 void launch_changed_rows(const int32_t* cur, const int32_t* orig, long long n, int N, int* list,
                          unsigned long long* count, cudaStream_t st);
 void launch_gather_list_rows(const int32_t* cur, const int* list, long long m, int N, int32_t* out,

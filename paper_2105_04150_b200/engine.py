@@ -45,6 +45,99 @@ class Backend:
     def _check(self, rc: int) -> None:
         check(rc, self._last)
 
+    # ---- stand-alone integrators (engine.hpp:38-62, engine.cpp:187-260) ----
+    def _integrate(self, name, state, forces, dt, damping, density):
+        fn = getattr(self.lib, self.prefix + name)
+        m = Marshal()
+        st = m.state(state)
+        if name == "verlet_drift":
+            fn.argtypes = [C.POINTER(abi.pd_state), C.c_double]
+            rc = fn(C.byref(st), float(dt))
+        else:
+            rho = m._k(abi.as_f64(density))
+            ff = m.forces(forces)
+            args = [C.byref(st), C.byref(ff), float(dt)]
+            types = [C.POINTER(abi.pd_state), C.POINTER(abi.pd_force_field), C.c_double]
+            if name == "verlet_kick":
+                args.append(float(damping))
+                types.append(C.c_double)
+            fn.argtypes = types + [C.POINTER(C.c_double), C.c_int64]
+            rc = fn(*args, abi.ptr(rho, C.c_double), rho.size)
+        self._check(rc)
+
+    def verlet_drift(self, state, dt) -> None:
+        self._integrate("verlet_drift", state, None, dt, 0.0, None)
+
+    def verlet_kick(self, state, forces, dt, damping, density) -> None:
+        self._integrate("verlet_kick", state, forces, dt, damping, density)
+
+    def step_euler(self, state, forces, dt, density) -> None:
+        self._integrate("step_euler", state, forces, dt, 0.0, density)
+
+    def step_euler_cromer(self, state, forces, dt, density) -> None:
+        self._integrate("step_euler_cromer", state, forces, dt, 0.0, density)
+
+    def step_velocity_verlet(self, state, force_eval, scratch, dt, damping, density) -> None:
+        """step_velocity_verlet (engine.cpp:254-260): drift, force_eval(state,
+        scratch), kick, ++step."""
+        self.verlet_drift(state, dt)
+        force_eval(state, scratch)
+        self.verlet_kick(state, scratch, dt, damping, density)
+        state.step += 1
+
+    # ---- boundary conditions (engine.hpp:64-78, engine.cpp:262-305) ----------
+    def apply_displacement_positions(self, state, bc, step) -> None:
+        m = Marshal()
+        st, b = m.state(state), m.boundary(bc)
+        fn = getattr(self.lib, self.prefix + "apply_displacement_positions")
+        fn.argtypes = [C.POINTER(abi.pd_state), C.POINTER(abi.pd_boundary), C.c_int64]
+        rc = fn(C.byref(st), C.byref(b), int(step))
+        if self.prefix == "pd_":
+            self._check(rc)
+
+    def apply_displacement_kinematics(self, state, bc, step, dt) -> None:
+        m = Marshal()
+        st, b = m.state(state), m.boundary(bc)
+        fn = getattr(self.lib, self.prefix + "apply_displacement_kinematics")
+        fn.argtypes = [C.POINTER(abi.pd_state), C.POINTER(abi.pd_boundary), C.c_int64,
+                       C.c_double]
+        rc = fn(C.byref(st), C.byref(b), int(step), float(dt))
+        if self.prefix == "pd_":
+            self._check(rc)
+
+    def accumulate_external_force(self, bc, step, out) -> None:
+        m = Marshal()
+        b = m.boundary(bc)
+        ff = m.forces(out)
+        n = out.external_force.size // 3
+        fn = getattr(self.lib, self.prefix + "accumulate_external_force")
+        if self.prefix == "pd_":
+            fn.argtypes = [C.POINTER(abi.pd_boundary), C.c_int64, C.POINTER(abi.pd_force_field),
+                           C.c_int64]
+            self._check(fn(C.byref(b), int(step), C.byref(ff), n))
+        else:
+            fn.argtypes = [C.POINTER(abi.pd_boundary), C.c_int64, C.POINTER(C.c_double), C.c_int64]
+            fn(C.byref(b), int(step), ff.external_force, n)
+
+    def apply_boundary(self, state, bc, step, dt, out) -> None:
+        """apply_boundary (engine.cpp:299-305)."""
+        if self.prefix == "pd_":
+            m = Marshal()
+            st, b, ff = m.state(state), m.boundary(bc), m.forces(out)
+            fn = self.lib.pd_apply_boundary
+            fn.argtypes = [C.POINTER(abi.pd_state), C.POINTER(abi.pd_boundary), C.c_int64,
+                           C.c_double, C.POINTER(abi.pd_force_field)]
+            self._check(fn(C.byref(st), C.byref(b), int(step), float(dt), C.byref(ff)))
+            return
+        m = Marshal()
+        b = m.boundary(bc)
+        fn = getattr(self.lib, self.prefix + "bc_validate")
+        fn.argtypes = [C.POINTER(abi.pd_boundary), C.c_int64]
+        self._check(fn(C.byref(b), state.size()))
+        self.apply_displacement_positions(state, bc, step)
+        self.apply_displacement_kinematics(state, bc, step, dt)
+        self.accumulate_external_force(bc, step, out)
+
     # compute_forces (engine.hpp:35-36, engine.cpp:163-169)
     def compute_forces(self, variant, state: SimulationState, particles, model, corrections,
                        out: ForceField) -> None:

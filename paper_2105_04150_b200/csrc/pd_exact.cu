@@ -5,13 +5,17 @@
 // reference's IEEE expression sequence.
 //
 // Mapping (one fused launch per time step):
-//   * a group of G = min(N, 32) lanes owns one node i; lane l owns slots
-//     k = l + G*m, m < M = N/G (M <= 8, so N <= 256);
+//   * a group of G lanes owns one node i (G = N for N < 32, 16 for the
+//     N = 128 lattice ball -- two nodes per warp share the per-node prologue
+//     and epilogue -- else 32); lane l owns slots k = l + G*m, m < M = N/G;
+//   * one PMB law without bond types or corrections (the bench lattice)
+//     takes a specialised slot body with the law in registers (slot_pmb);
 //   * each lane evaluates its slots like bond_contribution (engine.cpp:53-109):
 //     stretch, law, fused break into the alive bitmask (+ n_neigh), history;
 //   * the group sums the N contributions with reduce_group's halving-stride
-//     tree (engine.cpp:11-19): strides >= G are lane-local, strides < G are
-//     __shfl_down steps -- the same pairs in the same order, so the body force
+//     tree (engine.cpp:11-19): strides >= G are lane-local (evaluated in tree
+//     order, tree_sum), strides < G are __shfl_down steps -- the same pairs in
+//     the same order, so the body force
 //     is bit-identical to compute_forces_bond_parallel.  The node_parallel
 //     variant is a serial in-order sum (engine.cpp:152-158) via broadcasts;
 //   * lane 0 then runs the node's integrator epilogue in the reference's order:
@@ -22,6 +26,8 @@
 //   Double-buffered u removes the read/write race the paper cites as the
 //   reason integration cannot be fused.
 #include <cuda_runtime.h>
+
+#include <cstdlib>
 
 #include "pd_device.cuh"
 #include "pd_internal.h"
@@ -127,19 +133,77 @@ __device__ __forceinline__ Contribution slot_contribution(const DevArgs& A, long
     return c;
 }
 
-// 4 CTAs of 256 per SM (64 registers, small spill): 16.6 ms/step at 10M against 18.6 ms at
-// the compiler's 80 registers (3 CTAs) -- the kernel is gather-latency bound
-// (PD_EXACT_MINB for experiments)
+// The single-PMB-law model with no bond types and no corrections (the bench
+// lattice): bond_contribution (engine.cpp:53-109) with the law constants in
+// registers and no law-table, history or correction branches -- the same
+// IEEE operations in the same order, so the same bits.
+__device__ __forceinline__ Contribution slot_pmb(const DevArgs& A, int j, const double4& xi,
+                                                 const double4& ui, bool i_no_fail, bool& alive,
+                                                 int& broke) {
+    Contribution c{0.0, 0.0, 0.0};
+    if (!alive)
+        return c;
+    const double4 xj = A.xv[j];
+    const double4 uj = A.u_in[j];
+    const double rx = __dsub_rn(xj.x, xi.x), ry = __dsub_rn(xj.y, xi.y), rz = __dsub_rn(xj.z, xi.z);
+    const double cx = __dadd_rn(rx, __dsub_rn(uj.x, ui.x));
+    const double cy = __dadd_rn(ry, __dsub_rn(uj.y, ui.y));
+    const double cz = __dadd_rn(rz, __dsub_rn(uj.z, ui.z));
+    const double ref_len = norm3(rx, ry, rz);
+    const double cur_len = norm3(cx, cy, cz);
+    const double s = __ddiv_rn(__dsub_rn(cur_len, ref_len), ref_len);
+    // no-fail bonds never break (engine.cpp:83-86); PMB breaks at s >= s_c (:93-98)
+    if (!(i_no_fail || uj.w != 0.0) && s >= A.pmb_sc) {
+        alive = false;
+        ++broke;
+        return c;
+    }
+    const double f = __dmul_rn(A.pmb_c, s);
+    if (cur_len < 1e-30)
+        return c;
+    const double q = __ddiv_rn(__dmul_rn(f, xj.w), cur_len);
+    c.x = __dmul_rn(cx, q);
+    c.y = __dmul_rn(cy, q);
+    c.z = __dmul_rn(cz, q);
+    return c;
+}
+
+// reduce_group's lane-local strides (N/2 .. G: c[m] += c[m + h] for h = M/2 .. 1)
+// evaluated in tree order: the sum over slots {OFF, OFF + STRIDE, ...} is the
+// sum of its even half and its odd half, each formed the same way -- the same
+// pairs in the same order as the stride loop, but each slot's contribution is
+// added as soon as its partner exists, so at most log2(M) + 1 triples are live
+// instead of M.
+template <int M, int OFF, int STRIDE, class F>
+__device__ __forceinline__ Contribution tree_sum(F& eval) {
+    if constexpr (M == 1) {
+        return eval(OFF);
+    } else {
+        const Contribution l = tree_sum<M / 2, OFF, 2 * STRIDE>(eval);
+        const Contribution r = tree_sum<M / 2, OFF + STRIDE, 2 * STRIDE>(eval);
+        return Contribution{__dadd_rn(l.x, r.x), __dadd_rn(l.y, r.y), __dadd_rn(l.z, r.z)};
+    }
+}
+
+// 4 CTAs of 256 per SM (64 registers)
 #ifndef PD_EXACT_MINB
 #define PD_EXACT_MINB 4
 #endif
+#ifndef PD_EXACT_PF
+#define PD_EXACT_PF 2
+#endif
 // MODE: 0 = force pass only (compute_forces), 1 = velocity-Verlet step,
 //       2 = Euler step, 3 = Euler-Cromer step.
-template <int MODE, int M, bool NODE_SUM>
+// GT lanes own one node (GT = 0: G = N < 32 at run time, M = 1); lane l of a
+// node owns slots l + G m, m < M = N / G.  Several nodes per warp (G < 32)
+// share the warp's per-node prologue and integrator epilogue; reduce_group's
+// strides >= G stay lane-local (tree_sum), strides < G are shuffles within
+// the node's G lanes -- the reference's pairs for every G.
+template <int MODE, int GT, int M, bool NODE_SUM, bool PMB>
 __global__ void __launch_bounds__(256, PD_EXACT_MINB) exact_step_kernel(DevArgs A) {
     if (MODE != 0 && *(volatile long long*)A.err_step != kNoError)
         return; // a previous step saw non-finite u: the reference threw there
-    const int G = (M > 1) ? 32 : (A.N < 32 ? A.N : 32);
+    const int G = GT > 0 ? GT : (A.N < 32 ? A.N : 32);
     const int lane = threadIdx.x & 31;
     const int sub = lane / G;
     const int gl = lane - sub * G;
@@ -155,41 +219,90 @@ __global__ void __launch_bounds__(256, PD_EXACT_MINB) exact_step_kernel(DevArgs 
     }
     const bool i_no_fail = ui.w != 0.0;
 
-    Contribution c[M];
-    uint32_t old_words[M];
-    bool alive[M];
-    int broke = 0;
-    // every live slot's neighbour index first, and its x and u records
-    // prefetched into L1 (no registers held), before the first slot's long
-    // fp64 evaluation chain: otherwise each slot's gather waits on L2 in turn
+    // this lane's slots: live bits (from the row's alive words) and indices
+    constexpr int WMAX = GT > 0 ? (GT * M + 31) / 32 : 1;  // alive words per row
+    uint32_t old_words[WMAX];
+#pragma unroll
+    for (int w = 0; w < WMAX; ++w)
+        old_words[w] = valid && w < A.W ? A.alive[i * A.W + w] : 0u;
+    uint32_t live = 0;  // bit m: slot gl + G m is alive
     int jm[M];
 #pragma unroll
     for (int m = 0; m < M; ++m) {
         const int k = gl + G * m;
-        old_words[m] = valid ? A.alive[i * A.W + (k >> 5)] : 0u;
-        alive[m] = valid && ((old_words[m] >> (k & 31)) & 1u);
-        jm[m] = alive[m] ? __ldg(A.entries + i * N + k) : 0;
+        const bool al = valid && ((old_words[k >> 5] >> (k & 31)) & 1u);
+        live |= (al ? 1u : 0u) << m;
+        jm[m] = al ? __ldg(A.entries + i * N + k) : 0;
     }
-#pragma unroll
-    for (int m = 1; m < M; ++m)
-        if (alive[m]) {
+    // live slots' x and u records prefetched into L1 (no registers held)
+    // ahead of their long fp64 evaluation chains: all at once (PD_EXACT_PF =
+    // 0), or PD_EXACT_PF slots ahead in evaluation order (the tree order is
+    // the bit reversal of 0 .. M-1)
+    auto prefetch = [&](int m) {
+        if ((live >> m) & 1u) {
             asm volatile("prefetch.global.L1 [%0];" ::"l"(A.xv + jm[m]));
             asm volatile("prefetch.global.L1 [%0];" ::"l"(A.u_in + jm[m]));
         }
+    };
+    constexpr int PF = PD_EXACT_PF;
+    constexpr int LOGM = M >= 16 ? 4 : M >= 8 ? 3 : M >= 4 ? 2 : M >= 2 ? 1 : 0;
+    auto bitrev = [](int x) {
+        int r = 0;
 #pragma unroll
-    for (int m = 0; m < M; ++m) {
+        for (int b = 0; b < LOGM; ++b)
+            r |= ((x >> b) & 1) << (LOGM - 1 - b);
+        return r;
+    };
+    if (PF == 0 || NODE_SUM) {
+#pragma unroll
+        for (int m = 1; m < M; ++m)
+            prefetch(m);
+    } else {
+#pragma unroll
+        for (int p = 1; p < PF && p < M; ++p)
+            prefetch(bitrev(p));
+    }
+    int broke = 0;
+    auto eval = [&](int m) -> Contribution {
+        if (PF > 0 && !NODE_SUM && bitrev(m) + PF < M)
+            prefetch(bitrev(bitrev(m) + PF));  // the slot PF positions later
         const int k = gl + G * m;
-        c[m] = slot_contribution(A, i * N + k, jm[m], xi, ui, i_no_fail, alive[m], broke);
+        bool al = (live >> m) & 1u;
+        const Contribution c =
+            PMB ? slot_pmb(A, jm[m], xi, ui, i_no_fail, al, broke)
+                : slot_contribution(A, i * N + k, jm[m], xi, ui, i_no_fail, al, broke);
+        if (!al)
+            live &= ~(1u << m);
+        return c;
+    };
+    Contribution c0{};
+    Contribution c[NODE_SUM ? M : 1];
+    if (!NODE_SUM) {
+        c0 = tree_sum<M, 0, 1>(eval);  // reduce_group's lane-local strides
+    } else {
+#pragma unroll
+        for (int m = 0; m < M; ++m)
+            c[m] = eval(m);
     }
 
-    // fused break bookkeeping: alive words and n_neigh (engine.cpp:93-96)
+    // fused break bookkeeping: alive words and n_neigh (engine.cpp:93-96).
+    // Word w holds slots 32w .. 32w+31 = lanes gl of sub-slots m = w R + j
+    // (R = 32 / G), bit gl + G j.
+    const uint32_t gmask = G >= 32 ? 0xffffffffu : ((1u << G) - 1u);
+    constexpr int R = GT > 0 && GT < 32 ? 32 / GT : 1;
 #pragma unroll
-    for (int m = 0; m < M; ++m) {
-        uint32_t word = __ballot_sync(FULL, alive[m]);
-        if (G < 32)
-            word = (word >> (sub * G)) & (0xffffffffu >> (32 - G));
-        if (valid && gl == 0 && word != old_words[m])
-            A.alive[i * A.W + m] = word;
+    for (int w = 0; w < WMAX; ++w) {
+        uint32_t word = 0;
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+            const int m = w * R + j;
+            if (m < M) {
+                const uint32_t b = __ballot_sync(FULL, (live >> m) & 1u);
+                word |= (G >= 32 ? b : ((b >> (sub * G)) & gmask)) << (G * j);
+            }
+        }
+        if (valid && gl == 0 && w < A.W && word != old_words[w])
+            A.alive[i * A.W + w] = word;
     }
     if (__any_sync(FULL, broke != 0)) {
         for (int off = G / 2; off > 0; off /= 2)
@@ -200,27 +313,19 @@ __global__ void __launch_bounds__(256, PD_EXACT_MINB) exact_step_kernel(DevArgs 
 
     double fx, fy, fz;
     if (!NODE_SUM) {
-        // reduce_group (engine.cpp:11-19): strides N/2 .. G lane-local ...
-#pragma unroll
-        for (int h = M / 2; h >= 1; h /= 2)
-#pragma unroll
-            for (int mm = 0; mm < h; ++mm) {
-                c[mm].x = __dadd_rn(c[mm].x, c[mm + h].x);
-                c[mm].y = __dadd_rn(c[mm].y, c[mm + h].y);
-                c[mm].z = __dadd_rn(c[mm].z, c[mm + h].z);
-            }
-        // ... strides G/2 .. 1 across lanes: c[k] += c[k + stride]
+        // reduce_group (engine.cpp:11-19) strides G/2 .. 1 across lanes:
+        // c[k] += c[k + stride]
         for (int st = G / 2; st >= 1; st /= 2) {
-            const double ox = __shfl_down_sync(FULL, c[0].x, st, G);
-            const double oy = __shfl_down_sync(FULL, c[0].y, st, G);
-            const double oz = __shfl_down_sync(FULL, c[0].z, st, G);
-            c[0].x = __dadd_rn(c[0].x, ox);
-            c[0].y = __dadd_rn(c[0].y, oy);
-            c[0].z = __dadd_rn(c[0].z, oz);
+            const double ox = __shfl_down_sync(FULL, c0.x, st, G);
+            const double oy = __shfl_down_sync(FULL, c0.y, st, G);
+            const double oz = __shfl_down_sync(FULL, c0.z, st, G);
+            c0.x = __dadd_rn(c0.x, ox);
+            c0.y = __dadd_rn(c0.y, oy);
+            c0.z = __dadd_rn(c0.z, oz);
         }
-        fx = c[0].x;
-        fy = c[0].y;
-        fz = c[0].z;
+        fx = c0.x;
+        fy = c0.y;
+        fz = c0.z;
     } else {
         // compute_forces_node_parallel: serial left-to-right sum over slots
         fx = fy = fz = 0.0;
@@ -244,42 +349,41 @@ __global__ void __launch_bounds__(256, PD_EXACT_MINB) exact_step_kernel(DevArgs 
     node_epilogue<MODE>(A, i, ui, fx, fy, fz);
 }
 
-template <int MODE, bool NODE_SUM>
-cudaError_t launch_m(const DevArgs& A, int M, dim3 grid, cudaStream_t st) {
-    switch (M) {
-    case 1:
-        t_last_kernel = kernel_name<0, MODE, 1, NODE_SUM>("exact_step_kernel");
-        exact_step_kernel<MODE, 1, NODE_SUM><<<grid, 256, 0, st>>>(A);
-        break;
-    case 2:
-        t_last_kernel = kernel_name<0, MODE, 2, NODE_SUM>("exact_step_kernel");
-        exact_step_kernel<MODE, 2, NODE_SUM><<<grid, 256, 0, st>>>(A);
-        break;
-    case 4:
-        t_last_kernel = kernel_name<0, MODE, 4, NODE_SUM>("exact_step_kernel");
-        exact_step_kernel<MODE, 4, NODE_SUM><<<grid, 256, 0, st>>>(A);
-        break;
-    case 8:
-        t_last_kernel = kernel_name<0, MODE, 8, NODE_SUM>("exact_step_kernel");
-        exact_step_kernel<MODE, 8, NODE_SUM><<<grid, 256, 0, st>>>(A);
-        break;
-    default:
-        return cudaErrorInvalidValue;
-    }
+template <int MODE, int GT, int M, bool NODE_SUM, bool PMB>
+cudaError_t launch_gm(const DevArgs& A, dim3 grid, cudaStream_t st) {
+    t_last_kernel = kernel_name<0, MODE, GT, M, NODE_SUM, PMB>("exact_step_kernel");
+    exact_step_kernel<MODE, GT, M, NODE_SUM, PMB><<<grid, 256, 0, st>>>(A);
     return cudaGetLastError();
 }
 
-template <bool NODE_SUM>
-cudaError_t launch_mode(const DevArgs& A, int mode, int M, dim3 grid, cudaStream_t st) {
+// lanes per node: N < 32 -> G = N (M = 1); N = 32, 64 -> G = 32; N = 128 ->
+// G = 16 (two nodes per warp, 8 slots per lane); N = 256 -> G = 32
+template <int MODE, bool NODE_SUM, bool PMB>
+cudaError_t launch_m(const DevArgs& A, int G, int M, dim3 grid, cudaStream_t st) {
+    if (G < 32 && M == 1)
+        return launch_gm<MODE, 0, 1, NODE_SUM, PMB>(A, grid, st);
+    switch (G * 1000 + M) {
+    case 32001: return launch_gm<MODE, 32, 1, NODE_SUM, PMB>(A, grid, st);
+    case 32002: return launch_gm<MODE, 32, 2, NODE_SUM, PMB>(A, grid, st);
+    case 32004: return launch_gm<MODE, 32, 4, NODE_SUM, PMB>(A, grid, st);
+    case 16008: return launch_gm<MODE, 16, 8, NODE_SUM, PMB>(A, grid, st);
+    case 8016: return launch_gm<MODE, 8, 16, NODE_SUM, PMB>(A, grid, st);
+    case 32008: return launch_gm<MODE, 32, 8, NODE_SUM, PMB>(A, grid, st);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+template <bool NODE_SUM, bool PMB>
+cudaError_t launch_mode(const DevArgs& A, int mode, int G, int M, dim3 grid, cudaStream_t st) {
     switch (mode) {
     case 0:
-        return launch_m<0, NODE_SUM>(A, M, grid, st);
+        return launch_m<0, NODE_SUM, PMB>(A, G, M, grid, st);
     case 1:
-        return launch_m<1, NODE_SUM>(A, M, grid, st);
+        return launch_m<1, NODE_SUM, PMB>(A, G, M, grid, st);
     case 2:
-        return launch_m<2, NODE_SUM>(A, M, grid, st);
+        return launch_m<2, NODE_SUM, PMB>(A, G, M, grid, st);
     default:
-        return launch_m<3, NODE_SUM>(A, M, grid, st);
+        return launch_m<3, NODE_SUM, PMB>(A, G, M, grid, st);
     }
 }
 
@@ -290,15 +394,21 @@ template <class K> static void preload(K k) {
     cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(k));
 }
 
+template <int MODE, bool NS, bool PMB> static void preload_ns() {
+    preload(exact_step_kernel<MODE, 0, 1, NS, PMB>);
+    preload(exact_step_kernel<MODE, 32, 1, NS, PMB>);
+    preload(exact_step_kernel<MODE, 32, 2, NS, PMB>);
+    preload(exact_step_kernel<MODE, 32, 4, NS, PMB>);
+    preload(exact_step_kernel<MODE, 16, 8, NS, PMB>);
+    preload(exact_step_kernel<MODE, 8, 16, NS, PMB>);
+    preload(exact_step_kernel<MODE, 32, 8, NS, PMB>);
+}
+
 template <int MODE> static void preload_mode() {
-    preload(exact_step_kernel<MODE, 1, false>);
-    preload(exact_step_kernel<MODE, 2, false>);
-    preload(exact_step_kernel<MODE, 4, false>);
-    preload(exact_step_kernel<MODE, 8, false>);
-    preload(exact_step_kernel<MODE, 1, true>);
-    preload(exact_step_kernel<MODE, 2, true>);
-    preload(exact_step_kernel<MODE, 4, true>);
-    preload(exact_step_kernel<MODE, 8, true>);
+    preload_ns<MODE, false, false>();
+    preload_ns<MODE, true, false>();
+    preload_ns<MODE, false, true>();
+    preload_ns<MODE, true, true>();
 }
 
 void preload_exact() {
@@ -308,17 +418,29 @@ void preload_exact() {
     preload_mode<3>();
 }
 
-cudaError_t launch_exact(const DevArgs& A, int mode, bool node_sum, cudaStream_t st) {
+cudaError_t launch_exact(const DevArgs& A, int mode, bool node_sum, bool pmb, cudaStream_t st) {
     const long long nodes = A.end - A.begin;
     if (nodes <= 0)
         return cudaSuccess;
-    const int G = A.N < 32 ? A.N : 32;
+    int G = A.N < 32 ? A.N : 32;
+    // N = 128 (the 3dx / pi dx lattice ball): two nodes per warp.  PD_EXACT_G
+    // overrides (8, 16, 32) for experiments.
+    if (A.N == 128)
+        G = 16;
+    if (const char* e = std::getenv("PD_EXACT_G")) {
+        const int g = std::atoi(e);
+        if ((g == 8 || g == 16 || g == 32) && A.N == 128)
+            G = g;
+    }
     const int M = A.N / G;
     const long long per_warp = 32 / G;
     const long long warps = (nodes + per_warp - 1) / per_warp;
     const dim3 grid(unsigned((warps * 32 + 255) / 256));
-    return node_sum ? launch_mode<true>(A, mode, M, grid, st)
-                    : launch_mode<false>(A, mode, M, grid, st);
+    if (pmb)
+        return node_sum ? launch_mode<true, true>(A, mode, G, M, grid, st)
+                        : launch_mode<false, true>(A, mode, G, M, grid, st);
+    return node_sum ? launch_mode<true, false>(A, mode, G, M, grid, st)
+                    : launch_mode<false, false>(A, mode, G, M, grid, st);
 }
 
 } // namespace pdb

@@ -223,6 +223,8 @@ struct pd_ctx {
     bool history = false;
     bool has_bc = false;
     int n_laws = 0;
+    bool exact_pmb = false;  // one PMB law: the specialised exact kernel (pd_exact.cu slot_pmb)
+    double exact_c = 0, exact_sc = 0;
     double damping = 0, dt = 0;
     int64_t step = 0;
     int cur = 0;
@@ -356,6 +358,8 @@ struct pd_ctx {
         A.half_dt2 = dt * dt / 2;
         A.dt2 = dt * dt;
         A.damping = damping;
+        A.pmb_c = exact_c;
+        A.pmb_sc = exact_sc;
         A.store_forces = 0;
         A.do_drift = 0;
         A.xfer = world > 1 ? xfer.p : nullptr;
@@ -387,6 +391,9 @@ int upload_laws(pd_ctx* ctx, const pd_damage_model& m) {
     exact_set_laws(laws.data(), m.n_laws, ctx->stream);
     PD_CK(cudaGetLastError());
     ctx->n_laws = m.n_laws;
+    ctx->exact_pmb = m.n_laws == 1 && m.laws[0].n_breakpoints == 1;
+    ctx->exact_c = m.laws[0].stiffness;
+    ctx->exact_sc = m.laws[0].breakpoints[0];
     ctx->damping = m.damping;
     ctx->history = needs_history(m);
     return PD_OK;
@@ -935,7 +942,9 @@ int launch_step(pd_ctx* ctx, DevArgs& A, int mode) {
     else if (ctx->fast)
         PD_CK(launch_fast(A, ctx->fast_args(), mode, ctx->kind, ctx->lay.n_tiles, ctx->stream));
     else
-        PD_CK(launch_exact(A, mode, ctx->variant == PD_NODE_PARALLEL, ctx->stream));
+        PD_CK(launch_exact(A, mode, ctx->variant == PD_NODE_PARALLEL, ctx->exact_pmb && !A.btype &&
+                                                                   !A.lambda && !A.beta,
+                           ctx->stream));
     ctx->kernel = t_last_kernel;
     ++ctx->launches;
     return PD_OK;

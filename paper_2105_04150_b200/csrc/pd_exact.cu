@@ -7,7 +7,8 @@
 // Mapping (one fused launch per time step):
 //   * a group of G lanes owns one node i (G = N for N < 32, 16 for the
 //     N = 128 lattice ball -- two nodes per warp share the per-node prologue
-//     and epilogue -- else 32); lane l owns slots k = l + G*m, m < M = N/G;
+//     and epilogue -- else 32); lane l owns slots k = l + G*m, m < M = N/G
+//     (N <= 1024);
 //   * one PMB law without bond types or corrections (the bench lattice)
 //     takes a specialised slot body with the law in registers (slot_pmb);
 //   * each lane evaluates its slots like bond_contribution (engine.cpp:53-109):
@@ -245,7 +246,7 @@ __global__ void __launch_bounds__(256, PD_EXACT_MINB) exact_step_kernel(DevArgs 
         }
     };
     constexpr int PF = PD_EXACT_PF;
-    constexpr int LOGM = M >= 16 ? 4 : M >= 8 ? 3 : M >= 4 ? 2 : M >= 2 ? 1 : 0;
+    constexpr int LOGM = M >= 32 ? 5 : M >= 16 ? 4 : M >= 8 ? 3 : M >= 4 ? 2 : M >= 2 ? 1 : 0;
     auto bitrev = [](int x) {
         int r = 0;
 #pragma unroll
@@ -357,7 +358,7 @@ cudaError_t launch_gm(const DevArgs& A, dim3 grid, cudaStream_t st) {
 }
 
 // lanes per node: N < 32 -> G = N (M = 1); N = 32, 64 -> G = 32; N = 128 ->
-// G = 16 (two nodes per warp, 8 slots per lane); N = 256 -> G = 32
+// G = 16 (two nodes per warp, 8 slots per lane); N = 256 .. 1024 -> G = 32
 template <int MODE, bool NODE_SUM, bool PMB>
 cudaError_t launch_m(const DevArgs& A, int G, int M, dim3 grid, cudaStream_t st) {
     if (G < 32 && M == 1)
@@ -369,6 +370,8 @@ cudaError_t launch_m(const DevArgs& A, int G, int M, dim3 grid, cudaStream_t st)
     case 16008: return launch_gm<MODE, 16, 8, NODE_SUM, PMB>(A, grid, st);
     case 8016: return launch_gm<MODE, 8, 16, NODE_SUM, PMB>(A, grid, st);
     case 32008: return launch_gm<MODE, 32, 8, NODE_SUM, PMB>(A, grid, st);
+    case 32016: return launch_gm<MODE, 32, 16, NODE_SUM, PMB>(A, grid, st);
+    case 32032: return launch_gm<MODE, 32, 32, NODE_SUM, PMB>(A, grid, st);
     default: return cudaErrorInvalidValue;
     }
 }
@@ -402,6 +405,8 @@ template <int MODE, bool NS, bool PMB> static void preload_ns() {
     preload(exact_step_kernel<MODE, 16, 8, NS, PMB>);
     preload(exact_step_kernel<MODE, 8, 16, NS, PMB>);
     preload(exact_step_kernel<MODE, 32, 8, NS, PMB>);
+    preload(exact_step_kernel<MODE, 32, 16, NS, PMB>);
+    preload(exact_step_kernel<MODE, 32, 32, NS, PMB>);
 }
 
 template <int MODE> static void preload_mode() {

@@ -199,9 +199,11 @@ int bc_validate(const pd_boundary& bc, int64_t n) {
 int group_validate(int64_t N) {
     if (N < 1 || (N & (N - 1)) != 0)
         return fail(PD_E_INVALID_ARGUMENT, "NeighborList: group size must be a power of two");
-    if (N > 256)
+    // the device family builder sorts rows of up to 1024 members
+    // (pd_family.cu); the exact kernel gives each of 32 lanes N / 32 slots
+    if (N > 1024)
         return fail(PD_E_INVALID_ARGUMENT,
-                    "NeighborList: group size %lld exceeds the supported maximum of 256",
+                    "NeighborList: group size %lld exceeds the supported maximum of 1024",
                     (long long)N);
     return PD_OK;
 }

@@ -103,8 +103,8 @@ def test_gpu_random_configs_match_oracle(oracle, seed):
     """numpy analogue of make_random_config at up to 4000 nodes, both variants."""
     p, model, horizon, draws, rng = S.random_config_np(seed, (10, 4000) if seed % 3 == 0 else (10, 500))
     fam = oracle.build_family(p.coords, horizon)
-    if fam.group_size > 256:
-        pytest.skip("group size beyond the supported 256")
+    if fam.group_size > 1024:
+        pytest.skip("group size beyond the supported 1024")
     corr, st0 = S.finish_random_config(p, model, fam, draws, rng)
     hist0 = np.abs(rng.normal(0, 0.02, fam.entries.size)) * (seed % 2)
     for variant in EXACT:
@@ -120,6 +120,34 @@ def test_gpu_random_configs_match_oracle(oracle, seed):
             outs.append((f, st))
         assert same_bits(outs[0][0].body_force, outs[1][0].body_force), variant
         _assert_same_state(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("horizon,group", [(5.2, 1024), (4.2, 512)])
+def test_gpu_large_groups_match_oracle(oracle, horizon, group):
+    """Families beyond 256 members (the reference allows any power of two,
+    types.hpp:63-73): a lattice with a wide horizon, fracturing, both exact
+    variants and the fast variant's tile path, 20 velocity-Verlet steps."""
+    b, h, g = S.bench_lattice_bundle((14, 13, 12), s_c=2e-4, horizon=horizon)
+    fam = oracle.build_family(b.particles.coords, horizon, g.hint())
+    assert fam.group_size == group
+    dev = geometry.build_family(b.particles.coords, horizon, g)
+    assert np.array_equal(dev.entries, fam.entries)
+    u0 = S.seed_displacements(b.particles.coords) * 30.0
+    for variant in EXACT:
+        outs = []
+        for be in (oracle, engine.backend()):
+            st = make_state(fam, False)
+            st.u = u0.copy()
+            be.simulate(b, st, SimulateOptions(20, 0, 0, IntegratorKind.velocity_verlet, variant))
+            outs.append(st)
+        _assert_same_state(outs[0], outs[1])
+        assert int(fam.n_neigh.sum() - outs[1].connectivity.n_neigh.sum()) > 0
+    st = make_state(fam, False)
+    st.u = u0.copy()
+    engine.simulate(b, st, SimulateOptions(20, 0, 0, IntegratorKind.velocity_verlet,
+                                           KernelVariant.fast))
+    scale = np.abs(outs[0].u).max()
+    assert np.abs(st.u - outs[0].u).max() <= 5e-3 * scale
 
 
 def _plate(oracle, nx=40, ny=40, nz=4, steps=120):

@@ -18,6 +18,7 @@
 #include <chrono>
 #include <condition_variable>
 #include <cstring>
+#include <memory>
 #include <deque>
 #include <mutex>
 #include <thread>
@@ -129,6 +130,22 @@ bool needs_history(const pd_damage_model& m) {
         if (m.laws[k].n_breakpoints > 1)
             return true;
     return false;
+}
+
+// fn(b, e) over [0, n) in chunks on several host threads
+template <class Fn> void par_for(int64_t n, Fn fn) {
+    const int64_t parts = std::min<int64_t>(std::max(1u, std::thread::hardware_concurrency()),
+                                            n / (int64_t(1) << 16) + 1);
+    if (parts <= 1) {
+        fn(int64_t(0), n);
+        return;
+    }
+    std::vector<std::thread> th;
+    const int64_t step = (n + parts - 1) / parts;
+    for (int64_t p = 0; p < parts; ++p)
+        th.emplace_back([&, p] { fn(p * step, std::min(n, (p + 1) * step)); });
+    for (auto& t : th)
+        t.join();
 }
 
 // true when pred(k) holds for some k in [0, n): chunks on several host threads
@@ -645,19 +662,30 @@ int download(pd_ctx* ctx, pd_state* st, pd_force_field* forces, int32_t fields) 
                 PD_CK(cudaMemcpyAsync(&m, ctx->counter.p, sizeof m, cudaMemcpyDeviceToHost, s));
                 PD_CK(cudaStreamSynchronize(s));
                 ctx->launches += 1;
-                if (m > 0) {
+                if (m > 0 && 4 * (long long)m > n) {
+                    // most rows changed (a fracturing run): the whole array in
+                    // one pinned, multi-threaded copy beats a gather + scatter
+                    PD_CK(d2h_large(st->connectivity.entries, ctx->scratch_i32.p,
+                                    sizeof(int32_t) * slots, s));
+                } else if (m > 0) {
                     DevBuf<int32_t> rows;
-                    PD_CK(rows.alloc(size_t(m) * size_t(ctx->N)));
+                    const size_t N = size_t(ctx->N);
+                    PD_CK(rows.alloc(size_t(m) * N));
                     launch_gather_list_rows(ctx->scratch_i32.p, ctx->scratch_n.p, (long long)m,
                                             ctx->N, rows.p, s);
                     ++ctx->launches;
-                    std::vector<int> list(static_cast<size_t>(m));
-                    std::vector<int32_t> host_rows(size_t(m) * size_t(ctx->N));
-                    PD_CK(d2h_large(list.data(), ctx->scratch_n.p, sizeof(int) * m, s));
-                    PD_CK(d2h_large(host_rows.data(), rows.p, sizeof(int32_t) * host_rows.size(), s));
-                    for (size_t r = 0; r < list.size(); ++r)
-                        std::memcpy(st->connectivity.entries + size_t(list[r]) * size_t(ctx->N),
-                                    host_rows.data() + r * size_t(ctx->N), sizeof(int32_t) * ctx->N);
+                    std::unique_ptr<int[]> list(new int[size_t(m)]);
+                    std::unique_ptr<int32_t[]> host_rows(new int32_t[size_t(m) * N]);  // no zero fill
+                    PD_CK(d2h_large(list.get(), ctx->scratch_n.p, sizeof(int) * m, s));
+                    PD_CK(d2h_large(host_rows.get(), rows.p, sizeof(int32_t) * size_t(m) * N, s));
+                    int32_t* dst = st->connectivity.entries;
+                    const int32_t* src = host_rows.get();
+                    const int* rl = list.get();
+                    par_for((int64_t)m, [&](int64_t b, int64_t e) {
+                        for (int64_t r = b; r < e; ++r)
+                            std::memcpy(dst + size_t(rl[r]) * N, src + size_t(r) * N,
+                                        sizeof(int32_t) * N);
+                    });
                 }
             } else {
                 PD_CK(d2h_large(st->connectivity.entries, ctx->scratch_i32.p,

@@ -199,6 +199,8 @@ LAT_KERNELS = {  # PD_LAT_CFG -> the instantiation it selects on a 20x18x26 latt
     "4": "lattice_step_kernel<1,4,5,0,0>",  # 16x4x4 bricks at 5 CTAs/SM
     "5": "lattice_step_kernel<1,1,1,0,0>",  # the small-brick latency variant, forced
     "6": "lattice_step_kernel<1,4,6,0,0>",  # large-model rule without the waste test
+    "9": "lattice_step_kernel<1,9,2,0,0>",  # 16x4x9 bricks (27-plane slabs of 216 / 8 GPUs)
+    "10": "lattice_step_kernel<1,9,3,0,0>",  # 16x4x9 bricks at 3 CTAs/SM
 }
 
 

@@ -253,6 +253,8 @@ MESHES = {
     "lattice": "cubic lattice (the reference bench fixture)",
     "jitter": "irregular mesh: the same lattice with every coordinate jittered by a seeded "
               "uniform +-0.2 spacing (rows of 90-150 neighbours; the general tile kernel)",
+    "shuffled": "the jittered mesh with its nodes numbered in a seeded random order (no "
+                "spatial coherence in the input numbering)",
 }
 
 
@@ -271,9 +273,12 @@ def build_workload(counts, law="pmb", mesh="lattice"):
     from paper_2105_04150_b200 import geometry, make_state
     from paper_2105_04150_b200.types import DamageLaw
     bundle, h, g = S.bench_lattice_bundle(counts, s_c=S_C[law])
-    if mesh == "jitter":
+    if mesh in ("jitter", "shuffled"):
         bundle.particles.coords = jitter_coords(bundle.particles.coords)
         g = None
+    if mesh == "shuffled":
+        order = np.random.default_rng(7).permutation(bundle.particles.size())
+        bundle.particles.coords = bundle.particles.coords.reshape(-1, 3)[order].reshape(-1)
     if law == "trilinear":
         bundle.model.laws = [DamageLaw.trilinear(1.0, 1e-3, 2e-3, 1e6)]
     elif law == "multi":
@@ -385,7 +390,8 @@ def run_reference_arm(args):
 def _summary(args, value, ms_step, world, n, N, live, bytes_step, achieved, e2e, launches,
              clocks, cpu, variant_name, probe=None, extra_config=None):
     peak, peak_kind = measured_peaks()
-    mesh = "lattice" if args.mesh == "lattice" else "jittered lattice (irregular mesh)"
+    mesh = {"lattice": "lattice", "jitter": "jittered lattice (irregular mesh)",
+            "shuffled": "jittered lattice, randomly numbered (irregular mesh)"}[args.mesh]
     cfg = {"workload": f"cfg4 {mesh} {args.size}^3 = {n} nodes, delta=3dx (N={N}), "
                        f"{LAWS[args.law]}, velocity-Verlet, dt=1e-3, seeded u"
                        + (f", {world} z-slabs" if world > 1 else ""),

@@ -437,9 +437,10 @@ __global__ void gather_rows_kernel(const T* in, T* out, const int* map, long lon
 }
 
 // Per original row: rebuild entries (-1 where broken) and fp64 history from
-// the compact tile layout (live slots in slot order).
-__global__ void fast_materialize_kernel(const int32_t* entries0, const int* inv,
-                                        const int* tile_of, const int* tile_start,
+// the compact tile layout (live slots in slot order, or -- Morton tiles, with
+// origk -- in halo-record order, origk naming each slot's original position).
+__global__ void fast_materialize_kernel(const unsigned short* origk, const int32_t* entries0,
+                                        const int* inv, const int* tile_of, const int* tile_start,
                                         const long long* slot_off, int T,
                                         const unsigned short* lidx, const float* hist32,
                                         long long n, int N, int32_t* entries_out,
@@ -460,6 +461,24 @@ __global__ void fast_materialize_kernel(const int32_t* entries0, const int* inv,
     }
     const int t = ii - tile_start[tile];
     const long long base = slot_off[tile] + (long long)t * 8;
+    if (origk) {
+        int L = 0;
+        for (int k = 0; k < N; ++k) {
+            const int32_t e = entries0[i * N + k];
+            if (entries_out)
+                entries_out[i * N + k] = e < 0 ? -1 : e;
+            L += e >= 0;
+        }
+        for (int c = 0; c < L; ++c) {
+            const long long s = base + (long long)(c >> 3) * T * 8 + (c & 7);
+            const int k = origk[s];
+            if (entries_out && lidx[s] == 0)
+                entries_out[i * N + k] = -1;
+            if (hist_out && hist32)
+                hist_out[i * N + k] = double(hist32[s]);
+        }
+        return;
+    }
     int c = 0;
     for (int k = 0; k < N; ++k) {
         const int32_t e = entries0[i * N + k];
@@ -547,13 +566,14 @@ template void launch_gather_rows<int32_t, 1>(const int32_t*, int32_t*, const int
 template void launch_gather_rows<uint8_t, 3>(const uint8_t*, uint8_t*, const int*, long long,
                                              cudaStream_t);
 
-void launch_fast_materialize(const int32_t* entries0, const int* inv, const int* tile_of,
+void launch_fast_materialize(const unsigned short* origk, const int32_t* entries0, const int* inv,
+                             const int* tile_of,
                              const int* tile_start, const long long* slot_off, int T,
                              const unsigned short* lidx, const float* hist32, long long n, int N,
                              int32_t* entries_out, double* hist_out, cudaStream_t st) {
     if (n > 0)
         fast_materialize_kernel<<<unsigned((n + 127) / 128), 128, 0, st>>>(
-            entries0, inv, tile_of, tile_start, slot_off, T, lidx, hist32, n, N, entries_out,
+            origk, entries0, inv, tile_of, tile_start, slot_off, T, lidx, hist32, n, N, entries_out,
             hist_out);
 }
 

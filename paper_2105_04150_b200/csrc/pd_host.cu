@@ -642,7 +642,7 @@ int download(pd_ctx* ctx, pd_state* st, pd_force_field* forces, int32_t fields) 
                                                  ctx->own_end, n, ctx->N, ctx->lat,
                                                  ctx->scratch_i32.p, nullptr, s));
             else if (ctx->fast)
-                launch_fast_materialize(ctx->entries.p, ctx->lay.inv.p, ctx->lay.tile_of.p,
+                launch_fast_materialize(ctx->lay.origk.p, ctx->entries.p, ctx->lay.inv.p, ctx->lay.tile_of.p,
                                         ctx->lay.tile_start.p, ctx->lay.slot_off.p, ctx->fast_T, ctx->lay.lidx.p,
                                         nullptr, n, ctx->N, ctx->scratch_i32.p, nullptr, s);
             else
@@ -711,7 +711,7 @@ int download(pd_ctx* ctx, pd_state* st, pd_force_field* forces, int32_t fields) 
                                              ctx->hist.p, s));
             ++ctx->launches;
         } else if (ctx->history && ctx->permuted()) {
-            launch_fast_materialize(ctx->entries.p, ctx->lay.inv.p, ctx->lay.tile_of.p, ctx->lay.tile_start.p,
+            launch_fast_materialize(ctx->lay.origk.p, ctx->entries.p, ctx->lay.inv.p, ctx->lay.tile_of.p, ctx->lay.tile_start.p,
                                     ctx->lay.slot_off.p, ctx->fast_T, ctx->lay.lidx.p, ctx->lay.hist32.p, n,
                                     ctx->N, nullptr, ctx->hist.p, s);
             ++ctx->launches;
@@ -1435,7 +1435,7 @@ int pd_ctx_save_state(pd_ctx* ctx, const char* path) {
                                          ctx->own_end, n, ctx->N, ctx->lat, ctx->scratch_i32.p,
                                          nullptr, s));
     else if (ctx->fast)
-        launch_fast_materialize(ctx->entries.p, ctx->lay.inv.p, ctx->lay.tile_of.p,
+        launch_fast_materialize(ctx->lay.origk.p, ctx->entries.p, ctx->lay.inv.p, ctx->lay.tile_of.p,
                                 ctx->lay.tile_start.p, ctx->lay.slot_off.p, ctx->fast_T,
                                 ctx->lay.lidx.p, nullptr, n, ctx->N, ctx->scratch_i32.p, nullptr, s);
     else
@@ -1459,7 +1459,7 @@ int pd_ctx_save_state(pd_ctx* ctx, const char* path) {
                                              ctx->own_end, n, ctx->N, ctx->lat, nullptr,
                                              ctx->hist.p, s));
         else if (ctx->permuted())
-            launch_fast_materialize(ctx->entries.p, ctx->lay.inv.p, ctx->lay.tile_of.p,
+            launch_fast_materialize(ctx->lay.origk.p, ctx->entries.p, ctx->lay.inv.p, ctx->lay.tile_of.p,
                                     ctx->lay.tile_start.p, ctx->lay.slot_off.p, ctx->fast_T,
                                     ctx->lay.lidx.p, ctx->lay.hist32.p, n, ctx->N, nullptr,
                                     ctx->hist.p, s);

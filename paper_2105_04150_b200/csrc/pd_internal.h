@@ -105,6 +105,7 @@ struct FastLayoutDev {
     long long total_slots = 0;
     DevBuf<int> perm, inv, tile_of, tile_start, kmax8, wgroups, halo, nf_start;
     DevBuf<unsigned short> own_slot, lidx;
+    DevBuf<unsigned short> origk;  // Morton tiles: a compact slot's position in the original row
     DevBuf<long long> halo_off, slot_off;
     DevBuf<float> hist32, lambda32, beta32;
     DevBuf<uint8_t> btype_c;
@@ -132,7 +133,8 @@ cudaError_t launch_fast(const DevArgs& A, const FastDev& F, int mode, int kind, 
                         cudaStream_t st);
 template <class T, int W>
 void launch_gather_rows(const T* in, T* out, const int* map, long long n, cudaStream_t st);
-void launch_fast_materialize(const int32_t* entries0, const int* inv, const int* tile_of,
+void launch_fast_materialize(const unsigned short* origk, const int32_t* entries0, const int* inv,
+                             const int* tile_of,
                              const int* tile_start, const long long* slot_off, int T,
                              const unsigned short* lidx, const float* hist32, long long n, int N,
                              int32_t* entries_out, double* hist_out, cudaStream_t st);

@@ -146,6 +146,45 @@ __global__ void brick_key_kernel(const double4* xv, long long begin, long long c
     vals[k] = int(i);
 }
 
+// lexicographic key of a node's mean-spacing cell (z, y, x): the order a
+// lattice's reference numbering has, computed from the coordinates so Morton
+// tiles get it whatever the input numbering
+__global__ void lex_key_kernel(const double4* xv, long long n, BrickGrid g,
+                               unsigned long long* keys, int* vals) {
+    const long long i = blockIdx.x * (long long)TPB + threadIdx.x;
+    if (i >= n)
+        return;
+    const double4 x = xv[i];
+    const double c3[3] = {x.x, x.y, x.z};
+    unsigned long long q[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        const double v = floor((c3[d] - g.lo[d]) * g.inv_h);
+        q[d] = v < 0 ? 0ull : (v > 2097151.0 ? 2097151ull : (unsigned long long)v);
+    }
+    keys[i] = (q[2] << 42) | (q[1] << 21) | q[0];
+    vals[i] = int(i);
+}
+
+__global__ void rank_kernel(const int* sorted_ids, long long n, int* rank) {
+    const long long r = blockIdx.x * (long long)TPB + threadIdx.x;
+    if (r < n)
+        rank[sorted_ids[r]] = int(r);
+}
+
+__global__ void tile_lex_key_kernel(const int* perm, const int* tile_of, const int* lexrank,
+                                    long long n_own, unsigned long long* keys) {
+    const long long ii = blockIdx.x * (long long)TPB + threadIdx.x;
+    if (ii < n_own)
+        keys[ii] = ((unsigned long long)tile_of[ii] << 32) | (unsigned)lexrank[perm[ii]];
+}
+
+__global__ void compose_kernel(const int* inv, const int* sorted_ids, long long n, int* out) {
+    const long long r = blockIdx.x * (long long)TPB + threadIdx.x;
+    if (r < n)
+        out[r] = inv[sorted_ids[r]];
+}
+
 // perm[n_own + k] = k-th ghost (local order); inv = perm^-1
 __global__ void perm_tail_kernel(int* perm, long long n, long long own_begin, long long own_end) {
     const long long k = blockIdx.x * (long long)TPB + threadIdx.x;
@@ -272,6 +311,7 @@ struct SlotArgs {
     int N, T;
     unsigned short* lidx;
     unsigned short* own_slot;
+    unsigned short* origk;
     int* wgroups;
     float* hist32;
     uint8_t* btype_c;
@@ -299,6 +339,8 @@ __global__ void slot_kernel(SlotArgs S) {
         const long long pos = lower_bound_u64(S.hk, h0, h1, pair_key(t, S.nofail, S.inv, j)) - h0;
         const long long s = base + (long long)(c >> 3) * S.T * 8 + (c & 7);
         S.lidx[s] = (unsigned short)(pos + 1);
+        if (S.origk)
+            S.origk[s] = (unsigned short)k;
         if (S.hist32)
             S.hist32[s] = S.hist ? float(S.hist[idx]) : 0.f;
         if (S.btype_c)
@@ -312,6 +354,81 @@ __global__ void slot_kernel(SlotArgs S) {
     // per warp of tile threads: the 8-slot groups its longest row needs
     if (c > 0)
         atomicMax(S.wgroups + (long long)t * (S.T / 32) + (ii - S.tile_start[t]) / 32, (c + 7) / 8);
+}
+
+// Morton tiles: each node's compact slots re-ordered by halo record index, so
+// that at one slot the 32 lanes of a warp (Morton-consecutive nodes) read
+// records that sit close together in shared memory -- rows in the reference
+// order against a Morton-ordered halo scatter them over the banks (2x the
+// shared-memory wavefronts on a jittered lattice).  One warp per node: keys
+// (record << 10 | compact slot) bitonic-sorted in shared memory, then every
+// per-slot array gathered from a copy of the unsorted layout.
+struct SortArgs {
+    const int* live;  // compact row length + 1, per owned node (internal order)
+    const int* tile_of;
+    const int* tile_start;
+    const long long* slot_off;
+    long long n_own;
+    int T;
+    const unsigned short *lidx0, *origk0;
+    const float *hist0, *lambda0, *beta0;
+    const uint8_t* btype0;
+    unsigned short *lidx, *origk;
+    float *hist, *lambda, *beta;
+    uint8_t* btype;
+};
+
+constexpr int SORT_WARPS = 4;
+constexpr int SORT_MAX = 1024;
+
+__global__ void __launch_bounds__(SORT_WARPS * 32) sort_rows_kernel(SortArgs S) {
+    __shared__ unsigned keys[SORT_WARPS][SORT_MAX];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long ii = blockIdx.x * (long long)SORT_WARPS + w;
+    if (ii >= S.n_own)
+        return;
+    const int L = S.live[ii] - 1;
+    if (L <= 1)
+        return;
+    const int t = S.tile_of[ii];
+    const long long base = S.slot_off[t] + (long long)(ii - S.tile_start[t]) * 8;
+    auto slot = [&](int c) { return base + (long long)(c >> 3) * S.T * 8 + (c & 7); };
+    int P = 32;
+    while (P < L)
+        P <<= 1;
+    unsigned* k = keys[w];
+    for (int c = lane; c < P; c += 32)
+        k[c] = c < L ? (unsigned(S.lidx0[slot(c)]) << 10) | unsigned(c) : 0xffffffffu;
+    __syncwarp();
+    for (int size = 2; size <= P; size <<= 1)
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int c = lane; c < P; c += 32) {
+                const int o = c ^ stride;
+                if (o > c) {
+                    const bool up = (c & size) == 0;
+                    const unsigned a = k[c], b = k[o];
+                    if ((a > b) == up) {
+                        k[c] = b;
+                        k[o] = a;
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    for (int r = lane; r < L; r += 32) {
+        const int c = int(k[r] & 1023u);
+        const long long sn = slot(r), so = slot(c);
+        S.lidx[sn] = S.lidx0[so];
+        S.origk[sn] = S.origk0[so];
+        if (S.hist)
+            S.hist[sn] = S.hist0[so];
+        if (S.btype)
+            S.btype[sn] = S.btype0[so];
+        if (S.lambda)
+            S.lambda[sn] = S.lambda0[so];
+        if (S.beta)
+            S.beta[sn] = S.beta0[so];
+    }
 }
 
 template <class T> __global__ void fill_kernel(T* p, long long n, T v) {
@@ -476,14 +593,55 @@ cudaError_t gpu_build_layout(FastLayoutDev& L, const FastLayoutIn& in, int* erro
     LY_CK(cudaMemsetAsync(L.tile_of.p, 0xff, sizeof(int) * size_t(n), s));
     if (tiles > 0)
         tile_of_kernel<<<unsigned(tiles), TPB, 0, s>>>(L.tile_start.p, tiles, L.tile_of.p);
+    // Morton tiles: order each tile's nodes, and every halo, lexicographically
+    // by mean-spacing cell (lexrank), as a lattice's reference numbering is,
+    // so a warp's nodes are x-runs and the records its lanes read at one slot
+    // sit side by side in shared memory (rows are then sorted by record,
+    // sort_rows_kernel)
+    int *lexrank = nullptr, *lex_ids = nullptr, *lex_to_internal = nullptr;
+    if (g.morton && n > 0) {
+        unsigned long long *lk, *lk_sorted;
+        int* iota;
+        LY_CK(tmp.get(&lk, size_t(n)));
+        LY_CK(tmp.get(&lk_sorted, size_t(n)));
+        LY_CK(tmp.get(&iota, size_t(n)));
+        LY_CK(tmp.get(&lex_ids, size_t(n)));
+        LY_CK(tmp.get(&lexrank, size_t(n)));
+        LY_CK(tmp.get(&lex_to_internal, size_t(n)));
+        lex_key_kernel<<<blocks_for(n), TPB, 0, s>>>(in.xv, n, g, lk, iota);
+        size_t need = 0;
+        LY_CK(cub::DeviceRadixSort::SortPairs(nullptr, need, lk, lk_sorted, iota, lex_ids, int(n),
+                                              0, 63, s));
+        LY_CK(cub_reserve(need));
+        LY_CK(cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, lk, lk_sorted, iota, lex_ids,
+                                              int(n), 0, 63, s));
+        rank_kernel<<<blocks_for(n), TPB, 0, s>>>(lex_ids, n, lexrank);
+        if (n_own > 0) {
+            int* perm2;
+            LY_CK(tmp.get(&perm2, size_t(n_own)));
+            tile_lex_key_kernel<<<blocks_for(n_own), TPB, 0, s>>>(L.perm.p, L.tile_of.p, lexrank,
+                                                                 n_own, lk);
+            const int kb = 32 + bits_for((unsigned long long)std::max(tiles, 1));
+            need = 0;
+            LY_CK(cub::DeviceRadixSort::SortPairs(nullptr, need, lk, lk_sorted, L.perm.p, perm2,
+                                                  int(n_own), 0, kb, s));
+            LY_CK(cub_reserve(need));
+            LY_CK(cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, lk, lk_sorted, L.perm.p,
+                                                  perm2, int(n_own), 0, kb, s));
+            LY_CK(cudaMemcpyAsync(L.perm.p, perm2, sizeof(int) * size_t(n_own),
+                                  cudaMemcpyDeviceToDevice, s));
+        }
+    }
     if (n > n_own)
         perm_tail_kernel<<<blocks_for(n - n_own), TPB, 0, s>>>(L.perm.p, n, ob, oe);
     inv_kernel<<<blocks_for(n), TPB, 0, s>>>(L.perm.p, n, L.inv.p);
+    if (g.morton && n > 0)
+        compose_kernel<<<blocks_for(n), TPB, 0, s>>>(L.inv.p, lex_ids, n, lex_to_internal);
     LY_CK(cudaGetLastError());
 
-    // halo order: reference ids on bricks, internal ids on Morton tiles
-    const int* halo_key_inv = g.morton ? L.inv.p : nullptr;  // key -> order id map
-    const int* halo_by_ref = g.morton ? nullptr : L.inv.p;     // order id -> internal id
+    // halo order: reference ids on bricks, lexicographic cell rank on Morton tiles
+    const int* halo_key_inv = g.morton ? lexrank : nullptr;            // key -> order id
+    const int* halo_by_ref = g.morton ? lex_to_internal : L.inv.p;     // order id -> internal id
 
     // ---- 2. slot offsets -------------------------------------------------
     int *live, *kmax;
@@ -632,9 +790,59 @@ cudaError_t gpu_build_layout(FastLayoutDev& L, const FastLayoutIn& in, int* erro
     LY_CK(L.wgroups.alloc(size_t(std::max(tiles, 1)) * size_t(T / 32)));
     LY_CK(cudaMemsetAsync(L.wgroups.p, 0, sizeof(int) * size_t(std::max(tiles, 1)) * size_t(T / 32), s));
     S.wgroups = L.wgroups.p;
+    if (g.morton) {
+        LY_CK(L.origk.alloc(size_t(std::max(slots, 1LL))));
+        S.origk = L.origk.p;
+    } else {
+        L.origk.release();
+    }
     if (n_own > 0)
         slot_kernel<<<blocks_for(n_own), TPB, 0, s>>>(S);
     LY_CK(cudaGetLastError());
+    if (g.morton && n_own > 0 && slots > 0) {
+        // rows by halo record (sort_rows_kernel): sort from copies of the
+        // unsorted per-slot arrays
+        const size_t ns = size_t(slots);
+        unsigned short *lidx0, *origk0;
+        LY_CK(tmp.get(&lidx0, ns));
+        LY_CK(tmp.get(&origk0, ns));
+        LY_CK(cudaMemcpyAsync(lidx0, L.lidx.p, 2 * ns, cudaMemcpyDeviceToDevice, s));
+        LY_CK(cudaMemcpyAsync(origk0, L.origk.p, 2 * ns, cudaMemcpyDeviceToDevice, s));
+        SortArgs R{};
+        R.live = live;
+        R.tile_of = L.tile_of.p;
+        R.tile_start = L.tile_start.p;
+        R.slot_off = L.slot_off.p;
+        R.n_own = n_own;
+        R.T = T;
+        R.lidx0 = lidx0;
+        R.origk0 = origk0;
+        R.lidx = L.lidx.p;
+        R.origk = L.origk.p;
+        auto copy_f = [&](float* a, const float** a0, float** out) -> cudaError_t {
+            if (!a)
+                return cudaSuccess;
+            float* c0;
+            cudaError_t e = tmp.get(&c0, ns);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(c0, a, 4 * ns, cudaMemcpyDeviceToDevice, s);
+            *a0 = c0;
+            *out = a;
+            return e;
+        };
+        LY_CK(copy_f(L.hist32.p, &R.hist0, &R.hist));
+        LY_CK(copy_f(L.lambda32.p, &R.lambda0, &R.lambda));
+        LY_CK(copy_f(L.beta32.p, &R.beta0, &R.beta));
+        if (L.btype_c.p) {
+            uint8_t* b0;
+            LY_CK(tmp.get(&b0, ns));
+            LY_CK(cudaMemcpyAsync(b0, L.btype_c.p, ns, cudaMemcpyDeviceToDevice, s));
+            R.btype0 = b0;
+            R.btype = L.btype_c.p;
+        }
+        sort_rows_kernel<<<unsigned((n_own + SORT_WARPS - 1) / SORT_WARPS), SORT_WARPS * 32, 0, s>>>(R);
+        LY_CK(cudaGetLastError());
+    }
     L.inv_host.resize(size_t(n));
     LY_CK(cudaMemcpyAsync(L.inv_host.data(), L.inv.p, sizeof(int) * size_t(n),
                           cudaMemcpyDeviceToHost, s));

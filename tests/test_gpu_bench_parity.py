@@ -249,3 +249,24 @@ def test_collapsed_bond_kept_with_zero_force(monkeypatch, layout, law):
     assert fast.connectivity.entries[i * N + k] == j
     assert np.array_equal(ref.connectivity.entries, fast.connectivity.entries)
     assert max_rel_difference(ref.a, fast.a) <= FORCE_TOL
+
+
+@pytest.mark.parametrize("law", ["pmb", "trilinear"])
+def test_resynced_fracture_jittered_mesh(monkeypatch, law):
+    """An irregular mesh (the lattice jittered by +-0.2 h, 36 x 32 x 30): Morton
+    tiles with rows re-ordered by halo record (pd_layout.cu sort_rows_kernel),
+    20 fracturing velocity-Verlet steps, every step from the exact state; the
+    downloads go through the permuted-row materialisation."""
+    from paper_2105_04150_b200.types import DamageLaw
+    b, h, g = S.bench_lattice_bundle((36, 32, 30), s_c=1.5e-5)
+    b.particles.coords = b.particles.coords + np.random.default_rng(4).uniform(
+        -0.2, 0.2, b.particles.coords.shape)
+    if law == "trilinear":
+        b.model.laws = [DamageLaw.trilinear(1.0, 5e-6, 1e-5, 2e-5)]
+    fam = geometry.build_family(b.particles.coords, h)
+    st0 = make_state(fam, law == "trilinear")
+    st0.u = S.seed_displacements(b.particles.coords) * 3.0
+    nd, err, broken = _resynced(b, fam, st0, IntegratorKind.velocity_verlet, 20, {},
+                                monkeypatch, "fast_step")
+    print(f"jittered {law}: {broken} broken over 20 steps, {nd} slot differences within eps, "
+          f"worst force error {err:.2e}")

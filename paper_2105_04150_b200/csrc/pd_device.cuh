@@ -112,7 +112,9 @@ __device__ __forceinline__ void push_ghost(const DevArgs& A, long long i, const 
 
 // RampProfile::scale/rate/accel (types.cpp:119-169); same operation order, so
 // with FMA contraction disabled the device values equal the host's bit for bit.
-__device__ __forceinline__ double ramp_scale(const DevRamp& r, long long step) {
+// Not inlined: only boundary-condition node-axes call them, and three inlined
+// axes of fp64 divisions cost the unrolled kernels ~9 KB of instruction cache.
+static __device__ __noinline__ double ramp_scale(const DevRamp& r, long long step) {
     if (r.kind == PD_RAMP_CONSTANT)
         return r.target;
     if (r.rise <= 0 || step >= r.rise)
@@ -125,7 +127,7 @@ __device__ __forceinline__ double ramp_scale(const DevRamp& r, long long step) {
     return __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(r.target, t), t), t), inner);
 }
 
-__device__ __forceinline__ double ramp_rate(const DevRamp& r, long long step) {
+static __device__ __noinline__ double ramp_rate(const DevRamp& r, long long step) {
     if (r.kind == PD_RAMP_CONSTANT)
         return 0.0;
     if (r.rise <= 0 || step >= r.rise)
@@ -142,7 +144,7 @@ __device__ __forceinline__ double ramp_rate(const DevRamp& r, long long step) {
     return __ddiv_rn(x, (double)r.rise);
 }
 
-__device__ __forceinline__ double ramp_accel(const DevRamp& r, long long step) {
+static __device__ __noinline__ double ramp_accel(const DevRamp& r, long long step) {
     if (r.kind != PD_RAMP_QUINTIC)
         return 0.0;
     if (r.rise <= 0 || step >= r.rise)

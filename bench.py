@@ -80,24 +80,31 @@ class ClockSampler:
         except Exception:
             return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
 
-    def _nvml_loop(self, nv, h):
-        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+    def _nvml_sample(self, nv, h, mx):
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        self.samples.append((float(sm), float(mx),
+                             {k for k, b in self.REASONS.items() if bits & b}))
+
+    def _nvml_loop(self, nv, h, mx):
         while not self.stop.is_set():
             try:
-                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self._nvml_sample(nv, h, mx)
             except Exception:
                 break
-            self.samples.append((float(sm), float(mx),
-                                 {k for k, b in self.REASONS.items() if bits & b}))
+            self.live.set()
             time.sleep(0.002)
 
     def __enter__(self):
         try:
             nv, h = self._nvml_handle()
-            self.t = threading.Thread(target=self._nvml_loop, args=(nv, h), daemon=True)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            self._nv = (nv, h, mx)
+            self.t = threading.Thread(target=self._nvml_loop, args=(nv, h, mx), daemon=True)
             self.source = "nvml"
+            self.live = threading.Event()
             self.t.start()
+            self.live.wait(timeout=1.0)  # the sampler is running before the timed region
             return self
         except Exception:
             pass

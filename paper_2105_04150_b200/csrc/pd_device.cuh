@@ -114,7 +114,12 @@ __device__ __forceinline__ void push_ghost(const DevArgs& A, long long i, const 
 // with FMA contraction disabled the device values equal the host's bit for bit.
 // Not inlined: only boundary-condition node-axes call them, and three inlined
 // axes of fp64 divisions cost the unrolled kernels ~9 KB of instruction cache.
-static __device__ __noinline__ double ramp_scale(const DevRamp& r, long long step) {
+#ifdef PD_RAMP_INLINE
+#define PD_RAMP_FN __forceinline__
+#else
+#define PD_RAMP_FN __noinline__
+#endif
+static __device__ PD_RAMP_FN double ramp_scale(const DevRamp& r, long long step) {
     if (r.kind == PD_RAMP_CONSTANT)
         return r.target;
     if (r.rise <= 0 || step >= r.rise)
@@ -127,7 +132,7 @@ static __device__ __noinline__ double ramp_scale(const DevRamp& r, long long ste
     return __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(r.target, t), t), t), inner);
 }
 
-static __device__ __noinline__ double ramp_rate(const DevRamp& r, long long step) {
+static __device__ PD_RAMP_FN double ramp_rate(const DevRamp& r, long long step) {
     if (r.kind == PD_RAMP_CONSTANT)
         return 0.0;
     if (r.rise <= 0 || step >= r.rise)
@@ -144,7 +149,7 @@ static __device__ __noinline__ double ramp_rate(const DevRamp& r, long long step
     return __ddiv_rn(x, (double)r.rise);
 }
 
-static __device__ __noinline__ double ramp_accel(const DevRamp& r, long long step) {
+static __device__ PD_RAMP_FN double ramp_accel(const DevRamp& r, long long step) {
     if (r.kind != PD_RAMP_QUINTIC)
         return 0.0;
     if (r.rise <= 0 || step >= r.rise)

@@ -10,7 +10,7 @@ cfg4 is bench.py's default line.  cfg5's law set (several laws chosen by bond ty
 
 GPU: the fast and exact variants of one simulate() call (host buffers in, state out), after
 one untimed call.  Reference: the unmodified reference (oracle/_ref) on all host cores.
-Writes one JSON object (stdout, and gpurun_out/r01_configs.json when --save is given;
+Writes one JSON object (stdout, and gpurun_out/r02_configs.json when --save is given;
 profiles/r01_configs.json is a copy).
 """
 import json

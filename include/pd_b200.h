@@ -36,7 +36,7 @@ extern "C" {
 #endif
 
 #define PD_ABI_VERSION 1
-#define PD_MAX_BREAKPOINTS 8 /* per law; the reference allows any count (types.hpp:86) */
+#define PD_MAX_BREAKPOINTS 32 /* per law (the reference allows any count, types.hpp:86); the fast variant takes <= 8 */
 #define PD_MAX_LAWS 256      /* bond_type is uint8 (types.hpp:71) */
 
 /* Status codes.  Each maps to the exception type the reference throws. */

@@ -11,7 +11,7 @@ import os
 
 import numpy as np
 
-PD_MAX_BREAKPOINTS = 8
+PD_MAX_BREAKPOINTS = 32
 PD_MAX_LAWS = 256
 
 PD_OK = 0

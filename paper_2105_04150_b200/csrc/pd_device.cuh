@@ -76,6 +76,7 @@ struct DevArgs {
     double dt2;               // dt * dt
     double damping;
     double pmb_c, pmb_sc;     // the single-PMB-law model (exact kernel specialisation)
+    const DevLaw* laws;       // the law table (exact kernel)
     int store_forces;
     int do_drift;             // VV: produce next step's drifted u into u_out
     // multi-GPU slabs: owned nodes that are ghosts on the neighbouring ranks

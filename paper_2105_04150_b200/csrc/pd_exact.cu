@@ -35,12 +35,6 @@
 
 namespace pdb {
 
-__constant__ DevLaw c_laws[PD_MAX_LAWS];
-
-void exact_set_laws(const DevLaw* laws, int n, cudaStream_t stream) {
-    cudaMemcpyToSymbolAsync(c_laws, laws, sizeof(DevLaw) * size_t(n), 0,
-                            cudaMemcpyHostToDevice, stream);
-}
 
 namespace {
 
@@ -96,7 +90,9 @@ __device__ __forceinline__ Contribution slot_contribution(const DevArgs& A, long
     const double cur_len = norm3(cx, cy, cz);
     const double s = __ddiv_rn(__dsub_rn(cur_len, ref_len), ref_len);
 
-    const DevLaw& law = c_laws[A.btype ? int(__ldg(A.btype + idx)) : 0];
+    // the law table lives in global memory (up to 256 laws of 32 breakpoints:
+    // too large for the constant bank); a warp's reads of one type broadcast
+    const DevLaw& law = A.laws[A.btype ? int(__ldg(A.btype + idx)) : 0];
     double f;
     const bool no_fail = i_no_fail || uj.w != 0.0;
     if (no_fail) {

@@ -255,6 +255,7 @@ struct pd_ctx {
     DevBuf<uint8_t> btype, bc_kind, bc_ramp, nofail;
     DevBuf<double> bc_mag, scratch_f64;
     DevBuf<DevRamp> ramps;
+    DevBuf<DevLaw> laws;  // the exact kernel's law table
     DevBuf<long long> err, tip_offsets, tip_nodes;
     DevBuf<unsigned long long> counter;
     DevBuf<pd_tip_record> tips;
@@ -379,6 +380,7 @@ struct pd_ctx {
         A.damping = damping;
         A.pmb_c = exact_c;
         A.pmb_sc = exact_sc;
+        A.laws = laws.p;
         A.store_forces = 0;
         A.do_drift = 0;
         A.xfer = world > 1 ? xfer.p : nullptr;
@@ -407,8 +409,7 @@ int upload_laws(pd_ctx* ctx, const pd_damage_model& m) {
             d.f[b] = m.laws[k].forces[b];
         }
     }
-    exact_set_laws(laws.data(), m.n_laws, ctx->stream);
-    PD_CK(cudaGetLastError());
+    PD_CK(ctx->laws.upload(laws.data(), laws.size(), ctx->stream));
     ctx->n_laws = m.n_laws;
     ctx->exact_pmb = m.n_laws == 1 && m.laws[0].n_breakpoints == 1;
     ctx->exact_c = m.laws[0].stiffness;
@@ -739,6 +740,17 @@ int download(pd_ctx* ctx, pd_state* st, pd_force_field* forces, int32_t fields) 
 // kernels with brick-major per-bond arrays.  Returns false (and
 // leaves the context untouched) when the model does not qualify;
 // PD_FAST_LAYOUT=general forces the general tile layout.
+// the fast kernels keep their laws in 8-breakpoint tables
+int fast_laws_ok(const pd_damage_model& m) {
+    for (int k = 0; k < m.n_laws; ++k)
+        if (m.laws[k].n_breakpoints > 8)
+            return fail(PD_E_INVALID_ARGUMENT,
+                        "fast variant: law %d has %d breakpoints; the fast kernels take at most 8 "
+                        "(the exact variants take up to %d)",
+                        k, m.laws[k].n_breakpoints, PD_MAX_BREAKPOINTS);
+    return PD_OK;
+}
+
 int try_lattice(pd_ctx* ctx, const pd_particles& p, const pd_state& st, const pd_damage_model& m,
                 const pd_corrections& corr, const uint8_t* nofail, int64_t nofail_size,
                 bool* used) {
@@ -1695,6 +1707,7 @@ int upload_impl(pd_ctx* ctx, const pd_bundle* b, const pd_state* st, int32_t var
     tm.mark("upload: bc");
     if (variant == PD_FAST) {
         bool lattice = false;
+        PD_TRY(fast_laws_ok(b->model));
         PD_TRY(try_lattice(ctx, b->particles, *st, b->model, b->corrections, b->bc.no_failure,
                            b->bc.no_failure_size, &lattice));
         if (!lattice) {
@@ -1823,6 +1836,7 @@ int pd_compute_forces(int32_t variant, pd_state* state, const pd_particles* part
                          corr->no_failure_size));
     if (variant == PD_FAST) {
         bool lattice = false;
+        PD_TRY(fast_laws_ok(*model));
         PD_TRY(try_lattice(ctx, *particles, st, *model, *corr, corr->no_failure,
                            corr->no_failure_size, &lattice));
         if (!lattice)

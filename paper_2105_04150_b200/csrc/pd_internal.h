@@ -211,7 +211,6 @@ void preload_nlu_m2();
 void preload_nlu_m3();
 
 // pd_exact.cu
-void exact_set_laws(const DevLaw* laws, int n, cudaStream_t stream);
 // pmb: one PMB law, no bond types, no lambda / beta (A.pmb_c, A.pmb_sc set)
 cudaError_t launch_exact(const DevArgs& A, int mode, bool node_sum, bool pmb, cudaStream_t st);
 

@@ -300,3 +300,36 @@ def test_gpu_million_node_lattice_matches_oracle(oracle):
         be.simulate(b, st, SimulateOptions(3, 0, 0, IntegratorKind.velocity_verlet))
         outs.append(st)
     _assert_same_state(*outs)
+
+
+def test_gpu_many_breakpoint_law_matches_oracle(oracle, reference):
+    """A piecewise-linear softening law with 12 breakpoints (the reference
+    allows any count, types.hpp:75-91): the exact variants run it bitwise
+    against the C oracle and the reference; the fast variant, whose kernels
+    keep 8-breakpoint tables, refuses it with a clear error."""
+    from paper_2105_04150_b200.types import DamageLaw
+    b, h, g = S.bench_lattice_bundle((12, 11, 10), s_c=1e6)
+    bp = [2e-4 * (k + 1) for k in range(12)]
+    c = 1.0
+    f = [c * bp[0]] + [c * bp[0] * (1.0 - k / 11.0) for k in range(1, 12)]
+    law = DamageLaw(c, bp, f)
+    law.validate()
+    b.model.laws = [law]
+    fam = geometry.build_family(b.particles.coords, h, g)
+    u0 = S.seed_displacements(b.particles.coords) * 300.0
+    outs = []
+    for be in (oracle, reference, engine.backend()):
+        st = make_state(fam, True)
+        st.u = u0.copy()
+        be.simulate(b, st, SimulateOptions(15, 0, 0, IntegratorKind.velocity_verlet,
+                                           KernelVariant.bond_parallel))
+        outs.append(st)
+    for other in outs[1:]:
+        _assert_same_state(outs[0], other)
+    assert int(fam.n_neigh.sum() - outs[2].connectivity.n_neigh.sum()) > 0
+    assert np.count_nonzero(outs[2].bond_history) > 0
+    st = make_state(fam, True)
+    st.u = u0.copy()
+    with pytest.raises(abi.InvalidArgument, match="at most 8"):
+        engine.simulate(b, st, SimulateOptions(2, 0, 0, IntegratorKind.velocity_verlet,
+                                               KernelVariant.fast))

@@ -141,6 +141,18 @@ __global__ void break_kernel(int32_t* entries, int32_t* n_neigh, long long n, in
     }
 }
 
+// entries must name nodes of the list (or -1): a bad index would read past
+// the per-node arrays; the first offending row is reported
+__global__ void entry_range_kernel(const int32_t* entries, long long n, int N,
+                                   unsigned long long* first_bad) {
+    const long long idx = blockIdx.x * (long long)TPB + threadIdx.x;
+    if (idx >= n * N)
+        return;
+    const int32_t j = entries[idx];
+    if (j < -1 || j >= n)
+        atomicMin(first_bad, (unsigned long long)(idx / N));
+}
+
 // RAII device buffer for this translation unit
 template <class T> struct Buf {
     T* p = nullptr;
@@ -162,11 +174,29 @@ template <class T> struct Buf {
                                          cudaGetErrorString(e_)).c_str());                       \
     } while (0)
 
+int entries_in_range(const int32_t* dev_entries, long long n, int N, const char* who) {
+    Buf<unsigned long long> bad;
+    FO_CK(bad.alloc(1));
+    FO_CK(cudaMemset(bad.p, 0xff, sizeof(unsigned long long)));
+    if (n > 0)
+        entry_range_kernel<<<blocks_for(n * N), TPB>>>(dev_entries, n, N, bad.p);
+    FO_CK(cudaGetLastError());
+    unsigned long long first = 0;
+    FO_CK(cudaMemcpy(&first, bad.p, sizeof first, cudaMemcpyDeviceToHost));
+    if (first != ~0ull)
+        return set_error(PD_E_INVALID_ARGUMENT,
+                         (std::string(who) + ": NeighborList entry out of range in row " +
+                          std::to_string(first)).c_str());
+    return PD_OK;
+}
+
 int check_family(const pd_neighbor_list* f, const char* who) {
     if (!f || f->n < 0 || f->group_size < 1 || (f->n > 0 && (!f->entries || !f->n_neigh)))
         return set_error(PD_E_INVALID_ARGUMENT, (std::string(who) + ": bad family").c_str());
     return PD_OK;
 }
+
+template <class T> struct Buf;
 
 int device_ok() {
     int count = 0;
@@ -182,6 +212,8 @@ int neighborhood_volumes_dev(const pd_neighbor_list* f, const double* volumes, B
     const long long n = f->n, N = f->group_size;
     Buf<double> vol;
     FO_CK(ent.up(f->entries, size_t(n * N)));
+    if (entries_in_range(ent.p, n, int(N), "neighborhood_volumes") != PD_OK)
+        return PD_E_INVALID_ARGUMENT;
     FO_CK(vol.up(volumes, size_t(n)));
     FO_CK(nbhd.alloc(size_t(n)));
     if (n > 0)
@@ -231,6 +263,8 @@ int pd_classify_bonds(const double* coords, const pd_neighbor_list* family,
     FO_CK(regions.up(cls->regions, size_t(cls->n_regions)));
     FO_CK(table.up(cls->type_table, size_t(nc * nc)));
     FO_CK(ent.up(family->entries, size_t(n * N)));
+    if (entries_in_range(ent.p, n, int(N), "classify_bonds") != PD_OK)
+        return PD_E_INVALID_ARGUMENT;
     FO_CK(node_cls.alloc(size_t(n)));
     FO_CK(out.alloc(size_t(n * N)));
     if (n > 0) {
@@ -310,6 +344,8 @@ int pd_break_initial_bonds(pd_neighbor_list* family, const double* coords,
     Buf<int32_t> ent, nn;
     Buf<double> xyz;
     FO_CK(ent.up(family->entries, size_t(n * N)));
+    if (entries_in_range(ent.p, n, int(N), "break_initial_bonds") != PD_OK)
+        return PD_E_INVALID_ARGUMENT;
     FO_CK(nn.up(family->n_neigh, size_t(n)));
     FO_CK(xyz.up(coords, size_t(3 * n)));
     if (n > 0)

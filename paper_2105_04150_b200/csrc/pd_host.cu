@@ -2020,6 +2020,14 @@ static int boundary_host(int ops, pd_state* st, const pd_boundary* bc, int64_t s
                          pd_force_field* out, int64_t n) {
     if (n == 0)
         return ok();
+    // the device reads kind / magnitude / ramp_id for all 3n node-axes and
+    // the ramp each names: sizes and ids are checked first (the reference
+    // indexes them unchecked outside apply_boundary)
+    if (bc->kind_size != 3 * n || bc->magnitude_size != 3 * n || bc->ramp_id_size != 3 * n)
+        return fail(PD_E_INVALID_ARGUMENT,
+                    "BoundaryConditions: field lengths do not match node count");
+    if (bc->n_ramps < 1 || par_any(3 * n, [&](int64_t k) { return bc->ramp_id[k] >= bc->n_ramps; }))
+        return fail(PD_E_INVALID_ARGUMENT, "BoundaryConditions: ramp id out of range");
     pd_ctx* ctx = nullptr;
     PD_TRY(pd_ctx_create(0, &ctx));
     struct Guard {

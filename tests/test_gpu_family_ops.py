@@ -121,3 +121,18 @@ def test_rule_table_validation_on_cpu():
         geometry.classify_bonds(p.coords, fam, bad)
     with pytest.raises(abi.DomainError, match="V0 must be positive"):
         geometry.surface_correction_factors(np.ones(n), fam, -1.0)
+
+
+@pytest.mark.gpu
+def test_bad_entries_are_rejected():
+    """A row naming a node outside the list is an error, not a device fault."""
+    g, p = S.lattice_particles((4, 3, 3))
+    fam = geometry.build_family(p.coords, 1.5, g)
+    fam.entries[5] = fam.node_count() + 3
+    vol = np.ones(fam.node_count())
+    with pytest.raises(abi.InvalidArgument, match="out of range in row 0"):
+        geometry.neighborhood_volumes(vol, fam)
+    with pytest.raises(abi.InvalidArgument, match="out of range"):
+        geometry.classify_bonds(p.coords, fam, rc_beam_rules(4, 3, 3))
+    with pytest.raises(abi.InvalidArgument, match="out of range"):
+        geometry.break_plane(fam, p.coords, 0, 1.5)

@@ -88,6 +88,7 @@ struct DevArgs {
 };
 
 constexpr long long kPeerTimeout = -2;  // err_step value: a peer rank never arrived
+constexpr long long kBarrierTimeout = -3;  // err_step value: a persistent launch's grid barrier timed out
 
 // Store an owned node's new displacement into the ghost rows of the
 // neighbouring ranks (peer memory) and make it visible system-wide before the
@@ -164,6 +165,13 @@ static __device__ PD_RAMP_FN double ramp_accel(const DevRamp& r, long long step)
     return __ddiv_rn(x, __dmul_rn((double)r.rise, (double)r.rise));
 }
 
+// x / d for d > 0 (dt, dt^2): a zero numerator (a fixed support: magnitude 0)
+// gives the signed zero IEEE division gives, without __ddiv_rn's slow path
+// (taken for zero numerators)
+__device__ __forceinline__ double div_pos(double x, double d) {
+    return (x == 0.0 && d > 0.0) ? x : __ddiv_rn(x, d);
+}
+
 __device__ __forceinline__ bool finite3(double x, double y, double z) {
     return isfinite(x) && isfinite(y) && isfinite(z);
 }
@@ -195,11 +203,51 @@ __device__ __forceinline__ NodeIn load_node_in(const DevArgs& A, long long i) {
     return r;
 }
 
+// One node-axis's boundary condition (types.hpp:145-155): its kind, and for
+// a prescribed axis the magnitude and the ramp record.
+struct AxisBc {
+    int kind;
+    int rid;  // ramp id
+    double mag;
+    DevRamp ramp;
+};
+
+__device__ __forceinline__ AxisBc load_axis_bc(const DevArgs& A, long long i, int ax) {
+    AxisBc b{PD_BC_FREE, 0, 0.0, DevRamp{}};
+    b.kind = A.bc_kind ? int(A.bc_kind[3 * i + ax]) : PD_BC_FREE;
+    if (b.kind != PD_BC_FREE) {
+        b.mag = A.bc_mag[3 * i + ax];
+        b.rid = A.bc_ramp[3 * i + ax];
+        b.ramp = A.ramps[b.rid];
+    }
+    return b;
+}
+
+// The ramp values one step s needs (node_epilogue): scale(s), scale(s + 1),
+// scale(s + 2), rate(s + 1), accel(s + 1) -- the same calls, so the same bits.
+// A kernel that runs many nodes per step can evaluate them once per ramp.
+struct RampVals {
+    double sc0, sc1, sc2, rate1, acc1;
+};
+
+__device__ __forceinline__ RampVals ramp_vals(const DevRamp& r, long long s) {
+    return RampVals{ramp_scale(r, s), ramp_scale(r, s + 1), ramp_scale(r, s + 2), ramp_rate(r, s + 1),
+                    ramp_accel(r, s + 1)};
+}
+
 // BC = false: the caller guarantees A.bc_kind == NULL (no boundary conditions),
 // so the ramp code is compiled out (fewer registers in the fused kernels).
+// bc: the node's three AxisBc when the caller keeps them (the persistent
+// small-model kernel), else NULL (loaded here).  rv: this step's RampVals per
+// ramp id when the caller evaluated them, else NULL.  next / u_next: when given,
+// receive the node's new v, a (and 1/rho) and the u written to u_out (the
+// next step's u_in), so a kernel that owns the node across steps need not
+// reload them.
 template <int MODE, bool BC = true>
 __device__ __forceinline__ void node_epilogue(const DevArgs& A, long long i, const double4& ui,
-                                              double fx, double fy, double fz, const NodeIn& in) {
+                                              double fx, double fy, double fz, const NodeIn& in,
+                                              const AxisBc* bc = nullptr, NodeIn* next = nullptr,
+                                              double4* u_next = nullptr, const RampVals* rv = nullptr) {
     const double Fb[3] = {fx, fy, fz};
     const double u0[3] = {ui.x, ui.y, ui.z};
     const long long s = A.step;
@@ -210,29 +258,31 @@ __device__ __forceinline__ void node_epilogue(const DevArgs& A, long long i, con
     // records out of local memory
 #pragma unroll
     for (int ax = 0; ax < 3; ++ax) {
-        const int kind = (BC && A.bc_kind) ? int(A.bc_kind[3 * i + ax]) : PD_BC_FREE;
-        double mag = 0.0;
-        DevRamp ramp{};
-        if (kind != PD_BC_FREE) {
-            mag = A.bc_mag[3 * i + ax];
-            ramp = A.ramps[A.bc_ramp[3 * i + ax]];
-        }
-        Fe[ax] = kind == PD_BC_FORCE
-                     ? __dadd_rn(0.0, __dmul_rn(mag, ramp_scale(ramp, MODE == 1 ? s + 1 : s)))
-                     : 0.0;
+        AxisBc b{PD_BC_FREE, 0, 0.0, DevRamp{}};
+        if (BC)
+            b = bc ? bc[ax] : load_axis_bc(A, i, ax);
+        const int kind = b.kind;
+        const double mag = b.mag;
+        const DevRamp& ramp = b.ramp;
+        // ramp values: this step's table when given, else evaluated here
+        auto scale_at = [&](int ds) {  // ds = 0, 1, 2: scale(s + ds)
+            return rv ? (ds == 0 ? rv[b.rid].sc0 : ds == 1 ? rv[b.rid].sc1 : rv[b.rid].sc2)
+                      : ramp_scale(ramp, s + ds);
+        };
+        Fe[ax] = kind == PD_BC_FORCE ? __dadd_rn(0.0, __dmul_rn(mag, scale_at(MODE == 1 ? 1 : 0))) : 0.0;
         if (MODE == 1) {
             const double vh = __dadd_rn(in.v[ax], __dmul_rn(in.a[ax], A.half_dt));
             double an = __dmul_rn(__dsub_rn(__dadd_rn(Fb[ax], Fe[ax]), __dmul_rn(vh, A.damping)), inv);
             double vn = __dadd_rn(vh, __dmul_rn(an, A.half_dt));
             if (kind == PD_BC_DISPLACEMENT) {
-                vn = __ddiv_rn(__dmul_rn(mag, ramp_rate(ramp, s + 1)), dt);
-                an = __ddiv_rn(__dmul_rn(mag, ramp_accel(ramp, s + 1)), A.dt2);
+                vn = div_pos(__dmul_rn(mag, rv ? rv[b.rid].rate1 : ramp_rate(ramp, s + 1)), dt);
+                an = div_pos(__dmul_rn(mag, rv ? rv[b.rid].acc1 : ramp_accel(ramp, s + 1)), A.dt2);
             }
             v[ax] = vn;
             a[ax] = an;
             un[ax] = __dadd_rn(__dadd_rn(u0[ax], __dmul_rn(vn, dt)), __dmul_rn(an, A.half_dt2));
             if (kind == PD_BC_DISPLACEMENT)
-                un[ax] = __dmul_rn(mag, ramp_scale(ramp, s + 2));
+                un[ax] = __dmul_rn(mag, scale_at(2));
         } else {
             const double acc = __dmul_rn(__dadd_rn(Fb[ax], Fe[ax]), inv);
             const double v_old = in.v[ax];
@@ -241,9 +291,9 @@ __device__ __forceinline__ void node_epilogue(const DevArgs& A, long long i, con
             v[ax] = v_new;
             un[ax] = __dadd_rn(u0[ax], __dmul_rn(MODE == 2 ? v_old : v_new, dt));
             if (kind == PD_BC_DISPLACEMENT) {
-                un[ax] = __dmul_rn(mag, ramp_scale(ramp, s + 1));
-                v[ax] = __ddiv_rn(__dmul_rn(mag, ramp_rate(ramp, s + 1)), dt);
-                a[ax] = __ddiv_rn(__dmul_rn(mag, ramp_accel(ramp, s + 1)), A.dt2);
+                un[ax] = __dmul_rn(mag, scale_at(1));
+                v[ax] = div_pos(__dmul_rn(mag, rv ? rv[b.rid].rate1 : ramp_rate(ramp, s + 1)), dt);
+                a[ax] = div_pos(__dmul_rn(mag, rv ? rv[b.rid].acc1 : ramp_accel(ramp, s + 1)), A.dt2);
             }
         }
     }
@@ -252,6 +302,14 @@ __device__ __forceinline__ void node_epilogue(const DevArgs& A, long long i, con
     for (int ax = 0; ax < 3; ++ax) {
         A.v[3 * i + ax] = v[ax];
         A.a[3 * i + ax] = a[ax];
+    }
+    if (next) {
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+            next->v[ax] = v[ax];
+            next->a[ax] = a[ax];
+        }
+        next->inv_rho = in.inv_rho;
     }
     if (A.store_forces) {
 #pragma unroll
@@ -263,9 +321,13 @@ __device__ __forceinline__ void node_epilogue(const DevArgs& A, long long i, con
     if (write_u) {
         const double4 unew = make_double4(un[0], un[1], un[2], ui.w);
         A.u_out[i] = unew;
+        if (u_next)
+            *u_next = unew;
         push_ghost(A, i, unew);
         if (!finite3(un[0], un[1], un[2]))
             atomicMin((unsigned long long*)A.err_step, (unsigned long long)(s + 1));
+    } else if (u_next) {
+        *u_next = ui;
     }
 }
 

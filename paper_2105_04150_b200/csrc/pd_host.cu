@@ -271,6 +271,7 @@ struct pd_ctx {
     // multi-GPU slab world (pd_ctx_connect)
     int rank = 0, world = 1;
     DevBuf<unsigned long long> sync;     // 2 * PD_MAX_RANKS words (epochs, flags)
+    DevBuf<unsigned long long> bar;      // arrival counter of the persistent small-model launch
     unsigned long long epoch = 0;
     DevBuf<int2> xfer;
     double4* peer_u[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [lo/hi][parity]
@@ -1164,6 +1165,8 @@ struct HookStage {
     std::vector<int32_t> entries, n_neigh;
 };
 
+thread_local bool t_in_batch = false;  // a pd_simulate_batch worker thread
+
 int run_loop(pd_ctx* ctx, const pd_options& opt, pd_write_hook hook, void* user,
              int32_t hook_fields, pd_state* hook_state, pd_tip_record* tips_out,
              int64_t tips_capacity, int64_t* n_tips_out) {
@@ -1214,16 +1217,62 @@ int run_loop(pd_ctx* ctx, const pd_options& opt, pd_write_hook hook, void* user,
     int64_t rec = 0;
     int rc = PD_OK;
     int64_t failed_at = -1;
+    // Small lattice models on one GPU: every run of steps without host work
+    // in between (write steps, snapshots, the end) is one persistent launch
+    // (pd_lattice.cu lattice_small_kernel).  PD_LAT_PERSIST=0 turns it off.
+    // (not inside pd_simulate_batch: its models run concurrently on several
+    // streams, where one-step launches interleave and cooperative grids of
+    // several models would compete for residency)
+    const char* persist_var = std::getenv("PD_LAT_PERSIST");
+    const bool persist_env = !(persist_var && std::atoi(persist_var) == 0) && !t_in_batch;
+    const bool persist = persist_env && ctx->lattice && ctx->world <= 1 &&
+                         lattice_small_fits(ctx->lat, mode, ctx->has_bc);
+    const unsigned long long small_ctas = persist ? (unsigned long long)lattice_small_ctas(ctx->lat) : 0;
+    unsigned long long bar_base = 0;
+    int64_t chunk_left = 0;
+    if (persist) {
+        PD_CK(ctx->bar.alloc(1));
+        PD_CK(cudaMemsetAsync(ctx->bar.p, 0, sizeof(unsigned long long), s));
+    }
+    auto store_at = [&](int64_t st) {
+        // forces are kept at write steps and at the end of every run (so a
+        // download after the run sees the last step's force field)
+        const bool is_write = opt.write_every > 0 && (st + 1) % opt.write_every == 0;
+        return (is_write && (ctx->n_tip_sets > 0 || hook)) || st + 1 == last;
+    };
     for (int64_t st = first; st < last; ++st) {
         const bool is_write = opt.write_every > 0 && (st + 1) % opt.write_every == 0;
         A = ctx->args();
         A.step = st;
-        // forces are kept at write steps and at the end of every run (so a
-        // download after the run sees the last step's force field)
-        A.store_forces = (is_write && (ctx->n_tip_sets > 0 || hook)) || st + 1 == last;
+        A.store_forces = store_at(st);
         A.do_drift = st + 1 < last;
-        PD_TRY(launch_step(ctx, A, mode));
-        PD_TRY(slab_sync(ctx));
+        if (persist) {
+            if (chunk_left == 0) {
+                int64_t e = st;  // the chunk's last step: host work follows it
+                while (e + 1 < last && !(opt.write_every > 0 && (e + 1) % opt.write_every == 0) &&
+                       !(ctx->snap_every > 0 && (e + 1) % ctx->snap_every == 0))
+                    ++e;
+                SmallArgs S{};
+                S.u[0] = ctx->u[ctx->cur].p;
+                S.u[1] = ctx->u[ctx->cur ^ 1].p;
+                S.bar = ctx->bar.p;
+                S.bar_base = bar_base;
+                S.steps = int(std::min<int64_t>(e - st + 1, 1 << 30));
+                e = st + S.steps - 1;
+                S.store_last = store_at(e);
+                S.drift_last = e + 1 < last;
+                S.n_ramps = int(ctx->ramps.count);
+                PD_CK(launch_lattice_small(A, ctx->lat, mode, S, s));
+                ctx->kernel = t_last_kernel;
+                ++ctx->launches;
+                bar_base += small_ctas * (unsigned long long)(S.steps - 1);
+                chunk_left = S.steps;
+            }
+            --chunk_left;
+        } else {
+            PD_TRY(launch_step(ctx, A, mode));
+            PD_TRY(slab_sync(ctx));
+        }
         if (!vv)
             ctx->cur ^= 1;
         if (ctx->snap_every > 0 && (st + 1) % ctx->snap_every == 0) {
@@ -1249,6 +1298,8 @@ int run_loop(pd_ctx* ctx, const pd_options& opt, pd_write_hook hook, void* user,
                 if (err == kPeerTimeout)
                     return fail(PD_E_CUDA, "slab sync: a peer rank did not reach step %lld",
                                 (long long)(st + 1));
+                if (err == kBarrierTimeout)
+                    return fail(PD_E_CUDA, "persistent step launch: grid barrier timeout");
                 if (err <= st) {
                     failed_at = err;
                     break;
@@ -1307,6 +1358,8 @@ int run_loop(pd_ctx* ctx, const pd_options& opt, pd_write_hook hook, void* user,
     PD_TRY(snapshot_flush(ctx));
     if (err == kPeerTimeout)
         return fail(PD_E_CUDA, "slab sync: a peer rank did not arrive (timeout)");
+    if (err == kBarrierTimeout)
+        return fail(PD_E_CUDA, "persistent step launch: grid barrier timeout");
     if (failed_at < 0 && err < last)
         failed_at = err;
     int64_t keep = rec;
@@ -1908,6 +1961,7 @@ int pd_simulate_batch(int32_t k, const pd_bundle* bundles, pd_state* states,
     std::vector<std::string> msgs(static_cast<size_t>(k));
     std::atomic<int32_t> next{0};
     auto worker = [&] {
+        t_in_batch = true;
         for (;;) {
             const int32_t m = next.fetch_add(1);
             if (m >= k)

@@ -196,6 +196,27 @@ long long lattice_slot_count(const LatticeArgs& L);  // length of the brick-majo
 // more than 3 breakpoints and for shapes such as hardening-then-softening
 bool lattice_minmax_ok(const double* bp, const double* f, int nbp);
 cudaError_t launch_lattice(const DevArgs& A, const LatticeArgs& L, int mode, cudaStream_t st);
+// Small lattice models: one cooperative launch advancing `steps` steps
+// (pd_lattice.cu lattice_small_kernel).  Step k reads u[k & 1] and writes
+// u[(k & 1) ^ 1]; forces are stored and the next drift done (VV) as
+// store_last / drift_last say on the last step only, every other step drifts
+// and stores nothing.  bar counts CTA arrivals: step k waits for
+// bar_base + k * CTAs.
+struct SmallArgs {
+    double4* u[2];
+    unsigned long long* bar;
+    unsigned long long bar_base;
+    int steps;
+    int store_last;
+    int drift_last;
+    int n_ramps;  // ramp table length (the kernel evaluates each ramp once per step)
+};
+// CTAs the small kernel needs (0: not applicable) and whether they are all
+// co-resident for this mode / BC / NF combination
+long long lattice_small_ctas(const LatticeArgs& L);
+bool lattice_small_fits(const LatticeArgs& L, int mode, bool bc);
+cudaError_t launch_lattice_small(const DevArgs& A, const LatticeArgs& L, int mode, const SmallArgs& S,
+                                 cudaStream_t st);
 cudaError_t launch_lattice_materialize(const int32_t* entries0, const uint4* mask, long long begin,
                                        long long end, long long n, int N, const LatticeArgs& L,
                                        int32_t* out, double* hist_out, cudaStream_t st);

@@ -195,6 +195,400 @@ __global__ void __launch_bounds__(BX * BY * BZT, MINB) lattice_step_kernel(DevAr
     node_epilogue<MODE, BC>(A, i, A.u_in[i], fx, fy, fz);
 }
 
+// ---- small models: one persistent launch for a run of steps -------------------
+//
+// A model of a few thousand nodes (cfg1's 9,800-node beam) is a latency chain,
+// not a throughput problem: one thread per node walking 122 slots, a fresh
+// launch every step (profiles/r02_small_cfg1_ncu.md).  Here one cooperative
+// launch advances all the steps between two host events (write steps,
+// snapshots, the end of the run):
+//   * a CTA owns an SBX x 4 x 1 brick; each node's 122 slots are split over
+//     SP = 4 warps, one per 32-bit word of the row mask (warp w runs word
+//     w % 4, so the warps of one word share a scheduler);
+//   * each word is walked as a rolled loop over the slots some lane of the
+//     warp still has (rolled_word): a few hundred bytes of code, so the
+//     kernel stays in the SM's instruction cache (the unrolled slot parts,
+//     55 KB, streamed from L2 every step and measured no faster);
+//   * the words' forces meet in shared memory and are summed in word order
+//     (deterministic) by the node's word-0 thread, which keeps u, v, a and
+//     1/rho of its node in registers (the boundary conditions in shared
+//     memory) across the steps and runs the shared fp64 epilogue
+//     (node_epilogue) exactly as the one-step kernels do;
+//   * steps are separated by a grid barrier: an arrival counter in global
+//     memory (release add, acquire poll); u written by other CTAs is read
+//     with ld.global.cg, so no stale L1 line survives a step.
+// Co-residency is guaranteed by cudaLaunchCooperativeKernel; the host takes
+// this path only when the grid fits (lattice_small_fits).  A barrier that
+// never completes (impossible under a cooperative launch) ends the run after
+// a timeout with kBarrierTimeout instead of hanging the device.
+constexpr int SP = 4;
+
+inline int sm_count_small() {
+    static const int n = [] {
+        int dev = 0, v = 0;
+        cudaGetDevice(&dev);
+        return cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0
+                   ? v
+                   : 148;
+    }();
+    return n;
+}
+
+// The rolled walk of one mask word (slots 32 word .. 32 word + 31): only the
+// slots some lane of the warp still has (a warp-uniform bit loop, four slots
+// per iteration for ILP), each with bond_contribution's break test directly
+// (engine.cpp:90-98) -- no re-walk -- and slow_node's semantics for collapsed
+// and no-failure bonds.
+struct SlotGeo {
+    float4 d;  // dx, dy, dz, |d|^2
+    float4 e;  // |d|^4, |d|, record offset in the staged box (int bits), 0
+};
+
+template <bool NF>
+__device__ __forceinline__ void rolled_word(const float4* own, const float4& ri, unsigned mw, int word,
+                                            float sc, const SlotGeo* geo, float3& f, unsigned& dead) {
+    unsigned todo = __reduce_or_sync(0xffffffffu, mw);
+    float fx = 0.f, fy = 0.f, fz = 0.f;
+    unsigned dd = 0u;
+    while (todo) {
+        // four slots per iteration, branch free (a missing fourth slot
+        // re-reads slot b = 0 and is predicated away), so the scheduler can
+        // interleave their dependency chains
+        int b[4];
+        unsigned v = 0u;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            b[q] = todo != 0u ? __ffs(todo) - 1 : 0;
+            v |= (todo != 0u ? 1u : 0u) << q;
+            todo &= todo - 1u;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const SlotGeo g = geo[32 * word + b[q]];
+            const float4 rj = own[__float_as_int(g.e.z)];
+            // stretch_c's arithmetic with the offset from the table
+            const float2 dxy = make_float2(g.d.x, g.d.y);
+            const float2 hxy = __fadd2_rn(make_float2(rj.x, rj.y), make_float2(-ri.x, -ri.y));
+            const float hz = rj.z - ri.z;
+            const float2 cxy = __fadd2_rn(hxy, dxy);
+            const float2 txy = __fadd2_rn(cxy, dxy);
+            const float cz = hz + g.d.z, tz = cz + g.d.z;
+            const float2 pxy = __fmul2_rn(hxy, txy);
+            float num = __fadd_rn(pxy.x, pxy.y);
+            num = fmaf(hz, tz, num);
+            const float w = fmaf(num, g.d.w, g.e.x);
+            const float a = rsqrt_approx(w);
+            const float st = num * rcp_approx(fmaf(w, a, g.d.w));
+            // live, and not collapsed (|xi + eta| = 0: a = +inf, kept with no
+            // force as in slow_node, engine.cpp:61-65, 100-101)
+            const bool live = ((v >> q) & 1u) && ((mw >> b[q]) & 1u) && a != __int_as_float(0x7f800000);
+            // breaks unless a no-failure neighbour keeps it
+            const bool brk = live && !(st < sc) && !(rj.w < 0.f);
+            dd |= brk ? 1u << b[q] : 0u;
+            // selected, not multiplied by 0: a dead slot's record may be
+            // non-finite (fp32 overflow of a huge displacement)
+            const bool use = live && !brk;
+            const float scale = st * a * (NF ? fabsf(rj.w) : 1.f) * g.e.y;
+            fx = use ? fmaf(cxy.x, scale, fx) : fx;
+            fy = use ? fmaf(cxy.y, scale, fy) : fy;
+            fz = use ? fmaf(cz, scale, fz) : fz;
+        }
+    }
+    f = make_float3(fx, fy, fz);
+    dead = dd;
+}
+
+__device__ __forceinline__ double4 ldcg4(const double4* p) {
+    const double2 a = __ldcg(reinterpret_cast<const double2*>(p));
+    const double2 b = __ldcg(reinterpret_cast<const double2*>(p) + 1);
+    return make_double4(a.x, a.y, b.x, b.y);
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// The gate at the top of step s (= the launch's first step + k).  For k > 0,
+// arrive (release: this CTA's u / v / a stores, ordered before thread 0 by
+// the CTA barrier, become visible with the count) and wait until the count
+// reaches target (acquire: every other CTA's step s - 1 stores are visible).
+// Then stop if a step before s saw non-finite u (err_step <= s; a concurrent
+// step-s epilogue elsewhere can only write s + 1) or the barrier timed out.
+// Thread 0 decides for the whole CTA.
+__device__ __forceinline__ bool step_gate(bool wait, unsigned long long* count,
+                                          unsigned long long target, long long* err_step,
+                                          long long s) {
+    __shared__ int go;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        bool ok = true;
+        if (wait) {
+            asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(count) : "memory");
+            const unsigned long long t0 = globaltimer();
+            for (;;) {
+                unsigned long long c;
+                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(c) : "l"(count) : "memory");
+                if (c >= target)
+                    break;
+                if (globaltimer() - t0 > 4000000000ull) {  // 4 s: never under a cooperative launch
+                    *(volatile long long*)err_step = kBarrierTimeout;
+                    ok = false;
+                    break;
+                }
+            }
+        }
+        go = ok && !(*(volatile long long*)err_step <= s);
+    }
+    __syncthreads();
+    return go != 0;
+}
+
+template <int MODE, bool BC, bool NF, int SBX>
+__global__ void __launch_bounds__(SBX * BY * SP, 512 / (SBX * BY * SP)) lattice_small_kernel(DevArgs A, LatticeArgs L,
+                                                                          SmallArgs S) {
+    constexpr int NB = SBX * BY;               // nodes per brick
+    constexpr int NT = NB * SP;                // threads
+    constexpr int SHX = SBX + 6;               // halo box: SHX x HY x 7
+    constexpr int NR = SHX * HY * 7;
+    constexpr int NRT = (NR + NT - 1) / NT;    // records staged per thread
+    static_assert(NB % 32 == 0, "a warp holds 32 nodes of one brick");
+    __shared__ float4 rec[NR];
+    __shared__ float4 part_f[SP - 1][NB];
+    __shared__ uint4 part_d[SP - 1][NB];
+    __shared__ uint4 smask[NB];
+    __shared__ SlotGeo geo[128];
+    __shared__ AxisBc sbc[BC ? NB : 1][3];    // the nodes' boundary conditions, loaded once
+    constexpr int kMaxRamps = 32;             // larger tables: ramps evaluated per node
+    __shared__ RampVals srv[BC ? kMaxRamps : 1];  // this step's ramp values, per ramp
+    __shared__ double4 sU0;                    // the brick origin's u: the staging reference
+    const int t = threadIdx.x, wid = t / 32;
+    const int p = wid % SP;                    // the mask word of this warp (warp-uniform)
+    const int node = (wid / SP) * 32 + t % 32;
+    if (t < 128) {
+        SlotGeo g{};
+        if (t < NPAT) {
+            const int dx = c_pat[t][0], dy = c_pat[t][1], dz = c_pat[t][2], r2 = c_pat[t][3];
+            g.d = make_float4(float(dx), float(dy), float(dz), float(r2));
+            g.e = make_float4(float(r2 * r2), c_len[t], __int_as_float(dx + SHX * (dy + HY * dz)), 0.f);
+        }
+        geo[t] = g;
+    }
+    const int tx = node % SBX, ty = node / SBX;
+    const int gx0 = blockIdx.x * SBX, gy0 = blockIdx.y * BY, gz0 = L.z0 + blockIdx.z;
+    const int gx = gx0 + tx, gy = gy0 + ty;
+    const bool active = gx < L.nx && gy < L.ny;
+    const long long plane = (long long)L.nx * L.ny;
+    const long long i = gx + (long long)L.nx * gy + plane * gz0;
+    // the node's state only its word-0 thread touches stays in registers
+    // across the steps: u, v, a, 1/rho (and the BCs in shared memory)
+    NodeIn nin{};
+    double4 ui = make_double4(0.0, 0.0, 0.0, 0.0);
+    if (p == 0) {
+        smask[node] = active ? L.mask[i] : make_uint4(0, 0, 0, 0);
+        if (active) {
+            nin = load_node_in(A, i);
+            ui = ldcg4(S.u[0] + i);
+            if (BC)
+                for (int ax = 0; ax < 3; ++ax)
+                    sbc[node][ax] = load_axis_bc(A, i, ax);
+        }
+        if (node == 0)
+            sU0 = ui;  // node 0 of a brick is always inside the lattice
+    }
+    const unsigned long long nblocks = (unsigned long long)gridDim.x * gridDim.y * gridDim.z;
+    const float ih = float(L.inv_h);
+    // the records this thread stages: their source node and (NF) the constant
+    // signed volume ratio, computed once
+    // (-1: a record outside the lattice, staged as 0; measured faster than
+    // branch-free loads of a clamped neighbour, which load every record)
+    long long src[NRT];
+    float wv[NRT];
+#pragma unroll
+    for (int q = 0; q < NRT; ++q) {
+        const int r = t + q * NT;
+        const int pz = r / (SHX * HY), rr = r % (SHX * HY);
+        const int X = gx0 - 3 + rr % SHX, Y = gy0 - 3 + rr / SHX, Z = gz0 - 3 + pz;
+        const bool ok = r < NR && X >= 0 && X < L.nx && Y >= 0 && Y < L.ny && Z >= 0 && Z < L.nz_local;
+        src[q] = ok ? X + (long long)L.nx * Y + plane * Z : -1;
+        wv[q] = 0.f;
+        if (NF && ok) {
+            const float vf = L.vol_varies ? float(A.xv[src[q]].w * L.inv_v0) : 1.f;
+            wv[q] = S.u[0][src[q]].w != 0.0 ? -vf : vf;  // the no-failure flag rides in u.w
+        }
+    }
+    double4* const u0 = S.u[0];
+    double4* const u1 = S.u[1];
+    const float4* own = rec + (tx + 3) + SHX * ((ty + 3) + HY * 3);
+#ifdef PD_SMALL_PROF
+    long long pc[6] = {0, 0, 0, 0, 0, 0}, pt = clock64();
+#define PD_PROF_MARK(q) do { const long long n_ = clock64(); if (k > 0) pc[q] += n_ - pt; pt = n_; } while (0)
+#else
+#define PD_PROF_MARK(q) do { } while (0)
+#endif
+    for (int k = 0; k < S.steps; ++k) {
+        PD_PROF_MARK(3);
+        if (!step_gate(k > 0, S.bar, S.bar_base + nblocks * (unsigned long long)k, A.err_step,
+                       A.step + k))
+            return;
+        PD_PROF_MARK(0);
+        const double4* uin = (k & 1) ? u1 : u0;
+        double4* uout = (k & 1) ? u0 : u1;
+        if (BC && t < S.n_ramps && S.n_ramps <= kMaxRamps)  // read after the staging barrier
+            srv[t] = ramp_vals(A.ramps[t], A.step + k);
+        // every record's load in flight at once (no dependent load: the
+        // reference u of the brick origin is already in shared memory)
+        const double4 U0 = sU0;
+        double2 uxy[NRT];
+        double uz[NRT];
+#pragma unroll
+        for (int q = 0; q < NRT; ++q) {
+            uxy[q] = make_double2(0.0, 0.0);
+            uz[q] = 0.0;
+            if (src[q] >= 0) {
+                uxy[q] = __ldcg(reinterpret_cast<const double2*>(uin + src[q]));
+                uz[q] = __ldcg(&uin[src[q]].z);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < NRT; ++q) {
+            const int r = t + q * NT;
+            if (r < NR)
+                rec[r] = src[q] >= 0 ? make_float4(float(uxy[q].x - U0.x) * ih, float(uxy[q].y - U0.y) * ih,
+                                                   float(uz[q] - U0.z) * ih, wv[q])
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        __syncthreads();
+        PD_PROF_MARK(1);
+        const float4 ri = *own;
+        const uint4 m = smask[node];
+        const float sc = (NF && ri.w < 0.f) ? __int_as_float(0x7f800000) : L.sc;
+        const unsigned mw = p == 0 ? m.x : (p == 1 ? m.y : (p == 2 ? m.z : m.w));
+        float3 f;
+        unsigned dw;
+        rolled_word<NF>(own, ri, mw, p, sc, geo, f, dw);
+        if (p > 0) {
+            part_f[p - 1][node] = make_float4(f.x, f.y, f.z, 0.f);
+            part_d[p - 1][node] = make_uint4(p == 1 ? dw : 0u, p == 2 ? dw : 0u, p == 3 ? dw : 0u, 0u);
+        }
+        __syncthreads();
+        PD_PROF_MARK(2);
+        if (p != 0 || !active)
+            continue;
+        uint4 dead = make_uint4(dw, 0u, 0u, 0u);
+#pragma unroll
+        for (int q = 0; q < SP - 1; ++q) {  // word order: the same sum every run
+            const float4 g = part_f[q][node];
+            f.x += g.x;
+            f.y += g.y;
+            f.z += g.z;
+            const uint4 d = part_d[q][node];
+            dead = make_uint4(dead.x, dead.y | d.x, dead.z | d.y, dead.w | d.z);
+        }
+        if (dead.x | dead.y | dead.z | dead.w) {
+            const uint4 nm = make_uint4(m.x & ~dead.x, m.y & ~dead.y, m.z & ~dead.z, m.w & ~dead.w);
+            smask[node] = nm;
+            L.mask[i] = nm;
+            A.n_neigh[i] -= __popc(dead.x) + __popc(dead.y) + __popc(dead.z) + __popc(dead.w);
+        }
+        const double fx = double(f.x * L.cv), fy = double(f.y * L.cv), fz = double(f.z * L.cv);
+        PD_PROF_MARK(4);
+        DevArgs Ak = A;
+        Ak.u_in = uin;
+        Ak.u_out = uout;
+        Ak.step = A.step + k;
+        const bool last = k + 1 == S.steps;
+        Ak.store_forces = last ? S.store_last : 0;
+        Ak.do_drift = last ? S.drift_last : 1;
+        node_epilogue<MODE, BC>(Ak, i, ui, fx, fy, fz, nin, BC ? sbc[node] : nullptr, &nin, &ui,
+                                (BC && S.n_ramps <= kMaxRamps) ? srv : nullptr);
+        PD_PROF_MARK(5);
+        if (node == 0)
+            sU0 = ui;  // read by the next step's staging, after its gate
+    }
+#ifdef PD_SMALL_PROF
+    if (t == 0 && blockIdx.x == 0 && blockIdx.y == 0)
+        printf("small prof cta z=%d steps=%d cycles/step gate %lld stage %lld slots %lld combine %lld "
+               "epilogue %lld tail %lld\n",
+               blockIdx.z, S.steps, pc[0] / (S.steps - 1), pc[1] / (S.steps - 1), pc[2] / (S.steps - 1),
+               pc[4] / (S.steps - 1), pc[5] / (S.steps - 1), pc[3] / (S.steps - 1));
+#endif
+#undef PD_PROF_MARK
+}
+
+// Brick width of the small kernel: the per-step critical path is the SM with
+// the most CTAs, so take the width with the fewest brick-columns on the
+// busiest SM (cfg1's 50 x 14 x 14 beam: 224 16-wide CTAs put two on 76 SMs,
+// 392 8-wide ones three on some: 32 vs 24 columns).  PD_SMALL_BX = 8 / 16
+// forces one.
+inline int small_bx(const LatticeArgs& L) {
+    if (const char* e = std::getenv("PD_SMALL_BX")) {
+        const int v = std::atoi(e);
+        if (v == 8 || v == 16)
+            return v;
+    }
+    const long long sms = sm_count_small();
+    long long best = -1;
+    int bx = 16;
+    for (int w : {16, 8}) {
+        const long long ctas = (long long)((L.nx + w - 1) / w) * ((L.ny + BY - 1) / BY) * L.nz_own;
+        const long long cost = (ctas + sms - 1) / sms * w;
+        if (best < 0 || cost < best) {
+            best = cost;
+            bx = w;
+        }
+    }
+    return bx;
+}
+
+template <int MODE, bool BC, bool NF, int SBX>
+cudaError_t launch_small_w(const DevArgs& A, const LatticeArgs& L, const SmallArgs& S, cudaStream_t st) {
+    const dim3 grid{unsigned((L.nx + SBX - 1) / SBX), unsigned((L.ny + BY - 1) / BY), unsigned(L.nz_own)};
+    t_last_kernel = kernel_name<3, MODE, BC, NF, SBX>("lattice_small_kernel");
+    DevArgs a = A;
+    LatticeArgs l = L;
+    SmallArgs s = S;
+    void* args[] = {&a, &l, &s};
+    return cudaLaunchCooperativeKernel(
+        reinterpret_cast<const void*>(lattice_small_kernel<MODE, BC, NF, SBX>), grid, dim3(SBX * BY * SP),
+        args, 0, st);
+}
+
+template <int MODE, bool BC, bool NF>
+cudaError_t launch_small_t(const DevArgs& A, const LatticeArgs& L, const SmallArgs& S, cudaStream_t st) {
+    return small_bx(L) == 8 ? launch_small_w<MODE, BC, NF, 8>(A, L, S, st)
+                            : launch_small_w<MODE, BC, NF, 16>(A, L, S, st);
+}
+
+template <int MODE, bool BC, bool NF> int small_capacity(int bx) {
+    int per_sm = 0;
+    const cudaError_t e =
+        bx == 8 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lattice_small_kernel<MODE, BC, NF, 8>,
+                                                                8 * BY * SP, 0)
+                : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lattice_small_kernel<MODE, BC, NF, 16>,
+                                                                16 * BY * SP, 0);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return per_sm;
+}
+
+template <int MODE> int small_capacity_mode(bool bc, bool nf, int bx) {
+    return bc ? (nf ? small_capacity<MODE, true, true>(bx) : small_capacity<MODE, true, false>(bx))
+              : (nf ? small_capacity<MODE, false, true>(bx) : small_capacity<MODE, false, false>(bx));
+}
+
+template <int MODE>
+cudaError_t launch_small_mode(const DevArgs& A, const LatticeArgs& L, const SmallArgs& S, cudaStream_t st) {
+    if (L.nf)
+        return A.bc_kind ? launch_small_t<MODE, true, true>(A, L, S, st)
+                         : launch_small_t<MODE, false, true>(A, L, S, st);
+    return A.bc_kind ? launch_small_t<MODE, true, false>(A, L, S, st)
+                     : launch_small_t<MODE, false, false>(A, L, S, st);
+}
+
 // ---- n-linear laws, bond types, lambda / beta on the lattice (NL) -------------
 //
 // The general NL kernel (more than 8 laws or more than 3 breakpoints; the
@@ -639,6 +1033,16 @@ template <int MODE, bool BC, bool NF> void preload_bc() {
 }
 
 template <int MODE> void preload_mode() {
+    if constexpr (MODE != 0) {
+        preload_fn(lattice_small_kernel<MODE, true, true, 16>);
+        preload_fn(lattice_small_kernel<MODE, true, false, 16>);
+        preload_fn(lattice_small_kernel<MODE, false, true, 16>);
+        preload_fn(lattice_small_kernel<MODE, false, false, 16>);
+        preload_fn(lattice_small_kernel<MODE, true, true, 8>);
+        preload_fn(lattice_small_kernel<MODE, true, false, 8>);
+        preload_fn(lattice_small_kernel<MODE, false, true, 8>);
+        preload_fn(lattice_small_kernel<MODE, false, false, 8>);
+    }
     preload_bc<MODE, true, false>();
     preload_bc<MODE, false, false>();
     preload_bc<MODE, true, true>();
@@ -801,6 +1205,38 @@ cudaError_t launch_lattice(const DevArgs& A, const LatticeArgs& L, int mode, cud
     case 1: return launch_mode<1>(A, L, st);
     case 2: return launch_mode<2>(A, L, st);
     default: return launch_mode<3>(A, L, st);
+    }
+}
+
+long long lattice_small_ctas(const LatticeArgs& L) {
+    if (L.nl || L.cfg != 0)  // PD_LAT_CFG = 5 forces the one-step small-brick kernel
+        return 0;
+    const long long bricks4 = (long long)((L.nx + 15) / 16) * ((L.ny + 3) / 4) * ((L.nz_own + 3) / 4);
+    if (bricks4 >= 2LL * sm_count())
+        return 0;
+    const int bx = small_bx(L);
+    return (long long)((L.nx + bx - 1) / bx) * ((L.ny + BY - 1) / BY) * L.nz_own;
+}
+
+bool lattice_small_fits(const LatticeArgs& L, int mode, bool bc) {
+    const long long ctas = lattice_small_ctas(L);
+    if (ctas <= 0)
+        return false;
+    const bool nf = L.nf != 0;
+    const int bx = small_bx(L);
+    const int per_sm = mode == 1 ? small_capacity_mode<1>(bc, nf, bx)
+                     : mode == 2 ? small_capacity_mode<2>(bc, nf, bx)
+                                 : small_capacity_mode<3>(bc, nf, bx);
+    return ctas <= (long long)per_sm * sm_count();
+}
+
+cudaError_t launch_lattice_small(const DevArgs& A, const LatticeArgs& L, int mode, const SmallArgs& S,
+                                 cudaStream_t st) {
+    switch (mode) {
+    case 1: return launch_small_mode<1>(A, L, S, st);
+    case 2: return launch_small_mode<2>(A, L, S, st);
+    case 3: return launch_small_mode<3>(A, L, S, st);
+    default: return cudaErrorInvalidValue;
     }
 }
 

@@ -194,7 +194,7 @@ def test_fast_million_node_lattice(oracle):
 
 
 LAT_KERNELS = {  # PD_LAT_CFG -> the instantiation it selects on a 20x18x26 lattice
-    "0": "lattice_step_kernel<1,1,1,0,0>",  # by size: below two 16x4x4 bricks per SM
+    "0": "lattice_small_kernel<1,0,0,8>",  # by size (below two 16x4x4 bricks per SM): persistent
     "1": "lattice_step_kernel<1,8,3,0,0>",  # the BENCH instantiation (16x4x8, 3 CTAs/SM)
     "4": "lattice_step_kernel<1,4,5,0,0>",  # 16x4x4 bricks at 5 CTAs/SM
     "5": "lattice_step_kernel<1,1,1,0,0>",  # the small-brick latency variant, forced
@@ -308,13 +308,14 @@ def test_lattice_nl_kernel_matches_tiles_and_oracle(oracle, monkeypatch):
     assert fam.n_neigh.sum() > ref.connectivity.n_neigh.sum()  # it fractured
 
 
-@pytest.mark.parametrize("lat_cfg", ["5", "6"])
+@pytest.mark.parametrize("lat_cfg", ["0", "5", "6"])
 @pytest.mark.parametrize("integrator", [IntegratorKind.euler, IntegratorKind.velocity_verlet])
 def test_lattice_no_failure_and_volumes_match_oracle(oracle, integrator, monkeypatch, lat_cfg):
     """cfg1-style run on the lattice layout: the 3-point-bend beam (no-failure
     supports and load patch, PMB, quintic ramp) with per-node volumes, against
-    the fp64 oracle, on the small-brick (5) and 16x4x4-brick (6) kernels
-    (with no-failure nodes and BCs: 16x4x4 bricks at 5 CTAs/SM)."""
+    the fp64 oracle, on the persistent small-model launch (0), the one-step
+    small-brick kernel (5) and the 16x4x4-brick kernel (6) (with no-failure
+    nodes and BCs: 16x4x4 bricks at 5 CTAs/SM)."""
     monkeypatch.setenv("PD_LAT_CFG", lat_cfg)
     b, h, g = S.beam_bundle(30, 10, 10)
     rng = np.random.default_rng(11)
@@ -340,6 +341,52 @@ def test_lattice_no_failure_and_volumes_match_oracle(oracle, integrator, monkeyp
     diff = int((ref.connectivity.entries != fast.connectivity.entries).sum())
     assert diff <= max(4, 0.01 * broken), (diff, broken)
     assert max_rel_difference(ref.u, fast.u) <= FRACTURE_U_TOL
+
+
+@pytest.mark.parametrize("integrator", [IntegratorKind.euler, IntegratorKind.euler_cromer,
+                                        IntegratorKind.velocity_verlet])
+def test_lattice_persistent_launch_is_chunk_invariant(monkeypatch, integrator):
+    """The persistent small-model launch (lattice_small_kernel) runs every
+    step between two host events in one launch.  Cutting the run at write
+    steps (hook every 7 steps, tips) or into several run calls must give the
+    same bits: the per-step arithmetic does not depend on the chunking.  The
+    one-step kernel (PD_LAT_PERSIST=0; its slot sums run in another order)
+    and 16-wide bricks (PD_SMALL_BX=16; other fp32 staging references) agree
+    within the fast-path tolerance."""
+    b, h, g = S.beam_bundle(30, 10, 10)
+    b.bc.ramps[1].rise_steps = 150
+    b.bc.magnitude[:] = b.bc.magnitude * 3.0  # drive it to fracture
+    fam = geometry.build_family(b.particles.coords, h, g)
+    outs = {}
+    for name, persist, we, split in (("one", "1", 0, 1), ("hooked", "1", 7, 1), ("split", "1", 0, 3),
+                                     ("step", "0", 0, 1), ("bx16", "1", 0, 1)):
+        monkeypatch.setenv("PD_LAT_PERSIST", persist)
+        monkeypatch.setenv("PD_SMALL_BX", "16" if name == "bx16" else "0")
+        ctx = engine.Context(0)
+        st = make_state(fam, False)
+        ctx.upload(b, st, KernelVariant.fast)
+        done = 0
+        for part in range(split):
+            k = 200 // split if part + 1 < split else 200 - done
+            ctx.run(k, done, integrator, we, KernelVariant.fast)
+            done += k
+        kern = ctx.kernel()
+        ctx.download(st)
+        ctx.close()
+        assert kern.startswith("lattice_small_kernel" if persist == "1" else "lattice_step_kernel"), kern
+        outs[name] = st
+    ref = outs["one"]
+    assert fam.n_neigh.sum() > ref.connectivity.n_neigh.sum()  # it fractured
+    for name in ("hooked", "split"):
+        for f in ("u", "v", "a"):
+            assert np.array_equal(getattr(ref, f), getattr(outs[name], f)), (name, f)
+        assert np.array_equal(ref.connectivity.entries, outs[name].connectivity.entries), name
+    broken = fam.n_neigh.sum() - ref.connectivity.n_neigh.sum()
+    for name in ("step", "bx16"):
+        st = outs[name]
+        diff = int((ref.connectivity.entries != st.connectivity.entries).sum())
+        assert diff <= max(4, 0.01 * broken), (name, diff, broken)
+        assert max_rel_difference(ref.u, st.u) <= FRACTURE_U_TOL, name
 
 
 NLU_LAWS = {

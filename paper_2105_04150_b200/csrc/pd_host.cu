@@ -1226,6 +1226,7 @@ int run_loop(pd_ctx* ctx, const pd_options& opt, pd_write_hook hook, void* user,
     const char* persist_var = std::getenv("PD_LAT_PERSIST");
     const bool persist_env = !(persist_var && std::atoi(persist_var) == 0) && !t_in_batch;
     const bool persist = persist_env && ctx->lattice && ctx->world <= 1 &&
+                         (!ctx->has_bc || ctx->ramps.count <= 32) &&
                          lattice_small_fits(ctx->lat, mode, ctx->has_bc);
     const unsigned long long small_ctas = persist ? (unsigned long long)lattice_small_ctas(ctx->lat) : 0;
     unsigned long long bar_base = 0;

@@ -209,7 +209,7 @@ struct SmallArgs {
     int steps;
     int store_last;
     int drift_last;
-    int n_ramps;  // ramp table length (the kernel evaluates each ramp once per step)
+    int n_ramps;  // ramp table length, <= 32 (the kernel evaluates each ramp once per step)
 };
 // CTAs the small kernel needs (0: not applicable) and whether they are all
 // co-resident for this mode / BC / NF combination

@@ -222,6 +222,7 @@ __global__ void __launch_bounds__(BX * BY * BZT, MINB) lattice_step_kernel(DevAr
 // never completes (impossible under a cooperative launch) ends the run after
 // a timeout with kBarrierTimeout instead of hanging the device.
 constexpr int SP = 4;
+constexpr int kSmallMaxRamps = 32;  // ramp table of the small kernel (one per lane of a warp)
 
 inline int sm_count_small() {
     static const int n = [] {
@@ -360,8 +361,9 @@ __global__ void __launch_bounds__(SBX * BY * SP, 512 / (SBX * BY * SP)) lattice_
     __shared__ uint4 smask[NB];
     __shared__ SlotGeo geo[128];
     __shared__ AxisBc sbc[BC ? NB : 1][3];    // the nodes' boundary conditions, loaded once
-    constexpr int kMaxRamps = 32;             // larger tables: ramps evaluated per node
-    __shared__ RampVals srv[BC ? kMaxRamps : 1];  // this step's ramp values, per ramp
+    // the ramp values of steps k (srv[k & 1]) and k + 1, per ramp (the host
+    // takes this kernel only for at most kSmallMaxRamps ramps)
+    __shared__ RampVals srv[2][BC ? kSmallMaxRamps : 1];
     __shared__ double4 sU0;                    // the brick origin's u: the staging reference
     const int t = threadIdx.x, wid = t / 32;
     const int p = wid % SP;                    // the mask word of this warp (warp-uniform)
@@ -397,6 +399,8 @@ __global__ void __launch_bounds__(SBX * BY * SP, 512 / (SBX * BY * SP)) lattice_
         if (node == 0)
             sU0 = ui;  // node 0 of a brick is always inside the lattice
     }
+    if (BC && wid == 1 && t % 32 < S.n_ramps)  // step 0's ramp values (read after the first gate)
+        srv[0][t % 32] = ramp_vals(A.ramps[t % 32], A.step);
     const unsigned long long nblocks = (unsigned long long)gridDim.x * gridDim.y * gridDim.z;
     const float ih = float(L.inv_h);
     // the records this thread stages: their source node and (NF) the constant
@@ -435,8 +439,6 @@ __global__ void __launch_bounds__(SBX * BY * SP, 512 / (SBX * BY * SP)) lattice_
         PD_PROF_MARK(0);
         const double4* uin = (k & 1) ? u1 : u0;
         double4* uout = (k & 1) ? u0 : u1;
-        if (BC && t < S.n_ramps && S.n_ramps <= kMaxRamps)  // read after the staging barrier
-            srv[t] = ramp_vals(A.ramps[t], A.step + k);
         // every record's load in flight at once (no dependent load: the
         // reference u of the brick origin is already in shared memory)
         const double4 U0 = sU0;
@@ -474,8 +476,12 @@ __global__ void __launch_bounds__(SBX * BY * SP, 512 / (SBX * BY * SP)) lattice_
         }
         __syncthreads();
         PD_PROF_MARK(2);
-        if (p != 0 || !active)
+        if (p != 0 || !active) {
+            // warp 1 evaluates the next step's ramps while warp 0 integrates
+            if (BC && wid == 1 && t % 32 < S.n_ramps && k + 1 < S.steps)
+                srv[(k + 1) & 1][t % 32] = ramp_vals(A.ramps[t % 32], A.step + k + 1);
             continue;
+        }
         uint4 dead = make_uint4(dw, 0u, 0u, 0u);
 #pragma unroll
         for (int q = 0; q < SP - 1; ++q) {  // word order: the same sum every run
@@ -502,7 +508,7 @@ __global__ void __launch_bounds__(SBX * BY * SP, 512 / (SBX * BY * SP)) lattice_
         Ak.store_forces = last ? S.store_last : 0;
         Ak.do_drift = last ? S.drift_last : 1;
         node_epilogue<MODE, BC>(Ak, i, ui, fx, fy, fz, nin, BC ? sbc[node] : nullptr, &nin, &ui,
-                                (BC && S.n_ramps <= kMaxRamps) ? srv : nullptr);
+                                srv[k & 1]);
         PD_PROF_MARK(5);
         if (node == 0)
             sU0 = ui;  // read by the next step's staging, after its gate

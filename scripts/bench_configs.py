@@ -11,7 +11,7 @@ cfg4 is bench.py's default line.  cfg5's law set (several laws chosen by bond ty
 GPU: the fast and exact variants of one simulate() call (host buffers in, state out), after
 one untimed call.  Reference: the unmodified reference (oracle/_ref) on all host cores.
 Writes one JSON object (stdout, and gpurun_out/r02_configs.json when --save is given;
-profiles/r01_configs.json is a copy).
+profiles/r02_configs.json is a copy).
 """
 import json
 import os
@@ -84,7 +84,7 @@ def main():
     print(json.dumps(out))
     if "--save" in sys.argv:
         os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)  # merged back by gpurun
-        with open(os.path.join(ROOT, "gpurun_out", "r01_configs.json"), "w") as f:
+        with open(os.path.join(ROOT, "gpurun_out", "r02_configs.json"), "w") as f:
             json.dump(out, f, indent=1)
 
 

@@ -166,13 +166,15 @@ static __device__ PD_RAMP_FN double ramp_accel(const DevRamp& r, long long step)
 }
 
 // x / d for d > 0 (dt, dt^2): a zero numerator (a fixed support: magnitude 0)
-// gives the signed zero IEEE division gives, without __ddiv_rn's slow path
-// (taken for zero numerators).  The division still runs (the compiler
-// speculates it), on 1.0 instead of the zero.
+// gives the signed zero IEEE division gives, with no division at all (an
+// inlined __ddiv_rn is speculated past the test, and a zero numerator takes
+// its slow path); other numerators call the division out of line.
+static __device__ __noinline__ double div_call(double x, double d) { return __ddiv_rn(x, d); }
+
 __device__ __forceinline__ double div_pos(double x, double d) {
-    const bool z = x == 0.0 && d > 0.0;
-    const double q = __ddiv_rn(z ? 1.0 : x, d);
-    return z ? x : q;
+    if (x == 0.0 && d > 0.0)
+        return x;
+    return div_call(x, d);
 }
 
 __device__ __forceinline__ bool finite3(double x, double y, double z) {

@@ -514,10 +514,10 @@ __global__ void __launch_bounds__(SBX * BY * SP, 512 / (SBX * BY * SP)) lattice_
             sU0 = ui;  // read by the next step's staging, after its gate
     }
 #ifdef PD_SMALL_PROF
-    if (t == 0 && blockIdx.x == 0 && blockIdx.y == 0)
-        printf("small prof cta z=%d steps=%d cycles/step gate %lld stage %lld slots %lld combine %lld "
+    if (t == 0 && (blockIdx.x == 0 || blockIdx.x == 2) && blockIdx.y == 0 && blockIdx.z % 4 == 2)
+        printf("small prof cta x=%d z=%d steps=%d cycles/step gate %lld stage %lld slots %lld combine %lld "
                "epilogue %lld tail %lld\n",
-               blockIdx.z, S.steps, pc[0] / (S.steps - 1), pc[1] / (S.steps - 1), pc[2] / (S.steps - 1),
+               blockIdx.x, blockIdx.z, S.steps, pc[0] / (S.steps - 1), pc[1] / (S.steps - 1), pc[2] / (S.steps - 1),
                pc[4] / (S.steps - 1), pc[5] / (S.steps - 1), pc[3] / (S.steps - 1));
 #endif
 #undef PD_PROF_MARK

@@ -203,8 +203,9 @@ __global__ void __launch_bounds__(BX * BY * BZT, MINB) lattice_step_kernel(DevAr
 // launch advances all the steps between two host events (write steps,
 // snapshots, the end of the run):
 //   * a CTA owns an SBX x 4 x 1 brick; each node's 122 slots are split over
-//     SP = 4 warps, one per 32-bit word of the row mask (warp w runs word
-//     w % 4, so the warps of one word share a scheduler);
+//     SPN = 8 warps, one per half of a 32-bit word of the row mask (4 with
+//     16-wide bricks: a word each; warp w runs part w % SPN, so the warps of
+//     one part share a scheduler);
 //   * each word is walked as a rolled loop over the slots some lane of the
 //     warp still has (rolled_word): a few hundred bytes of code, so the
 //     kernel stays in the SM's instruction cache (the unrolled slot parts,
@@ -221,7 +222,6 @@ __global__ void __launch_bounds__(BX * BY * BZT, MINB) lattice_step_kernel(DevAr
 // this path only when the grid fits (lattice_small_fits).  A barrier that
 // never completes (impossible under a cooperative launch) ends the run after
 // a timeout with kBarrierTimeout instead of hanging the device.
-constexpr int SP = 4;
 constexpr int kSmallMaxRamps = 32;  // ramp table of the small kernel (one per lane of a warp)
 
 inline int sm_count_small() {
@@ -246,7 +246,7 @@ struct SlotGeo {
 };
 
 template <bool NF>
-__device__ __forceinline__ void rolled_word(const float4* own, const float4& ri, unsigned mw, int word,
+__device__ __forceinline__ void rolled_word(const float4* own, const float4& ri, unsigned mw, int gbase,
                                             float sc, const SlotGeo* geo, float3& f, unsigned& dead) {
     unsigned todo = __reduce_or_sync(0xffffffffu, mw);
     float fx = 0.f, fy = 0.f, fz = 0.f;
@@ -265,7 +265,7 @@ __device__ __forceinline__ void rolled_word(const float4* own, const float4& ri,
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            const SlotGeo g = geo[32 * word + b[q]];
+            const SlotGeo g = geo[gbase + b[q]];
             const float4 rj = own[__float_as_int(g.e.z)];
             // stretch_c's arithmetic with the offset from the table
             const float2 dxy = make_float2(g.d.x, g.d.y);
@@ -346,18 +346,19 @@ __device__ __forceinline__ bool step_gate(bool wait, unsigned long long* count,
     return go != 0;
 }
 
-template <int MODE, bool BC, bool NF, int SBX>
-__global__ void __launch_bounds__(SBX * BY * SP, 512 / (SBX * BY * SP)) lattice_small_kernel(DevArgs A, LatticeArgs L,
-                                                                          SmallArgs S) {
+// SPN slot parts per node: 4 (a mask word each) or 8 (half a word each)
+template <int MODE, bool BC, bool NF, int SBX, int SPN>
+__global__ void __launch_bounds__(SBX * BY * SPN, SPN == 8 ? 3 : 512 / (SBX * BY * SPN))
+    lattice_small_kernel(DevArgs A, LatticeArgs L, SmallArgs S) {
     constexpr int NB = SBX * BY;               // nodes per brick
-    constexpr int NT = NB * SP;                // threads
+    constexpr int NT = NB * SPN;               // threads
     constexpr int SHX = SBX + 6;               // halo box: SHX x HY x 7
     constexpr int NR = SHX * HY * 7;
     constexpr int NRT = (NR + NT - 1) / NT;    // records staged per thread
     static_assert(NB % 32 == 0, "a warp holds 32 nodes of one brick");
     __shared__ float4 rec[NR];
-    __shared__ float4 part_f[SP - 1][NB];
-    __shared__ uint4 part_d[SP - 1][NB];
+    __shared__ float4 part_f[SPN - 1][NB];
+    __shared__ unsigned part_d[SPN - 1][NB];  // broken bits of the part, relative to its first slot
     __shared__ uint4 smask[NB];
     __shared__ SlotGeo geo[128];
     __shared__ AxisBc sbc[BC ? NB : 1][3];    // the nodes' boundary conditions, loaded once
@@ -366,8 +367,10 @@ __global__ void __launch_bounds__(SBX * BY * SP, 512 / (SBX * BY * SP)) lattice_
     __shared__ RampVals srv[2][BC ? kSmallMaxRamps : 1];
     __shared__ double4 sU0;                    // the brick origin's u: the staging reference
     const int t = threadIdx.x, wid = t / 32;
-    const int p = wid % SP;                    // the mask word of this warp (warp-uniform)
-    const int node = (wid / SP) * 32 + t % 32;
+    const int p = wid % SPN;                   // the slot part of this warp (warp-uniform)
+    const int node = (wid / SPN) * 32 + t % 32;
+    const int pword = SPN == 4 ? p : p / 2;    // its mask word
+    const int pshift = SPN == 4 ? 0 : 16 * (p % 2);
     if (t < 128) {
         SlotGeo g{};
         if (t < NPAT) {
@@ -466,13 +469,14 @@ __global__ void __launch_bounds__(SBX * BY * SP, 512 / (SBX * BY * SP)) lattice_
         const float4 ri = *own;
         const uint4 m = smask[node];
         const float sc = (NF && ri.w < 0.f) ? __int_as_float(0x7f800000) : L.sc;
-        const unsigned mw = p == 0 ? m.x : (p == 1 ? m.y : (p == 2 ? m.z : m.w));
+        const unsigned mw = pword == 0 ? m.x : (pword == 1 ? m.y : (pword == 2 ? m.z : m.w));
         float3 f;
         unsigned dw;
-        rolled_word<NF>(own, ri, mw, p, sc, geo, f, dw);
+        rolled_word<NF>(own, ri, SPN == 4 ? mw : (mw >> pshift) & 0xffffu, 32 * pword + pshift, sc, geo,
+                        f, dw);
         if (p > 0) {
             part_f[p - 1][node] = make_float4(f.x, f.y, f.z, 0.f);
-            part_d[p - 1][node] = make_uint4(p == 1 ? dw : 0u, p == 2 ? dw : 0u, p == 3 ? dw : 0u, 0u);
+            part_d[p - 1][node] = dw;
         }
         __syncthreads();
         PD_PROF_MARK(2);
@@ -482,16 +486,16 @@ __global__ void __launch_bounds__(SBX * BY * SP, 512 / (SBX * BY * SP)) lattice_
                 srv[(k + 1) & 1][t % 32] = ramp_vals(A.ramps[t % 32], A.step + k + 1);
             continue;
         }
-        uint4 dead = make_uint4(dw, 0u, 0u, 0u);
+        unsigned dd[4] = {dw, 0u, 0u, 0u};
 #pragma unroll
-        for (int q = 0; q < SP - 1; ++q) {  // word order: the same sum every run
-            const float4 g = part_f[q][node];
+        for (int q = 1; q < SPN; ++q) {  // part order: the same sum every run
+            const float4 g = part_f[q - 1][node];
             f.x += g.x;
             f.y += g.y;
             f.z += g.z;
-            const uint4 d = part_d[q][node];
-            dead = make_uint4(dead.x, dead.y | d.x, dead.z | d.y, dead.w | d.z);
+            dd[SPN == 4 ? q : q / 2] |= part_d[q - 1][node] << (SPN == 4 ? 0 : 16 * (q % 2));
         }
+        const uint4 dead = make_uint4(dd[0], dd[1], dd[2], dd[3]);
         if (dead.x | dead.y | dead.z | dead.w) {
             const uint4 nm = make_uint4(m.x & ~dead.x, m.y & ~dead.y, m.z & ~dead.z, m.w & ~dead.w);
             smask[node] = nm;
@@ -548,37 +552,53 @@ inline int small_bx(const LatticeArgs& L) {
     return bx;
 }
 
-template <int MODE, bool BC, bool NF, int SBX>
+// Slot parts per node: 8 (half a mask word per warp) with 8-wide bricks,
+// else 4.  PD_SMALL_P = 4 / 8 forces one (8 only with 8-wide bricks).
+inline int small_parts(int bx) {
+    if (const char* e = std::getenv("PD_SMALL_P")) {
+        const int v = std::atoi(e);
+        if (v == 4 || (v == 8 && bx == 8))
+            return v;
+    }
+    return bx == 8 ? 8 : 4;
+}
+
+template <int MODE, bool BC, bool NF, int SBX, int SPN>
 cudaError_t launch_small_w(const DevArgs& A, const LatticeArgs& L, const SmallArgs& S, cudaStream_t st) {
     const dim3 grid{unsigned((L.nx + SBX - 1) / SBX), unsigned((L.ny + BY - 1) / BY), unsigned(L.nz_own)};
-    t_last_kernel = kernel_name<3, MODE, BC, NF, SBX>("lattice_small_kernel");
+    t_last_kernel = kernel_name<3, MODE, BC, NF, SBX, SPN>("lattice_small_kernel");
     DevArgs a = A;
     LatticeArgs l = L;
     SmallArgs s = S;
     void* args[] = {&a, &l, &s};
     return cudaLaunchCooperativeKernel(
-        reinterpret_cast<const void*>(lattice_small_kernel<MODE, BC, NF, SBX>), grid, dim3(SBX * BY * SP),
-        args, 0, st);
+        reinterpret_cast<const void*>(lattice_small_kernel<MODE, BC, NF, SBX, SPN>), grid,
+        dim3(SBX * BY * SPN), args, 0, st);
 }
 
 template <int MODE, bool BC, bool NF>
 cudaError_t launch_small_t(const DevArgs& A, const LatticeArgs& L, const SmallArgs& S, cudaStream_t st) {
-    return small_bx(L) == 8 ? launch_small_w<MODE, BC, NF, 8>(A, L, S, st)
-                            : launch_small_w<MODE, BC, NF, 16>(A, L, S, st);
+    const int bx = small_bx(L);
+    if (bx == 16)
+        return launch_small_w<MODE, BC, NF, 16, 4>(A, L, S, st);
+    return small_parts(8) == 8 ? launch_small_w<MODE, BC, NF, 8, 8>(A, L, S, st)
+                               : launch_small_w<MODE, BC, NF, 8, 4>(A, L, S, st);
 }
 
-template <int MODE, bool BC, bool NF> int small_capacity(int bx) {
+template <auto Kernel> int occupancy(int threads) {
     int per_sm = 0;
-    const cudaError_t e =
-        bx == 8 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lattice_small_kernel<MODE, BC, NF, 8>,
-                                                                8 * BY * SP, 0)
-                : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lattice_small_kernel<MODE, BC, NF, 16>,
-                                                                16 * BY * SP, 0);
-    if (e != cudaSuccess) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, Kernel, threads, 0) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }
     return per_sm;
+}
+
+template <int MODE, bool BC, bool NF> int small_capacity(int bx) {
+    if (bx == 16)
+        return occupancy<lattice_small_kernel<MODE, BC, NF, 16, 4>>(16 * BY * 4);
+    return small_parts(8) == 8 ? occupancy<lattice_small_kernel<MODE, BC, NF, 8, 8>>(8 * BY * 8)
+                               : occupancy<lattice_small_kernel<MODE, BC, NF, 8, 4>>(8 * BY * 4);
 }
 
 template <int MODE> int small_capacity_mode(bool bc, bool nf, int bx) {
@@ -1038,16 +1058,18 @@ template <int MODE, bool BC, bool NF> void preload_bc() {
     }
 }
 
+template <int MODE, bool BC, bool NF> void preload_small() {
+    preload_fn(lattice_small_kernel<MODE, BC, NF, 16, 4>);
+    preload_fn(lattice_small_kernel<MODE, BC, NF, 8, 4>);
+    preload_fn(lattice_small_kernel<MODE, BC, NF, 8, 8>);
+}
+
 template <int MODE> void preload_mode() {
     if constexpr (MODE != 0) {
-        preload_fn(lattice_small_kernel<MODE, true, true, 16>);
-        preload_fn(lattice_small_kernel<MODE, true, false, 16>);
-        preload_fn(lattice_small_kernel<MODE, false, true, 16>);
-        preload_fn(lattice_small_kernel<MODE, false, false, 16>);
-        preload_fn(lattice_small_kernel<MODE, true, true, 8>);
-        preload_fn(lattice_small_kernel<MODE, true, false, 8>);
-        preload_fn(lattice_small_kernel<MODE, false, true, 8>);
-        preload_fn(lattice_small_kernel<MODE, false, false, 8>);
+        preload_small<MODE, true, true>();
+        preload_small<MODE, true, false>();
+        preload_small<MODE, false, true>();
+        preload_small<MODE, false, false>();
     }
     preload_bc<MODE, true, false>();
     preload_bc<MODE, false, false>();

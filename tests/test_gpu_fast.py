@@ -194,7 +194,7 @@ def test_fast_million_node_lattice(oracle):
 
 
 LAT_KERNELS = {  # PD_LAT_CFG -> the instantiation it selects on a 20x18x26 lattice
-    "0": "lattice_small_kernel<1,0,0,8>",  # by size (below two 16x4x4 bricks per SM): persistent
+    "0": "lattice_small_kernel<1,0,0,8,8>",  # by size (below two 16x4x4 bricks per SM): persistent
     "1": "lattice_step_kernel<1,8,3,0,0>",  # the BENCH instantiation (16x4x8, 3 CTAs/SM)
     "4": "lattice_step_kernel<1,4,5,0,0>",  # 16x4x4 bricks at 5 CTAs/SM
     "5": "lattice_step_kernel<1,1,1,0,0>",  # the small-brick latency variant, forced
@@ -350,18 +350,20 @@ def test_lattice_persistent_launch_is_chunk_invariant(monkeypatch, integrator):
     step between two host events in one launch.  Cutting the run at write
     steps (hook every 7 steps, tips) or into several run calls must give the
     same bits: the per-step arithmetic does not depend on the chunking.  The
-    one-step kernel (PD_LAT_PERSIST=0; its slot sums run in another order)
-    and 16-wide bricks (PD_SMALL_BX=16; other fp32 staging references) agree
-    within the fast-path tolerance."""
+    one-step kernel (PD_LAT_PERSIST=0; its slot sums run in another order),
+    16-wide bricks (PD_SMALL_BX=16; other fp32 staging references) and four
+    slot parts per node instead of eight (PD_SMALL_P=4; another sum order)
+    agree within the fast-path tolerance."""
     b, h, g = S.beam_bundle(30, 10, 10)
     b.bc.ramps[1].rise_steps = 150
     b.bc.magnitude[:] = b.bc.magnitude * 3.0  # drive it to fracture
     fam = geometry.build_family(b.particles.coords, h, g)
     outs = {}
     for name, persist, we, split in (("one", "1", 0, 1), ("hooked", "1", 7, 1), ("split", "1", 0, 3),
-                                     ("step", "0", 0, 1), ("bx16", "1", 0, 1)):
+                                     ("step", "0", 0, 1), ("bx16", "1", 0, 1), ("p4", "1", 0, 1)):
         monkeypatch.setenv("PD_LAT_PERSIST", persist)
         monkeypatch.setenv("PD_SMALL_BX", "16" if name == "bx16" else "0")
+        monkeypatch.setenv("PD_SMALL_P", "4" if name == "p4" else "0")
         ctx = engine.Context(0)
         st = make_state(fam, False)
         ctx.upload(b, st, KernelVariant.fast)
@@ -382,7 +384,7 @@ def test_lattice_persistent_launch_is_chunk_invariant(monkeypatch, integrator):
             assert np.array_equal(getattr(ref, f), getattr(outs[name], f)), (name, f)
         assert np.array_equal(ref.connectivity.entries, outs[name].connectivity.entries), name
     broken = fam.n_neigh.sum() - ref.connectivity.n_neigh.sum()
-    for name in ("step", "bx16"):
+    for name in ("step", "bx16", "p4"):
         st = outs[name]
         diff = int((ref.connectivity.entries != st.connectivity.entries).sum())
         assert diff <= max(4, 0.01 * broken), (name, diff, broken)

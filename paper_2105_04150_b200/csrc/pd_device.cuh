@@ -166,15 +166,27 @@ static __device__ PD_RAMP_FN double ramp_accel(const DevRamp& r, long long step)
 }
 
 // x / d for d > 0 (dt, dt^2): a zero numerator (a fixed support: magnitude 0)
-// gives the signed zero IEEE division gives, with no division at all (an
-// inlined __ddiv_rn is speculated past the test, and a zero numerator takes
-// its slow path); other numerators call the division out of line.
+// gives the signed zero IEEE division gives, without __ddiv_rn's slow path
+// (taken for zero numerators).  OOL = false: the division is inlined (the
+// compiler speculates it past the test, so it runs on 1.0 instead of the
+// zero); OOL = true (the persistent small-model kernel, where the supports'
+// divisions are the per-step critical path): no division for a zero
+// numerator, an out-of-line call otherwise.  An out-of-line call in the big
+// unrolled kernels costs them registers around the call site (cfg2's
+// n-linear step: 87 -> 112 us), so they keep the inline form.
 static __device__ __noinline__ double div_call(double x, double d) { return __ddiv_rn(x, d); }
 
+template <bool OOL>
 __device__ __forceinline__ double div_pos(double x, double d) {
-    if (x == 0.0 && d > 0.0)
-        return x;
-    return div_call(x, d);
+    if constexpr (OOL) {
+        if (x == 0.0 && d > 0.0)
+            return x;
+        return div_call(x, d);
+    } else {
+        const bool z = x == 0.0 && d > 0.0;
+        const double q = __ddiv_rn(z ? 1.0 : x, d);
+        return z ? x : q;
+    }
 }
 
 __device__ __forceinline__ bool finite3(double x, double y, double z) {
@@ -248,7 +260,7 @@ __device__ __forceinline__ RampVals ramp_vals(const DevRamp& r, long long s) {
 // receive the node's new v, a (and 1/rho) and the u written to u_out (the
 // next step's u_in), so a kernel that owns the node across steps need not
 // reload them.
-template <int MODE, bool BC = true>
+template <int MODE, bool BC = true, bool OOL_DIV = false>
 __device__ __forceinline__ void node_epilogue(const DevArgs& A, long long i, const double4& ui,
                                               double fx, double fy, double fz, const NodeIn& in,
                                               const AxisBc* bc = nullptr, NodeIn* next = nullptr,
@@ -280,8 +292,8 @@ __device__ __forceinline__ void node_epilogue(const DevArgs& A, long long i, con
             double an = __dmul_rn(__dsub_rn(__dadd_rn(Fb[ax], Fe[ax]), __dmul_rn(vh, A.damping)), inv);
             double vn = __dadd_rn(vh, __dmul_rn(an, A.half_dt));
             if (kind == PD_BC_DISPLACEMENT) {
-                vn = div_pos(__dmul_rn(mag, rv ? rv[b.rid].rate1 : ramp_rate(ramp, s + 1)), dt);
-                an = div_pos(__dmul_rn(mag, rv ? rv[b.rid].acc1 : ramp_accel(ramp, s + 1)), A.dt2);
+                vn = div_pos<OOL_DIV>(__dmul_rn(mag, rv ? rv[b.rid].rate1 : ramp_rate(ramp, s + 1)), dt);
+                an = div_pos<OOL_DIV>(__dmul_rn(mag, rv ? rv[b.rid].acc1 : ramp_accel(ramp, s + 1)), A.dt2);
             }
             v[ax] = vn;
             a[ax] = an;
@@ -297,8 +309,8 @@ __device__ __forceinline__ void node_epilogue(const DevArgs& A, long long i, con
             un[ax] = __dadd_rn(u0[ax], __dmul_rn(MODE == 2 ? v_old : v_new, dt));
             if (kind == PD_BC_DISPLACEMENT) {
                 un[ax] = __dmul_rn(mag, scale_at(1));
-                v[ax] = div_pos(__dmul_rn(mag, rv ? rv[b.rid].rate1 : ramp_rate(ramp, s + 1)), dt);
-                a[ax] = div_pos(__dmul_rn(mag, rv ? rv[b.rid].acc1 : ramp_accel(ramp, s + 1)), A.dt2);
+                v[ax] = div_pos<OOL_DIV>(__dmul_rn(mag, rv ? rv[b.rid].rate1 : ramp_rate(ramp, s + 1)), dt);
+                a[ax] = div_pos<OOL_DIV>(__dmul_rn(mag, rv ? rv[b.rid].acc1 : ramp_accel(ramp, s + 1)), A.dt2);
             }
         }
     }

@@ -511,8 +511,8 @@ __global__ void __launch_bounds__(SBX * BY * SPN, SPN == 8 ? 3 : 512 / (SBX * BY
         const bool last = k + 1 == S.steps;
         Ak.store_forces = last ? S.store_last : 0;
         Ak.do_drift = last ? S.drift_last : 1;
-        node_epilogue<MODE, BC>(Ak, i, ui, fx, fy, fz, nin, BC ? sbc[node] : nullptr, &nin, &ui,
-                                srv[k & 1]);
+        node_epilogue<MODE, BC, true>(Ak, i, ui, fx, fy, fz, nin, BC ? sbc[node] : nullptr, &nin, &ui,
+                                      srv[k & 1]);
         PD_PROF_MARK(5);
         if (node == 0)
             sU0 = ui;  // read by the next step's staging, after its gate

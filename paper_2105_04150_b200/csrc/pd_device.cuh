@@ -165,28 +165,20 @@ static __device__ PD_RAMP_FN double ramp_accel(const DevRamp& r, long long step)
     return __ddiv_rn(x, __dmul_rn((double)r.rise, (double)r.rise));
 }
 
-// x / d for d > 0 (dt, dt^2): a zero numerator (a fixed support: magnitude 0)
-// gives the signed zero IEEE division gives, without __ddiv_rn's slow path
-// (taken for zero numerators).  OOL = false: the division is inlined (the
-// compiler speculates it past the test, so it runs on 1.0 instead of the
-// zero); OOL = true (the persistent small-model kernel, where the supports'
-// divisions are the per-step critical path): no division for a zero
-// numerator, an out-of-line call otherwise.  An out-of-line call in the big
-// unrolled kernels costs them registers around the call site (cfg2's
-// n-linear step: 87 -> 112 us), so they keep the inline form.
+// x / d for d > 0 (dt, dt^2) in the persistent small-model kernel, where the
+// supports' divisions are the per-step critical path: a zero numerator (a
+// fixed support: magnitude 0) gives the signed zero IEEE division gives with
+// no division at all (__ddiv_rn takes its slow path for zero numerators, and
+// an inlined one is speculated past a test), others call it out of line.
+// The one-step kernels keep the plain inline division: an out-of-line call
+// costs the big unrolled kernels registers around the call site (cfg2's
+// n-linear step: 87 -> 112 us).
 static __device__ __noinline__ double div_call(double x, double d) { return __ddiv_rn(x, d); }
 
-template <bool OOL>
 __device__ __forceinline__ double div_pos(double x, double d) {
-    if constexpr (OOL) {
-        if (x == 0.0 && d > 0.0)
-            return x;
-        return div_call(x, d);
-    } else {
-        const bool z = x == 0.0 && d > 0.0;
-        const double q = __ddiv_rn(z ? 1.0 : x, d);
-        return z ? x : q;
-    }
+    if (x == 0.0 && d > 0.0)
+        return x;
+    return div_call(x, d);
 }
 
 __device__ __forceinline__ bool finite3(double x, double y, double z) {
@@ -254,13 +246,14 @@ __device__ __forceinline__ RampVals ramp_vals(const DevRamp& r, long long s) {
 
 // BC = false: the caller guarantees A.bc_kind == NULL (no boundary conditions),
 // so the ramp code is compiled out (fewer registers in the fused kernels).
-// bc: the node's three AxisBc when the caller keeps them (the persistent
-// small-model kernel), else NULL (loaded here).  rv: this step's RampVals per
-// ramp id when the caller evaluated them, else NULL.  next / u_next: when given,
-// receive the node's new v, a (and 1/rho) and the u written to u_out (the
-// next step's u_in), so a kernel that owns the node across steps need not
-// reload them.
-template <int MODE, bool BC = true, bool OOL_DIV = false>
+// KEEP = true (the persistent small-model kernel, which owns its nodes across
+// steps): bc holds the node's three AxisBc (shared memory), rv this step's
+// RampVals per ramp id, and next / u_next receive the node's new v, a (and
+// 1/rho) and the u written to u_out (the next step's u_in), so nothing is
+// reloaded; zero-numerator divisions skip the division (div_pos).  KEEP =
+// false compiles to the one-step kernels' original code (the extra state
+// cost the exact kernel 3 % at 216^3 in registers and spills).
+template <int MODE, bool BC = true, bool KEEP = false>
 __device__ __forceinline__ void node_epilogue(const DevArgs& A, long long i, const double4& ui,
                                               double fx, double fy, double fz, const NodeIn& in,
                                               const AxisBc* bc = nullptr, NodeIn* next = nullptr,
@@ -275,16 +268,46 @@ __device__ __forceinline__ void node_epilogue(const DevArgs& A, long long i, con
     // records out of local memory
 #pragma unroll
     for (int ax = 0; ax < 3; ++ax) {
-        AxisBc b{PD_BC_FREE, 0, 0.0, DevRamp{}};
-        if (BC)
-            b = bc ? bc[ax] : load_axis_bc(A, i, ax);
-        const int kind = b.kind;
-        const double mag = b.mag;
-        const DevRamp& ramp = b.ramp;
-        // ramp values: this step's table when given, else evaluated here
-        auto scale_at = [&](int ds) {  // ds = 0, 1, 2: scale(s + ds)
-            return rv ? (ds == 0 ? rv[b.rid].sc0 : ds == 1 ? rv[b.rid].sc1 : rv[b.rid].sc2)
-                      : ramp_scale(ramp, s + ds);
+        int kind = PD_BC_FREE, rid = 0;
+        double mag = 0.0;
+        DevRamp ramp{};
+        if constexpr (KEEP) {
+            if constexpr (BC) {
+                kind = bc[ax].kind;
+                mag = bc[ax].mag;
+                rid = bc[ax].rid;
+            }
+        } else {
+            kind = (BC && A.bc_kind) ? int(A.bc_kind[3 * i + ax]) : PD_BC_FREE;
+            if (kind != PD_BC_FREE) {
+                mag = A.bc_mag[3 * i + ax];
+                ramp = A.ramps[A.bc_ramp[3 * i + ax]];
+            }
+        }
+        // RampProfile values at s + ds: this step's table (KEEP), else evaluated here
+        auto scale_at = [&](int ds) {
+            if constexpr (KEEP)
+                return ds == 0 ? rv[rid].sc0 : ds == 1 ? rv[rid].sc1 : rv[rid].sc2;
+            else
+                return ramp_scale(ramp, s + ds);
+        };
+        auto rate1 = [&] {
+            if constexpr (KEEP)
+                return rv[rid].rate1;
+            else
+                return ramp_rate(ramp, s + 1);
+        };
+        auto accel1 = [&] {
+            if constexpr (KEEP)
+                return rv[rid].acc1;
+            else
+                return ramp_accel(ramp, s + 1);
+        };
+        auto div = [&](double x, double d) {
+            if constexpr (KEEP)
+                return div_pos(x, d);
+            else
+                return __ddiv_rn(x, d);
         };
         Fe[ax] = kind == PD_BC_FORCE ? __dadd_rn(0.0, __dmul_rn(mag, scale_at(MODE == 1 ? 1 : 0))) : 0.0;
         if (MODE == 1) {
@@ -292,8 +315,8 @@ __device__ __forceinline__ void node_epilogue(const DevArgs& A, long long i, con
             double an = __dmul_rn(__dsub_rn(__dadd_rn(Fb[ax], Fe[ax]), __dmul_rn(vh, A.damping)), inv);
             double vn = __dadd_rn(vh, __dmul_rn(an, A.half_dt));
             if (kind == PD_BC_DISPLACEMENT) {
-                vn = div_pos<OOL_DIV>(__dmul_rn(mag, rv ? rv[b.rid].rate1 : ramp_rate(ramp, s + 1)), dt);
-                an = div_pos<OOL_DIV>(__dmul_rn(mag, rv ? rv[b.rid].acc1 : ramp_accel(ramp, s + 1)), A.dt2);
+                vn = div(__dmul_rn(mag, rate1()), dt);
+                an = div(__dmul_rn(mag, accel1()), A.dt2);
             }
             v[ax] = vn;
             a[ax] = an;
@@ -309,8 +332,8 @@ __device__ __forceinline__ void node_epilogue(const DevArgs& A, long long i, con
             un[ax] = __dadd_rn(u0[ax], __dmul_rn(MODE == 2 ? v_old : v_new, dt));
             if (kind == PD_BC_DISPLACEMENT) {
                 un[ax] = __dmul_rn(mag, scale_at(1));
-                v[ax] = div_pos<OOL_DIV>(__dmul_rn(mag, rv ? rv[b.rid].rate1 : ramp_rate(ramp, s + 1)), dt);
-                a[ax] = div_pos<OOL_DIV>(__dmul_rn(mag, rv ? rv[b.rid].acc1 : ramp_accel(ramp, s + 1)), A.dt2);
+                v[ax] = div(__dmul_rn(mag, rate1()), dt);
+                a[ax] = div(__dmul_rn(mag, accel1()), A.dt2);
             }
         }
     }
@@ -320,7 +343,7 @@ __device__ __forceinline__ void node_epilogue(const DevArgs& A, long long i, con
         A.v[3 * i + ax] = v[ax];
         A.a[3 * i + ax] = a[ax];
     }
-    if (next) {
+    if constexpr (KEEP) {
 #pragma unroll
         for (int ax = 0; ax < 3; ++ax) {
             next->v[ax] = v[ax];
@@ -338,12 +361,12 @@ __device__ __forceinline__ void node_epilogue(const DevArgs& A, long long i, con
     if (write_u) {
         const double4 unew = make_double4(un[0], un[1], un[2], ui.w);
         A.u_out[i] = unew;
-        if (u_next)
+        if constexpr (KEEP)
             *u_next = unew;
         push_ghost(A, i, unew);
         if (!finite3(un[0], un[1], un[2]))
             atomicMin((unsigned long long*)A.err_step, (unsigned long long)(s + 1));
-    } else if (u_next) {
+    } else if constexpr (KEEP) {
         *u_next = ui;
     }
 }
